@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py — GSGP hot path on B200: precompute points/s (W^T W + W^T y) on the 3-D
+radar-like config (BASELINE.json configs[2]: n = 1.2e8 fp32 rows, grid 80×80×20, cubic),
+plus factorized-CG iterations/s of the posterior-mean solve on the resulting statistics.
+
+One JSON line on rank 0 (contract in the task prompt):
+  value   — whole-job precompute throughput, inputs resident in HBM (CUDA events, max over ranks)
+  e2e     — same metric through the public API with HOST (pinned) rows: H2D of the rows and
+            D2H of W^T y, y^T y, n inside the timed region
+  roofline— K1 (per-cell moments kernel) vs measured HBM and measured FP64 peaks
+  cpu_baseline — the oracle restatement of the reference (hash-map accumulation, all
+            host threads) on a bounded prefix sample of the same workload
+`--impl reference` times only the reference CPU path (the oracle port: the reference
+itself cannot be built here) on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "precompute points/sec (W^T W+W^T y) & factorized-CG iters/sec; % of HBM roofline"
+PUBLISHED_PTS_PER_S = 120e6 / 4861.60  # 1.2e8-point radar precompute, Xeon Gold 6240
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=3)
+    p.add_argument("--n", type=int, default=0, help="rows per rank (default: the config's n)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-cg", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "traffic.json"))
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        rows = []
+        for ln in open(self.path):
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return float("nan")
+
+        sm = np.array([num(r[1]) for r in rows])
+        mx = np.nanmax([num(r[2]) for r in rows])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        load = sm[sm > 0.5 * np.nanmax(sm)] if np.isfinite(sm).any() else sm
+        return {"sm_mhz": float(np.nanmedian(load)), "sm_max_mhz": float(mx), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- roofline arithmetic
+def algorithmic_bytes(n, m, s_min, b_pt):
+    """B_pre = n·b_pt + 8·m·(S_min + 1)."""
+    return n * b_pt + 8.0 * m * (s_min + 1)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- CPU (oracle) timing
+def cpu_rate(x, y, grid_o, scheme, nthreads, target_s):
+    """Points/s of the oracle restatement (reference algorithm) on a prefix sample."""
+    import oracle as O
+
+    n_all = x.shape[0]
+    s = min(n_all, 2000 * nthreads)
+    while True:
+        t0 = time.perf_counter()
+        st = O.sufficient_stats(grid_o, x[:s], y[:s], scheme=scheme, nthreads=nthreads)
+        el = time.perf_counter() - t0
+        del st
+        if el >= target_s / 3 or s >= n_all:
+            return s / el, s, el
+        s = min(n_all, int(s * max(2.0, (target_s / 2) / max(el, 1e-3))))
+
+
+def oracle_grid(grid):
+    import oracle as O
+
+    d = grid.dim()
+    return O.Grid([grid.min(k) for k in range(d)], [grid.max(k) for k in range(d)], [grid.size(k) for k in range(d)])
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2101_11751_b200 import synthetic as S
+
+    O.build()
+    cfg = S.CONFIGS[args.config]
+    n_sample_max = 4_000_000
+    x, y = S.generate(args.config, n=min(cfg.n, n_sample_max))
+    grid = S.grid_for(cfg)
+    og = oracle_grid(grid)
+    threads = os.cpu_count() or 1
+    # size one step: ~target seconds of all-core work
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    rate, s, el = cpu_rate(x, y, og, 1, threads, per_step)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        st = O.sufficient_stats(og, x[:s], y[:s], scheme=1, nthreads=threads)
+        el = time.perf_counter() - t0
+        del st
+        if i >= args.warmup:
+            times.append(el)
+    ms = 1e3 * float(np.mean(times))
+    value = s / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": value / PUBLISHED_PTS_PER_S, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config} ({cfg.name}) prefix sample", "sample_rows": s,
+                   "grid": list(cfg.sizes), "scheme": "cubic"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": f"first {s} rows of config {args.config} per step (oracle restatement: "
+                                   f"std::unordered_map accumulation, interp.cpp:179-221; threads shard rows "
+                                   f"and merge(), interp.cpp:202-210)"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_2101_11751_b200 as G
+    from paper_2101_11751_b200 import synthetic as S
+    from paper_2101_11751_b200.build import build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    build()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2101_11751_b200.distributed import allreduce_stats
+
+    cfg = S.CONFIGS[args.config]
+    n = args.n or cfg.n
+    ctx = G.Context(local)
+    ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    rows = S.generate_torch(args.config, n, device=f"cuda:{local}", seed=rank)
+    torch.cuda.synchronize()
+    grid = S.grid_for(cfg)
+    spec = S.kernel_for(cfg)
+    acc = G.SufficientStatsAccumulator(grid, G.InterpScheme.Cubic, ctx=ctx)
+
+    def step(src):
+        acc.reset()
+        acc.add(src)
+        st = acc.finalize()
+        if world > 1:
+            allreduce_stats(st)
+        return st
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(rows)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count
+    barrier()
+    e0.record(ext)
+    for _ in range(args.steps):
+        st = step(rows)
+    e1.record(ext)
+    e1.synchronize()
+    barrier()
+    launches = ctx.launch_count - l0
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    value = world * n / (ms / 1e3)
+
+    # per-phase device times (separate pass: phase events add host syncs)
+    ctx.enable_phase_timing(True)
+    ctx.reset_phase_times()
+    for _ in range(args.steps):
+        step(rows)
+    phases = ctx.phase_times()
+    ctx.enable_phase_timing(False)
+    ph_ms = {k: v[0] / max(v[1], 1) for k, v in phases.items()}
+    k1_ms = ph_ms.get("moments", float("nan"))
+
+    m = grid.num_points()
+    s_min = st.n_offsets()
+    b_pt = (cfg.d + 1) * (4 if cfg.dtype == "f32" else 8)
+    b_pre = algorithmic_bytes(n, m, s_min, b_pt)
+    hbm_peak, peak_src = load_peaks()
+    fp64_peak = ctx.fp64_peak_tflops()
+    W = 4
+    qx, qy = (2 * W - 1) ** cfg.d, W ** cfg.d
+    flops_pt = 2.0 * (qx + qy)  # minimal FP64 work per point: one FMA per moment
+    traffic = None
+    if os.path.exists(args.traffic_file):
+        try:
+            tf = json.load(open(args.traffic_file))
+            traffic = tf.get(f"config{args.config}", {}).get("k_moments_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    achieved = b_pre / (k1_ms / 1e3) / 1e9
+    roofline = {
+        "bound": "hbm", "kernel": "k_moments_d3c (K1: per-cell polynomial moments)",
+        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+        "traffic": traffic, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
+        "algorithmic_bytes_per_launch": b_pre,
+        "k1_ms": k1_ms, "phase_ms": ph_ms,
+        "step_achieved_gbs": b_pre / (ms / 1e3) / 1e9 / 1.0,
+        "fp64": {"achieved": flops_pt * n / (k1_ms / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                 "frac": flops_pt * n / (k1_ms / 1e3) / 1e12 / fp64_peak, "flops_per_point": flops_pt,
+                 "peak_source": "measured (gsgpc_diag_fp64_peak DFMA loop, this run)",
+                 "note": "K1 is FP64-bound at d=3: 407 moment FMAs per 16-byte point"},
+    }
+
+    # factorized CG (posterior mean to tol 1e-6) on the merged statistics
+    cg = None
+    if not args.no_cg:
+        kg = G.ToeplitzOperator(grid, spec, ctx=ctx)
+        res = []
+        for i in range(args.warmup + args.steps):
+            model = G.posterior_mean_gsgp(st, kg, spec, G.InterpScheme.Cubic, cfg.noise_std, cfg.tol, 5000)
+            if i >= args.warmup:
+                res.append((model.solve_iterations, model.loop_seconds))
+        iters = sum(r[0] for r in res)
+        secs = sum(r[1] for r in res)
+        ips = iters / secs if secs > 0 else float("nan")
+        b_it = 8.0 * m * s_min + 128.0 * m
+        cg = {"iters_per_sec": ips, "iterations": res[0][0], "ms_per_iter": 1e3 / ips,
+              "tol": cfg.tol, "roofline": {"bound": "hbm", "kernel": "k_cg_spmv (K3 stencil SpMV) + K_G + updates",
+                                            "algorithmic_bytes_per_iter": b_it,
+                                            "achieved": b_it * ips / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                            "frac": b_it * ips / 1e9 / hbm_peak}}
+
+    # end-to-end through the public API with host (pinned) rows
+    e2e = None
+    if not args.no_e2e:
+        host_rows = rows.cpu().pin_memory()
+        st = step(host_rows)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st = step(host_rows)
+            wty = st.wty()
+            yty = st.yty()
+            nn = st.n()
+        barrier()
+        el = (time.perf_counter() - t0) / args.steps
+        el = max_over_ranks(el)
+        e2e = {"value": world * n / el, "unit": "points/s", "h2d_bytes_per_step": int(host_rows.numel() *
+                                                                                        host_rows.element_size()),
+               "d2h_bytes_per_step": int(wty.nbytes + 16), "ms_per_step": el * 1e3,
+               "timing": "host perf_counter around synchronous API calls (H2D staging + compute + D2H)"}
+        assert nn == n * world and np.isfinite(yty)
+        del host_rows
+
+    # CPU baseline: oracle restatement on a prefix sample (rank 0, N=1 only)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        import oracle as O
+
+        O.build()
+        samp = rows[: min(n, 4_000_000)].cpu().numpy()
+        threads = os.cpu_count() or 1
+        rate, s, el = cpu_rate(samp[:, : cfg.d], samp[:, cfg.d], oracle_grid(grid), 1, threads, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "points/s", "cores": threads, "kind": "port",
+               "sample": f"first {s} rows of the bench workload ({el:.1f} s, {threads} threads, oracle "
+                         f"hash-map restatement of SufficientStatsAccumulator::add)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": value / PUBLISHED_PTS_PER_S, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config{args.config}: {cfg.name}, n={n} rows/rank "
+                                   f"({'fp32' if cfg.dtype == 'f32' else 'fp64'} (x, y) rows), grid "
+                                   f"{'x'.join(map(str, cfg.sizes))} (m={m}), cubic, fp64 accumulation",
+                       "n_per_rank": n, "grid": list(cfg.sizes), "scheme": "cubic",
+                       "parallelism": f"dp{world} (rows sharded, NCCL all-reduce of statistics)",
+                       "l2": f"inputs {n * b_pt / 1e9:.2f} GB per rank > 126 MB L2"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "cg": cg, "clocks": clk,
+            "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+            "version": G.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,240 @@
+/*
+ * gsgpc.h — C ABI of the B200-native GSGP hot path (libgsgpc.so).
+ *
+ * Drop-in boundary for the reference's proj/include/gsgp C++ API
+ * (/root/reference/proj/include/gsgp/{interp,grid,solvers,gp,io}.hpp).  Each entry point
+ * names the reference interface it replaces (file:line).  Plain pointers and sizes only:
+ * no torch, no Eigen, no exceptions cross this boundary.
+ *
+ * Memory: every `const double* / double*` array argument may live in host memory
+ * (pageable or pinned) or in device memory of the context's GPU; the library detects
+ * which (cudaPointerGetAttributes) and stages host arrays through the context's stream.
+ * Handles own their device buffers; callers own their arrays.
+ *
+ * Errors: functions return a gsgpc_status; gsgpc_last_error(ctx) holds the reference's
+ * message text ("sufficient_stats: stream row 17: interp_weights: point outside grid",
+ * "factorized_cg_grid_rhs: p^T A p <= 0, ...").  OUT_OF_GRID also records the 1-based
+ * minimum offending row (gsgpc_last_error_row), i.e. the row at which the reference's
+ * single pass would have thrown.  A failed call leaves its handles unchanged.
+ *
+ * Threading: one CUDA stream per context; calls on one context are serialised by the
+ * caller (the C++/Python wrappers do this).  Contexts on different devices are
+ * independent; multi-GPU precompute combines per-device statistics with an all-reduce
+ * over gsgpc_stats_reduce_buffer() (merge() semantics, interp.cpp:202-210).
+ */
+#ifndef GSGPC_H
+#define GSGPC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSGPC_MAX_DIM 3
+
+typedef enum {
+  GSGPC_OK = 0,
+  GSGPC_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  GSGPC_OUT_OF_GRID = 2,      /* std::invalid_argument from interp_weights (interp.cpp:53-55,119-124) */
+  GSGPC_BREAKDOWN = 3,        /* SolverBreakdown (solvers.hpp:73-76) */
+  GSGPC_NONCONVERGENCE = 4,   /* SolverNonConvergence (gp.hpp:17-23) */
+  GSGPC_CUDA_ERROR = 5,
+  GSGPC_UNSUPPORTED = 6,      /* valid for the reference, outside this build (e.g. d > 3) */
+  GSGPC_RUNTIME_ERROR = 7,    /* std::runtime_error (negative Ritz value, gp.cpp:44-47) */
+} gsgpc_status;
+
+/* InterpScheme (interp.hpp:15); the numeric values match the stats-file encoding
+ * (io.cpp:205: 0 = Linear, 1 = Cubic). */
+typedef enum { GSGPC_LINEAR = 0, GSGPC_CUBIC = 1 } gsgpc_scheme;
+
+typedef enum { GSGPC_F32 = 0, GSGPC_F64 = 1 } gsgpc_dtype;
+
+typedef struct gsgpc_ctx gsgpc_ctx;
+typedef struct gsgpc_stats gsgpc_stats;
+typedef struct gsgpc_kg gsgpc_kg;
+
+/* gsgp::Grid / GridDim (grid.hpp:15-44): row-major flattening, last dimension fastest. */
+typedef struct {
+  int32_t dim;
+  double min[GSGPC_MAX_DIM];
+  double max[GSGPC_MAX_DIM];
+  int64_t size[GSGPC_MAX_DIM];
+} gsgpc_grid;
+
+/* A batch of data rows — the RowStream::next (interp.hpp:150-155) source, in memory.
+ * Coordinate k of row i is at  x[i*x_row_stride + x_col_offset[k]],  the response at
+ * y[i*y_stride]  (element units of `dtype`).  Covers SoA, AoS (x..., y) rows such as the
+ * reference's GSGPDAT1 f64 rows (io.hpp:31-45), and packed fp32 float4 (x1,x2,x3,y). */
+typedef struct {
+  int32_t dtype; /* gsgpc_dtype, shared by x and y */
+  const void* x;
+  int64_t x_row_stride;
+  int64_t x_col_offset[GSGPC_MAX_DIM];
+  const void* y;
+  int64_t y_stride;
+} gsgpc_points;
+
+/* ---------------------------------------------------------------- context */
+gsgpc_status gsgpc_ctx_create(int device, gsgpc_ctx** out);
+void gsgpc_ctx_destroy(gsgpc_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own one. */
+gsgpc_status gsgpc_ctx_set_stream(gsgpc_ctx* ctx, void* cuda_stream);
+void* gsgpc_ctx_stream(gsgpc_ctx* ctx);
+gsgpc_status gsgpc_ctx_synchronize(gsgpc_ctx* ctx);
+const char* gsgpc_last_error(const gsgpc_ctx* ctx);
+int64_t gsgpc_last_error_row(const gsgpc_ctx* ctx);
+/* Number of library kernels launched on this context so far (instrumentation). */
+uint64_t gsgpc_ctx_launch_count(const gsgpc_ctx* ctx);
+/* Per-phase device timing (CUDA events on the context stream), off by default.
+ * Phases: 0 classify/count, 1 scan, 2 scatter, 3 moments (K1), 4 finalize, 5 H2D. */
+gsgpc_status gsgpc_ctx_enable_phase_timing(gsgpc_ctx* ctx, int enable);
+gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out /*[8]*/, int64_t* calls_out /*[8]*/);
+gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx);
+/* Diagnostics: measured FP64 FMA throughput of this GPU (TFLOP/s, 2 flops per DFMA) from a
+ * register-resident DFMA loop over all SMs — the denominator of the precompute's FP64 roofline. */
+gsgpc_status gsgpc_diag_fp64_peak(gsgpc_ctx* ctx, double* tflops);
+/* Library build identification ("gsgpc sm_100a <git> ..."). */
+const char* gsgpc_version(void);
+
+/* ---------------------------------------------------------------- grid helpers */
+/* fit_grid_to_data (interp.hpp:168-172, interp.cpp:286-306). */
+gsgpc_status gsgpc_fit_grid_to_data(int dim, const double* lo, const double* hi,
+                                    const int64_t* sizes, int scheme, gsgpc_grid* out);
+
+/* interp_weights (interp.hpp:38-41, interp.cpp:79-134) for n points, bit-exact: idx/w are
+ * n × (2r)^d (row i holds nnz[i] entries in the reference's order, exact zeros dropped);
+ * status[i] = 0 ok, 1 point outside grid, 2 stencil leaves the grid. Arrays host or device. */
+gsgpc_status gsgpc_interp_weights(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme,
+                                  const gsgpc_points* pts, int64_t n, int64_t* idx, double* w,
+                                  int32_t* nnz, int32_t* status);
+
+/* ---------------------------------------------------------------- sufficient statistics */
+/* SufficientStatsAccumulator(Grid, InterpScheme) (interp.hpp:87-91, interp.cpp:179-186). */
+gsgpc_status gsgpc_stats_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme,
+                                gsgpc_stats** out);
+void gsgpc_stats_destroy(gsgpc_stats* stats);
+/* SufficientStatsAccumulator::add over a batch of n rows (interp.cpp:188-200), rows
+ * numbered after the rows already added.  Optional probe_words (n × ceil(P/64) uint64, bit p of
+ * row i = sign of the p-th Rademacher probe, +1 when set) accumulate the probe images W^T v_p
+ * used by the factorized SLQ (gp.cpp:97-99); pass NULL / 0 otherwise. */
+gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* stats, const gsgpc_points* pts,
+                             int64_t n, const uint64_t* probe_words, int probes);
+/* Reset an accumulator to the freshly constructed state (no rows), keeping its buffers —
+ * equivalent to constructing a new SufficientStatsAccumulator on the same grid. */
+gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* stats);
+/* SufficientStatsAccumulator::merge (interp.cpp:202-210): dst += src (same device). */
+gsgpc_status gsgpc_stats_merge(gsgpc_ctx* ctx, gsgpc_stats* dst, const gsgpc_stats* src);
+/* SufficientStatsAccumulator::finalize (interp.cpp:212-221): cell moments → W^T W stencil,
+ * W^T y.  Called implicitly by every consumer below. */
+gsgpc_status gsgpc_stats_finalize(gsgpc_ctx* ctx, gsgpc_stats* stats);
+/* sufficient_stats (interp.hpp:159-160, interp.cpp:244-263): create + add + finalize. */
+gsgpc_status gsgpc_sufficient_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme,
+                                    const gsgpc_points* pts, int64_t n, gsgpc_stats** out);
+
+/* SufficientStats accessors (interp.hpp:128-146): grid_size() m, n(), yty(), and the
+ * stored W^T W layout: n_offsets = (S+1)/2 symmetric stencil offsets, S = (4r-1)^d. */
+gsgpc_status gsgpc_stats_info(gsgpc_ctx* ctx, gsgpc_stats* stats, int64_t* m, int64_t* n,
+                              double* yty, int64_t* n_offsets, int32_t* probes);
+gsgpc_status gsgpc_stats_grid(const gsgpc_stats* stats, gsgpc_grid* grid, int* scheme);
+/* W^T y (m doubles). */
+gsgpc_status gsgpc_stats_copy_wty(gsgpc_ctx* ctx, gsgpc_stats* stats, double* out);
+/* W^T W as the symmetric stencil: values n_offsets × m (offset-major), offsets n_offsets × dim
+ * integer displacements (lexicographically non-negative half, offset 0 first). */
+gsgpc_status gsgpc_stats_copy_stencil(gsgpc_ctx* ctx, gsgpc_stats* stats, double* values,
+                                      int32_t* offsets);
+/* Probe images W^T v_p (probes × m) accumulated by gsgpc_stats_add. */
+gsgpc_status gsgpc_stats_copy_probe_images(gsgpc_ctx* ctx, gsgpc_stats* stats, double* out);
+/* SufficientStats::wtw() as RowMajor CSR (interp.hpp:129): exact zeros are not stored,
+ * columns ascending.  nnz first (values may be NULL), then fill host arrays. */
+gsgpc_status gsgpc_stats_csr_nnz(gsgpc_ctx* ctx, gsgpc_stats* stats, int64_t* nnz,
+                                 int64_t* max_row_nnz);
+gsgpc_status gsgpc_stats_export_csr(gsgpc_ctx* ctx, gsgpc_stats* stats, int64_t* row_ptr,
+                                    int64_t* col, double* val);
+/* SufficientStats::apply_wtw (interp.hpp:135-136, interp.cpp:227-233). */
+gsgpc_status gsgpc_stats_apply_wtw(gsgpc_ctx* ctx, gsgpc_stats* stats, const double* v,
+                                   double* out);
+/* Contiguous device buffer [stencil | W^T y | probe images | yty | n] of a finalized
+ * stats object, for an in-place sum all-reduce across ranks (NCCL via torch.distributed);
+ * call gsgpc_stats_mark_reduced() afterwards (the object then accepts no more add()). */
+gsgpc_status gsgpc_stats_reduce_buffer(gsgpc_ctx* ctx, gsgpc_stats* stats, double** dev_ptr,
+                                       int64_t* count);
+gsgpc_status gsgpc_stats_mark_reduced(gsgpc_ctx* ctx, gsgpc_stats* stats);
+/* save_stats / load_stats (io.hpp:82-97, io.cpp:192-262), "GSGPSST1" layout. */
+gsgpc_status gsgpc_stats_save(gsgpc_ctx* ctx, gsgpc_stats* stats, const char* path);
+gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** out);
+
+/* ---------------------------------------------------------------- K_G operator */
+/* ToeplitzOperator(Grid, KernelSpec) (grid.hpp:58-90) for the SE-ARD kernel
+ * (kernels.hpp:11-47: noise_std, lengthscales[dim], outputscale). */
+gsgpc_status gsgpc_kg_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* lengthscales,
+                             double outputscale, double noise_std, gsgpc_kg** out);
+void gsgpc_kg_destroy(gsgpc_kg* kg);
+/* ToeplitzOperator::apply (grid.hpp:82-83, grid.cpp:193-235): out = K_G v. */
+gsgpc_status gsgpc_kg_apply(gsgpc_ctx* ctx, gsgpc_kg* kg, const double* v, double* out);
+gsgpc_status gsgpc_kg_info(const gsgpc_kg* kg, int64_t* m, double* noise_variance);
+
+/* ---------------------------------------------------------------- solvers */
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double residual_sq;
+  double loop_seconds; /* device time of the iteration loop (CUDA events) */
+} gsgpc_solve_info;
+
+/* factorized_cg_grid_rhs (solvers.hpp:127-151, solvers.cpp:271-336).  GridRhsTolerance:
+ * eps_abs >= 0 wins, else rel_tol.  Traces (optional, host or device): residual_trace
+ * maxiter+1, alphas maxiter, betas maxiter. */
+gsgpc_status gsgpc_factorized_cg_grid_rhs(gsgpc_ctx* ctx, gsgpc_kg* kg, gsgpc_stats* stats,
+                                          const double* rhat0, double sigma, double eps_abs,
+                                          double rel_tol, int maxiter, double* xhat_d,
+                                          gsgpc_solve_info* info, double* residual_trace,
+                                          double* alphas, double* betas);
+/* posterior_mean_gsgp (gp.hpp:119-122, gp.cpp:326-352): mean_coeffs = K_G(x̂_d + W^T y/σ²).
+ * Returns NONCONVERGENCE (info filled) when maxiter is hit. */
+gsgpc_status gsgpc_posterior_mean_gsgp(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc_kg* kg,
+                                       double sigma, double tol, int maxiter,
+                                       double* mean_coeffs, gsgpc_solve_info* info);
+/* PosteriorModel::predict_mean (gp.hpp:112-113, gp.cpp:309-324). */
+gsgpc_status gsgpc_predict_mean(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme,
+                                const double* mean_coeffs, const gsgpc_points* pts, int64_t n,
+                                double* out);
+
+/* factorized_lanczos_fused (solvers.hpp:178-183, solvers.cpp:464-538) for P start vectors at
+ * once (probe-batched EFLA).  kgwt_z0 / wt_z0 are P × m, z0_sq P.  Outputs per probe:
+ * alpha P × k, beta P × k (first order-1 used), order P. */
+gsgpc_status gsgpc_factorized_lanczos_fused(gsgpc_ctx* ctx, gsgpc_kg* kg, gsgpc_stats* stats,
+                                            int probes, const double* kgwt_z0,
+                                            const double* wt_z0, const double* z0_sq,
+                                            double sigma_sq, int k, double* alpha,
+                                            double* beta, int32_t* order);
+
+typedef struct {
+  double solve_tol;   /* LoglikOptions::solve_tol (gp.hpp:75) */
+  int32_t probes;     /* LoglikOptions::probes */
+  int32_t max_depth;  /* SlqOptions::max_depth (gp.hpp:25-29) */
+  double quad_tol;    /* SlqOptions::quad_tol */
+  uint64_t seed;      /* LoglikOptions::seed */
+  int32_t maxiter;    /* LoglikOptions::maxiter */
+} gsgpc_loglik_options;
+
+typedef struct {
+  double loglik, logdet_term, quad_term, const_term; /* LoglikResult (gp.hpp:62-72) */
+  int32_t probes_used;
+  int32_t solver_iterations;
+  int32_t max_depth_used;
+} gsgpc_loglik_result;
+
+/* log_likelihood_gsgp (gp.hpp:86-90, gp.cpp:158-240) on the SkiOperator route
+ * (slq_logdet_ski_factorized, gp.cpp:85-111) with the probe images W^T v_p accumulated
+ * during the precompute (gsgpc_stats_add with probe words of the reference's
+ * rademacher_probe streams, gp.cpp:16-25). */
+gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc_kg* kg,
+                                       double sigma, const gsgpc_loglik_options* opts,
+                                       gsgpc_loglik_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSGPC_H */

@@ -1,0 +1,1390 @@
+// api.cu — the C ABI (include/gsgpc.h): handles, host/device staging, the precompute
+// pipeline, the EFCG driver (CUDA-graph replay with device-resident scalars), posterior
+// mean, prediction and the GSGPSST1 stats file.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/gsgpc.h"
+#include "internal.cuh"
+#include "precompute.cuh"
+
+#ifndef GSGPC_GIT
+#define GSGPC_GIT "unknown"
+#endif
+
+using namespace gsgpc;
+
+namespace gsgpc {
+double measure_fp64_peak(cudaStream_t s);
+void run_add_div(const Launch& L, int64_t n, const double* x, double sx, const double* y, double b, double* out);
+}
+
+namespace {
+
+// ------------------------------------------------------------------ device buffers
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    GSGPC_CUDA(cudaMalloc(&p, std::max<size_t>(b, 256)));
+    bytes = std::max<size_t>(b, 256);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    GSGPC_CUDA(cudaMallocHost(&p, std::max<size_t>(b, 256)));
+    bytes = std::max<size_t>(b, 256);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handles
+struct CgCache;
+
+struct gsgpc_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t err_row = 0;
+  uint64_t launches = 0;
+  bool timing = false;
+  double phase_ms[8] = {0};
+  int64_t phase_calls[8] = {0};
+  std::map<std::string, std::unique_ptr<DBuf>> bufs;
+  PinnedBuf pin;
+  std::unique_ptr<CgCache> cg;
+  Launch L() { return Launch{stream, &launches}; }
+  DBuf& buf(const std::string& name) {
+    auto& b = bufs[name];
+    if (!b) b.reset(new DBuf());
+    return *b;
+  }
+};
+
+struct gsgpc_stats {
+  int device = 0;
+  gsgpc_grid grid{};
+  int scheme = 1;
+  GridDev g{};
+  int Q = 0, QY = 0, S_min = 0;
+  DBuf mom;      // cells × Q
+  DBuf pmom;     // cells × P × QY
+  DBuf yty;      // device scalar Σ y²
+  DBuf fin;      // [S_min·m | m | P·m | yty | n]
+  int probes = 0;
+  int64_t n = 0;
+  bool finalized = false;
+  bool reduced = false;
+  int64_t fin_count() const { return static_cast<int64_t>(S_min) * g.m + g.m + static_cast<int64_t>(probes) * g.m + 2; }
+  double* stencil() const { return fin.as<double>(); }
+  double* wty() const { return fin.as<double>() + static_cast<int64_t>(S_min) * g.m; }
+  double* pimg() const { return wty() + g.m; }
+  double* tail() const { return pimg() + static_cast<int64_t>(probes) * g.m; }
+};
+
+struct gsgpc_kg {
+  int device = 0;
+  gsgpc_grid grid{};
+  int64_t m = 0;
+  double noise_std = 1.0;
+  DBuf gen[GSGPC_MAX_DIM];
+  KgDev dev{};
+};
+
+struct CgCache {
+  // buffers + a captured graph of B iterations for one (stats, kg) pairing
+  const gsgpc_stats* stats = nullptr;
+  const gsgpc_kg* kg = nullptr;
+  int64_t m = 0;
+  DBuf r, u, s, z, x, kt0, kt1, pa, pb, tr, al, be, st;
+  int trace_cap = 0;
+  cudaGraphExec_t exec = nullptr;
+  int B = 0;
+  ~CgCache() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+namespace {
+
+template <class F>
+gsgpc_status guard(gsgpc_ctx* ctx, F&& f) {
+  try {
+    if (ctx) GSGPC_CUDA(cudaSetDevice(ctx->device));
+    f();
+    return GSGPC_OK;
+  } catch (const Error& e) {
+    if (ctx) {
+      ctx->err = e.what();
+      ctx->err_row = e.row;
+    }
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    if (ctx) ctx->err = std::string("out of host memory: ") + e.what();
+    return GSGPC_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return GSGPC_RUNTIME_ERROR;
+  }
+}
+
+int scheme_width(int scheme) {
+  if (scheme == GSGPC_CUBIC) return 4;
+  if (scheme == GSGPC_LINEAR) return 2;
+  invalid("unknown interpolation scheme");
+  return 0;
+}
+
+// Grid::Grid validation (grid.cpp:12-23) + the device descriptor.
+GridDev make_grid(const gsgpc_grid* gr, int scheme) {
+  if (!gr) invalid("grid is NULL");
+  if (gr->dim < 1) invalid("Grid: need at least one dimension");
+  if (gr->dim > GSGPC_MAX_DIM) {
+    throw Error(GSGPC_UNSUPPORTED, "grid dimension " + std::to_string(gr->dim) + " > 3 is not supported by this build");
+  }
+  GridDev g{};
+  g.d = gr->dim;
+  g.W = scheme_width(scheme);
+  g.m = 1;
+  g.cells = 1;
+  for (int k = 0; k < g.d; ++k) {
+    if (gr->size[k] < 2) invalid("Grid: size must be >= 2 per dimension");
+    if (!(gr->max[k] > gr->min[k])) invalid("Grid: max must exceed min");
+    g.mn[k] = gr->min[k];
+    g.sp[k] = (gr->max[k] - gr->min[k]) / static_cast<double>(gr->size[k] - 1);
+    g.sz[k] = gr->size[k];
+    g.nc[k] = gr->size[k] - 1;
+    g.m *= g.sz[k];
+    g.cells *= g.nc[k];
+  }
+  return g;
+}
+
+StencilDesc stencil_desc(const gsgpc_stats* s) {
+  StencilDesc sd{};
+  sd.d = s->g.d;
+  sd.W = s->g.W;
+  sd.S_min = s->S_min;
+  for (int k = 0; k < sd.d; ++k) sd.sz[k] = s->g.sz[k];
+  sd.m = s->g.m;
+  return sd;
+}
+
+// Host/device array staging ----------------------------------------------------------
+// Input: returns a device pointer holding `count` doubles of `p` (copied if host memory).
+const double* dev_in(gsgpc_ctx* ctx, const double* p, int64_t count, const char* slot) {
+  if (!p) invalid(std::string("NULL array argument (") + slot + ")");
+  if (is_device_ptr(p)) return p;
+  DBuf& b = ctx->buf(slot);
+  b.ensure(sizeof(double) * count);
+  GSGPC_CUDA(cudaMemcpyAsync(b.p, p, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+  return b.as<double>();
+}
+
+// Output: device destination to write `count` doubles into, then finish() copies back.
+struct DevOut {
+  gsgpc_ctx* ctx;
+  double* user;
+  double* dev;
+  int64_t count;
+  bool host;
+  DevOut(gsgpc_ctx* c, double* u, int64_t n, const char* slot) : ctx(c), user(u), count(n) {
+    if (!u) invalid(std::string("NULL output array (") + slot + ")");
+    host = !is_device_ptr(u);
+    if (host) {
+      DBuf& b = ctx->buf(slot);
+      b.ensure(sizeof(double) * n);
+      dev = b.as<double>();
+    } else {
+      dev = u;
+    }
+  }
+  void finish() {
+    if (host) {
+      GSGPC_CUDA(cudaMemcpyAsync(user, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+      GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+};
+
+void copy_out(gsgpc_ctx* ctx, void* user, const void* dev, size_t bytes) {
+  GSGPC_CUDA(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDefault, ctx->stream));
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+double read_scalar(gsgpc_ctx* ctx, const double* dev) {
+  double v = 0.0;
+  copy_out(ctx, &v, dev, sizeof(double));
+  return v;
+}
+
+// Phase timing (events on the context stream) ----------------------------------------
+struct PhaseTimer {
+  gsgpc_ctx* ctx;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> ev;
+  explicit PhaseTimer(gsgpc_ctx* c) : ctx(c) {}
+  int begin(int phase) {
+    if (!ctx->timing) return -1;
+    cudaEvent_t a, b;
+    GSGPC_CUDA(cudaEventCreate(&a));
+    GSGPC_CUDA(cudaEventCreate(&b));
+    GSGPC_CUDA(cudaEventRecord(a, ctx->stream));
+    ev.emplace_back(phase, a, b);
+    return static_cast<int>(ev.size()) - 1;
+  }
+  void end(int h) {
+    if (h < 0) return;
+    GSGPC_CUDA(cudaEventRecord(std::get<2>(ev[h]), ctx->stream));
+  }
+  ~PhaseTimer() {
+    if (ev.empty()) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& e : ev) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, std::get<1>(e), std::get<2>(e)) == cudaSuccess) {
+        ctx->phase_ms[std::get<0>(e)] += ms;
+        ctx->phase_calls[std::get<0>(e)] += 1;
+      }
+      cudaEventDestroy(std::get<1>(e));
+      cudaEventDestroy(std::get<2>(e));
+    }
+  }
+};
+
+// Points validation + device descriptor ----------------------------------------------
+size_t dtype_size(int dt) {
+  if (dt == GSGPC_F32) return 4;
+  if (dt == GSGPC_F64) return 8;
+  invalid("unknown dtype");
+  return 0;
+}
+
+PointsDev points_dev(const gsgpc_points* p, int d, int64_t row0) {
+  PointsDev q{};
+  const size_t es = dtype_size(p->dtype);
+  q.x = static_cast<const char*>(p->x) + es * row0 * p->x_row_stride;
+  q.y = static_cast<const char*>(p->y) + es * row0 * p->y_stride;
+  q.xs = p->x_row_stride;
+  for (int k = 0; k < GSGPC_MAX_DIM; ++k) q.xo[k] = k < d ? p->x_col_offset[k] : 0;
+  q.ys = p->y_stride;
+  return q;
+}
+
+void check_points(const gsgpc_points* p, int64_t n, bool need_y) {
+  if (!p) invalid("points descriptor is NULL");
+  if (n < 0) invalid("negative row count");
+  if (n == 0) return;
+  if (!p->x) invalid("points: x is NULL");
+  if (need_y && !p->y) invalid("points: y is NULL");
+  dtype_size(p->dtype);
+}
+
+// Stage rows [r0, r1) of a host-resident point set into device memory; returns the device
+// descriptor for that chunk (row 0 = r0).
+PointsDev stage_points(gsgpc_ctx* ctx, const gsgpc_points* p, int d, int64_t r0, int64_t r1, bool need_y,
+                       const char* slot) {
+  const size_t es = dtype_size(p->dtype);
+  const int64_t rows = r1 - r0;
+  PointsDev q{};
+  const char* hx = static_cast<const char*>(p->x);
+  const char* hy = static_cast<const char*>(p->y);
+  int64_t maxo = 0;
+  for (int k = 0; k < d; ++k) maxo = std::max(maxo, p->x_col_offset[k]);
+  const bool columns = p->x_row_stride == 1 && d > 1;
+  const int64_t xelems = columns ? rows * d : rows * p->x_row_stride;
+  // y inside the x rows (AoS (x..., y))?
+  const int64_t yoff = (hy - hx) / static_cast<int64_t>(es);
+  const bool y_in_x = need_y && !columns && p->y_stride == p->x_row_stride && hy >= hx &&
+                      (hy - hx) % static_cast<int64_t>(es) == 0 && yoff < p->x_row_stride;
+  const int64_t yelems = (!need_y || y_in_x) ? 0 : rows * p->y_stride;
+  DBuf& b = ctx->buf(slot);
+  b.ensure(es * (xelems + yelems) + 64);
+  char* dx = b.as<char>();
+  if (columns) {
+    for (int k = 0; k < d; ++k) {
+      GSGPC_CUDA(cudaMemcpyAsync(dx + es * k * rows, hx + es * (p->x_col_offset[k] + r0), es * rows,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+      q.xo[k] = k * rows;
+    }
+    q.xs = 1;
+  } else {
+    if (maxo >= p->x_row_stride && rows > 1) {
+      throw Error(GSGPC_UNSUPPORTED, "host points: column offset beyond the row stride");
+    }
+    const int64_t span = (rows - 1) * p->x_row_stride + std::max(maxo, y_in_x ? yoff : 0) + 1;
+    GSGPC_CUDA(cudaMemcpyAsync(dx, hx + es * r0 * p->x_row_stride, es * span, cudaMemcpyHostToDevice, ctx->stream));
+    q.xs = p->x_row_stride;
+    for (int k = 0; k < d; ++k) q.xo[k] = p->x_col_offset[k];
+  }
+  q.x = dx;
+  if (!need_y) {
+    q.y = dx;
+    q.ys = 0;
+  } else if (y_in_x) {
+    q.y = dx + es * yoff;
+    q.ys = p->y_stride;
+  } else {
+    char* dy = dx + es * xelems;
+    const int64_t span = (rows - 1) * p->y_stride + 1;
+    GSGPC_CUDA(cudaMemcpyAsync(dy, hy + es * r0 * p->y_stride, es * span, cudaMemcpyHostToDevice, ctx->stream));
+    q.y = dy;
+    q.ys = p->y_stride;
+  }
+  return q;
+}
+
+void ensure_fin(gsgpc_stats* s) {
+  s->fin.ensure(sizeof(double) * s->fin_count());
+}
+
+void finalize_stats(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  if (s->reduced || s->finalized) return;
+  PhaseTimer pt(ctx);
+  const int h = pt.begin(4);
+  ensure_fin(s);
+  const Launch L = ctx->L();
+  const int64_t ws = finalize_ws_elems(s->g);
+  DBuf& w = ctx->buf("finalize_ws");
+  w.ensure(sizeof(double) * ws);
+  run_finalize(L, s->g, s->mom.as<double>(), s->probes, s->probes ? s->pmom.as<double>() : nullptr, s->stencil(),
+               s->wty(), s->pimg(), w.as<double>(), ws);
+  // tail: yty, n
+  GSGPC_CUDA(cudaMemcpyAsync(s->tail(), s->yty.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  const double nd = static_cast<double>(s->n);
+  double* pin = static_cast<double*>(ctx->pin.p);
+  ctx->pin.ensure(64);
+  pin = static_cast<double*>(ctx->pin.p);
+  pin[0] = nd;
+  GSGPC_CUDA(cudaMemcpyAsync(s->tail() + 1, pin, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  pt.end(h);
+  s->finalized = true;
+}
+
+double stats_yty(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  if (s->reduced) return read_scalar(ctx, s->tail());
+  return read_scalar(ctx, s->yty.as<double>());
+}
+
+gsgpc_stats* new_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme) {
+  std::unique_ptr<gsgpc_stats> s(new gsgpc_stats());
+  s->device = ctx->device;
+  s->g = make_grid(grid, scheme);
+  s->grid = *grid;
+  s->scheme = scheme;
+  s->Q = moments_per_cell(s->g.d, s->g.W);
+  int qy = 1, S = 1;
+  for (int k = 0; k < s->g.d; ++k) {
+    qy *= s->g.W;
+    S *= 2 * s->g.W - 1;
+  }
+  s->QY = qy;
+  s->S_min = (S + 1) / 2;
+  s->mom.ensure(sizeof(double) * s->g.cells * s->Q);
+  GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * s->g.cells * s->Q, ctx->stream));
+  s->yty.ensure(sizeof(double));
+  GSGPC_CUDA(cudaMemsetAsync(s->yty.p, 0, sizeof(double), ctx->stream));
+  return s.release();
+}
+
+// The precompute pipeline on one device-resident chunk.
+void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, int64_t n, int64_t row0,
+               const uint64_t* pw_dev, int probes) {
+  const Launch L = ctx->L();
+  const GridDev& g = s->g;
+  PhaseTimer pt(ctx);
+  DBuf& hist = ctx->buf("hist");
+  hist.ensure(sizeof(int) * (g.cells + 1));
+  DBuf& off = ctx->buf("off");
+  off.ensure(sizeof(int64_t) * (g.cells + 2));
+  DBuf& bsum = ctx->buf("scan_bs");
+  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(g.cells) + 1));
+  DBuf& err = ctx->buf("err");
+  err.ensure(sizeof(unsigned long long) * 2);
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)));
+  DBuf& part = ctx->buf("yty_part");
+  part.ensure(sizeof(double) * nblk);
+  DBuf& ychunk = ctx->buf("yty_chunk");
+  ychunk.ensure(sizeof(double));
+
+  int h = pt.begin(0);
+  GSGPC_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
+  run_classify(L, dtype, P, n, row0, g, hist.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk);
+  run_sum_partials(L, part.as<double>(), nblk, ychunk.as<double>());
+  pt.end(h);
+  h = pt.begin(1);
+  run_scan(L, hist.as<int>(), g.cells, off.as<int64_t>(), bsum.as<int64_t>());
+  pt.end(h);
+  // one sync: error row + number of valid rows
+  struct {
+    unsigned long long err;
+    int64_t nvalid;
+  } hs{};
+  ctx->pin.ensure(64);
+  char* pin = static_cast<char*>(ctx->pin.p);
+  GSGPC_CUDA(cudaMemcpyAsync(pin, err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(pin + 8, off.as<int64_t>() + g.cells, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(&hs.err, pin, 8);
+  std::memcpy(&hs.nvalid, pin + 8, 8);
+  if (hs.err != ~0ull) {
+    const int64_t row = static_cast<int64_t>(hs.err >> 2);
+    const int kind = static_cast<int>(hs.err & 3);
+    const std::string what =
+        kind == PT_OUTSIDE ? "interp_weights: point outside grid"
+                           : "interp_weights: stencil leaves the grid (point too close to the boundary for the "
+                             "requested scheme)";
+    throw Error(GSGPC_OUT_OF_GRID, "sufficient_stats: stream row " + std::to_string(row) + ": " + what, row);
+  }
+  // commit: yty, scatter, moments
+  run_axpby(L, 1, 1.0, s->yty.as<double>(), 1.0, ychunk.as<double>(), s->yty.as<double>());
+  const int64_t nvalid = hs.nvalid;
+  if (nvalid > 0) {
+    const size_t es = dtype_size(dtype);
+    DBuf& pay = ctx->buf("payload");
+    pay.ensure(es * 4 * nvalid);
+    DBuf& cur = ctx->buf("cursor");
+    cur.ensure(sizeof(int) * (g.cells + 1));
+    const int nw = probes > 0 ? (probes + 63) / 64 : 0;
+    DBuf& pws = ctx->buf("probe_sorted");
+    if (nw) pws.ensure(sizeof(uint64_t) * nw * nvalid);
+    h = pt.begin(2);
+    GSGPC_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
+    run_scatter(L, dtype, P, n, g, off.as<int64_t>(), cur.as<int>(), pay.p, pw_dev, nw,
+                nw ? pws.as<uint64_t>() : nullptr, nblk);
+    pt.end(h);
+    h = pt.begin(3);
+    run_moments(L, dtype, pay.p, off.as<int64_t>(), nvalid, g, s->mom.as<double>());
+    if (probes > 0) {
+      run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), nvalid, g, probes,
+                        s->pmom.as<double>());
+    }
+    pt.end(h);
+  }
+  s->n += n;
+  s->finalized = false;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* gsgpc_version(void) {
+  return "gsgpc sm_100a " GSGPC_GIT " (precompute: cell-sorted polynomial moments; K_G: Kronecker Toeplitz)";
+}
+
+gsgpc_status gsgpc_ctx_create(int device, gsgpc_ctx** out) {
+  if (!out) return GSGPC_INVALID_ARGUMENT;
+  *out = nullptr;
+  std::unique_ptr<gsgpc_ctx> c(new gsgpc_ctx());
+  c->device = device;
+  const gsgpc_status st = guard(c.get(), [&] {
+    int ndev = 0;
+    GSGPC_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) invalid("gsgpc_ctx_create: bad device ordinal");
+    GSGPC_CUDA(cudaSetDevice(device));
+    GSGPC_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+  });
+  if (st != GSGPC_OK) {
+    std::fprintf(stderr, "gsgpc_ctx_create: %s\n", c->err.c_str());
+    return st;
+  }
+  *out = c.release();
+  return GSGPC_OK;
+}
+
+void gsgpc_ctx_destroy(gsgpc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->cg.reset();
+  ctx->bufs.clear();
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+gsgpc_status gsgpc_ctx_set_stream(gsgpc_ctx* ctx, void* s) {
+  if (!ctx) return GSGPC_INVALID_ARGUMENT;
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+  ctx->cg.reset();
+  return GSGPC_OK;
+}
+
+void* gsgpc_ctx_stream(gsgpc_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+gsgpc_status gsgpc_ctx_synchronize(gsgpc_ctx* ctx) {
+  return guard(ctx, [&] { GSGPC_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+const char* gsgpc_last_error(const gsgpc_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+int64_t gsgpc_last_error_row(const gsgpc_ctx* ctx) { return ctx ? ctx->err_row : 0; }
+uint64_t gsgpc_ctx_launch_count(const gsgpc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+gsgpc_status gsgpc_ctx_enable_phase_timing(gsgpc_ctx* ctx, int enable) {
+  if (!ctx) return GSGPC_INVALID_ARGUMENT;
+  ctx->timing = enable != 0;
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out, int64_t* calls_out) {
+  if (!ctx) return GSGPC_INVALID_ARGUMENT;
+  for (int i = 0; i < 8; ++i) {
+    if (ms_out) ms_out[i] = ctx->phase_ms[i];
+    if (calls_out) calls_out[i] = ctx->phase_calls[i];
+  }
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx) {
+  if (!ctx) return GSGPC_INVALID_ARGUMENT;
+  for (int i = 0; i < 8; ++i) {
+    ctx->phase_ms[i] = 0;
+    ctx->phase_calls[i] = 0;
+  }
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_diag_fp64_peak(gsgpc_ctx* ctx, double* tflops) {
+  return guard(ctx, [&] {
+    if (!tflops) invalid("tflops is NULL");
+    *tflops = gsgpc::measure_fp64_peak(ctx->stream);
+  });
+}
+
+gsgpc_status gsgpc_fit_grid_to_data(int dim, const double* lo, const double* hi, const int64_t* sizes, int scheme,
+                                    gsgpc_grid* out) {
+  try {
+    if (!out || !lo || !hi || !sizes) return GSGPC_INVALID_ARGUMENT;
+    if (dim < 1 || dim > GSGPC_MAX_DIM) return dim < 1 ? GSGPC_INVALID_ARGUMENT : GSGPC_UNSUPPORTED;
+    const int r = scheme == GSGPC_LINEAR ? 1 : 2;
+    gsgpc_grid g{};
+    g.dim = dim;
+    for (int k = 0; k < dim; ++k) {
+      const int64_t m = sizes[k];
+      if (m < 2 * r + 2) return GSGPC_INVALID_ARGUMENT;  // "need at least 2r+2 points per dimension"
+      if (!(hi[k] > lo[k])) return GSGPC_INVALID_ARGUMENT;  // "empty data range"
+      const double s = (hi[k] - lo[k]) / static_cast<double>(m - 1 - 2 * r);
+      g.min[k] = lo[k] - r * s;
+      g.max[k] = hi[k] + r * s;
+      g.size[k] = m;
+    }
+    *out = g;
+    return GSGPC_OK;
+  } catch (...) {
+    return GSGPC_RUNTIME_ERROR;
+  }
+}
+
+gsgpc_status gsgpc_interp_weights(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme, const gsgpc_points* pts,
+                                  int64_t n, int64_t* idx, double* w, int32_t* nnz, int32_t* status) {
+  return guard(ctx, [&] {
+    const GridDev g = make_grid(grid, scheme);
+    check_points(pts, n, false);
+    if (n == 0) return;
+    int width = 1;
+    for (int k = 0; k < g.d; ++k) width *= g.W;
+    const bool dev = is_device_ptr(pts->x);
+    const PointsDev P = dev ? points_dev(pts, g.d, 0) : stage_points(ctx, pts, g.d, 0, n, false, "iw_stage");
+    DBuf& bi = ctx->buf("iw_idx");
+    DBuf& bw = ctx->buf("iw_w");
+    DBuf& bn = ctx->buf("iw_nnz");
+    DBuf& bs = ctx->buf("iw_st");
+    bi.ensure(sizeof(int64_t) * n * width);
+    bw.ensure(sizeof(double) * n * width);
+    bn.ensure(sizeof(int) * n);
+    bs.ensure(sizeof(int) * n);
+    run_interp_weights(ctx->L(), pts->dtype, P, n, g, bi.as<int64_t>(), bw.as<double>(), bn.as<int>(), bs.as<int>());
+    if (idx) GSGPC_CUDA(cudaMemcpyAsync(idx, bi.p, sizeof(int64_t) * n * width, cudaMemcpyDefault, ctx->stream));
+    if (w) GSGPC_CUDA(cudaMemcpyAsync(w, bw.p, sizeof(double) * n * width, cudaMemcpyDefault, ctx->stream));
+    if (nnz) GSGPC_CUDA(cudaMemcpyAsync(nnz, bn.p, sizeof(int) * n, cudaMemcpyDefault, ctx->stream));
+    if (status) GSGPC_CUDA(cudaMemcpyAsync(status, bs.p, sizeof(int) * n, cudaMemcpyDefault, ctx->stream));
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gsgpc_status gsgpc_stats_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme, gsgpc_stats** out) {
+  return guard(ctx, [&] {
+    if (!out) invalid("out is NULL");
+    *out = new_stats(ctx, grid, scheme);
+  });
+}
+
+void gsgpc_stats_destroy(gsgpc_stats* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  cudaDeviceSynchronize();
+  delete s;
+}
+
+gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points* pts, int64_t n,
+                             const uint64_t* probe_words, int probes) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    if (s->reduced) invalid("SufficientStatsAccumulator::add: statistics were all-reduced; create a new accumulator");
+    check_points(pts, n, true);
+    if (probes < 0 || probes > 64) throw Error(GSGPC_UNSUPPORTED, "probes must be in [0, 64]");
+    if (probes > 0 && !probe_words) invalid("probe words are NULL");
+    if (probes > 0) {
+      if (s->probes == 0) {
+        if (s->n > 0) invalid("probes must be supplied from the first row on");
+        s->probes = probes;
+        s->pmom.ensure(sizeof(double) * s->g.cells * probes * s->QY);
+        GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * probes * s->QY, ctx->stream));
+      } else if (s->probes != probes) {
+        invalid("probe count differs from the earlier batches");
+      }
+    } else if (s->probes > 0 && n > 0) {
+      invalid("this accumulator carries probe images: every batch needs probe words");
+    }
+    if (n == 0) return;
+    const bool dev = is_device_ptr(pts->x);
+    const int nw = probes > 0 ? (probes + 63) / 64 : 0;
+    const bool pw_dev = nw ? is_device_ptr(probe_words) : true;
+    const int64_t CH = dev ? (int64_t{1} << 27) : (int64_t{1} << 24);
+    for (int64_t r0 = 0; r0 < n; r0 += CH) {
+      const int64_t r1 = std::min(n, r0 + CH);
+      PointsDev P;
+      if (dev) {
+        P = points_dev(pts, s->g.d, r0);
+      } else {
+        PhaseTimer pt(ctx);
+        const int h = pt.begin(5);
+        P = stage_points(ctx, pts, s->g.d, r0, r1, true, "stage");
+        pt.end(h);
+      }
+      const uint64_t* pw = nullptr;
+      if (nw) {
+        if (pw_dev) {
+          pw = probe_words + r0 * nw;
+        } else {
+          DBuf& b = ctx->buf("probe_stage");
+          b.ensure(sizeof(uint64_t) * nw * (r1 - r0));
+          GSGPC_CUDA(cudaMemcpyAsync(b.p, probe_words + r0 * nw, sizeof(uint64_t) * nw * (r1 - r0),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+          pw = b.as<uint64_t>();
+        }
+      }
+      add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
+    }
+  });
+}
+
+gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * s->g.cells * s->Q, ctx->stream));
+    if (s->probes) {
+      GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * s->probes * s->QY, ctx->stream));
+    }
+    GSGPC_CUDA(cudaMemsetAsync(s->yty.p, 0, sizeof(double), ctx->stream));
+    s->n = 0;
+    s->finalized = false;
+    s->reduced = false;
+  });
+}
+
+gsgpc_status gsgpc_stats_merge(gsgpc_ctx* ctx, gsgpc_stats* dst, const gsgpc_stats* src) {
+  return guard(ctx, [&] {
+    if (!dst || !src) invalid("stats is NULL");
+    if (dst->reduced || src->reduced) invalid("SufficientStatsAccumulator::merge: all-reduced statistics");
+    bool same = dst->scheme == src->scheme && dst->g.d == src->g.d && dst->probes == src->probes;
+    for (int k = 0; same && k < dst->g.d; ++k) {
+      same = dst->grid.size[k] == src->grid.size[k] && dst->grid.min[k] == src->grid.min[k] &&
+             dst->grid.max[k] == src->grid.max[k];
+    }
+    if (!same) invalid("SufficientStatsAccumulator::merge: mismatched shards");
+    const Launch L = ctx->L();
+    const int64_t nm = dst->g.cells * dst->Q;
+    run_axpby(L, nm, 1.0, dst->mom.as<double>(), 1.0, src->mom.as<double>(), dst->mom.as<double>());
+    if (dst->probes) {
+      const int64_t np = dst->g.cells * dst->probes * dst->QY;
+      run_axpby(L, np, 1.0, dst->pmom.as<double>(), 1.0, src->pmom.as<double>(), dst->pmom.as<double>());
+    }
+    run_axpby(L, 1, 1.0, dst->yty.as<double>(), 1.0, src->yty.as<double>(), dst->yty.as<double>());
+    dst->n += src->n;
+    dst->finalized = false;
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+gsgpc_status gsgpc_stats_finalize(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    finalize_stats(ctx, s);
+  });
+}
+
+gsgpc_status gsgpc_sufficient_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme, const gsgpc_points* pts,
+                                    int64_t n, gsgpc_stats** out) {
+  if (!out) return GSGPC_INVALID_ARGUMENT;
+  *out = nullptr;
+  gsgpc_stats* s = nullptr;
+  gsgpc_status st = gsgpc_stats_create(ctx, grid, scheme, &s);
+  if (st != GSGPC_OK) return st;
+  st = gsgpc_stats_add(ctx, s, pts, n, nullptr, 0);
+  if (st == GSGPC_OK) st = gsgpc_stats_finalize(ctx, s);
+  if (st != GSGPC_OK) {
+    gsgpc_stats_destroy(s);
+    return st;
+  }
+  *out = s;
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_stats_info(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t* m, int64_t* n, double* yty,
+                              int64_t* n_offsets, int32_t* probes) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    if (m) *m = s->g.m;
+    if (n) *n = s->reduced ? static_cast<int64_t>(read_scalar(ctx, s->tail() + 1)) : s->n;
+    if (yty) *yty = stats_yty(ctx, s);
+    if (n_offsets) *n_offsets = s->S_min;
+    if (probes) *probes = s->probes;
+  });
+}
+
+gsgpc_status gsgpc_stats_grid(const gsgpc_stats* s, gsgpc_grid* grid, int* scheme) {
+  if (!s) return GSGPC_INVALID_ARGUMENT;
+  if (grid) *grid = s->grid;
+  if (scheme) *scheme = s->scheme;
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_stats_copy_wty(gsgpc_ctx* ctx, gsgpc_stats* s, double* out) {
+  return guard(ctx, [&] {
+    if (!s || !out) invalid("NULL argument");
+    finalize_stats(ctx, s);
+    copy_out(ctx, out, s->wty(), sizeof(double) * s->g.m);
+  });
+}
+
+gsgpc_status gsgpc_stats_copy_stencil(gsgpc_ctx* ctx, gsgpc_stats* s, double* values, int32_t* offsets) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    finalize_stats(ctx, s);
+    if (values) copy_out(ctx, values, s->stencil(), sizeof(double) * s->S_min * s->g.m);
+    if (offsets) {
+      const int E = 2 * s->g.W - 1, d = s->g.d;
+      int S = 1;
+      for (int k = 0; k < d; ++k) S *= E;
+      const int c0 = (S - 1) / 2;
+      for (int i = 0; i < s->S_min; ++i) {
+        int q = c0 + i;
+        for (int k = d - 1; k >= 0; --k) {
+          offsets[i * d + k] = q % E - (s->g.W - 1);
+          q /= E;
+        }
+      }
+    }
+  });
+}
+
+gsgpc_status gsgpc_stats_copy_probe_images(gsgpc_ctx* ctx, gsgpc_stats* s, double* out) {
+  return guard(ctx, [&] {
+    if (!s || !out) invalid("NULL argument");
+    if (s->probes == 0) invalid("no probe images were accumulated");
+    finalize_stats(ctx, s);
+    copy_out(ctx, out, s->pimg(), sizeof(double) * s->probes * s->g.m);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Host CSR view of the stencil (SufficientStats::wtw() layout).
+struct HostCsr {
+  std::vector<int64_t> rp, col;
+  std::vector<double> val;
+};
+
+HostCsr build_csr(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  finalize_stats(ctx, s);
+  const int64_t m = s->g.m;
+  const int d = s->g.d, W = s->g.W, E = 2 * W - 1;
+  std::vector<double> st(static_cast<size_t>(s->S_min) * m);
+  copy_out(ctx, st.data(), s->stencil(), sizeof(double) * st.size());
+  int S = 1;
+  for (int k = 0; k < d; ++k) S *= E;
+  const int c0 = (S - 1) / 2;
+  // full offset list in lexicographic order
+  std::vector<std::array<int, 3>> dl(S);
+  std::vector<int64_t> fl(S);
+  for (int q = 0; q < S; ++q) {
+    int r = q;
+    std::array<int, 3> dd{0, 0, 0};
+    for (int k = d - 1; k >= 0; --k) {
+      dd[k] = r % E - (W - 1);
+      r /= E;
+    }
+    dl[q] = dd;
+    int64_t f = 0;
+    for (int k = 0; k < d; ++k) f = f * s->g.sz[k] + dd[k];
+    fl[q] = f;
+  }
+  HostCsr c;
+  c.rp.assign(m + 1, 0);
+  std::vector<std::pair<int64_t, double>> row;
+  for (int64_t a = 0; a < m; ++a) {
+    int64_t co[3] = {0, 0, 0};
+    int64_t r = a;
+    for (int k = d - 1; k >= 0; --k) {
+      co[k] = r % s->g.sz[k];
+      r /= s->g.sz[k];
+    }
+    row.clear();
+    for (int q = 0; q < S; ++q) {
+      bool ok = true;
+      for (int k = 0; k < d; ++k) {
+        const int64_t v = co[k] + dl[q][k];
+        ok = ok && v >= 0 && v < s->g.sz[k];
+      }
+      if (!ok) continue;
+      const int64_t b = a + fl[q];
+      double v;
+      if (q >= c0) v = st[static_cast<size_t>(q - c0) * m + a];
+      else v = st[static_cast<size_t>((S - 1 - q) - c0) * m + b];
+      if (v != 0.0) row.emplace_back(b, v);
+    }
+    std::sort(row.begin(), row.end());
+    for (auto& e : row) {
+      c.col.push_back(e.first);
+      c.val.push_back(e.second);
+    }
+    c.rp[a + 1] = static_cast<int64_t>(c.col.size());
+  }
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+gsgpc_status gsgpc_stats_csr_nnz(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t* nnz, int64_t* max_row_nnz) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    const HostCsr c = build_csr(ctx, s);
+    if (nnz) *nnz = static_cast<int64_t>(c.val.size());
+    if (max_row_nnz) {
+      int64_t b = 0;
+      for (size_t i = 0; i + 1 < c.rp.size(); ++i) b = std::max(b, c.rp[i + 1] - c.rp[i]);
+      *max_row_nnz = b;
+    }
+  });
+}
+
+gsgpc_status gsgpc_stats_export_csr(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t* row_ptr, int64_t* col, double* val) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    const HostCsr c = build_csr(ctx, s);
+    if (row_ptr) std::memcpy(row_ptr, c.rp.data(), sizeof(int64_t) * c.rp.size());
+    if (col) std::memcpy(col, c.col.data(), sizeof(int64_t) * c.col.size());
+    if (val) std::memcpy(val, c.val.data(), sizeof(double) * c.val.size());
+  });
+}
+
+gsgpc_status gsgpc_stats_apply_wtw(gsgpc_ctx* ctx, gsgpc_stats* s, const double* v, double* out) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    finalize_stats(ctx, s);
+    const StencilDesc sd = stencil_desc(s);
+    upload_stencil_offsets(sd, ctx->stream);
+    const double* dv = dev_in(ctx, v, sd.m, "wtw_in");
+    DevOut o(ctx, out, sd.m, "wtw_out");
+    run_spmv(ctx->L(), sd, s->stencil(), dv, o.dev);
+    o.finish();
+  });
+}
+
+gsgpc_status gsgpc_stats_reduce_buffer(gsgpc_ctx* ctx, gsgpc_stats* s, double** dev_ptr, int64_t* count) {
+  return guard(ctx, [&] {
+    if (!s || !dev_ptr || !count) invalid("NULL argument");
+    finalize_stats(ctx, s);
+    *dev_ptr = s->fin.as<double>();
+    *count = s->fin_count();
+  });
+}
+
+gsgpc_status gsgpc_stats_mark_reduced(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    if (!s->finalized && !s->reduced) invalid("gsgpc_stats_mark_reduced: call gsgpc_stats_reduce_buffer first");
+    s->reduced = true;
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    s->n = static_cast<int64_t>(read_scalar(ctx, s->tail() + 1));
+  });
+}
+
+// ---------------------------------------------------------------- GSGPSST1 (io.cpp:192-262)
+gsgpc_status gsgpc_stats_save(gsgpc_ctx* ctx, gsgpc_stats* s, const char* path) {
+  return guard(ctx, [&] {
+    if (!s || !path) invalid("NULL argument");
+    const HostCsr c = build_csr(ctx, s);
+    std::vector<double> wty(s->g.m);
+    copy_out(ctx, wty.data(), s->wty(), sizeof(double) * s->g.m);
+    const double yty = stats_yty(ctx, s);
+    std::ofstream f(path, std::ios::binary);
+    if (!f) invalid(std::string("cannot open for writing: ") + path);
+    auto u64 = [&](uint64_t v) { f.write(reinterpret_cast<const char*>(&v), 8); };
+    auto f64 = [&](double v) { f.write(reinterpret_cast<const char*>(&v), 8); };
+    f.write("GSGPSST1", 8);
+    u64(static_cast<uint64_t>(s->grid.dim));
+    for (int k = 0; k < s->grid.dim; ++k) {
+      f64(s->grid.min[k]);
+      f64(s->grid.max[k]);
+      u64(static_cast<uint64_t>(s->grid.size[k]));
+    }
+    u64(s->scheme == GSGPC_LINEAR ? 0 : 1);
+    u64(static_cast<uint64_t>(s->g.m));
+    u64(static_cast<uint64_t>(s->n));
+    u64(static_cast<uint64_t>(c.val.size()));
+    f64(yty);
+    for (double v : wty) f64(v);
+    // triplets in CSR row order
+    std::vector<char> blob(24 * c.val.size());
+    size_t o = 0;
+    for (int64_t r = 0; r + 1 < static_cast<int64_t>(c.rp.size()); ++r) {
+      for (int64_t k = c.rp[r]; k < c.rp[r + 1]; ++k) {
+        const uint64_t rr = static_cast<uint64_t>(r), cc = static_cast<uint64_t>(c.col[k]);
+        std::memcpy(&blob[o], &rr, 8);
+        std::memcpy(&blob[o + 8], &cc, 8);
+        std::memcpy(&blob[o + 16], &c.val[k], 8);
+        o += 24;
+      }
+    }
+    f.write(blob.data(), static_cast<std::streamsize>(blob.size()));
+    if (!f) invalid(std::string("write failed: ") + path);
+  });
+}
+
+gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** out) {
+  return guard(ctx, [&] {
+    if (!path || !out) invalid("NULL argument");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) invalid(std::string("cannot open stats file: ") + path);
+    char magic[8];
+    if (!f.read(magic, 8) || std::memcmp(magic, "GSGPSST1", 8) != 0) {
+      invalid(std::string("bad magic in stats file: ") + path);
+    }
+    auto u64 = [&](const char* what) {
+      uint64_t v;
+      if (!f.read(reinterpret_cast<char*>(&v), 8)) invalid(std::string("truncated file while reading ") + what);
+      return v;
+    };
+    auto f64 = [&](const char* what) {
+      double v;
+      if (!f.read(reinterpret_cast<char*>(&v), 8)) invalid(std::string("truncated file while reading ") + what);
+      return v;
+    };
+    const int d = static_cast<int>(u64("grid dimension"));
+    if (d < 1 || d > 64) invalid("stats file: bad grid dimension");
+    if (d > GSGPC_MAX_DIM) throw Error(GSGPC_UNSUPPORTED, "stats file: grid dimension > 3 is not supported");
+    gsgpc_grid g{};
+    g.dim = d;
+    for (int k = 0; k < d; ++k) {
+      g.min[k] = f64("grid min");
+      g.max[k] = f64("grid max");
+      g.size[k] = static_cast<int64_t>(u64("grid size"));
+    }
+    const int scheme = u64("scheme") == 0 ? GSGPC_LINEAR : GSGPC_CUBIC;
+    const int64_t m = static_cast<int64_t>(u64("grid size"));
+    const int64_t n = static_cast<int64_t>(u64("row count"));
+    const int64_t nnz = static_cast<int64_t>(u64("nnz"));
+    const double yty = f64("yty");
+    std::unique_ptr<gsgpc_stats> s(new_stats(ctx, &g, scheme));
+    if (s->g.m != m) invalid("stats file: grid/statistics size mismatch");
+    std::vector<double> wty(m);
+    for (int64_t i = 0; i < m; ++i) wty[i] = f64("wty");
+    const int W = s->g.W, E = 2 * W - 1;
+    int S = 1;
+    for (int k = 0; k < d; ++k) S *= E;
+    const int c0 = (S - 1) / 2;
+    std::vector<double> st(static_cast<size_t>(s->S_min) * m, 0.0);
+    for (int64_t i = 0; i < nnz; ++i) {
+      const int64_t r = static_cast<int64_t>(u64("triplet row"));
+      const int64_t c = static_cast<int64_t>(u64("triplet col"));
+      const double v = f64("triplet value");
+      if (r < 0 || r >= m || c < 0 || c >= m) invalid("stats file: triplet index out of range");
+      // stencil offset of (r, c); stored once, on the row whose offset is non-negative
+      int64_t rr = r, cc = c;
+      int q = 0;
+      bool ok = true;
+      int dig[3];
+      for (int k = d - 1; k >= 0; --k) {
+        const int64_t ar = rr % s->g.sz[k], ac = cc % s->g.sz[k];
+        rr /= s->g.sz[k];
+        cc /= s->g.sz[k];
+        const int64_t dd = ac - ar;
+        if (dd < -(W - 1) || dd > W - 1) ok = false;
+        dig[k] = static_cast<int>(dd);
+      }
+      if (!ok) throw Error(GSGPC_UNSUPPORTED, "stats file: W^T W entry outside the grid stencil");
+      for (int k = 0; k < d; ++k) q = q * E + dig[k] + (W - 1);
+      if (q >= c0) st[static_cast<size_t>(q - c0) * m + r] = v;
+    }
+    s->fin.ensure(sizeof(double) * s->fin_count());
+    GSGPC_CUDA(cudaMemcpyAsync(s->stencil(), st.data(), sizeof(double) * st.size(), cudaMemcpyHostToDevice, ctx->stream));
+    GSGPC_CUDA(cudaMemcpyAsync(s->wty(), wty.data(), sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+    const double tail[2] = {yty, static_cast<double>(n)};
+    GSGPC_CUDA(cudaMemcpyAsync(s->tail(), tail, sizeof(tail), cudaMemcpyHostToDevice, ctx->stream));
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    s->n = n;
+    s->finalized = true;
+    s->reduced = true;  // loaded statistics carry no moments: no further add()
+    *out = s.release();
+  });
+}
+
+// ---------------------------------------------------------------- K_G
+gsgpc_status gsgpc_kg_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* ls, double outputscale,
+                             double noise_std, gsgpc_kg** out) {
+  return guard(ctx, [&] {
+    if (!out || !ls) invalid("NULL argument");
+    const GridDev g = make_grid(grid, GSGPC_CUBIC);
+    if (!(noise_std > 0.0)) invalid("Hyperparams: noise_std must be positive");
+    if (!(outputscale > 0.0)) invalid("Hyperparams: outputscale must be positive");
+    for (int k = 0; k < g.d; ++k) {
+      if (!(ls[k] > 0.0)) invalid("Hyperparams: lengthscales must be positive");
+    }
+    std::unique_ptr<gsgpc_kg> kg(new gsgpc_kg());
+    kg->device = ctx->device;
+    kg->grid = *grid;
+    kg->m = g.m;
+    kg->noise_std = noise_std;
+    kg->dev.d = g.d;
+    kg->dev.m = g.m;
+    for (int k = 0; k < g.d; ++k) {
+      // 1-D generator: k(g_0, g_j) along dim k (grid.cpp:42-52 / kernels.cpp:43-55 per factor):
+      // d = (x[k] - x2[k]) / ℓ_k with x = min, x2 = min + j·spacing (Grid::point).
+      std::vector<double> col(g.sz[k]);
+      for (int64_t j = 0; j < g.sz[k]; ++j) {
+        const double x2 = g.mn[k] + static_cast<double>(j) * g.sp[k];
+        const double dd = (g.mn[k] - x2) / ls[k];
+        col[j] = std::exp(-0.5 * (dd * dd));
+        if (k == 0) col[j] *= outputscale;
+      }
+      kg->gen[k].ensure(sizeof(double) * g.sz[k]);
+      GSGPC_CUDA(cudaMemcpyAsync(kg->gen[k].p, col.data(), sizeof(double) * g.sz[k], cudaMemcpyHostToDevice,
+                                 ctx->stream));
+      kg->dev.sz[k] = g.sz[k];
+      kg->dev.gen[k] = kg->gen[k].as<double>();
+    }
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = kg.release();
+  });
+}
+
+void gsgpc_kg_destroy(gsgpc_kg* kg) {
+  if (!kg) return;
+  cudaSetDevice(kg->device);
+  cudaDeviceSynchronize();
+  delete kg;
+}
+
+gsgpc_status gsgpc_kg_info(const gsgpc_kg* kg, int64_t* m, double* noise_variance) {
+  if (!kg) return GSGPC_INVALID_ARGUMENT;
+  if (m) *m = kg->m;
+  if (noise_variance) *noise_variance = kg->noise_std * kg->noise_std;
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_kg_apply(gsgpc_ctx* ctx, gsgpc_kg* kg, const double* v, double* out) {
+  return guard(ctx, [&] {
+    if (!kg) invalid("kg is NULL");
+    const double* dv = dev_in(ctx, v, kg->m, "kg_in");
+    DevOut o(ctx, out, kg->m, "kg_out");
+    DBuf& t0 = ctx->buf("kg_t0");
+    DBuf& t1 = ctx->buf("kg_t1");
+    t0.ensure(sizeof(double) * kg->m);
+    t1.ensure(sizeof(double) * kg->m);
+    run_kg_apply(ctx->L(), kg->dev, dv, o.dev, t0.as<double>(), t1.as<double>());
+    o.finish();
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- EFCG driver
+namespace {
+
+constexpr int kGraphIters = 16;
+
+CgCache& cg_setup(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, int maxiter) {
+  const int64_t m = s->g.m;
+  if (!ctx->cg || ctx->cg->stats != s || ctx->cg->kg != kg || ctx->cg->m != m || ctx->cg->trace_cap < maxiter + 1) {
+    ctx->cg.reset(new CgCache());
+    CgCache& c = *ctx->cg;
+    c.stats = s;
+    c.kg = kg;
+    c.m = m;
+    for (DBuf* b : {&c.r, &c.u, &c.s, &c.z, &c.x, &c.kt0, &c.kt1}) b->ensure(sizeof(double) * m);
+    const int np = cg_partials_needed(m) + 4096;
+    c.pa.ensure(sizeof(double) * np);
+    c.pb.ensure(sizeof(double) * np * 4);
+    c.trace_cap = std::max(maxiter + 1, 1024);
+    c.tr.ensure(sizeof(double) * (c.trace_cap + 1));
+    c.al.ensure(sizeof(double) * (c.trace_cap + 1));
+    c.be.ensure(sizeof(double) * (c.trace_cap + 1));
+    c.st.ensure(sizeof(CgState));
+  }
+  return *ctx->cg;
+}
+
+CgBufs cg_bufs(CgCache& c) {
+  CgBufs b{};
+  b.r = c.r.as<double>();
+  b.u = c.u.as<double>();
+  b.s = c.s.as<double>();
+  b.z = c.z.as<double>();
+  b.x = c.x.as<double>();
+  b.kt0 = c.kt0.as<double>();
+  b.kt1 = c.kt1.as<double>();
+  b.part_a = c.pa.as<double>();
+  b.part_b = c.pb.as<double>();
+  b.trace = c.tr.as<double>();
+  b.alphas = c.al.as<double>();
+  b.betas = c.be.as<double>();
+  b.st = c.st.as<CgState>();
+  return b;
+}
+
+struct CgOutcome {
+  int iterations = 0;
+  bool converged = false;
+  bool breakdown = false;
+  double residual_sq = 0.0;
+  double loop_ms = 0.0;
+};
+
+// factorized_cg_grid_rhs on device buffers; rhat0_dev and xhat_out_dev are device arrays.
+CgOutcome run_efcg(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, const double* rhat0_dev, double sigma,
+                   double eps_abs, double rel_tol, int maxiter, double* xhat_out_dev, double* trace_out,
+                   double* alphas_out, double* betas_out) {
+  if (kg->m != s->g.m) invalid("factorized_cg_grid_rhs: dimension mismatch");
+  if (eps_abs < 0.0 && rel_tol < 0.0) invalid("factorized_cg_grid_rhs: set eps_abs or rel_tol");
+  if (maxiter < 0) invalid("factorized_cg_grid_rhs: maxiter must be >= 0");
+  finalize_stats(ctx, s);
+  const int64_t m = s->g.m;
+  CgCache& c = cg_setup(ctx, s, kg, maxiter);
+  const CgBufs b = cg_bufs(c);
+  const StencilDesc sd = stencil_desc(s);
+  upload_stencil_offsets(sd, ctx->stream);
+  const Launch L = ctx->L();
+  CgState st0{};
+  st0.eps_abs = eps_abs;
+  st0.rel_tol = rel_tol;
+  st0.sigma_sq = sigma * sigma;
+  st0.maxiter = maxiter;
+  ctx->pin.ensure(sizeof(CgState) + 64);
+  std::memcpy(ctx->pin.p, &st0, sizeof(CgState));
+  GSGPC_CUDA(cudaMemcpyAsync(b.st, ctx->pin.p, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(b.r, rhat0_dev, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(b.s, 0, sizeof(double) * m, ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(b.z, 0, sizeof(double) * m, ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(b.x, 0, sizeof(double) * m, ctx->stream));
+  run_cg_init(L, sd, s->stencil(), kg->dev, b, m);
+  // capture (once per cache) a graph of kGraphIters iterations
+  if (!c.exec) {
+    cudaGraph_t graph;
+    uint64_t dummy = 0;
+    const Launch Lc{ctx->stream, &dummy};
+    GSGPC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kGraphIters; ++i) run_cg_iter(Lc, sd, s->stencil(), kg->dev, b, m);
+    GSGPC_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    GSGPC_CUDA(cudaGraphInstantiate(&c.exec, graph, 0));
+    GSGPC_CUDA(cudaGraphDestroy(graph));
+    c.B = kGraphIters;
+  }
+  // kernels per iteration (counted per replay)
+  const int per_iter = 2 + s->g.d;
+  cudaEvent_t e0, e1;
+  GSGPC_CUDA(cudaEventCreate(&e0));
+  GSGPC_CUDA(cudaEventCreate(&e1));
+  GSGPC_CUDA(cudaEventRecord(e0, ctx->stream));
+  CgState h{};
+  for (;;) {
+    GSGPC_CUDA(cudaMemcpyAsync(ctx->pin.p, b.st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(&h, ctx->pin.p, sizeof(CgState));
+    if (h.done) break;
+    GSGPC_CUDA(cudaGraphLaunch(c.exec, ctx->stream));
+    ctx->launches += static_cast<uint64_t>(per_iter) * c.B;
+  }
+  GSGPC_CUDA(cudaEventRecord(e1, ctx->stream));
+  GSGPC_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  GSGPC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CgOutcome o;
+  o.iterations = h.iter;
+  o.converged = h.converged != 0;
+  o.breakdown = h.breakdown != 0;
+  o.residual_sq = h.rho;
+  o.loop_ms = ms;
+  if (xhat_out_dev) {
+    GSGPC_CUDA(cudaMemcpyAsync(xhat_out_dev, b.x, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (trace_out) {
+    GSGPC_CUDA(cudaMemcpyAsync(trace_out, b.trace, sizeof(double) * (o.iterations + 1), cudaMemcpyDefault, ctx->stream));
+  }
+  if (alphas_out && o.iterations > 0) {
+    GSGPC_CUDA(cudaMemcpyAsync(alphas_out, b.alphas, sizeof(double) * o.iterations, cudaMemcpyDefault, ctx->stream));
+  }
+  const int nb = o.converged ? std::max(0, o.iterations - 1) : o.iterations;
+  if (betas_out && nb > 0) {
+    GSGPC_CUDA(cudaMemcpyAsync(betas_out, b.betas, sizeof(double) * nb, cudaMemcpyDefault, ctx->stream));
+  }
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (o.breakdown) {
+    throw Error(GSGPC_BREAKDOWN, "factorized_cg_grid_rhs: p^T A p <= 0, operator is not positive definite");
+  }
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+gsgpc_status gsgpc_factorized_cg_grid_rhs(gsgpc_ctx* ctx, gsgpc_kg* kg, gsgpc_stats* s, const double* rhat0,
+                                          double sigma, double eps_abs, double rel_tol, int maxiter,
+                                          double* xhat_d, gsgpc_solve_info* info, double* residual_trace,
+                                          double* alphas, double* betas) {
+  return guard(ctx, [&] {
+    if (!kg || !s) invalid("NULL handle");
+    const double* r0 = dev_in(ctx, rhat0, s->g.m, "cg_r0");
+    DevOut o(ctx, xhat_d, s->g.m, "cg_x");
+    const CgOutcome r = run_efcg(ctx, s, kg, r0, sigma, eps_abs, rel_tol, maxiter, o.dev, residual_trace, alphas, betas);
+    o.finish();
+    if (info) {
+      info->iterations = r.iterations;
+      info->converged = r.converged ? 1 : 0;
+      info->residual_sq = r.residual_sq;
+      info->loop_seconds = r.loop_ms * 1e-3;
+    }
+  });
+}
+
+gsgpc_status gsgpc_posterior_mean_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, double sigma, double tol,
+                                       int maxiter, double* mean_coeffs, gsgpc_solve_info* info) {
+  gsgpc_status nonconv = GSGPC_OK;
+  const gsgpc_status st = guard(ctx, [&] {
+    if (!kg || !s) invalid("posterior_mean_gsgp: null inputs");
+    finalize_stats(ctx, s);
+    const int64_t m = s->g.m;
+    if (kg->m != m) invalid("posterior_mean_gsgp: kernel/grid size mismatch");
+    const double sigma_sq = sigma * sigma;
+    const Launch L = ctx->L();
+    DBuf& t0 = ctx->buf("pm_t0");
+    DBuf& t1 = ctx->buf("pm_t1");
+    DBuf& kw = ctx->buf("pm_kw");
+    DBuf& r0 = ctx->buf("pm_r0");
+    DBuf& xd = ctx->buf("pm_x");
+    for (DBuf* b : {&t0, &t1, &kw, &r0, &xd}) b->ensure(sizeof(double) * m);
+    // rhat0 = -K_G W^T y / σ²  (gp.cpp:331)
+    run_kg_apply(L, kg->dev, s->wty(), kw.as<double>(), t0.as<double>(), t1.as<double>());
+    run_add_div(L, m, nullptr, 0.0, kw.as<double>(), -sigma_sq, r0.as<double>());
+    const double yty = stats_yty(ctx, s);
+    const double eps_abs = tol * tol * yty;  // gp.cpp:333
+    const CgOutcome r = run_efcg(ctx, s, kg, r0.as<double>(), sigma, eps_abs, -1.0, maxiter, xd.as<double>(),
+                                 nullptr, nullptr, nullptr);
+    if (info) {
+      info->iterations = r.iterations;
+      info->converged = r.converged ? 1 : 0;
+      info->residual_sq = r.residual_sq;
+      info->loop_seconds = r.loop_ms * 1e-3;
+    }
+    if (!r.converged) {
+      nonconv = GSGPC_NONCONVERGENCE;
+      throw Error(GSGPC_NONCONVERGENCE, "posterior_mean_gsgp: solver hit maxiter");
+    }
+    // mean_coeffs = K_G (x̂_d + W^T y / σ²)  (gp.cpp:345)
+    run_add_div(L, m, xd.as<double>(), 1.0, s->wty(), sigma_sq, r0.as<double>());
+    DevOut o(ctx, mean_coeffs, m, "pm_out");
+    run_kg_apply(L, kg->dev, r0.as<double>(), o.dev, t0.as<double>(), t1.as<double>());
+    o.finish();
+  });
+  (void)nonconv;
+  return st;
+}
+
+gsgpc_status gsgpc_predict_mean(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme, const double* mean_coeffs,
+                                const gsgpc_points* pts, int64_t n, double* out) {
+  return guard(ctx, [&] {
+    const GridDev g = make_grid(grid, scheme);
+    check_points(pts, n, false);
+    if (n == 0) return;
+    const double* c = dev_in(ctx, mean_coeffs, g.m, "pred_coeffs");
+    const bool dev = is_device_ptr(pts->x);
+    const PointsDev P = dev ? points_dev(pts, g.d, 0) : stage_points(ctx, pts, g.d, 0, n, false, "pred_stage");
+    DevOut o(ctx, out, n, "pred_out");
+    DBuf& st = ctx->buf("pred_status");
+    st.ensure(sizeof(int) * n);
+    run_predict(ctx->L(), pts->dtype, P, n, g, c, o.dev, st.as<int>());
+    o.finish();
+    std::vector<int> hs(n);
+    copy_out(ctx, hs.data(), st.p, sizeof(int) * n);
+    for (int64_t i = 0; i < n; ++i) {
+      if (hs[i] == PT_OUTSIDE) throw Error(GSGPC_OUT_OF_GRID, "interp_weights: point outside grid", i + 1);
+      if (hs[i] == PT_LEAVES) {
+        throw Error(GSGPC_OUT_OF_GRID,
+                    "interp_weights: stencil leaves the grid (point too close to the boundary for the requested "
+                    "scheme)",
+                    i + 1);
+      }
+    }
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- EFLA / log-likelihood
+// (implemented in efla.cu)

@@ -1,0 +1,511 @@
+// operators.cu — per-iteration operators of the factorized solvers.
+//
+//   K3  k_spmv / k_cg_spmv : W^T W as a symmetric 7^d (3^d linear) stencil SpMV over the
+//                            regular grid (replaces SufficientStats::apply_wtw's CSR SpMV,
+//                            interp.cpp:227-233).  Only the lexicographically non-negative
+//                            half of the offsets is stored; the mirrored half is read at the
+//                            shifted node (A[s][a-δ] x[a-δ]).
+//   K4  k_toep             : K_G v as d Toeplitz mode products (K_G = ⊗_k T_k for the
+//                            SE-ARD kernel, kernels.cpp:43-55), replacing the circulant-
+//                            embedding FFT of ToeplitzOperator::apply (grid.cpp:193-235).
+//   K5  k_cg_*             : fused EFCG vector updates with device-resident α, β, ρ, pap
+//                            (factorized_cg_grid_rhs, solvers.cpp:271-336); dots use
+//                            per-block partials + a last-block reduction (deterministic).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+#include "precompute.cuh"
+
+namespace gsgpc {
+
+constexpr int MAX_SMIN = 172;  // (7^3 + 1) / 2
+__constant__ long long c_off_flat[MAX_SMIN];
+__constant__ signed char c_off_d[MAX_SMIN][4];
+
+void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
+  const int E = 2 * sd.W - 1;
+  int S = 1;
+  for (int k = 0; k < sd.d; ++k) S *= E;
+  const int c0 = (S - 1) / 2;
+  long long flat[MAX_SMIN];
+  signed char dd[MAX_SMIN][4] = {};
+  for (int s2 = 0; s2 < sd.S_min; ++s2) {
+    int q = c0 + s2;
+    long long f = 0;
+    int dig[3] = {0, 0, 0};
+    for (int k = sd.d - 1; k >= 0; --k) {
+      dig[k] = q % E - (sd.W - 1);
+      q /= E;
+    }
+    for (int k = 0; k < sd.d; ++k) {
+      f = f * sd.sz[k] + dig[k];
+      dd[s2][k] = static_cast<signed char>(dig[k]);
+    }
+    flat[s2] = f;
+  }
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_flat, flat, sizeof(long long) * sd.S_min, 0,
+                                     cudaMemcpyHostToDevice, s));
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_d, dd, sizeof(dd[0]) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
+}
+
+// ------------------------------------------------------------------ K3 stencil SpMV
+__device__ __forceinline__ double spmv_node(const StencilDesc& sd, const double* __restrict__ A,
+                                            const double* __restrict__ v, int64_t a) {
+  int64_t co[3] = {0, 0, 0};
+  int64_t r = a;
+  bool interior = true;
+  const int R = sd.W - 1;
+#pragma unroll
+  for (int k = GSGPC_MAX_DIM - 1; k >= 0; --k) {
+    if (k < sd.d) {
+      co[k] = r % sd.sz[k];
+      r /= sd.sz[k];
+      interior = interior && co[k] >= R && co[k] < sd.sz[k] - R;
+    }
+  }
+  const int64_t m = sd.m;
+  double acc = A[a] * v[a];
+  if (interior) {
+    for (int s = 1; s < sd.S_min; ++s) {
+      const int64_t o = c_off_flat[s];
+      acc = fma(A[s * m + a], v[a + o], acc);
+      acc = fma(A[s * m + a - o], v[a - o], acc);
+    }
+  } else {
+    for (int s = 1; s < sd.S_min; ++s) {
+      const int64_t o = c_off_flat[s];
+      bool fwd = true, bwd = true;
+#pragma unroll
+      for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
+        if (k < sd.d) {
+          const int64_t dk = c_off_d[s][k];
+          fwd = fwd && co[k] + dk >= 0 && co[k] + dk < sd.sz[k];
+          bwd = bwd && co[k] - dk >= 0 && co[k] - dk < sd.sz[k];
+        }
+      }
+      if (fwd) acc = fma(A[s * m + a], v[a + o], acc);
+      if (bwd) acc = fma(A[s * m + a - o], v[a - o], acc);
+    }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_spmv(StencilDesc sd, const double* __restrict__ A,
+                                              const double* __restrict__ v, double* __restrict__ out) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= sd.m) return;
+  out[a] = spmv_node(sd, A, v, a);
+}
+
+void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out) {
+  k_spmv<<<static_cast<unsigned>(ceil_div(sd.m, 256)), 256, 0, L.s>>>(sd, A, v, out);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ last-block reduction
+__device__ __forceinline__ bool arrive_last(unsigned* cnt) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(cnt, 1u);
+    last = prev == gridDim.x * gridDim.y - 1;
+  }
+  __syncthreads();
+  return last;
+}
+
+template <int NT>
+__device__ __forceinline__ double reduce_partials(const double* part, int np, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < np; i += NT) v += part[i];
+  return block_sum<NT>(v, sh);
+}
+
+// ------------------------------------------------------------------ K4 Toeplitz mode product
+struct ToepArgs {
+  const double* X;
+  double* Y;
+  const double* gen;
+  int64_t n, inner, outer, L;
+  int TL, TA;
+};
+
+struct CgEpi {
+  const double *r, *u;
+  double *s, *z;
+  double* part;
+  CgState* st;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_toep(ToepArgs t, CgEpi e) {
+  extern __shared__ double smem[];
+  if (e.st != nullptr && e.st->done) return;
+  const int64_t n = t.n;
+  double* Ts = smem;              // 2n-1 symmetric generator
+  double* Xs = smem + 2 * n - 1;  // [n][TL]
+  const int64_t l0 = static_cast<int64_t>(blockIdx.x) * t.TL;
+  const int nl = static_cast<int>(imin64(t.TL, t.L - l0));
+  const int64_t a0 = static_cast<int64_t>(blockIdx.y) * t.TA;
+  const int na = static_cast<int>(imin64(t.TA, n - a0));
+  for (int64_t q = threadIdx.x; q < 2 * n - 1; q += blockDim.x) {
+    const int64_t dd = q - (n - 1);
+    Ts[q] = t.gen[dd < 0 ? -dd : dd];
+  }
+  if (t.inner == 1) {
+    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(nl) * n; q += blockDim.x) {
+      const int64_t tl = q / n, j = q % n;
+      Xs[j * t.TL + tl] = t.X[(l0 + tl) * n + j];
+    }
+  } else {
+    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(t.TL) * n; q += blockDim.x) {
+      const int tl = static_cast<int>(q % t.TL);
+      const int64_t j = q / t.TL;
+      if (tl < nl) {
+        const int64_t l = l0 + tl, o = l / t.inner, i = l % t.inner;
+        Xs[j * t.TL + tl] = t.X[(o * n + j) * t.inner + i];
+      }
+    }
+  }
+  __syncthreads();
+  double dot = 0.0;
+  const int total = nl * na;
+  for (int u = threadIdx.x; u < total; u += blockDim.x) {
+    int tl, ar;
+    if (t.inner == 1) {
+      ar = u % na;
+      tl = u / na;
+    } else {
+      tl = u % nl;
+      ar = u / nl;
+    }
+    const int64_t a = a0 + ar;
+    const double* tp = Ts + (n - 1 + a);
+    double acc = 0.0;
+    for (int64_t j = 0; j < n; ++j) acc = fma(tp[-j], Xs[j * t.TL + tl], acc);
+    const int64_t l = l0 + tl, o = l / t.inner, i = l % t.inner;
+    const int64_t g = (o * n + a) * t.inner + i;
+    if (MODE == 0) {
+      t.Y[g] = acc;
+    } else {
+      const double beta = e.st->beta;
+      const double v = acc + e.st->sigma_sq * e.r[g];
+      const double s = e.u[g] + beta * e.s[g];
+      const double z = v + beta * e.z[g];
+      e.s[g] = s;
+      e.z[g] = z;
+      dot = fma(s, z, dot);
+    }
+  }
+  if (MODE == 1) {
+    __shared__ double sh[8];
+    const double bs = block_sum<256>(dot, sh);
+    if (threadIdx.x == 0) e.part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
+    if (arrive_last(&e.st->cnt_b)) {
+      const double pap = reduce_partials<256>(e.part, gridDim.x * gridDim.y, sh);
+      if (threadIdx.x == 0) {
+        e.st->pap = pap;
+        e.st->cnt_b = 0;
+      }
+    }
+  }
+}
+
+static void toep_config(int64_t n, int64_t inner, int64_t outer, ToepArgs& t, dim3& grid, size_t& smem) {
+  t.n = n;
+  t.inner = inner;
+  t.outer = outer;
+  t.L = inner * outer;
+  const int64_t cap = 8192;  // doubles of dynamic smem (64 KB)
+  if (3 * n > cap) throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2730 nodes is not supported");
+  int64_t TL = std::min<int64_t>(32, (cap - 2 * n) / n);
+  TL = std::max<int64_t>(1, std::min<int64_t>(TL, t.L));
+  t.TL = static_cast<int>(TL);
+  const int64_t tiles = ceil_div(t.L, TL);
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(296, tiles), ceil_div(n, 32)));
+  t.TA = static_cast<int>(ceil_div(n, chunks));
+  chunks = ceil_div(n, t.TA);
+  grid = dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
+  smem = sizeof(double) * (2 * n - 1 + TL * n);
+}
+
+static void launch_toep(const Launch& L, int mode, ToepArgs t, dim3 grid, size_t smem, CgEpi e) {
+  if (mode == 0) {
+    if (smem > 48 * 1024) {
+      GSGPC_CUDA(cudaFuncSetAttribute(k_toep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    }
+    k_toep<0><<<grid, 256, smem, L.s>>>(t, e);
+  } else {
+    if (smem > 48 * 1024) {
+      GSGPC_CUDA(cudaFuncSetAttribute(k_toep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    }
+    k_toep<1><<<grid, 256, smem, L.s>>>(t, e);
+  }
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+// Applies T_{d-1}, ..., T_1 (plain) and T_0 (MODE, possibly with the CG epilogue).
+static void kg_chain(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1,
+                     int last_mode, CgEpi e) {
+  const double* cur = v;
+  for (int k = kg.d - 1; k >= 0; --k) {
+    int64_t inner = 1, outer = 1;
+    for (int j = k + 1; j < kg.d; ++j) inner *= kg.sz[j];
+    for (int j = 0; j < k; ++j) outer *= kg.sz[j];
+    ToepArgs t{};
+    dim3 grid;
+    size_t smem;
+    toep_config(kg.sz[k], inner, outer, t, grid, smem);
+    t.X = cur;
+    t.gen = kg.gen[k];
+    double* dst = k == 0 ? out : (cur == tmp0 ? tmp1 : tmp0);
+    t.Y = dst;
+    launch_toep(L, k == 0 ? last_mode : 0, t, grid, smem, e);
+    cur = dst;
+  }
+}
+
+void run_kg_apply(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1) {
+  CgEpi e{};
+  kg_chain(L, kg, v, out, tmp0, tmp1, 0, e);
+}
+
+int cg_partials_needed(int64_t m) {
+  return static_cast<int>(std::max<int64_t>(ceil_div(m, 256), 4096));
+}
+
+// ------------------------------------------------------------------ K5 EFCG kernels
+__global__ void __launch_bounds__(256) k_cg_update(CgBufs b, int64_t m) {
+  CgState* st = b.st;
+  if (st->done) return;
+  if (st->iter >= st->maxiter) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->done = 1;
+    return;
+  }
+  const double pap = st->pap;
+  if (pap <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = 1;
+      st->done = 1;
+    }
+    return;
+  }
+  const double alpha = st->rho / pap;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) {
+    b.x[i] += alpha * b.s[i];
+    b.r[i] -= alpha * b.z[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->alpha = alpha;
+    b.alphas[st->iter] = alpha;
+  }
+}
+
+template <int INIT>
+__global__ void __launch_bounds__(256) k_cg_spmv(StencilDesc sd, const double* __restrict__ A, CgBufs b) {
+  CgState* st = b.st;
+  if (st->done) return;
+  __shared__ double sh[8];
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double d = 0.0;
+  if (a < sd.m) {
+    const double u = spmv_node(sd, A, b.r, a);
+    b.u[a] = u;
+    d = u * b.r[a];
+  }
+  const double bs = block_sum<256>(d, sh);
+  if (threadIdx.x == 0) b.part_a[blockIdx.x] = bs;
+  if (arrive_last(&st->cnt_a)) {
+    const double rho_new = reduce_partials<256>(b.part_a, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      st->cnt_a = 0;
+      if (INIT) {
+        st->rho = rho_new;
+        st->eps = st->eps_abs >= 0.0 ? st->eps_abs : st->rel_tol * st->rel_tol * rho_new;
+        b.trace[0] = rho_new;
+        st->beta = 0.0;
+        if (rho_new <= st->eps) {
+          st->converged = 1;
+          st->done = 1;
+        }
+      } else {
+        st->iter += 1;
+        b.trace[st->iter] = rho_new;
+        if (rho_new <= st->eps) {
+          st->converged = 1;
+          st->done = 1;
+          st->rho = rho_new;
+        } else {
+          const double beta = rho_new / st->rho;
+          st->beta = beta;
+          b.betas[st->iter - 1] = beta;
+          st->rho = rho_new;
+        }
+      }
+    }
+  }
+}
+
+void run_cg_init(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
+                 int64_t m) {
+  k_cg_spmv<1><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b);
+  L.count();
+  CgEpi e{b.r, b.u, b.s, b.z, b.part_b, b.st};
+  kg_chain(L, kg, b.u, nullptr, b.kt0, b.kt1, 1, e);
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+void run_cg_iter(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
+                 int64_t m) {
+  k_cg_update<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(b, m);
+  k_cg_spmv<0><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b);
+  L.count(2);
+  CgEpi e{b.r, b.u, b.s, b.z, b.part_b, b.st};
+  kg_chain(L, kg, b.u, nullptr, b.kt0, b.kt1, 1, e);
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ vector helpers
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b, const double* __restrict__ y,
+                        double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a * x[i] + b * y[i];
+}
+// out = x + y / b (the reference's  x̂_d + W^T y / σ²  and  -K w / σ²  forms: division, not
+// multiplication by the reciprocal)
+__global__ void k_add_div(int64_t n, const double* __restrict__ x, const double* __restrict__ y, double b, double sx,
+                          double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (x ? sx * x[i] : 0.0) + y[i] / b;
+}
+
+void run_axpby(const Launch& L, int64_t n, double a, const double* x, double b, const double* y, double* out) {
+  k_axpby<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, L.s>>>(n, a, x, b, y, out);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+void run_add_div(const Launch& L, int64_t n, const double* x, double sx, const double* y, double b, double* out) {
+  k_add_div<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, L.s>>>(n, x, y, b, sx, out);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ pointwise interpolation
+// interp_weights (interp.cpp:79-134), bit-exact, one thread per point.
+template <typename T, bool PREDICT>
+__global__ void __launch_bounds__(128) k_interp(PointsDev p, int64_t n, GridDev g, int64_t* __restrict__ idx,
+                                                double* __restrict__ w, int* __restrict__ nnz,
+                                                int* __restrict__ status, const double* __restrict__ coeffs,
+                                                double* __restrict__ pred) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x[GSGPC_MAX_DIM], y;
+  const T* X = static_cast<const T*>(p.x);
+#pragma unroll
+  for (int k = 0; k < GSGPC_MAX_DIM; ++k) x[k] = k < g.d ? static_cast<double>(X[i * p.xs + p.xo[k]]) : 0.0;
+  (void)y;
+  int64_t st0[GSGPC_MAX_DIM];
+  double wk[GSGPC_MAX_DIM][4];
+  int stt = PT_VALID;
+  for (int k = 0; k < g.d; ++k) {
+    int64_t i0 = 0;
+    double t = 0.0;
+    const int s = stencil_dim(x[k], g.mn[k], g.sp[k], g.sz[k], i0, t);
+    if (s == PT_OUTSIDE) {
+      stt = PT_OUTSIDE;
+      break;
+    }
+    if (s == PT_EMPTY) {
+      // NaN: the reference's floor()/cast yields an index whose weights are all zero
+      for (int o = 0; o < 4; ++o) wk[k][o] = 0.0;
+      st0[k] = 0;
+      continue;
+    }
+    weights_1d(t, g.W, wk[k]);
+    st0[k] = g.W == 4 ? i0 - 1 : i0;
+  }
+  int cnt = 0;
+  double out = 0.0;
+  const int width = g.W;
+  const int64_t cap = PREDICT ? 0 : 1;
+  (void)cap;
+  if (stt == PT_VALID) {
+    int combos = 1;
+    for (int k = 0; k < g.d; ++k) combos *= width;
+    const int64_t rowcap = combos;
+    for (int c = 0; c < combos; ++c) {
+      int offs[GSGPC_MAX_DIM];
+      int cc = c;
+      for (int k = g.d - 1; k >= 0; --k) {
+        offs[k] = cc % width;
+        cc /= width;
+      }
+      double wv = 1.0;
+      int64_t flat = 0;
+      bool in_range = true;
+      for (int k = 0; k < g.d; ++k) {
+        const double wkk = wk[k][offs[k]];
+        if (wkk == 0.0) {
+          wv = 0.0;
+          break;
+        }
+        const int64_t j = st0[k] + offs[k];
+        if (j < 0 || j >= g.sz[k]) {
+          in_range = false;
+          break;
+        }
+        wv = __dmul_rn(wv, wkk);
+        flat = flat * g.sz[k] + j;
+      }
+      if (wv != 0.0) {
+        if (!in_range) {
+          stt = PT_LEAVES;
+          break;
+        }
+        if (PREDICT) {
+          out = __dadd_rn(out, __dmul_rn(wv, coeffs[flat]));
+        } else {
+          idx[i * rowcap + cnt] = flat;
+          w[i * rowcap + cnt] = wv;
+        }
+        ++cnt;
+      }
+    }
+  }
+  if (stt != PT_VALID) cnt = 0;
+  if (PREDICT) {
+    pred[i] = stt == PT_VALID ? out : 0.0;
+    if (status) status[i] = stt == PT_VALID ? 0 : stt;
+  } else {
+    nnz[i] = cnt;
+    status[i] = stt == PT_VALID ? 0 : stt;
+  }
+}
+
+void run_interp_weights(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, int64_t* idx,
+                        double* w, int* nnz, int* status) {
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 128));
+  if (dtype == GSGPC_F32) k_interp<float, false><<<blocks, 128, 0, L.s>>>(p, n, g, idx, w, nnz, status, nullptr, nullptr);
+  else k_interp<double, false><<<blocks, 128, 0, L.s>>>(p, n, g, idx, w, nnz, status, nullptr, nullptr);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+void run_predict(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const double* coeffs,
+                 double* out, int* status) {
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 128));
+  if (dtype == GSGPC_F32) k_interp<float, true><<<blocks, 128, 0, L.s>>>(p, n, g, nullptr, nullptr, nullptr, status, coeffs, out);
+  else k_interp<double, true><<<blocks, 128, 0, L.s>>>(p, n, g, nullptr, nullptr, nullptr, status, coeffs, out);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+}  // namespace gsgpc

@@ -1,0 +1,103 @@
+// precompute.cuh — host entry points of the kernels in precompute.cu / operators.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace gsgpc {
+
+// Stream + launch counter (every library kernel launch is counted: gsgpc_ctx_launch_count).
+struct Launch {
+  cudaStream_t s;
+  uint64_t* counter;
+  void count(int k = 1) const { *counter += static_cast<uint64_t>(k); }
+};
+
+// ---- precompute.cu
+int moments_per_cell(int d, int W);
+int64_t scan_scratch_elems(int64_t n);
+int64_t finalize_ws_elems(const GridDev& g);
+void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
+                  int* hist, unsigned long long* err, double* part, int nblk);
+void run_sum_partials(const Launch& L, const double* part, int np, double* acc);
+void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* block_sums);
+void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const int64_t* off,
+                 int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out, int nblk);
+void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t nvalid,
+                 const GridDev& g, double* mom);
+void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
+                       int64_t nvalid, const GridDev& g, int probes, double* pmom);
+void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
+                  double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems);
+void run_gather_probe(const Launch& L, const double* pmom, int64_t cells, int probes, int QY, int pj,
+                      double* out);
+
+// ---- operators.cu
+// Symmetric half stencil: offsets s = 0..S_min-1 (lexicographically non-negative), per-dim
+// displacements in [-(W-1), W-1].
+struct StencilDesc {
+  int d, W, S_min;
+  int64_t sz[GSGPC_MAX_DIM];
+  int64_t m;
+};
+void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s);
+// out = (W^T W) v ; if dot_out != nullptr also dot(out, dotv) via deterministic partials.
+void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out);
+
+// Kronecker K_G (Toeplitz mode products)
+struct KgDev {
+  int d;
+  int64_t sz[GSGPC_MAX_DIM];
+  int64_t m;
+  const double* gen[GSGPC_MAX_DIM];  // per-dim generator columns (outputscale folded into dim 0)
+};
+void run_kg_apply(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1);
+
+// EFCG (see operators.cu)
+struct CgState {
+  double rho, rho_new, pap, alpha, beta, eps, eps_abs, rel_tol, sigma_sq;
+  int iter, maxiter, done, converged, breakdown;
+  unsigned int cnt_a, cnt_b;
+};
+struct CgBufs {
+  double *r, *u, *s, *z, *x;     // rhat, uhat, shat, zbar, xhat_d
+  double *kt0, *kt1;             // K_G temporaries
+  double *part_a, *part_b;       // block partials for the two dots
+  double *trace, *alphas, *betas;
+  CgState* st;
+};
+void run_cg_init(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
+                 int64_t m);
+void run_cg_iter(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
+                 int64_t m);
+int cg_partials_needed(int64_t m);
+
+// Vector helpers
+void run_axpby(const Launch& L, int64_t n, double a, const double* x, double b, const double* y, double* out);
+void run_scale(const Launch& L, int64_t n, double a, const double* x, double* out);
+
+// Point-wise interpolation (bit-exact weights)
+void run_interp_weights(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g,
+                        int64_t* idx, double* w, int* nnz, int* status);
+void run_predict(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const double* coeffs,
+                 double* out, int* status);
+
+// Batched EFLA (probe-batched factorized Lanczos)
+struct EflaBufs {
+  int P, k;
+  int64_t m;
+  double *Q, *Ph;          // P × k × m bases (Q̂, P̂ = W^T W Q̂)
+  double *q, *qprev, *sbar, *pcur, *wv, *pnext, *snext, *wt0, *kwt0;  // P × m
+  double *kt0, *kt1;       // K_G temporaries P × m
+  double *scal;            // per-probe scalars (see operators.cu)
+  double *lambda;          // P × k
+  double *tq, *dvec;       // P × k
+  double *alpha, *beta;    // P × k
+  int *done;               // P
+};
+void run_efla(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const EflaBufs& b,
+              double sigma_sq);
+
+}  // namespace gsgpc

@@ -1,0 +1,853 @@
+"""Python mirror of the reference's ``gsgp`` C++ API (proj/include/gsgp/*.hpp) on libgsgpc.
+
+Same names, argument meaning and error behaviour as the reference for the hot path:
+
+* ``Grid`` / ``GridDim`` / ``fit_grid_to_data``            grid.hpp:15-44, interp.hpp:168-172
+* ``interp_weights``                                        interp.hpp:38-41
+* ``SufficientStatsAccumulator`` / ``SufficientStats`` /
+  ``sufficient_stats``                                      interp.hpp:87-160
+* ``ToeplitzOperator``                                      grid.hpp:58-90
+* ``factorized_cg_grid_rhs`` / ``GridRhsTolerance``         solvers.hpp:127-151
+* ``posterior_mean_gsgp`` / ``PosteriorModel``              gp.hpp:101-122
+* ``factorized_lanczos_fused`` (probe-batched)              solvers.hpp:178-183
+* ``log_likelihood_gsgp`` / ``LoglikOptions``               gp.hpp:62-90
+* ``save_stats`` / ``load_stats``                           io.hpp:82-97
+
+Errors: ``InvalidArgument`` (a ``ValueError``; the reference's ``std::invalid_argument``,
+with ``.row`` = 1-based stream row for out-of-grid points), ``SolverBreakdown``,
+``SolverNonConvergence`` (``.residual_sq``, ``.iterations``), ``RuntimeError``.
+
+Arrays: numpy arrays and CPU torch tensors are host memory; CUDA torch tensors are passed
+to the library as device pointers (zero copy).  All compute runs in libgsgpc.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as _L
+
+try:  # torch is optional for the API, required for device-resident inputs
+    import torch
+except Exception:  # noqa: BLE001
+    torch = None
+
+
+# ---------------------------------------------------------------- errors
+class InvalidArgument(ValueError):
+    def __init__(self, msg, row=0):
+        super().__init__(msg)
+        self.row = row
+
+
+class SolverBreakdown(RuntimeError):
+    pass
+
+
+class SolverNonConvergence(RuntimeError):
+    def __init__(self, msg, residual_sq=float("nan"), iterations=0):
+        super().__init__(msg)
+        self.residual_sq = residual_sq
+        self.iterations = iterations
+
+
+class GsgpcCudaError(RuntimeError):
+    pass
+
+
+def _raise(ctx, code, info=None):
+    lib = _L.load()
+    msg = lib.gsgpc_last_error(ctx).decode() if ctx else f"gsgpc error {code}"
+    row = int(lib.gsgpc_last_error_row(ctx)) if ctx else 0
+    if code in (_L.INVALID_ARGUMENT, _L.OUT_OF_GRID):
+        raise InvalidArgument(msg, row)
+    if code == _L.BREAKDOWN:
+        raise SolverBreakdown(msg)
+    if code == _L.NONCONVERGENCE:
+        raise SolverNonConvergence(msg, info.residual_sq if info else float("nan"), info.iterations if info else 0)
+    if code == _L.UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if code == _L.CUDA_ERROR:
+        raise GsgpcCudaError(msg)
+    raise RuntimeError(msg)
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """One device + one CUDA stream (gsgpc_ctx)."""
+
+    def __init__(self, device: int = 0):
+        lib = _L.load()
+        h = C.c_void_p()
+        code = lib.gsgpc_ctx_create(int(device), C.byref(h))
+        if code != _L.OK:
+            raise GsgpcCudaError(f"gsgpc_ctx_create(device={device}) failed with status {code}")
+        self._h = h
+        self.device = int(device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, code, info=None):
+        if code != _L.OK:
+            _raise(self._h, code, info)
+
+    def synchronize(self):
+        self.check(_L.load().gsgpc_ctx_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int):
+        self.check(_L.load().gsgpc_ctx_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    @property
+    def stream(self) -> int:
+        return int(_L.load().gsgpc_ctx_stream(self._h) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(_L.load().gsgpc_ctx_launch_count(self._h))
+
+    def enable_phase_timing(self, on=True):
+        self.check(_L.load().gsgpc_ctx_enable_phase_timing(self._h, 1 if on else 0))
+
+    def phase_times(self):
+        ms = (C.c_double * 8)()
+        calls = (C.c_int64 * 8)()
+        self.check(_L.load().gsgpc_ctx_phase_times(self._h, ms, calls))
+        names = ["classify", "scan", "scatter", "moments", "finalize", "h2d", "p6", "p7"]
+        return {names[i]: (ms[i], calls[i]) for i in range(8) if calls[i]}
+
+    def fp64_peak_tflops(self) -> float:
+        v = C.c_double()
+        self.check(_L.load().gsgpc_diag_fp64_peak(self._h, C.byref(v)))
+        return v.value
+
+    def reset_phase_times(self):
+        self.check(_L.load().gsgpc_ctx_reset_phase_times(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _L.load().gsgpc_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+_default_ctx = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def version() -> str:
+    return _L.load().gsgpc_version().decode()
+
+
+# ---------------------------------------------------------------- array plumbing
+class _Arr:
+    """A pointer into host or device memory plus a keep-alive reference."""
+
+    def __init__(self, obj, dtype, writable=False):
+        if torch is not None and isinstance(obj, torch.Tensor):
+            want = torch.float32 if dtype == np.float32 else (torch.float64 if dtype == np.float64 else None)
+            t = obj
+            if want is not None and t.dtype != want:
+                if writable:
+                    raise InvalidArgument(f"output tensor must be {want}")
+                t = t.to(want)
+            if not t.is_contiguous():
+                if writable:
+                    raise InvalidArgument("output tensor must be contiguous")
+                t = t.contiguous()
+            self.keep = t
+            self.ptr = t.data_ptr()
+            self.device = t.is_cuda
+            self.shape = tuple(t.shape)
+        else:
+            a = np.asarray(obj)
+            if writable:
+                if a.dtype != dtype or not a.flags.c_contiguous:
+                    raise InvalidArgument("output array must be C-contiguous " + str(np.dtype(dtype)))
+            else:
+                a = np.ascontiguousarray(a, dtype=dtype)
+            self.keep = a
+            self.ptr = a.ctypes.data
+            self.device = False
+            self.shape = a.shape
+
+    @property
+    def vp(self):
+        return C.c_void_p(self.ptr)
+
+
+def _dtype_code(obj):
+    if torch is not None and isinstance(obj, torch.Tensor):
+        return _L.F32 if obj.dtype == torch.float32 else _L.F64
+    a = np.asarray(obj)
+    return _L.F32 if a.dtype == np.float32 else _L.F64
+
+
+def _points(x, y, d):
+    """gsgpc_points for coordinates x (n×d) and responses y (n), or packed rows x (n×(d+1)) with y=None."""
+    dt = _L.F32 if (_dtype_code(x) == _L.F32 and (y is None or _dtype_code(y) == _L.F32)) else _L.F64
+    npdt = np.float32 if dt == _L.F32 else np.float64
+    xa = _Arr(x, npdt)
+    shp = xa.shape if len(xa.shape) > 1 else (xa.shape[0], 1)
+    n = shp[0]
+    p = _L.Points_t()
+    p.dtype = dt
+    p.x = xa.ptr
+    keep = [xa]
+    if y is None:
+        if shp[1] != d + 1:
+            raise InvalidArgument(f"packed rows need d+1 = {d + 1} columns, got {shp[1]}")
+        p.x_row_stride = d + 1
+        for k in range(d):
+            p.x_col_offset[k] = k
+        p.y = xa.ptr + (d) * (4 if dt == _L.F32 else 8)
+        p.y_stride = d + 1
+    else:
+        if shp[1] != d:
+            raise InvalidArgument(f"sufficient_stats: stream/grid dimension mismatch ({shp[1]} vs {d})")
+        p.x_row_stride = d
+        for k in range(d):
+            p.x_col_offset[k] = k
+        ya = _Arr(y, npdt)
+        if ya.shape[0] != n:
+            raise InvalidArgument("x and y row counts differ")
+        keep.append(ya)
+        p.y = ya.ptr
+        p.y_stride = 1
+    return p, n, keep
+
+
+def _coords(x, d):
+    dt = _dtype_code(x)
+    npdt = np.float32 if dt == _L.F32 else np.float64
+    xa = _Arr(x, npdt)
+    shp = xa.shape if len(xa.shape) > 1 else (xa.shape[0], 1)
+    if shp[1] != d:
+        raise InvalidArgument(f"interp_weights: dimension mismatch ({shp[1]} vs {d})")
+    p = _L.Points_t()
+    p.dtype = dt
+    p.x = xa.ptr
+    p.x_row_stride = d
+    for k in range(d):
+        p.x_col_offset[k] = k
+    p.y = xa.ptr
+    p.y_stride = 0
+    return p, shp[0], [xa]
+
+
+def _out_like(n, device_like=None):
+    if device_like is not None and torch is not None and isinstance(device_like, torch.Tensor) and device_like.is_cuda:
+        return torch.empty(n, dtype=torch.float64, device=device_like.device)
+    return np.zeros(n, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- grid
+class InterpScheme(enum.IntEnum):
+    Linear = 0
+    Cubic = 1
+
+
+def stencil_radius(scheme) -> int:
+    return 1 if int(scheme) == InterpScheme.Linear else 2
+
+
+@dataclass
+class GridDim:
+    min: float = 0.0
+    max: float = 1.0
+    size: int = 2
+
+
+class Grid:
+    """Regular lattice, row-major flattening with the last dimension fastest (grid.hpp:20-44)."""
+
+    def __init__(self, dims: Sequence[GridDim]):
+        dims = list(dims)
+        if not dims:
+            raise InvalidArgument("Grid: need at least one dimension")
+        for d in dims:
+            if d.size < 2:
+                raise InvalidArgument("Grid: size must be >= 2 per dimension")
+            if not d.max > d.min:
+                raise InvalidArgument("Grid: max must exceed min")
+        self._dims = [GridDim(float(d.min), float(d.max), int(d.size)) for d in dims]
+
+    def dim(self) -> int:
+        return len(self._dims)
+
+    def size(self, k) -> int:
+        return self._dims[k].size
+
+    def min(self, k) -> float:
+        return self._dims[k].min
+
+    def max(self, k) -> float:
+        return self._dims[k].max
+
+    def spacing(self, k) -> float:
+        d = self._dims[k]
+        return (d.max - d.min) / float(d.size - 1)
+
+    def num_points(self) -> int:
+        return int(np.prod([d.size for d in self._dims]))
+
+    def dims(self) -> List[GridDim]:
+        return list(self._dims)
+
+    def flat_index(self, multi) -> int:
+        f = 0
+        for k, i in enumerate(multi):
+            f = f * self._dims[k].size + int(i)
+        return f
+
+    def point(self, flat) -> np.ndarray:
+        x = np.zeros(self.dim())
+        for k in range(self.dim() - 1, -1, -1):
+            i = flat % self._dims[k].size
+            flat //= self._dims[k].size
+            x[k] = self._dims[k].min + float(i) * self.spacing(k)
+        return x
+
+    def _c(self) -> _L.Grid_t:
+        g = _L.Grid_t()
+        g.dim = self.dim()
+        for k, d in enumerate(self._dims):
+            if k < _L.MAX_DIM:
+                g.min[k], g.max[k], g.size[k] = d.min, d.max, d.size
+        return g
+
+    def __eq__(self, other):
+        return isinstance(other, Grid) and self._dims == other._dims
+
+    def __repr__(self):
+        return "Grid(" + ", ".join(f"[{d.min}:{d.max}:{d.size}]" for d in self._dims) + ")"
+
+
+def fit_grid_to_data(lo, hi, sizes, scheme=InterpScheme.Cubic) -> Grid:
+    """interp.cpp:286-306: pad the data box by stencil_radius(scheme) cells per side."""
+    lo = np.asarray(lo, dtype=np.float64).reshape(-1)
+    hi = np.asarray(hi, dtype=np.float64).reshape(-1)
+    sizes = [int(s) for s in sizes]
+    if lo.size != hi.size or lo.size != len(sizes):
+        raise InvalidArgument("fit_grid_to_data: dimension mismatch")
+    r = stencil_radius(scheme)
+    dims = []
+    for k, m in enumerate(sizes):
+        if m < 2 * r + 2:
+            raise InvalidArgument(f"fit_grid_to_data: need at least {2 * r + 2} points per dimension")
+        if not hi[k] > lo[k]:
+            raise InvalidArgument("fit_grid_to_data: empty data range")
+        s = (hi[k] - lo[k]) / float(m - 1 - 2 * r)
+        dims.append(GridDim(lo[k] - r * s, hi[k] + r * s, m))
+    return Grid(dims)
+
+
+# ---------------------------------------------------------------- kernels
+@dataclass
+class Hyperparams:
+    noise_std: float = 1.0
+    lengthscales: Sequence[float] = field(default_factory=lambda: [1.0])
+    outputscale: float = 1.0
+
+    def __post_init__(self):
+        if not self.noise_std > 0.0:
+            raise InvalidArgument("Hyperparams: noise_std must be positive")
+        if len(self.lengthscales) == 0:
+            raise InvalidArgument("Hyperparams: need at least one lengthscale")
+        if any(not float(v) > 0.0 for v in self.lengthscales):
+            raise InvalidArgument("Hyperparams: lengthscales must be positive")
+        if not self.outputscale > 0.0:
+            raise InvalidArgument("Hyperparams: outputscale must be positive")
+
+    def dim(self) -> int:
+        return len(self.lengthscales)
+
+    def noise_variance(self) -> float:
+        return self.noise_std * self.noise_std
+
+
+@dataclass
+class KernelSpec:
+    hyper: Hyperparams
+
+
+# ---------------------------------------------------------------- interpolation weights
+def interp_weights(grid: Grid, x, scheme=InterpScheme.Cubic, ctx: Optional[Context] = None):
+    """Weights of one point: (indices, values), exact zeros dropped (interp.cpp:79-134)."""
+    idx, w, nnz, st = interp_weights_batch(grid, np.asarray(x, dtype=np.float64).reshape(1, -1), scheme, ctx)
+    if st[0] == 1:
+        raise InvalidArgument("interp_weights: point outside grid")
+    if st[0] == 2:
+        raise InvalidArgument("interp_weights: stencil leaves the grid (point too close to the boundary for the "
+                              "requested scheme)")
+    return idx[0, : nnz[0]].copy(), w[0, : nnz[0]].copy()
+
+
+def interp_weights_batch(grid: Grid, x, scheme=InterpScheme.Cubic, ctx: Optional[Context] = None):
+    """Weights of n points on the GPU: idx (n×(2r)^d), w, nnz, status (0 ok, 1 outside, 2 leaves)."""
+    ctx = ctx or default_context()
+    d = grid.dim()
+    p, n, keep = _coords(x, d)
+    width = (2 * stencil_radius(scheme)) ** d
+    idx = np.zeros((n, width), np.int64)
+    w = np.zeros((n, width), np.float64)
+    nnz = np.zeros(n, np.int32)
+    st = np.zeros(n, np.int32)
+    g = grid._c()
+    ctx.check(_L.load().gsgpc_interp_weights(ctx.handle, C.byref(g), int(scheme), C.byref(p), n,
+                                             idx.ctypes.data, w.ctypes.data, nnz.ctypes.data, st.ctypes.data))
+    return idx, w, nnz, st
+
+
+# ---------------------------------------------------------------- sufficient statistics
+class SufficientStats:
+    """Device-resident W^T W (symmetric 7^d-offset stencil), W^T y, y^T y, n."""
+
+    def __init__(self, handle, grid: Grid, scheme, ctx: Context, owner=None):
+        self._h = handle
+        self._grid = grid
+        self._scheme = InterpScheme(int(scheme))
+        self._ctx = ctx
+        self._owner = owner  # the accumulator that owns the handle, if any
+        self._wtw_count = 0
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def context(self):
+        return self._ctx
+
+    def _info(self):
+        m, n, yty, so = C.c_int64(), C.c_int64(), C.c_double(), C.c_int64()
+        pr = C.c_int32()
+        self._ctx.check(_L.load().gsgpc_stats_info(self._ctx.handle, self._h, C.byref(m), C.byref(n), C.byref(yty),
+                                                   C.byref(so), C.byref(pr)))
+        return m.value, n.value, yty.value, so.value, pr.value
+
+    def grid(self) -> Grid:
+        return self._grid
+
+    def scheme(self) -> InterpScheme:
+        return self._scheme
+
+    def grid_size(self) -> int:
+        return self._grid.num_points()
+
+    def n(self) -> int:
+        return self._info()[1]
+
+    def yty(self) -> float:
+        return self._info()[2]
+
+    def n_offsets(self) -> int:
+        return self._info()[3]
+
+    def probes(self) -> int:
+        return self._info()[4]
+
+    def wty(self, out=None):
+        out = np.zeros(self.grid_size()) if out is None else out
+        oa = _Arr(out, np.float64, writable=True)
+        self._ctx.check(_L.load().gsgpc_stats_copy_wty(self._ctx.handle, self._h, oa.vp))
+        return out
+
+    def stencil(self):
+        """(values (n_offsets × m), offsets (n_offsets × d)) of the symmetric half stencil."""
+        so = self.n_offsets()
+        vals = np.zeros((so, self.grid_size()))
+        offs = np.zeros((so, self._grid.dim()), np.int32)
+        self._ctx.check(_L.load().gsgpc_stats_copy_stencil(self._ctx.handle, self._h, vals.ctypes.data,
+                                                           offs.ctypes.data))
+        return vals, offs
+
+    def probe_images(self):
+        p = self.probes()
+        out = np.zeros((p, self.grid_size()))
+        self._ctx.check(_L.load().gsgpc_stats_copy_probe_images(self._ctx.handle, self._h, out.ctypes.data))
+        return out
+
+    def csr(self):
+        lib = _L.load()
+        nnz, mx = C.c_int64(), C.c_int64()
+        self._ctx.check(lib.gsgpc_stats_csr_nnz(self._ctx.handle, self._h, C.byref(nnz), C.byref(mx)))
+        m = self.grid_size()
+        rp = np.zeros(m + 1, np.int64)
+        col = np.zeros(nnz.value, np.int64)
+        val = np.zeros(nnz.value, np.float64)
+        self._ctx.check(lib.gsgpc_stats_export_csr(self._ctx.handle, self._h, rp.ctypes.data, col.ctypes.data,
+                                                   val.ctypes.data))
+        return rp, col, val
+
+    def wtw(self):
+        """SufficientStats::wtw() as a scipy CSR matrix (interp.hpp:129)."""
+        import scipy.sparse as sp
+
+        rp, col, val = self.csr()
+        m = self.grid_size()
+        return sp.csr_matrix((val, col, rp), shape=(m, m))
+
+    def max_row_nnz(self) -> int:
+        nnz, mx = C.c_int64(), C.c_int64()
+        self._ctx.check(_L.load().gsgpc_stats_csr_nnz(self._ctx.handle, self._h, C.byref(nnz), C.byref(mx)))
+        return mx.value
+
+    def apply_wtw(self, v, out=None):
+        m = self.grid_size()
+        va = _Arr(v, np.float64)
+        if va.shape[0] != m:
+            raise InvalidArgument("SufficientStats::apply_wtw: length mismatch")
+        out = _out_like(m, v) if out is None else out
+        oa = _Arr(out, np.float64, writable=True)
+        self._ctx.check(_L.load().gsgpc_stats_apply_wtw(self._ctx.handle, self._h, va.vp, oa.vp))
+        self._wtw_count += 1
+        return out
+
+    def matvec_count(self) -> int:
+        return self._wtw_count
+
+    def reduce_buffer(self):
+        """(device pointer, count) of the finalized [stencil|W^T y|probe images|yty|n] buffer."""
+        p, c = C.c_void_p(), C.c_int64()
+        self._ctx.check(_L.load().gsgpc_stats_reduce_buffer(self._ctx.handle, self._h, C.byref(p), C.byref(c)))
+        return int(p.value), int(c.value)
+
+    def mark_reduced(self):
+        self._ctx.check(_L.load().gsgpc_stats_mark_reduced(self._ctx.handle, self._h))
+
+    def save(self, path: str):
+        self._ctx.check(_L.load().gsgpc_stats_save(self._ctx.handle, self._h, path.encode()))
+
+    def __del__(self):
+        if self._owner is None and getattr(self, "_h", None):
+            try:
+                _L.load().gsgpc_stats_destroy(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+
+def memory_footprint(stats: SufficientStats) -> int:
+    """interp.cpp:277-284 (GSGP mode): nnz(W^T W) + 2m."""
+    rp, _, _ = stats.csr()
+    return int(rp[-1]) + 2 * stats.grid_size()
+
+
+class SufficientStatsAccumulator:
+    """interp.hpp:87-105: one-pass accumulation; ``add`` takes a batch of rows."""
+
+    def __init__(self, grid: Grid, scheme=InterpScheme.Cubic, ctx: Optional[Context] = None):
+        self._ctx = ctx or default_context()
+        self._grid = grid
+        self._scheme = InterpScheme(int(scheme))
+        h = C.c_void_p()
+        g = grid._c()
+        self._ctx.check(_L.load().gsgpc_stats_create(self._ctx.handle, C.byref(g), int(scheme), C.byref(h)))
+        self._h = h
+        self._rows = 0
+
+    def add(self, x, y=None, probe_words=None, probes: int = 0):
+        """Add rows: x (n×d) + y (n), or packed rows x (n×(d+1)) with y None."""
+        p, n, keep = _points(x, y, self._grid.dim())
+        pw = None
+        if probes:
+            pw = _Arr(probe_words, None) if (torch is not None and isinstance(probe_words, torch.Tensor)) else \
+                _Arr(np.asarray(probe_words, dtype=np.uint64), np.uint64)
+        self._ctx.check(_L.load().gsgpc_stats_add(self._ctx.handle, self._h, C.byref(p), n,
+                                                  pw.vp if pw else None, int(probes)))
+        self._rows += n
+
+    def reset(self):
+        """Back to the freshly constructed state (buffers kept)."""
+        self._ctx.check(_L.load().gsgpc_stats_reset(self._ctx.handle, self._h))
+        self._rows = 0
+
+    def merge(self, other: "SufficientStatsAccumulator"):
+        self._ctx.check(_L.load().gsgpc_stats_merge(self._ctx.handle, self._h, other._h))
+        self._rows += other._rows
+
+    def finalize(self) -> SufficientStats:
+        self._ctx.check(_L.load().gsgpc_stats_finalize(self._ctx.handle, self._h))
+        return SufficientStats(self._h, self._grid, self._scheme, self._ctx, owner=self)
+
+    def rows_seen(self) -> int:
+        return self._rows
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                _L.load().gsgpc_stats_destroy(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+
+class _OwnedStats(SufficientStats):
+    pass
+
+
+def sufficient_stats(grid: Grid, scheme, x, y=None, ctx: Optional[Context] = None) -> SufficientStats:
+    """interp.cpp:244-263: single pass over the rows (in-memory stream)."""
+    ctx = ctx or default_context()
+    p, n, keep = _points(x, y, grid.dim())
+    h = C.c_void_p()
+    g = grid._c()
+    ctx.check(_L.load().gsgpc_sufficient_stats(ctx.handle, C.byref(g), int(scheme), C.byref(p), n, C.byref(h)))
+    return SufficientStats(h, grid, scheme, ctx)
+
+
+def save_stats(path: str, stats: SufficientStats, grid: Grid = None, scheme=None):
+    if grid is not None and grid.num_points() != stats.grid_size():
+        raise InvalidArgument("save_stats: grid does not match the statistics")
+    stats.save(path)
+
+
+@dataclass
+class StatsFile:
+    grid: Grid
+    scheme: InterpScheme
+    stats: SufficientStats
+
+
+def load_stats(path: str, ctx: Optional[Context] = None) -> StatsFile:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    ctx.check(_L.load().gsgpc_stats_load(ctx.handle, path.encode(), C.byref(h)))
+    g = _L.Grid_t()
+    sch = C.c_int()
+    _L.load().gsgpc_stats_grid(h, C.byref(g), C.byref(sch))
+    grid = Grid([GridDim(g.min[k], g.max[k], g.size[k]) for k in range(g.dim)])
+    st = SufficientStats(h, grid, sch.value, ctx)
+    return StatsFile(grid, InterpScheme(sch.value), st)
+
+
+# ---------------------------------------------------------------- K_G
+class ToeplitzOperator:
+    """K_G on the grid for the SE-ARD kernel (grid.hpp:58-90)."""
+
+    def __init__(self, grid: Grid, spec: KernelSpec, ctx: Optional[Context] = None):
+        self._ctx = ctx or default_context()
+        if spec.hyper.dim() != grid.dim():
+            raise InvalidArgument("build_toeplitz_operator: kernel/grid dimension mismatch")
+        self._grid = grid
+        self._spec = spec
+        ls = np.asarray(spec.hyper.lengthscales, dtype=np.float64)
+        h = C.c_void_p()
+        g = grid._c()
+        self._ctx.check(_L.load().gsgpc_kg_create(self._ctx.handle, C.byref(g), ls.ctypes.data,
+                                                  float(spec.hyper.outputscale), float(spec.hyper.noise_std),
+                                                  C.byref(h)))
+        self._h = h
+        self._count = 0
+
+    @property
+    def handle(self):
+        return self._h
+
+    def dim(self) -> int:
+        return self._grid.num_points()
+
+    def noise_variance(self) -> float:
+        return self._spec.hyper.noise_variance()
+
+    def grid(self) -> Grid:
+        return self._grid
+
+    def apply(self, v, out=None):
+        m = self.dim()
+        va = _Arr(v, np.float64)
+        if va.shape[0] != m:
+            raise InvalidArgument("ToeplitzOperator::apply: length mismatch")
+        out = _out_like(m, v) if out is None else out
+        oa = _Arr(out, np.float64, writable=True)
+        self._ctx.check(_L.load().gsgpc_kg_apply(self._ctx.handle, self._h, va.vp, oa.vp))
+        self._count += 1
+        return out
+
+    def matvec_count(self) -> int:
+        return self._count
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                _L.load().gsgpc_kg_destroy(self._h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+
+def build_toeplitz_operator(grid: Grid, spec: KernelSpec, ctx: Optional[Context] = None) -> ToeplitzOperator:
+    return ToeplitzOperator(grid, spec, ctx)
+
+
+# ---------------------------------------------------------------- solvers
+kDefaultMaxIter = 1000
+
+
+@dataclass
+class GridRhsTolerance:
+    eps_abs: float = -1.0
+    rel_tol: float = -1.0
+
+
+@dataclass
+class GridSolveResult:
+    xhat_d: np.ndarray
+    iterations: int = 0
+    converged: bool = False
+    residual_sq: float = 0.0
+    residual_trace: np.ndarray = None
+    alphas: np.ndarray = None
+    betas: np.ndarray = None
+    loop_seconds: float = 0.0
+
+
+def factorized_cg_grid_rhs(kg: ToeplitzOperator, stats: SufficientStats, rhat0, sigma: float,
+                           tol: GridRhsTolerance, maxiter: int = kDefaultMaxIter) -> GridSolveResult:
+    """solvers.cpp:271-336 on the GPU (device-resident α, β, ρ; CUDA-graph replay)."""
+    ctx = stats.context
+    m = kg.dim()
+    ra = _Arr(rhat0, np.float64)
+    if ra.shape[0] != m:
+        raise InvalidArgument("factorized_cg_grid_rhs: dimension mismatch")
+    x = np.zeros(m)
+    tr = np.zeros(maxiter + 1)
+    al = np.zeros(max(maxiter, 1))
+    be = np.zeros(max(maxiter, 1))
+    info = _L.SolveInfo_t()
+    ctx.check(_L.load().gsgpc_factorized_cg_grid_rhs(ctx.handle, kg.handle, stats.handle, ra.vp, float(sigma),
+                                                     float(tol.eps_abs), float(tol.rel_tol), int(maxiter),
+                                                     x.ctypes.data, C.byref(info), tr.ctypes.data, al.ctypes.data,
+                                                     be.ctypes.data), info)
+    k = info.iterations
+    nb = k - 1 if info.converged else k
+    return GridSolveResult(x, k, bool(info.converged), info.residual_sq, tr[: k + 1].copy(), al[:k].copy(),
+                           be[: max(nb, 0)].copy(), info.loop_seconds)
+
+
+@dataclass
+class PosteriorModel:
+    spec: KernelSpec
+    scheme: InterpScheme
+    sigma: float
+    mean_coeffs: np.ndarray
+    kg: ToeplitzOperator
+    stats: SufficientStats
+    solve_iterations: int = 0
+    solve_residual_sq: float = 0.0
+    fit_path: str = "gsgp"
+    loop_seconds: float = 0.0
+
+    def grid(self) -> Grid:
+        return self.kg.grid()
+
+    def predict_mean(self, points, ctx: Optional[Context] = None):
+        """PosteriorModel::predict_mean (gp.cpp:309-324) for one point or a batch."""
+        ctx = ctx or self.stats.context
+        pts = np.asarray(points, dtype=np.float64) if not (torch is not None and isinstance(points, torch.Tensor)) \
+            else points
+        single = getattr(pts, "ndim", 2) == 1
+        if single:
+            pts = pts.reshape(1, -1)
+        d = self.grid().dim()
+        p, n, keep = _coords(pts, d)
+        out = np.zeros(n)
+        mc = _Arr(self.mean_coeffs, np.float64)
+        g = self.grid()._c()
+        ctx.check(_L.load().gsgpc_predict_mean(ctx.handle, C.byref(g), int(self.scheme), mc.vp, C.byref(p), n,
+                                               out.ctypes.data))
+        return float(out[0]) if single else out
+
+
+def posterior_mean_gsgp(stats: SufficientStats, kg: ToeplitzOperator, spec: KernelSpec, scheme, sigma: float,
+                        tol: float, maxiter: int = kDefaultMaxIter) -> PosteriorModel:
+    """gp.cpp:326-352."""
+    ctx = stats.context
+    m = kg.dim()
+    out = np.zeros(m)
+    info = _L.SolveInfo_t()
+    ctx.check(_L.load().gsgpc_posterior_mean_gsgp(ctx.handle, stats.handle, kg.handle, float(sigma), float(tol),
+                                                  int(maxiter), out.ctypes.data, C.byref(info)), info)
+    return PosteriorModel(spec, InterpScheme(int(scheme)), float(sigma), out, kg, stats, info.iterations,
+                          info.residual_sq, "gsgp", info.loop_seconds)
+
+
+# ---------------------------------------------------------------- Lanczos / log-likelihood
+@dataclass
+class SlqOptions:
+    max_depth: int = 100
+    quad_tol: float = 0.01
+
+
+@dataclass
+class LoglikOptions:
+    solve_tol: float = 0.01
+    probes: int = 30
+    slq: SlqOptions = field(default_factory=SlqOptions)
+    seed: int = 0
+    maxiter: int = kDefaultMaxIter
+
+
+@dataclass
+class LoglikResult:
+    loglik: float = 0.0
+    logdet_term: float = 0.0
+    quad_term: float = 0.0
+    const_term: float = 0.0
+    probes_used: int = 0
+    solver_iterations: int = 0
+    logdet_route: str = "ski-operator-slq"
+    max_depth_used: int = 0
+
+
+def factorized_lanczos_fused(kg: ToeplitzOperator, stats: SufficientStats, kgwt_z0, wt_z0, z0_sq, sigma_sq: float,
+                             k: int):
+    """Probe-batched EFLA (solvers.cpp:464-538): kgwt_z0 / wt_z0 are P×m, z0_sq P.
+    Returns (alpha P×k, beta P×k, order P)."""
+    ctx = stats.context
+    kw = np.ascontiguousarray(np.atleast_2d(kgwt_z0), dtype=np.float64)
+    w0 = np.ascontiguousarray(np.atleast_2d(wt_z0), dtype=np.float64)
+    zs = np.ascontiguousarray(np.atleast_1d(z0_sq), dtype=np.float64)
+    P = kw.shape[0]
+    alpha = np.zeros((P, k))
+    beta = np.zeros((P, k))
+    order = np.zeros(P, np.int32)
+    ctx.check(_L.load().gsgpc_factorized_lanczos_fused(ctx.handle, kg.handle, stats.handle, P, kw.ctypes.data,
+                                                       w0.ctypes.data, zs.ctypes.data, float(sigma_sq), int(k),
+                                                       alpha.ctypes.data, beta.ctypes.data, order.ctypes.data))
+    return alpha, beta, order
+
+
+def log_likelihood_gsgp(stats: SufficientStats, kg: ToeplitzOperator, sigma: float,
+                        opts: LoglikOptions = None) -> LoglikResult:
+    """gp.cpp:158-240, SkiOperator route with the probe images accumulated in the precompute."""
+    opts = opts or LoglikOptions()
+    ctx = stats.context
+    o = _L.LoglikOptions_t()
+    o.solve_tol = opts.solve_tol
+    o.probes = opts.probes
+    o.max_depth = opts.slq.max_depth
+    o.quad_tol = opts.slq.quad_tol
+    o.seed = opts.seed
+    o.maxiter = opts.maxiter
+    r = _L.LoglikResult_t()
+    ctx.check(_L.load().gsgpc_log_likelihood_gsgp(ctx.handle, stats.handle, kg.handle, float(sigma), C.byref(o),
+                                                  C.byref(r)))
+    return LoglikResult(r.loglik, r.logdet_term, r.quad_term, r.const_term, r.probes_used, r.solver_iterations,
+                        "ski-operator-slq", r.max_depth_used)

@@ -1,0 +1,165 @@
+"""Seeded synthetic stand-ins for BASELINE.json configs 1–5.
+
+The paper's sound / radar / precipitation datasets are not available here; these
+generators reproduce the shapes, sizes and value distributions BASELINE.json states
+(SURVEY.md §8(d)).  numpy versions feed the parity tests (identical arrays go to the
+oracle and to the GPU); the torch versions generate the full-size bench inputs directly
+in HBM.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+
+@dataclass
+class Config:
+    name: str
+    d: int
+    n: int
+    sizes: Tuple[int, ...]
+    lengthscales: Tuple[float, ...]
+    noise_variance: float
+    outputscale: float
+    dtype: str           # storage dtype of x and y ("f32" / "f64")
+    explicit_bounds: Optional[Tuple[Tuple[float, float], ...]] = None  # else fit_grid_to_data(0, 1)
+    tol: float = 1e-6
+
+    @property
+    def noise_std(self) -> float:
+        return float(np.sqrt(self.noise_variance))
+
+    @property
+    def m(self) -> int:
+        return int(np.prod(self.sizes))
+
+
+CONFIGS = {
+    1: Config("1d-sine", 1, 1_000_000, (1000,), (0.5,), 0.01, 1.0, "f64", ((-10.5, 10.5),)),
+    2: Config("2d-sincos", 2, 10_000_000, (256, 256), (0.05, 0.05), 0.0025, 1.0, "f32"),
+    3: Config("3d-radar-like", 3, 120_000_000, (80, 80, 20), (0.03, 0.03, 0.1), 0.01, 1.0, "f32"),
+    4: Config("2d-sweep", 2, 1_000_000, (1024, 1024), (0.05, 0.05), 1.0, 1.0, "f32"),
+    5: Config("3d-loglik", 3, 50_000_000, (64, 64, 64), (0.1, 0.1, 0.1), 0.01, 1.0, "f64"),
+}
+
+
+def grid_for(cfg: Config, scheme=1):
+    from .gsgp import Grid, GridDim, fit_grid_to_data
+
+    if cfg.explicit_bounds is not None:
+        return Grid([GridDim(lo, hi, s) for (lo, hi), s in zip(cfg.explicit_bounds, cfg.sizes)])
+    return fit_grid_to_data(np.zeros(cfg.d), np.ones(cfg.d), cfg.sizes, scheme)
+
+
+def kernel_for(cfg: Config):
+    from .gsgp import Hyperparams, KernelSpec
+
+    return KernelSpec(Hyperparams(cfg.noise_std, list(cfg.lengthscales), cfg.outputscale))
+
+
+# ---------------------------------------------------------------- numpy generators
+def _radar_params(rng):
+    centres = rng.random((20, 2))
+    bump_c = rng.random((50, 3))
+    bump_w = rng.uniform(0.05, 0.2, 50)
+    bump_a = rng.standard_normal(50)
+    return centres, bump_c, bump_w, bump_a
+
+
+def _rff_params(rng, d=3, nf=100, ls=0.1):
+    omega = rng.standard_normal((nf, d)) / ls
+    phase = rng.uniform(0.0, 2.0 * np.pi, nf)
+    amp = rng.standard_normal(nf)
+    return omega, phase, amp
+
+
+def generate(cfg_id: int, n: Optional[int] = None, seed: Optional[int] = None):
+    """Rows of config `cfg_id` as numpy (x (n×d), y (n)) in the config's storage dtype."""
+    cfg = CONFIGS[cfg_id]
+    n = cfg.n if n is None else int(n)
+    rng = np.random.default_rng(2101 + cfg_id if seed is None else seed)
+    if cfg_id == 1:
+        x = rng.uniform(-10.0, 10.0, (n, 1))
+        y = np.sin(x[:, 0]) + 0.1 * rng.standard_normal(n)
+    elif cfg_id == 2:
+        x = rng.random((n, 2))
+        y = np.sin(2 * np.pi * x[:, 0]) * np.cos(2 * np.pi * x[:, 1]) + 0.05 * rng.standard_normal(n)
+    elif cfg_id == 3:
+        centres, bc, bw, ba = _radar_params(np.random.default_rng(3101))
+        comp = rng.integers(0, 20, n)
+        x12 = np.clip(centres[comp] + 0.08 * rng.standard_normal((n, 2)), 0.0, 1.0)
+        x3 = rng.beta(2.0, 5.0, n)
+        x = np.column_stack([x12, x3])
+        y = np.zeros(n)
+        for j in range(50):
+            r2 = ((x - bc[j]) ** 2).sum(axis=1)
+            y += ba[j] * np.exp(-r2 / (2.0 * bw[j] ** 2))
+        y += 0.1 * rng.standard_normal(n)
+    elif cfg_id == 4:
+        x = rng.random((n, 2))
+        y = rng.standard_normal(n)
+    elif cfg_id == 5:
+        om, ph, am = _rff_params(np.random.default_rng(5101))
+        x = rng.random((n, 3))
+        y = np.sqrt(2.0 / om.shape[0]) * (np.cos(x @ om.T + ph) @ am) + 0.1 * rng.standard_normal(n)
+    else:
+        raise ValueError(cfg_id)
+    if cfg.dtype == "f32":
+        return x.astype(np.float32), y.astype(np.float32)
+    return x.astype(np.float64), y.astype(np.float64)
+
+
+# ---------------------------------------------------------------- torch (device) generators
+def generate_torch(cfg_id: int, n: Optional[int] = None, device="cuda", seed: int = 0, packed: bool = True,
+                   chunk: int = 1 << 24):
+    """Full-size rows generated on `device`; packed → (n, d+1) rows (x..., y)."""
+    import torch
+
+    cfg = CONFIGS[cfg_id]
+    n = cfg.n if n is None else int(n)
+    dt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(7919 * cfg_id + seed)
+    out = torch.empty((n, cfg.d + 1), dtype=dt, device=device)
+    if cfg_id == 3:
+        centres, bc, bw, ba = (torch.as_tensor(a, device=device, dtype=torch.float64)
+                               for a in _radar_params(np.random.default_rng(3101)))
+    if cfg_id == 5:
+        om, ph, am = (torch.as_tensor(a, device=device, dtype=torch.float64)
+                      for a in _rff_params(np.random.default_rng(5101)))
+    for s in range(0, n, chunk):
+        k = min(chunk, n - s)
+        if cfg_id == 1:
+            x = torch.rand((k, 1), generator=g, device=device, dtype=torch.float64) * 20.0 - 10.0
+            y = torch.sin(x[:, 0]) + 0.1 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
+        elif cfg_id == 2:
+            x = torch.rand((k, 2), generator=g, device=device, dtype=torch.float64)
+            y = torch.sin(2 * np.pi * x[:, 0]) * torch.cos(2 * np.pi * x[:, 1]) + \
+                0.05 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
+        elif cfg_id == 3:
+            comp = torch.randint(0, 20, (k,), generator=g, device=device)
+            x12 = (centres[comp] + 0.08 * torch.randn((k, 2), generator=g, device=device,
+                                                       dtype=torch.float64)).clamp_(0.0, 1.0)
+            # Beta(2,5) via the order-statistic construction: the 2nd smallest of 6 uniforms
+            u = torch.rand((k, 6), generator=g, device=device, dtype=torch.float64)
+            x3 = u.kthvalue(2, dim=1).values
+            x = torch.cat([x12, x3[:, None]], dim=1)
+            y = torch.zeros(k, device=device, dtype=torch.float64)
+            for j in range(50):
+                r2 = ((x - bc[j]) ** 2).sum(dim=1)
+                y += ba[j] * torch.exp(-r2 / (2.0 * bw[j] ** 2))
+            y += 0.1 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
+        elif cfg_id == 4:
+            x = torch.rand((k, 2), generator=g, device=device, dtype=torch.float64)
+            y = torch.randn(k, generator=g, device=device, dtype=torch.float64)
+        elif cfg_id == 5:
+            x = torch.rand((k, 3), generator=g, device=device, dtype=torch.float64)
+            y = np.sqrt(2.0 / om.shape[0]) * (torch.cos(x @ om.T + ph) @ am) + \
+                0.1 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
+        out[s:s + k, : cfg.d] = x.to(dt)
+        out[s:s + k, cfg.d] = y.to(dt)
+    if packed:
+        return out
+    return out[:, : cfg.d].contiguous(), out[:, cfg.d].contiguous()

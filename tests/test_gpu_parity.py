@@ -1,0 +1,309 @@
+"""GPU parity: libgsgpc (sm_100a) against the CPU oracle and the golden fixtures.
+
+Tolerances: stencil indices and weights bit-exact; W^T W, W^T y
+≤ 1e-10 relative (normwise and entrywise against the diagonal scale); yty ≤ 1e-12;
+n exact; K_G v ≤ 1e-10; posterior mean / predictions ≤ 1e-5; CG iterations ±1.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2101_11751_b200 as G
+from helpers import csr_to_half_stencil, half_offsets, rel_err
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def ogrid(g):
+    return O.Grid([g.min(k) for k in range(g.dim())], [g.max(k) for k in range(g.dim())],
+                  [g.size(k) for k in range(g.dim())])
+
+
+def points(d, n, seed, dtype=np.float64, edge=True):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    if edge and n > 20:
+        x[:4] = 0.0
+        x[4:8] = 1.0
+        x[8:12, 0] = 0.5
+    y = np.cos(4 * x).sum(axis=1) + 0.1 * rng.standard_normal(n)
+    return x.astype(dtype), y.astype(dtype)
+
+
+def compare_stats(gs, os_, W, sizes, tol=1e-10):
+    vals, offs = gs.stencil()
+    assert np.array_equal(offs, half_offsets(len(sizes), W))
+    rp, col, val, wty = os_.csr()
+    ref = csr_to_half_stencil(rp, col, val, sizes, W)
+    diag = np.abs(ref[0]).max()
+    err = np.abs(vals - ref)
+    assert err.max() <= tol * max(diag, 1e-300), (err.max(), diag)
+    assert rel_err(gs.wty(), wty) <= tol
+    assert abs(gs.yty() - os_.yty) <= 1e-12 * max(os_.yty, 1e-300)
+    assert gs.n() == os_.n
+
+
+CASES = [
+    (1, G.InterpScheme.Cubic, np.float64, (37,), 5000),
+    (1, G.InterpScheme.Linear, np.float32, (37,), 5000),
+    (2, G.InterpScheme.Cubic, np.float32, (23, 17), 20000),
+    (2, G.InterpScheme.Linear, np.float64, (23, 17), 20000),
+    (3, G.InterpScheme.Cubic, np.float32, (11, 9, 8), 6000),
+    (3, G.InterpScheme.Cubic, np.float64, (9, 10, 7), 6000),
+    (3, G.InterpScheme.Linear, np.float32, (11, 9, 8), 6000),
+]
+
+
+@pytest.mark.parametrize("d,scheme,dtype,sizes,n", CASES)
+def test_precompute_matches_oracle(d, scheme, dtype, sizes, n):
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes, scheme)
+    og = O.fit_grid_to_data(np.zeros(d), np.ones(d), sizes, int(scheme))
+    assert np.array_equal(og.mins, [g.min(k) for k in range(d)])
+    x, y = points(d, n, 100 + d)
+    x, y = x.astype(dtype), y.astype(dtype)
+    gs = G.sufficient_stats(g, scheme, x, y)
+    os_ = O.sufficient_stats(og, x, y, scheme=int(scheme), nthreads=4)
+    compare_stats(gs, os_, 4 if scheme == G.InterpScheme.Cubic else 2, sizes)
+    # CSR export = SufficientStats::wtw() structure
+    rp, col, val = gs.csr()
+    orp, ocol, oval, _ = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert rel_err(val, oval) <= 1e-10
+    assert gs.max_row_nnz() == os_.max_row_nnz() <= (7 if scheme == G.InterpScheme.Cubic else 3) ** d
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_interp_weights_bit_exact(d):
+    sizes = (13, 11, 9)[:d]
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    og = ogrid(g)
+    rng = np.random.default_rng(d)
+    x = rng.random((400, d))
+    x[:10] = 0.0
+    x[10:20] = 1.0
+    # points exactly on nodes and within the snap tolerance of nodes
+    nodes = np.array([[g.min(k) + 3 * g.spacing(k) for k in range(d)]])
+    x[20:25] = nodes
+    x[25:30] = nodes + 1e-12
+    for scheme in (G.InterpScheme.Cubic, G.InterpScheme.Linear):
+        idx, w, nnz, st = G.interp_weights_batch(g, x, scheme)
+        for i in range(x.shape[0]):
+            oi, ow = O.interp_weights(og, x[i], scheme=int(scheme))
+            assert st[i] == 0
+            assert nnz[i] == len(oi)
+            assert np.array_equal(idx[i, : nnz[i]], oi)
+            assert np.array_equal(w[i, : nnz[i]], ow), (i, x[i])
+
+
+def test_out_of_grid_errors_report_first_row():
+    g = G.Grid([G.GridDim(0.0, 10.0, 11)])
+    x = np.array([[2.0], [3.3], [0.5], [11.0], [-1.0]] + [[5.0]] * 10)
+    y = np.ones(x.shape[0])
+    with pytest.raises(G.InvalidArgument) as e:
+        G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    assert e.value.row == 3
+    assert "stream row 3" in str(e.value) and "leaves the grid" in str(e.value)
+    x[2] = 2.0
+    with pytest.raises(G.InvalidArgument) as e:
+        G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    assert e.value.row == 4 and "outside grid" in str(e.value)
+    # a failed batch leaves the accumulator unchanged
+    acc = G.SufficientStatsAccumulator(g, G.InterpScheme.Cubic)
+    acc.add(np.array([[2.0], [3.0]]), np.array([1.0, 2.0]))
+    with pytest.raises(G.InvalidArgument):
+        acc.add(x, y)
+    st = acc.finalize()
+    assert st.n() == 2 and st.yty() == 5.0
+
+
+def test_nan_rows_count_but_do_not_interpolate():
+    g = G.Grid([G.GridDim(0.0, 10.0, 11), G.GridDim(0.0, 1.0, 6)])
+    x = np.array([[2.5, 0.5], [np.nan, 0.5], [3.5, 0.4]])
+    y = np.array([1.0, 2.0, 3.0])
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(ogrid(g), x, y)
+    assert gs.n() == 3 and os_.n == 3
+    compare_stats(gs, os_, 4, (11, 6))
+
+
+def test_empty_stream():
+    g = G.fit_grid_to_data([0.0], [1.0], [16])
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, np.zeros((0, 1)), np.zeros(0))
+    assert gs.n() == 0 and gs.yty() == 0.0
+    assert np.all(gs.stencil()[0] == 0.0) and np.all(gs.wty() == 0.0)
+
+
+def test_batches_merge_and_devices():
+    import torch
+
+    d, sizes = 2, (31, 29)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    x, y = points(d, 30000, 7)
+    full = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    acc = G.SufficientStatsAccumulator(g)
+    acc.add(x[:10000], y[:10000])
+    acc.add(torch.as_tensor(x[10000:20000]).cuda(), torch.as_tensor(y[10000:20000]).cuda())  # device rows
+    other = G.SufficientStatsAccumulator(g)
+    other.add(np.column_stack([x[20000:], y[20000:]]))  # packed (x, y) host rows
+    acc.merge(other)
+    st = acc.finalize()
+    assert st.n() == 30000
+    v0, _ = full.stencil()
+    v1, _ = st.stencil()
+    assert rel_err(v1, v0) <= 1e-12
+    assert rel_err(st.wty(), full.wty()) <= 1e-12
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_operators_match_oracle(d):
+    sizes = (40, 23, 12)[:d]
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    og = ogrid(g)
+    x, y = points(d, 20000, 3 + d)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(og, x, y, nthreads=4)
+    v = np.random.default_rng(0).standard_normal(g.num_points())
+    assert rel_err(gs.apply_wtw(v), os_.apply_wtw(v)) <= 1e-10
+    spec = G.KernelSpec(G.Hyperparams(0.1, [0.2, 0.15, 0.3][:d], 1.7))
+    kg = G.ToeplitzOperator(g, spec)
+    okg = O.ToeplitzOperator(og, [0.2, 0.15, 0.3][:d], 1.7, 0.1)
+    assert rel_err(kg.apply(v), okg.apply(v)) <= 1e-10
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_efcg_and_posterior_mean_match_oracle(d):
+    sizes = (60, 24, 10)[:d]
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    og = ogrid(g)
+    x, y = points(d, 30000, 40 + d)
+    ls = [0.1, 0.12, 0.2][:d]
+    sigma = 0.1
+    spec = G.KernelSpec(G.Hyperparams(sigma, ls, 1.0))
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(og, x, y, nthreads=4)
+    kg = G.ToeplitzOperator(g, spec)
+    okg = O.ToeplitzOperator(og, ls, 1.0, sigma)
+    r0 = -okg.apply(os_.wty) / (sigma * sigma)
+    ores = O.factorized_cg_grid_rhs(okg, os_, r0, sigma, eps_abs=1e-12 * os_.yty, maxiter=2000)
+    gres = G.factorized_cg_grid_rhs(kg, gs, r0, sigma, G.GridRhsTolerance(eps_abs=1e-12 * os_.yty), 2000)
+    assert ores.converged and gres.converged
+    assert abs(gres.iterations - ores.iterations) <= 1
+    assert rel_err(gres.xhat_d, ores.xhat_d) <= 1e-5
+    k = min(gres.iterations, ores.iterations)
+    assert rel_err(gres.alphas[: min(k, 5)], ores.alphas[: min(k, 5)]) <= 1e-8
+    mc, it, _ = O.posterior_mean_gsgp(okg, os_, sigma, 1e-6, 2000)
+    model = G.posterior_mean_gsgp(gs, kg, spec, G.InterpScheme.Cubic, sigma, 1e-6, 2000)
+    assert abs(model.solve_iterations - it) <= 1
+    assert rel_err(model.mean_coeffs, mc) <= 1e-5
+    tp = np.random.default_rng(9).random((500, d)) * 0.98 + 0.01
+    assert rel_err(model.predict_mean(tp), O.predict_mean(og, mc, tp)) <= 1e-5
+
+
+def test_predict_mean_bit_exact_given_coeffs():
+    d, sizes = 3, (12, 10, 9)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    coeffs = np.random.default_rng(4).standard_normal(g.num_points())
+    tp = np.random.default_rng(5).random((300, d))
+    spec = G.KernelSpec(G.Hyperparams(0.1, [0.2] * 3, 1.0))
+    model = G.PosteriorModel(spec, G.InterpScheme.Cubic, 0.1, coeffs, G.ToeplitzOperator(g, spec), None)
+    out = model.predict_mean(tp, ctx=G.default_context())
+    assert np.array_equal(out, O.predict_mean(ogrid(g), coeffs, tp))
+
+
+def test_breakdown_and_nonconvergence():
+    g = G.fit_grid_to_data([0.0], [1.0], [50])
+    x, y = points(1, 2000, 77)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    spec = G.KernelSpec(G.Hyperparams(0.01, [0.05], 1.0))
+    kg = G.ToeplitzOperator(g, spec)
+    with pytest.raises(G.SolverNonConvergence) as e:
+        G.posterior_mean_gsgp(gs, kg, spec, G.InterpScheme.Cubic, 0.01, 1e-14, 3)
+    assert e.value.iterations == 3
+    r0 = np.zeros(g.num_points())
+    res = G.factorized_cg_grid_rhs(kg, gs, r0, 0.01, G.GridRhsTolerance(eps_abs=0.0), 10)
+    assert res.converged and res.iterations == 0  # r̂0 = 0 → x̂_d = 0 in 0 iterations
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_golden_dense_truth(d):
+    z = np.load(os.path.join(GOLD, f"small_{d}d.npz"))
+    g = G.Grid([G.GridDim(a, b, int(s)) for a, b, s in zip(z["mins"], z["maxs"], z["sizes"])])
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, z["x"], z["y"])
+    assert rel_err(gs.wtw().toarray(), z["wtw"]) <= 1e-12
+    assert rel_err(gs.wty(), z["wty"]) <= 1e-12
+    spec = G.KernelSpec(G.Hyperparams(float(z["noise_std"]), list(z["lengthscales"]), float(z["outputscale"])))
+    kg = G.ToeplitzOperator(g, spec)
+    assert rel_err(kg.apply(z["v"]), z["Kv"]) <= 1e-10
+    model = G.posterior_mean_gsgp(gs, kg, spec, G.InterpScheme.Cubic, float(z["noise_std"]), 1e-10, 5000)
+    assert rel_err(model.mean_coeffs, z["mean_coeffs"]) <= 1e-6
+    assert rel_err(model.predict_mean(z["test_pts"]), z["pred"]) <= 1e-6
+
+
+def test_stats_file_roundtrip(tmp_path):
+    d, sizes = 2, (20, 18)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    x, y = points(d, 5000, 8)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    p = str(tmp_path / "s.gsgpsst")
+    G.save_stats(p, gs, g)
+    sf = G.load_stats(p)
+    assert sf.grid == g and sf.scheme == G.InterpScheme.Cubic
+    assert sf.stats.n() == 5000 and sf.stats.yty() == gs.yty()
+    assert np.array_equal(sf.stats.stencil()[0], gs.stencil()[0])
+    assert np.array_equal(sf.stats.wty(), gs.wty())
+    # a file laid out exactly as the reference's save_stats writes it (io.cpp:192-221)
+    os_ = O.sufficient_stats(ogrid(g), x, y)
+    rp, col, val, wty = os_.csr()
+    q = str(tmp_path / "ref.gsgpsst")
+    with open(q, "wb") as f:
+        f.write(b"GSGPSST1")
+        hdr = [np.uint64(d)]
+        f.write(np.array(hdr, np.uint64).tobytes())
+        for k in range(d):
+            f.write(np.array([g.min(k), g.max(k)], np.float64).tobytes())
+            f.write(np.array([g.size(k)], np.uint64).tobytes())
+        f.write(np.array([1, g.num_points(), os_.n, len(val)], np.uint64).tobytes())
+        f.write(np.array([os_.yty], np.float64).tobytes())
+        f.write(wty.tobytes())
+        rows = np.repeat(np.arange(g.num_points()), np.diff(rp))
+        trip = np.zeros(len(val), dtype=[("r", "<u8"), ("c", "<u8"), ("v", "<f8")])
+        trip["r"], trip["c"], trip["v"] = rows, col, val
+        f.write(trip.tobytes())
+    sr = G.load_stats(q)
+    ref = csr_to_half_stencil(rp, col, val, sizes, 4)
+    assert np.array_equal(sr.stats.stencil()[0], ref)
+    v = np.random.default_rng(1).standard_normal(g.num_points())
+    assert rel_err(sr.stats.apply_wtw(v), os_.apply_wtw(v)) <= 1e-12
+
+
+def test_full_size_config3_properties():
+    """Config 3 at full n = 1.2e8 (size-independent invariants): partition of unity
+    Σ_ab (W^T W)_ab = n, Σ_a (W^T y)_a = Σ y, and batch-split invariance."""
+    import torch
+
+    from paper_2101_11751_b200 import synthetic as S
+
+    cfg = S.CONFIGS[3]
+    rows = S.generate_torch(3, device="cuda")
+    g = S.grid_for(cfg)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, rows)
+    n = rows.shape[0]
+    assert gs.n() == n
+    vals, offs = gs.stencil()
+    total = vals[0].sum() + 2.0 * vals[1:].sum()
+    assert abs(total - n) <= 1e-9 * n
+    ysum = rows[:, 3].double().sum().item()
+    assert abs(gs.wty().sum() - ysum) <= 1e-9 * max(abs(ysum), 1.0) + 1e-6
+    yty = (rows[:, 3].double() ** 2).sum().item()
+    assert abs(gs.yty() - yty) <= 1e-10 * yty
+    acc = G.SufficientStatsAccumulator(g)
+    h = n // 3
+    acc.add(rows[:h])
+    acc.add(rows[h:])
+    st2 = acc.finalize()
+    assert rel_err(st2.stencil()[0], vals) <= 1e-10
+    del rows
+    torch.cuda.empty_cache()
