@@ -121,6 +121,12 @@ void gsgpc_stats_destroy(gsgpc_stats* stats);
  * used by the factorized SLQ (gp.cpp:97-99); pass NULL / 0 otherwise. */
 gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* stats, const gsgpc_points* pts,
                              int64_t n, const uint64_t* probe_words, int probes);
+/* Accumulate probe images of the reference's Rademacher probes (rademacher_probe,
+ * gp.cpp:16-25: std::seed_seq{seed_lo, seed_hi, p_lo, p_hi} + std::mt19937_64, one draw per
+ * row in stream order) for p = 0..probes-1 in every following gsgpc_stats_add; the library
+ * generates the streams itself (host threads), continuing across batches.  Call before the
+ * first row is added.  probes <= 64. */
+gsgpc_status gsgpc_stats_enable_probes(gsgpc_ctx* ctx, gsgpc_stats* stats, int probes, uint64_t seed);
 /* Reset an accumulator to the freshly constructed state (no rows), keeping its buffers —
  * equivalent to constructing a new SufficientStatsAccumulator on the same grid. */
 gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* stats);

@@ -11,6 +11,8 @@
 #include <fstream>
 #include <map>
 #include <memory>
+#include <random>
+#include <thread>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -119,6 +121,10 @@ struct gsgpc_stats {
   int64_t n = 0;
   bool finalized = false;
   bool reduced = false;
+  // seeded Rademacher probes (gsgpc_stats_enable_probes): one generator per probe
+  bool probe_seeded = false;
+  uint64_t probe_seed = 0;
+  std::vector<std::mt19937_64> gens;
   int64_t fin_count() const { return static_cast<int64_t>(S_min) * g.m + g.m + static_cast<int64_t>(probes) * g.m + 2; }
   double* stencil() const { return fin.as<double>(); }
   double* wty() const { return fin.as<double>() + static_cast<int64_t>(S_min) * g.m; }
@@ -511,6 +517,34 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   s->finalized = false;
 }
 
+// Draw the next `rows` values of every probe stream and pack them (bit p of word i = probe p
+// is +1 at row i), then upload to the "probe_stage" device buffer.
+void gen_probe_words(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t rows) {
+  const int P = s->probes;
+  std::vector<uint64_t> words(rows, 0ull);
+  std::vector<std::vector<uint8_t>> bits(P);
+  auto work = [&](int p) {
+    bits[p].assign(rows, 0);
+    std::mt19937_64& g = s->gens[p];
+    for (int64_t i = 0; i < rows; ++i) bits[p][i] = static_cast<uint8_t>(g() & 1ull);
+  };
+  const int nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), static_cast<unsigned>(P)));
+  for (int p0 = 0; p0 < P; p0 += nt) {
+    std::vector<std::thread> th;
+    for (int p = p0; p < std::min(P, p0 + nt); ++p) th.emplace_back(work, p);
+    for (auto& t : th) t.join();
+  }
+  for (int p = 0; p < P; ++p) {
+    const uint64_t bit = 1ull << p;
+    const uint8_t* b = bits[p].data();
+    for (int64_t i = 0; i < rows; ++i) words[i] |= b[i] ? bit : 0ull;
+  }
+  DBuf& st = ctx->buf("probe_stage");
+  st.ensure(sizeof(uint64_t) * rows);
+  GSGPC_CUDA(cudaMemcpyAsync(st.p, words.data(), sizeof(uint64_t) * rows, cudaMemcpyHostToDevice, ctx->stream));
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -671,7 +705,11 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
     if (s->reduced) invalid("SufficientStatsAccumulator::add: statistics were all-reduced; create a new accumulator");
     check_points(pts, n, true);
     if (probes < 0 || probes > 64) throw Error(GSGPC_UNSUPPORTED, "probes must be in [0, 64]");
-    if (probes > 0 && !probe_words) invalid("probe words are NULL");
+    if (s->probe_seeded) {
+      if (probe_words) invalid("this accumulator generates its probes (gsgpc_stats_enable_probes)");
+      probes = s->probes;
+    }
+    if (probes > 0 && !probe_words && !s->probe_seeded) invalid("probe words are NULL");
     if (probes > 0) {
       if (s->probes == 0) {
         if (s->n > 0) invalid("probes must be supplied from the first row on");
@@ -687,6 +725,7 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
     if (n == 0) return;
     const bool dev = is_device_ptr(pts->x);
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
+    const std::vector<std::mt19937_64> gens_backup = s->gens;  // restored if a batch fails
     const bool pw_dev = nw ? is_device_ptr(probe_words) : true;
     const int64_t CH = dev ? (int64_t{1} << 27) : (int64_t{1} << 24);
     for (int64_t r0 = 0; r0 < n; r0 += CH) {
@@ -701,7 +740,10 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
         pt.end(h);
       }
       const uint64_t* pw = nullptr;
-      if (nw) {
+      if (s->probe_seeded && !probe_words) {
+        gen_probe_words(ctx, s, r1 - r0);
+        pw = ctx->buf("probe_stage").as<uint64_t>();
+      } else if (nw) {
         if (pw_dev) {
           pw = probe_words + r0 * nw;
         } else {
@@ -712,8 +754,34 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
           pw = b.as<uint64_t>();
         }
       }
-      add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
+      try {
+        add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
+      } catch (...) {
+        s->gens = gens_backup;
+        throw;
+      }
     }
+  });
+}
+
+gsgpc_status gsgpc_stats_enable_probes(gsgpc_ctx* ctx, gsgpc_stats* s, int probes, uint64_t seed) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    if (probes < 1 || probes > 64) throw Error(GSGPC_UNSUPPORTED, "probes must be in [1, 64]");
+    if (s->n > 0 || s->probes > 0) invalid("gsgpc_stats_enable_probes: call before the first row is added");
+    s->probes = probes;
+    s->probe_seeded = true;
+    s->probe_seed = seed;
+    s->gens.clear();
+    for (int p = 0; p < probes; ++p) {
+      // rademacher_probe (gp.cpp:16-25)
+      std::seed_seq seq{static_cast<std::uint32_t>(seed), static_cast<std::uint32_t>(seed >> 32),
+                        static_cast<std::uint32_t>(static_cast<uint64_t>(p)),
+                        static_cast<std::uint32_t>(static_cast<uint64_t>(p) >> 32)};
+      s->gens.emplace_back(seq);
+    }
+    s->pmom.ensure(sizeof(double) * s->g.cells * probes * s->QY);
+    GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * probes * s->QY, ctx->stream));
   });
 }
 
@@ -1387,4 +1455,122 @@ gsgpc_status gsgpc_predict_mean(gsgpc_ctx* ctx, const gsgpc_grid* grid, int sche
 }  // extern "C"
 
 // ---------------------------------------------------------------- EFLA / log-likelihood
-// (implemented in efla.cu)
+extern "C" {
+
+gsgpc_status gsgpc_factorized_lanczos_fused(gsgpc_ctx* ctx, gsgpc_kg* kg, gsgpc_stats* s, int probes,
+                                            const double* kgwt_z0, const double* wt_z0, const double* z0_sq,
+                                            double sigma_sq, int k, double* alpha, double* beta, int32_t* order) {
+  return guard(ctx, [&] {
+    if (!kg || !s || !alpha || !beta || !order || !z0_sq) invalid("NULL argument");
+    if (probes < 1) invalid("factorized_lanczos_fused: need at least one start vector");
+    if (k < 1) invalid("factorized_lanczos_fused: bad k");
+    finalize_stats(ctx, s);
+    const int64_t m = s->g.m;
+    if (kg->m != m) invalid("factorized_lanczos_fused: dimension mismatch");
+    std::vector<double> zs(probes);
+    copy_out(ctx, zs.data(), z0_sq, sizeof(double) * probes);
+    for (double v : zs) {
+      if (!(v > 0.0)) invalid("factorized_lanczos_fused: start vector is zero");
+    }
+    const double* kw = dev_in(ctx, kgwt_z0, static_cast<int64_t>(probes) * m, "efla_kw");
+    const double* w0 = dev_in(ctx, wt_z0, static_cast<int64_t>(probes) * m, "efla_w0");
+    DBuf& zd = ctx->buf("efla_z0");
+    zd.ensure(sizeof(double) * probes);
+    GSGPC_CUDA(cudaMemcpyAsync(zd.p, zs.data(), sizeof(double) * probes, cudaMemcpyHostToDevice, ctx->stream));
+    const StencilDesc sd = stencil_desc(s);
+    for (int p0 = 0; p0 < probes; p0 += 32) {
+      const int P = std::min(32, probes - p0);
+      const EflaOut o = efla_run(ctx->L(), sd, s->stencil(), kg->dev, P, kw + static_cast<int64_t>(p0) * m,
+                                 w0 + static_cast<int64_t>(p0) * m, zd.as<double>() + p0, sigma_sq, k);
+      std::vector<double> ha(o.alpha), hb(o.beta);
+      std::vector<int32_t> ho(o.order.begin(), o.order.end());
+      copy_out(ctx, alpha + static_cast<int64_t>(p0) * k, ha.data(), sizeof(double) * P * k);
+      copy_out(ctx, beta + static_cast<int64_t>(p0) * k, hb.data(), sizeof(double) * P * k);
+      copy_out(ctx, order + p0, ho.data(), sizeof(int32_t) * P);
+    }
+  });
+}
+
+gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, double sigma,
+                                       const gsgpc_loglik_options* opts, gsgpc_loglik_result* out) {
+  return guard(ctx, [&] {
+    if (!s || !kg || !opts || !out) invalid("NULL argument");
+    finalize_stats(ctx, s);
+    const int64_t m = s->g.m;
+    if (kg->m != m) invalid("log_likelihood_gsgp: kernel/grid size mismatch");
+    const int P = opts->probes;
+    if (P < 1) invalid("slq_logdet_ski_factorized: need at least one probe");
+    if (s->probes < P) {
+      invalid("log_likelihood_gsgp: the SkiOperator logdet route needs probe images W^T v_p accumulated in the "
+              "precompute (gsgpc_stats_enable_probes)");
+    }
+    if (s->probe_seeded && s->probe_seed != opts->seed) {
+      invalid("log_likelihood_gsgp: probe images were accumulated with seed " + std::to_string(s->probe_seed));
+    }
+    const Launch L = ctx->L();
+    const double n = static_cast<double>(s->reduced ? static_cast<int64_t>(read_scalar(ctx, s->tail() + 1)) : s->n);
+    const double sigma_sq = sigma * sigma;
+    const double yty = stats_yty(ctx, s);
+    // quadratic term (gp.cpp:166-178)
+    DBuf& t0 = ctx->buf("ll_t0");
+    DBuf& t1 = ctx->buf("ll_t1");
+    DBuf& kw = ctx->buf("ll_kw");
+    DBuf& r0 = ctx->buf("ll_r0");
+    DBuf& xd = ctx->buf("ll_x");
+    for (DBuf* b : {&t0, &t1, &kw, &r0, &xd}) b->ensure(sizeof(double) * m);
+    run_kg_apply(L, kg->dev, s->wty(), kw.as<double>(), t0.as<double>(), t1.as<double>());
+    run_add_div(L, m, nullptr, 0.0, kw.as<double>(), -sigma_sq, r0.as<double>());
+    const double eps_abs = opts->solve_tol * opts->solve_tol * yty;
+    const CgOutcome cg = run_efcg(ctx, s, kg, r0.as<double>(), sigma, eps_abs, -1.0, opts->maxiter, xd.as<double>(),
+                                  nullptr, nullptr, nullptr);
+    if (!cg.converged) throw Error(GSGPC_NONCONVERGENCE, "log_likelihood_gsgp: mean solve did not converge");
+    run_add_div(L, m, xd.as<double>(), 1.0, s->wty(), sigma_sq, r0.as<double>());
+    run_kg_apply(L, kg->dev, r0.as<double>(), kw.as<double>(), t0.as<double>(), t1.as<double>());
+    std::vector<double> hw(m), hz(m);
+    copy_out(ctx, hw.data(), s->wty(), sizeof(double) * m);
+    copy_out(ctx, hz.data(), kw.p, sizeof(double) * m);
+    double wz = 0.0;
+    for (int64_t i = 0; i < m; ++i) wz += hw[i] * hz[i];
+    const double quad = (yty - wz) / sigma_sq;
+    // SLQ over the probe images (gp.cpp:85-111)
+    const int depth = static_cast<int>(std::min<double>(opts->max_depth, n));
+    if (depth < 1) invalid("slq: need at least one Lanczos step");
+    DBuf& kwt = ctx->buf("ll_kwt");
+    DBuf& kt0 = ctx->buf("ll_kt0");
+    DBuf& kt1 = ctx->buf("ll_kt1");
+    kwt.ensure(sizeof(double) * P * m);
+    kt0.ensure(sizeof(double) * P * m);
+    kt1.ensure(sizeof(double) * P * m);
+    run_kg_batched(L, kg->dev, P, s->pimg(), kwt.as<double>(), kt0.as<double>(), kt1.as<double>());
+    DBuf& zd = ctx->buf("ll_z0");
+    zd.ensure(sizeof(double) * P);
+    std::vector<double> zs(P, n);  // v·v = n for ±1 probes
+    GSGPC_CUDA(cudaMemcpyAsync(zd.p, zs.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+    const StencilDesc sd = stencil_desc(s);
+    double total = 0.0;
+    int max_used = 0;
+    for (int p0 = 0; p0 < P; p0 += 32) {
+      const int Pb = std::min(32, P - p0);
+      const EflaOut o = efla_run(L, sd, s->stencil(), kg->dev, Pb, kwt.as<double>() + static_cast<int64_t>(p0) * m,
+                                 s->pimg() + static_cast<int64_t>(p0) * m, zd.as<double>() + p0, sigma_sq, depth);
+      for (int p = 0; p < Pb; ++p) {
+        const auto q = quadrature_logdet_host(o.alpha.data() + static_cast<size_t>(p) * depth,
+                                              o.beta.data() + static_cast<size_t>(p) * depth, o.order[p], n,
+                                              opts->quad_tol);
+        total += q.first;
+        max_used = std::max(max_used, q.second);
+      }
+    }
+    const double slq = total / P;
+    const double kLog2Pi = 1.8378770664093453;
+    out->logdet_term = slq - (n - static_cast<double>(m)) * std::log(sigma_sq);
+    out->quad_term = quad;
+    out->const_term = n * kLog2Pi + (n - static_cast<double>(m)) * std::log(sigma_sq);
+    out->loglik = -0.5 * (out->logdet_term + out->quad_term + out->const_term);
+    out->probes_used = P;
+    out->solver_iterations = cg.iterations;
+    out->max_depth_used = max_used;
+  });
+}
+
+}  // extern "C"

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+#include <vector>
+
 #include "internal.cuh"
 
 namespace gsgpc {
@@ -84,20 +87,15 @@ void run_interp_weights(const Launch& L, int dtype, const PointsDev& p, int64_t 
 void run_predict(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const double* coeffs,
                  double* out, int* status);
 
-// Batched EFLA (probe-batched factorized Lanczos)
-struct EflaBufs {
-  int P, k;
-  int64_t m;
-  double *Q, *Ph;          // P × k × m bases (Q̂, P̂ = W^T W Q̂)
-  double *q, *qprev, *sbar, *pcur, *wv, *pnext, *snext, *wt0, *kwt0;  // P × m
-  double *kt0, *kt1;       // K_G temporaries P × m
-  double *scal;            // per-probe scalars (see operators.cu)
-  double *lambda;          // P × k
-  double *tq, *dvec;       // P × k
-  double *alpha, *beta;    // P × k
-  int *done;               // P
+// ---- efla.cu: probe-batched EFLA (P <= 32 per call; inputs device arrays P × m)
+struct EflaOut {
+  std::vector<double> alpha, beta;  // P × k
+  std::vector<int> order;
 };
-void run_efla(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const EflaBufs& b,
-              double sigma_sq);
+EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, const double* kwt_in,
+                 const double* wt_in, const double* z0sq_dev, double s2, int k);
+std::pair<double, int> quadrature_logdet_host(const double* alpha, const double* beta, int k, double probe_sq,
+                                              double quad_tol);
+void run_kg_batched(const Launch& L, const KgDev& kg, int P, const double* v, double* out, double* t0, double* t1);
 
 }  // namespace gsgpc

@@ -573,6 +573,11 @@ class SufficientStatsAccumulator:
                                                   pw.vp if pw else None, int(probes)))
         self._rows += n
 
+    def enable_probes(self, probes: int = 30, seed: int = 0):
+        """Accumulate W^T v_p for the reference's Rademacher probes p < probes (gp.cpp:16-25),
+        generated in stream order by the library; call before adding rows."""
+        self._ctx.check(_L.load().gsgpc_stats_enable_probes(self._ctx.handle, self._h, int(probes), int(seed)))
+
     def reset(self):
         """Back to the freshly constructed state (buffers kept)."""
         self._ctx.check(_L.load().gsgpc_stats_reset(self._ctx.handle, self._h))

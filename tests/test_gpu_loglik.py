@@ -1,0 +1,105 @@
+"""GPU parity of the probe images, probe-batched EFLA and the SLQ log-likelihood
+(SkiOperator route) against the oracle on identical probes (same reference generator)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2101_11751_b200 as G
+from helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def ogrid(g):
+    return O.Grid([g.min(k) for k in range(g.dim())], [g.max(k) for k in range(g.dim())],
+                  [g.size(k) for k in range(g.dim())])
+
+
+def make_case(d=3, sizes=(10, 9, 8), n=6000, seed=5):
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    om = rng.standard_normal((20, d)) / 0.3
+    y = np.cos(x @ om.T).sum(axis=1) / 5.0 + 0.1 * rng.standard_normal(n)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    return g, x, y
+
+
+@pytest.mark.parametrize("d,sizes", [(1, (40,)), (2, (16, 14)), (3, (10, 9, 8))])
+def test_probe_images_match_oracle(d, sizes):
+    g, x, y = make_case(d, sizes, n=5000)
+    acc = G.SufficientStatsAccumulator(g)
+    acc.enable_probes(5, seed=7)
+    acc.add(x[:2000], y[:2000])  # streams continue across batches
+    acc.add(x[2000:], y[2000:])
+    st = acc.finalize()
+    img = st.probe_images()
+    og = ogrid(g)
+    for p in range(5):
+        v = O.rademacher_probe(x.shape[0], 7, p)
+        ref = O.wt_apply(og, x, v)
+        assert rel_err(img[p], ref) <= 1e-10, p
+
+
+def test_efla_matches_oracle():
+    g, x, y = make_case()
+    sigma = 0.1
+    spec = G.KernelSpec(G.Hyperparams(sigma, [0.2, 0.25, 0.3], 1.0))
+    st = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    og = ogrid(g)
+    ost = O.sufficient_stats(og, x, y)
+    okg = O.ToeplitzOperator(og, [0.2, 0.25, 0.3], 1.0, sigma)
+    kg = G.ToeplitzOperator(g, spec)
+    P, k = 3, 25
+    wts, kwts, z = [], [], []
+    for p in range(P):
+        v = O.rademacher_probe(x.shape[0], 0, p)
+        w = O.wt_apply(og, x, v)
+        wts.append(w)
+        kwts.append(okg.apply(w))
+        z.append(float(v @ v))
+    a, b, order = G.factorized_lanczos_fused(kg, st, np.array(kwts), np.array(wts), np.array(z), sigma * sigma, k)
+    for p in range(P):
+        ref = O.factorized_lanczos_fused(okg, ost, kwts[p], wts[p], z[p], sigma * sigma, k)
+        assert order[p] == len(ref["alpha"])
+        o = order[p]
+        assert rel_err(a[p, :o], ref["alpha"]) <= 1e-6
+        assert rel_err(b[p, : o - 1], ref["beta"]) <= 1e-6
+
+
+def test_loglik_matches_oracle():
+    g, x, y = make_case(n=8000)
+    sigma = 0.1
+    ls = [0.2, 0.25, 0.3]
+    spec = G.KernelSpec(G.Hyperparams(sigma, ls, 1.0))
+    acc = G.SufficientStatsAccumulator(g)
+    acc.enable_probes(30, seed=0)
+    acc.add(x, y)
+    st = acc.finalize()
+    kg = G.ToeplitzOperator(g, spec)
+    opts = G.LoglikOptions(solve_tol=1e-6, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.0), seed=0)
+    r = G.log_likelihood_gsgp(st, kg, sigma, opts)
+    og = ogrid(g)
+    ost = O.sufficient_stats(og, x, y)
+    okg = O.ToeplitzOperator(og, ls, 1.0, sigma)
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-6, probes=30, max_depth=50,
+                                quad_tol=0.0, seed=0, route="ski-operator")
+    assert abs(r.const_term - ref["const_term"]) <= 1e-12 * abs(ref["const_term"])
+    assert abs(r.quad_term - ref["quad_term"]) <= 1e-5 * abs(ref["quad_term"])
+    assert abs(r.logdet_term - ref["logdet_term"]) <= 1e-5 * abs(ref["logdet_term"])
+    assert abs(r.loglik - ref["loglik"]) <= 1e-5 * abs(ref["loglik"])
+    assert abs(r.solver_iterations - ref["solver_iterations"]) <= 1
+    assert r.probes_used == 30
+    # default quad_tol (0.01) early-stop path
+    opts2 = G.LoglikOptions(solve_tol=1e-6, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.01), seed=0)
+    r2 = G.log_likelihood_gsgp(st, kg, sigma, opts2)
+    ref2 = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-6, probes=30, max_depth=50,
+                                 quad_tol=0.01, seed=0, route="ski-operator")
+    assert abs(r2.loglik - ref2["loglik"]) <= 1e-5 * abs(ref2["loglik"])
+
+
+def test_loglik_requires_probe_images():
+    g, x, y = make_case(n=2000)
+    st = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    spec = G.KernelSpec(G.Hyperparams(0.1, [0.2, 0.25, 0.3], 1.0))
+    with pytest.raises(G.InvalidArgument):
+        G.log_likelihood_gsgp(st, G.ToeplitzOperator(g, spec), 0.1)
