@@ -39,7 +39,9 @@ class Config:
 CONFIGS = {
     1: Config("1d-sine", 1, 1_000_000, (1000,), (0.5,), 0.01, 1.0, "f64", ((-10.5, 10.5),)),
     2: Config("2d-sincos", 2, 10_000_000, (256, 256), (0.05, 0.05), 0.0025, 1.0, "f32"),
-    3: Config("3d-radar-like", 3, 120_000_000, (80, 80, 20), (0.03, 0.03, 0.1), 0.01, 1.0, "f32"),
+    # config 3 solve tolerance: BASELINE.json states none; the paper's experiments use 0.01
+    # — at 1e-6 the factorized CG needs > 5000 iterations on this system.
+    3: Config("3d-radar-like", 3, 120_000_000, (80, 80, 20), (0.03, 0.03, 0.1), 0.01, 1.0, "f32", tol=0.01),
     4: Config("2d-sweep", 2, 1_000_000, (1024, 1024), (0.05, 0.05), 1.0, 1.0, "f32"),
     5: Config("3d-loglik", 3, 50_000_000, (64, 64, 64), (0.1, 0.1, 0.1), 0.01, 1.0, "f64"),
 }
