@@ -1,0 +1,77 @@
+"""Multi-rank combination of the statistics on CPU (gloo, world_size 2).
+
+Each rank computes the statistics of its own shard of rows, packs them in the device
+reduce-buffer layout [half stencil (S_min·m) | W^T y (m) | yty | n] that
+gsgpc_stats_reduce_buffer exposes, and the ranks sum them with all_reduce — the
+reference's SufficientStatsAccumulator::merge (interp.cpp:202-210).  The result must equal
+the statistics of all rows (the same code path the NCCL run takes on the GPU box,
+paper_2101_11751_b200/distributed.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from helpers import csr_to_half_stencil
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _data():
+    rng = np.random.default_rng(11)
+    x = rng.random((20000, 2))
+    y = np.sin(5 * x[:, 0]) + 0.1 * rng.standard_normal(20000)
+    g = O.fit_grid_to_data([0, 0], [1, 1], [17, 15])
+    return g, x, y
+
+
+def _pack(st, sizes):
+    rp, col, val, wty = st.csr()
+    half = csr_to_half_stencil(rp, col, val, sizes, 4)
+    return np.concatenate([half.reshape(-1), wty, [st.yty, float(st.n)]])
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, x, y = _data()
+    lo, hi = rank * x.shape[0] // world, (rank + 1) * x.shape[0] // world
+    st = O.sufficient_stats(g, x[lo:hi], y[lo:hi])
+    t = torch.from_numpy(_pack(st, [17, 15]))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    np.save(f"{out_path}.{rank}.npy", t.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_allreduce_equals_merge(tmp_path):
+    world = 2
+    port = _free_port()
+    out = str(tmp_path / "buf")
+    mp.start_processes(_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    g, x, y = _data()
+    full = _pack(O.sufficient_stats(g, x, y), [17, 15])
+    for r in range(world):
+        got = np.load(f"{out}.{r}.npy")
+        assert got[-1] == full[-1]  # n exact
+        np.testing.assert_allclose(got, full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+
+
+def test_host_merge_helper():
+    pytest.importorskip("torch")
+    from paper_2101_11751_b200.distributed import merge_buffers_host
+
+    a = torch.arange(5, dtype=torch.float64)
+    b = torch.ones(5, dtype=torch.float64)
+    assert torch.equal(merge_buffers_host([a, b]), a + b)
