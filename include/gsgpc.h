@@ -95,6 +95,9 @@ gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx);
 /* Diagnostics: measured FP64 FMA throughput of this GPU (TFLOP/s, 2 flops per DFMA) from a
  * register-resident DFMA loop over all SMs — the denominator of the precompute's FP64 roofline. */
 gsgpc_status gsgpc_diag_fp64_peak(gsgpc_ctx* ctx, double* tflops);
+/* Diagnostics: FP64 tensor-core (mma.sync m8n8k4 f64) throughput, alone and interleaved
+ * with DFMA chains in the same warps (TFLOP/s). */
+gsgpc_status gsgpc_diag_fp64_tensor(gsgpc_ctx* ctx, double* dmma_tflops, double* mixed_tflops);
 /* Library build identification ("gsgpc sm_100a <git> ..."). */
 const char* gsgpc_version(void);
 

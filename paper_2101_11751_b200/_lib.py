@@ -70,6 +70,7 @@ SIGNATURES = {
     "gsgpc_stats_reset": (_i, [_vp, _vp]),
     "gsgpc_stats_enable_probes": (_i, [_vp, _vp, _i, C.c_uint64]),
     "gsgpc_diag_fp64_peak": (_i, [_vp, _P(_d)]),
+    "gsgpc_diag_fp64_tensor": (_i, [_vp, _P(_d), _P(_d)]),
     "gsgpc_stats_finalize": (_i, [_vp, _vp]),
     "gsgpc_sufficient_stats": (_i, [_vp, _P(Grid_t), _i, _P(Points_t), _i64, _P(_vp)]),
     "gsgpc_stats_info": (_i, [_vp, _vp, _P(_i64), _P(_i64), _P(_d), _P(_i64), _P(C.c_int32)]),

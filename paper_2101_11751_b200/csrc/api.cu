@@ -29,6 +29,7 @@ using namespace gsgpc;
 
 namespace gsgpc {
 double measure_fp64_peak(cudaStream_t s);
+void measure_fp64_tensor(cudaStream_t s, double* dmma_tflops, double* mixed_tflops);
 void run_add_div(const Launch& L, int64_t n, const double* x, double sx, const double* y, double b, double* out);
 }
 
@@ -630,6 +631,13 @@ gsgpc_status gsgpc_diag_fp64_peak(gsgpc_ctx* ctx, double* tflops) {
   return guard(ctx, [&] {
     if (!tflops) invalid("tflops is NULL");
     *tflops = gsgpc::measure_fp64_peak(ctx->stream);
+  });
+}
+
+gsgpc_status gsgpc_diag_fp64_tensor(gsgpc_ctx* ctx, double* dmma, double* mixed) {
+  return guard(ctx, [&] {
+    if (!dmma || !mixed) invalid("NULL argument");
+    gsgpc::measure_fp64_tensor(ctx->stream, dmma, mixed);
   });
 }
 

@@ -126,6 +126,12 @@ class Context:
         self.check(_L.load().gsgpc_diag_fp64_peak(self._h, C.byref(v)))
         return v.value
 
+    def fp64_tensor_tflops(self):
+        """(DMMA alone, DMMA + DFMA interleaved) TFLOP/s."""
+        a, b = C.c_double(), C.c_double()
+        self.check(_L.load().gsgpc_diag_fp64_tensor(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def reset_phase_times(self):
         self.check(_L.load().gsgpc_ctx_reset_phase_times(self._h))
 
