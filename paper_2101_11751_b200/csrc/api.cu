@@ -203,6 +203,7 @@ GridDev make_grid(const gsgpc_grid* gr, int scheme) {
     if (!(gr->max[k] > gr->min[k])) invalid("Grid: max must exceed min");
     g.mn[k] = gr->min[k];
     g.sp[k] = (gr->max[k] - gr->min[k]) / static_cast<double>(gr->size[k] - 1);
+    g.isp[k] = 1.0 / g.sp[k];
     g.sz[k] = gr->size[k];
     g.nc[k] = gr->size[k] - 1;
     g.m *= g.sz[k];

@@ -40,6 +40,7 @@ struct GridDev {
   int W;                  // stencil width per dimension: 4 cubic, 2 linear
   double mn[GSGPC_MAX_DIM];
   double sp[GSGPC_MAX_DIM];
+  double isp[GSGPC_MAX_DIM];     // 1 / spacing (fast classification path)
   int64_t sz[GSGPC_MAX_DIM];     // nodes per dimension
   int64_t nc[GSGPC_MAX_DIM];     // cells per dimension = sz - 1
   int64_t m;              // Π sz
@@ -93,6 +94,25 @@ __device__ __forceinline__ int stencil_dim(double x, double mn, double sp, int64
   return PT_VALID;
 }
 
+// Same result as stencil_dim for the cell index i0 and the status, with t to within a few
+// ulp: u ≈ (x - min)·(1/spacing) differs from the correctly rounded quotient by ≤ 2 ulp
+// (≤ 5e-13 for u < 2^11), so whenever u is more than 4e-9 from every integer the snap rule
+// cannot fire, floor(u) and the range tests agree with the exact path; otherwise (snap zone,
+// cell boundaries, range ends, NaN, inf) fall back to the exact division.  Used by the
+// precompute (cell binning + moments, tolerance 1e-10), never for reported weights.
+__device__ __forceinline__ int stencil_dim_fast(double x, double mn, double sp, double isp, int64_t size,
+                                                int64_t& i0, double& t) {
+  const double u = __dsub_rn(x, mn) * isp;
+  const double r = round(u);
+  if (!(fabs(u - r) > 4e-9)) return stencil_dim(x, mn, sp, size, i0, t);
+  if (u < 0.0 || u > static_cast<double>(size - 1)) return PT_OUTSIDE;
+  int64_t i = static_cast<int64_t>(floor(u));
+  if (i > size - 2) i = size - 2;
+  i0 = i;
+  t = u - static_cast<double>(i);
+  return PT_VALID;
+}
+
 // 1-D weights in the reference order (cubic: start i0-1, [c(t+1), c(t), c(1-t), c(2-t)];
 // linear: start i0, [l(t), l(1-t)]).
 __device__ __forceinline__ void weights_1d(double t, int W, double* w) {
@@ -133,7 +153,7 @@ __device__ __forceinline__ int classify(const GridDev& g, const double* x, int64
 #pragma unroll
   for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
     if (k < g.d) {
-      st[k] = stencil_dim(x[k], g.mn[k], g.sp[k], g.sz[k], i0[k], t[k]);
+      st[k] = stencil_dim_fast(x[k], g.mn[k], g.sp[k], g.isp[k], g.sz[k], i0[k], t[k]);
     }
   }
 #pragma unroll

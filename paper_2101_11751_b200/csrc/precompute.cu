@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(256) k_classify_count(PointsDev pts, int64_t n
         atomicMin(err, code);
       }
     }
-    agg_inc(hist, cell, active);
+    if (active) atomicAdd(&hist[cell], 1);  // RED: no return value needed
   }
   const double s = block_sum<256>(ysq, sh);
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s;
@@ -230,9 +231,8 @@ __global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, GridD
       double t[GSGPC_MAX_DIM];
       active = classify(g, x, i0, t, cell) == PT_VALID;
     }
-    const int slot = agg_inc(cur, cell, active);
     if (active) {
-      const int64_t pos = off[cell] + slot;
+      const int64_t pos = off[cell] + atomicAdd(&cur[cell], 1);
       out[pos] = r;
       for (int w = 0; w < nw; ++w) pw_out[pos * nw + w] = pw_in[i * nw + w];
     }
@@ -257,7 +257,7 @@ __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double
     if (k < g.d) {
       int64_t i0;
       t[k] = 0.0;
-      stencil_dim(static_cast<double>(r.v[k]), g.mn[k], g.sp[k], g.sz[k], i0, t[k]);
+      stencil_dim_fast(static_cast<double>(r.v[k]), g.mn[k], g.sp[k], g.isp[k], g.sz[k], i0, t[k]);
     }
   }
   y = static_cast<double>(r.v[3]);
@@ -401,6 +401,126 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
       for (int j = 0; j < 7; ++j) acc[i][j] = 0.0;
 #pragma unroll
     for (int a = 0; a < 4; ++a) yacc[a][0] = yacc[a][1] = 0.0;
+    p = seg_end;
+  }
+}
+
+// ------------------------------------------------------------------ K1, d = 3 cubic, FP64 MMA
+// The per-cell moment sums are a GEMM over the cell's points:
+//   M[e0][(e1,e2)] = Σ_p t0^e0 · (t1^e1 t2^e2),   Y[a][(b,c)] = Σ_p y t0^a t1^b t2^c.
+// One warp runs mma.sync.m8n8k4.f64 (D 8×8 += A 8×4 · B 4×8, k = 4 points per step):
+//   x tiles t = 0..6 : A rows e0 = 0..6 plus row 7 = y  (row 7 yields Y[0][t][c]),
+//                      B[k][n] = t1^t · t2^n  (n = 0..6, column 7 zero);
+//   y tiles j = 0..1 : A rows ρ = 8j + r → (a, b) = (1 + ρ/4, ρ%4), value y t0^a t1^b (ρ < 12),
+//                      B[k][n] = t2^n for n < 4.
+// Accumulators stay in the MMA fragments (18 doubles per lane); at a cell boundary every
+// lane writes its own fragment entries — no cross-lane reduction.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
+                                                            const int64_t* __restrict__ off, int64_t cells,
+                                                            int64_t nvalid, GridDev g, double* __restrict__ mom,
+                                                            int64_t range) {
+  __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
+  const int64_t r0 = warp * range;
+  if (r0 >= nvalid) return;
+  const int64_t rend = min(r0 + range, nvalid);
+  double* S = sm[wib];
+  const int r = lane >> 2;   // A row / B column / D row
+  const int kq = lane & 3;   // A column / B row: the point of the 4-point step
+  const int cb = 2 * (lane & 3);  // D columns cb, cb+1
+  // y-tile row meaning for this lane
+  const int rho0 = r, rho1 = 8 + r;
+  const int ya0 = 1 + rho0 / 4, yb0 = rho0 % 4;
+  const int ya1 = 1 + rho1 / 4, yb1 = rho1 % 4;
+  const bool yv1 = rho1 < 12;
+
+  double dx[7][2], dy[2][2];
+#pragma unroll
+  for (int t = 0; t < 7; ++t) dx[t][0] = dx[t][1] = 0.0;
+  dy[0][0] = dy[0][1] = dy[1][0] = dy[1][1] = 0.0;
+
+  int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
+  int64_t p = r0;
+  while (p < rend) {
+    if (off[c + 1] <= p) c = upper_bound_i64(off, cells + 1, p) - 1;
+    const int64_t cs = off[c], ce = off[c + 1];
+    const int64_t seg_end = min(ce, rend);
+    const bool owned = cs >= r0 && ce <= rend;
+    for (int64_t b = p; b < seg_end; b += 32) {
+      const int nb = static_cast<int>(imin64(32, seg_end - b));
+      {
+        double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
+        const bool v = lane < nb;
+        if (v) row_t<T>(g, pay[b + lane], t, y);
+        double* P = S + lane * D3C_STRIDE;
+        double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
+#pragma unroll
+        for (int e = 0; e < 7; ++e) {
+          P[e] = q0;
+          P[8 + e] = q1;
+          P[16 + e] = q2;
+          q0 *= t[0];
+          q1 *= t[1];
+          q2 *= t[2];
+        }
+        P[7] = v ? y : 0.0;
+      }
+      __syncwarp();
+      const int steps = (nb + 3) >> 2;
+      for (int st = 0; st < steps; ++st) {
+        const double* P = S + (4 * st + kq) * D3C_STRIDE;
+        const double y = P[7];
+        const double ax = P[r];            // r < 7: t0^r ; r == 7: y
+        const double t1 = P[9];
+        const double t2n = r < 7 ? P[16 + r] : 0.0;
+        const double ay0 = y * P[ya0] * P[8 + yb0];
+        const double ay1 = yv1 ? y * P[ya1] * P[8 + yb1] : 0.0;
+        const double by = r < 4 ? t2n : 0.0;
+        double bt = t2n;
+#pragma unroll
+        for (int tt = 0; tt < 7; ++tt) {
+          dmma(dx[tt][0], dx[tt][1], ax, bt);
+          bt *= t1;
+        }
+        dmma(dy[0][0], dy[0][1], ay0, by);
+        dmma(dy[1][0], dy[1][1], ay1, by);
+      }
+      __syncwarp();
+    }
+    // flush this lane's fragment entries
+    double* M = mom + c * D3C_Q;
+#pragma unroll
+    for (int tt = 0; tt < 7; ++tt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = cb + i;
+        if (col < 7) {
+          if (r < 7) {
+            flush_val(M + r * 49 + tt * 7 + col, dx[tt][i], owned);
+          } else if (tt < 4 && col < 4) {
+            flush_val(M + D3C_QX + tt * 4 + col, dx[tt][i], owned);  // Y[a=0][b=tt][c=col]
+          }
+        }
+        dx[tt][i] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int col = cb + i;
+      if (col < 4) {
+        flush_val(M + D3C_QX + ya0 * 16 + yb0 * 4 + col, dy[0][i], owned);
+        if (yv1) flush_val(M + D3C_QX + ya1 * 16 + yb1 * 4 + col, dy[1][i], owned);
+      }
+      dy[0][i] = dy[1][i] = 0.0;
+    }
     p = seg_end;
   }
 }
@@ -579,85 +699,103 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
 }
 
 // ------------------------------------------------------------------ finalize kernels
-// cell-major [cell][Q] → moment-major X[q][cell] (q < QX), Y[q][cell] (q < QY).
-__global__ void k_transpose_moments(const double* __restrict__ mom, int64_t cells, int Q, int QX,
-                                    double* __restrict__ X, double* __restrict__ Y) {
-  extern __shared__ double tile[];  // 32 × Q
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
-  const int nc = static_cast<int>(imin64(32, cells - c0));
-  for (int e = threadIdx.x; e < nc * Q; e += blockDim.x) tile[e] = mom[c0 * Q + e];
-  __syncthreads();
-  for (int e = threadIdx.x; e < nc * Q; e += blockDim.x) {
-    const int q = e / nc, cc = e % nc;
-    const double v = tile[cc * Q + q];
-    if (q < QX) X[static_cast<int64_t>(q) * cells + c0 + cc] = v;
-    else Y[static_cast<int64_t>(q - QX) * cells + c0 + cc] = v;
-  }
-}
-
+// One separable transform along dimension k maps (cell c_k, exponent e_k) to (node a_k,
+// offset δ_k) (x-moments → W^T W stencil) or to node a_k alone (y-/probe-moments → W^T y /
+// W^T v_p).  A thread owns one (line, node): it loads the W·E moments of the W cells whose
+// 4^d block contains the node once and produces every output offset from them.
 struct XformDims {
-  int d, W, k;             // transform dimension k
-  int shift;               // node a = c - shift + i  (cubic 1, linear 0)
-  int64_t ext_in[3], ext_out[3];   // spatial extents (mixed cells / nodes)
-  int64_t sp_in, sp_out;   // Π extents
-  int64_t qext_in[3], qext_out[3]; // index extents per dim
-  int64_t q_in, q_out;     // Π index extents
-  int64_t q_begin;         // first output index computed (half stencil on the last pass)
-  int64_t nc_k;            // cells along k
+  int d, W, k;
+  int shift;               // cell of node a at slot i: c = a + shift - i (cubic 1, linear 0)
+  int ymode;               // 1: exponent digit collapses to one output (no offset)
+  int64_t ext_in[3], ext_out[3];   // spatial extents (cells / nodes)
+  int64_t qext_in[3], qext_out[3]; // index extents
+  int64_t sp_in, sp_out;           // Π spatial extents
+  int64_t nc_k;
+  // input addressing: moment-major In[q * sp_in + sp]  or cell-major In[sp * cstride + qoff + q]
+  int cell_major;
+  int64_t cstride, qoff;
+  // output: moment-major Out[q * sp_out + sp], or the half stencil (last x pass): q >= c0 only
+  int half;
+  int64_t c0;
 };
 
-// x-moment transform along dim k: (cell c_k, exponent e_k) → (node a_k, offset δ_k).
-__global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, double* __restrict__ out,
-                                               XformDims x, int y_mode) {
-  const int64_t nq = x.q_out - x.q_begin;
-  const int64_t total = nq * x.sp_out;
+__global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, double* __restrict__ out, XformDims x) {
+  int64_t qrest_total = 1;
+  for (int j = 0; j < x.d; ++j)
+    if (j != x.k) qrest_total *= x.qext_out[j];
+  const int64_t total = qrest_total * x.sp_out;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int64_t sp = idx % x.sp_out;
-  const int64_t q = x.q_begin + idx / x.sp_out;
-  // spatial digits: split sp at dim k
+  const int64_t qrest = idx / x.sp_out;
   int64_t inner_sp = 1;
   for (int j = x.k + 1; j < x.d; ++j) inner_sp *= x.ext_out[j];
   const int64_t sp_lo = sp % inner_sp;
   const int64_t a = (sp / inner_sp) % x.ext_out[x.k];
   const int64_t sp_hi = sp / (inner_sp * x.ext_out[x.k]);
-  int64_t inner_q_out = 1, inner_q_in = 1;
+  // index digits: qrest enumerates digits j != k (row-major)
+  int64_t inner_q_in = 1, inner_q_out = 1;
   for (int j = x.k + 1; j < x.d; ++j) {
-    inner_q_out *= x.qext_out[j];
     inner_q_in *= x.qext_in[j];
+    inner_q_out *= x.qext_out[j];
   }
-  const int64_t q_lo = q % inner_q_out;
-  const int64_t qd = (q / inner_q_out) % x.qext_out[x.k];
-  const int64_t q_hi = q / (inner_q_out * x.qext_out[x.k]);
+  const int64_t q_lo = qrest % inner_q_out;  // digits after k (same extents in and out)
+  const int64_t q_hi = qrest / inner_q_out;
   const int W = x.W;
   const int E_in = static_cast<int>(x.qext_in[x.k]);
-  double acc = 0.0;
-  if (!y_mode) {
-    const int delta = static_cast<int>(qd) - (W - 1);
-    const int ilo = max(0, -delta), ihi = min(W - 1, W - 1 - delta);
-    for (int i = ilo; i <= ihi; ++i) {
+  double v[4][7];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int e = 0; e < 7; ++e) v[i][e] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < W) {
       const int64_t c = a + x.shift - i;
-      if (c < 0 || c >= x.nc_k) continue;
-      const int64_t spi = (sp_hi * x.ext_in[x.k] + c) * inner_sp + sp_lo;
-      const double* coef = c_C + (i * 4 + (i + delta)) * 7;
-      for (int e = 0; e < E_in; ++e) {
-        const int64_t qi = (q_hi * E_in + e) * inner_q_in + q_lo;
-        acc = fma(in[qi * x.sp_in + spi], coef[e], acc);
-      }
-    }
-  } else {
-    for (int i = 0; i < W; ++i) {
-      const int64_t c = a + x.shift - i;
-      if (c < 0 || c >= x.nc_k) continue;
-      const int64_t spi = (sp_hi * x.ext_in[x.k] + c) * inner_sp + sp_lo;
-      const double* coef = c_P + i * 4;
-      for (int e = 0; e < E_in; ++e) {
-        const int64_t qi = (q_hi * E_in + e) * inner_q_in + q_lo;
-        acc = fma(in[qi * x.sp_in + spi], coef[e], acc);
+      if (c >= 0 && c < x.nc_k) {
+        const int64_t spi = (sp_hi * x.ext_in[x.k] + c) * inner_sp + sp_lo;
+#pragma unroll
+        for (int e = 0; e < 7; ++e) {
+          if (e < E_in) {
+            const int64_t qi = (q_hi * E_in + e) * inner_q_in + q_lo;
+            v[i][e] = x.cell_major ? in[spi * x.cstride + x.qoff + qi] : in[qi * x.sp_in + spi];
+          }
+        }
       }
     }
   }
-  out[(q - x.q_begin) * x.sp_out + sp] = acc;
+  if (x.ymode) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (i < W && e < E_in) acc = fma(v[i][e], c_P[i * 4 + e], acc);
+    const int64_t qo = q_hi * inner_q_out + q_lo;  // digit k collapsed to extent 1
+    out[qo * x.sp_out + sp] = acc;
+    return;
+  }
+  const int E = 2 * W - 1;
+#pragma unroll
+  for (int dq = 0; dq < 7; ++dq) {
+    if (dq >= E) break;
+    const int delta = dq - (W - 1);
+    const int64_t qo = (q_hi * E + dq) * inner_q_out + q_lo;
+    if (x.half && qo < x.c0) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = i + delta;
+      if (i < W && j >= 0 && j < W) {
+        const double* coef = c_C + (i * 4 + j) * 7;
+#pragma unroll
+        for (int e = 0; e < 7; ++e)
+          if (e < E_in) acc = fma(v[i][e], coef[e], acc);
+      }
+    }
+    if (x.half) out[(qo - x.c0) * x.sp_out + sp] = acc;
+    else out[qo * x.sp_out + sp] = acc;
+  }
 }
 
 // ================================================================== host side
@@ -722,7 +860,16 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
   if (g.d == 3 && g.W == 4) {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid, range);
-    k_moments_d3c<T><<<static_cast<unsigned>(ceil_div(warps, 4)), 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    static const bool use_dfma = [] {
+      const char* e = getenv("GSGPC_K1_DFMA");
+      return e && e[0] == '1';
+    }();
+    if (use_dfma) {
+      k_moments_d3c<T><<<static_cast<unsigned>(ceil_div(warps, 4)), 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    } else {
+      k_moments_d3c_mma<T><<<static_cast<unsigned>(ceil_div(warps, 4)), 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom,
+                                                                                       range);
+    }
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid, range);
@@ -769,8 +916,8 @@ void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64
   GSGPC_CUDA(cudaGetLastError());
 }
 
-// moments (cell-major) → stencil [S_min][m] and W^T y [m]; optional probe moments
-// (cells × P × QY) → probe images [P][m].  ws must hold 2 × max-intermediate doubles.
+// moments (cell-major [cell][QX+QY]) → stencil [S_min][m] and W^T y [m]; optional probe
+// moments (cell-major [cell][P][QY]) → probe images [P][m].
 void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
                   double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems) {
   const int d = g.d, W = g.W, E = 2 * W - 1;
@@ -783,38 +930,25 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
   upload_poly_tables(W, L.s);
   double* bufA = ws;
   double* bufB = ws + ws_elems / 2;
-  // --- x part: transpose then transforms k = d-1 .. 0
-  double* X = bufA;
-  double* Yb = bufA + static_cast<int64_t>(QX) * g.cells;  // y moments stored after X in bufA
-  {
-    const unsigned blocks = static_cast<unsigned>(ceil_div(g.cells, 32));
-    const size_t smem = sizeof(double) * 32 * Q;
-    if (smem > 48 * 1024) {
-      GSGPC_CUDA(cudaFuncSetAttribute(k_transpose_moments, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-    }
-    k_transpose_moments<<<blocks, 256, smem, L.s>>>(mom, g.cells, Q, QX, X, Yb);
-    L.count();
-  }
-  auto run_chain = [&](bool ymode, const double* src, int64_t qk_in0, double* final_out, int64_t q_begin_last,
-                       double* scratch0, double* scratch1) {
+  // chain over k = d-1 .. 0; the first pass reads the cell-major moments directly
+  auto chain = [&](bool ymode, const double* src, int64_t cstride, int64_t qoff, int qk0, double* final_out,
+                   int64_t c0) {
     XformDims x{};
     x.d = d;
     x.W = W;
     x.shift = W == 4 ? 1 : 0;
+    x.ymode = ymode ? 1 : 0;
     int64_t ext[3], qext[3];
     for (int k = 0; k < d; ++k) {
       ext[k] = g.nc[k];
-      qext[k] = qk_in0;
+      qext[k] = qk0;
     }
     const double* cur = src;
+    bool first = true;
     for (int k = d - 1; k >= 0; --k) {
       x.k = k;
       x.nc_k = g.nc[k];
-      x.sp_in = 1;
-      x.sp_out = 1;
-      x.q_in = 1;
-      x.q_out = 1;
+      x.sp_in = x.sp_out = 1;
       for (int j = 0; j < d; ++j) {
         x.ext_in[j] = ext[j];
         x.ext_out[j] = j == k ? g.sz[k] : ext[j];
@@ -822,67 +956,35 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
         x.qext_out[j] = j == k ? (ymode ? 1 : E) : qext[j];
         x.sp_in *= x.ext_in[j];
         x.sp_out *= x.ext_out[j];
-        x.q_in *= x.qext_in[j];
-        x.q_out *= x.qext_out[j];
       }
+      x.cell_major = first ? 1 : 0;
+      x.cstride = cstride;
+      x.qoff = qoff;
       const bool last = k == 0;
-      x.q_begin = last ? q_begin_last : 0;
-      double* dst = last ? final_out : (cur == scratch0 ? scratch1 : scratch0);
-      const int64_t total = (x.q_out - x.q_begin) * x.sp_out;
-      k_xform<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, L.s>>>(cur, dst, x, ymode ? 1 : 0);
+      x.half = (last && !ymode) ? 1 : 0;
+      x.c0 = c0;
+      double* dst = last ? final_out : (cur == bufA ? bufB : bufA);
+      int64_t qrest = 1;
+      for (int j = 0; j < d; ++j)
+        if (j != k) qrest *= x.qext_out[j];
+      const int64_t total = qrest * x.sp_out;
+      k_xform<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, L.s>>>(cur, dst, x);
       L.count();
       cur = dst;
+      first = false;
       for (int j = 0; j < d; ++j) {
         ext[j] = x.ext_out[j];
         qext[j] = x.qext_out[j];
       }
     }
   };
-  // x chain: X (in bufA) → bufB ↔ (bufA after Y consumed?) — keep Y safe: run y chain first.
-  // y chain: Yb → small scratch in bufB → wty
-  {
-    const int64_t yelems = static_cast<int64_t>(QY) * std::max<int64_t>(g.m, g.cells);
-    double* s0 = bufB;
-    double* s1 = bufB + yelems;
-    run_chain(true, Yb, W, wty, 0, s0, s1);
-  }
-  {
-    const int64_t c0 = (static_cast<int64_t>(QX) - 1) / 2;
-    // X occupies the front of bufA; ping-pong between bufB and the tail of bufA is unsafe,
-    // so use bufB and the front of bufA (X is dead after the first pass).
-    run_chain(false, X, E, stencil, c0, bufB, bufA);
-  }
-  if (probes > 0 && pmom != nullptr) {
-    // probe moments [cell][P][QY] → per probe: transpose to [q][cell] then the y chain.
-    for (int pj = 0; pj < probes; ++pj) {
-      // gather probe pj's moments into moment-major layout in bufA
-      const unsigned blocks = static_cast<unsigned>(ceil_div(g.cells, 32));
-      const size_t smem = sizeof(double) * 32 * QY * probes;
-      (void)smem;
-      // simple strided gather (probe images are a secondary path)
-      extern void run_gather_probe(const Launch&, const double*, int64_t, int, int, int, double*);
-      run_gather_probe(L, pmom, g.cells, probes, QY, pj, bufA);
-      (void)blocks;
-      const int64_t yelems = static_cast<int64_t>(QY) * std::max<int64_t>(g.m, g.cells);
-      run_chain(true, bufA, W, pimg + static_cast<int64_t>(pj) * g.m, 0, bufB, bufB + yelems);
-    }
+  chain(true, mom, Q, QX, W, wty, 0);
+  chain(false, mom, Q, 0, E, stencil, (static_cast<int64_t>(QX) - 1) / 2);
+  for (int pj = 0; pj < probes && pmom != nullptr; ++pj) {
+    chain(true, pmom, static_cast<int64_t>(probes) * QY, static_cast<int64_t>(pj) * QY, W,
+          pimg + static_cast<int64_t>(pj) * g.m, 0);
   }
   GSGPC_CUDA(cudaGetLastError());
-}
-
-__global__ void k_gather_probe(const double* __restrict__ pmom, int64_t cells, int probes, int QY, int pj,
-                               double* __restrict__ out) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= cells * QY) return;
-  const int64_t c = idx % cells;
-  const int64_t q = idx / cells;
-  out[q * cells + c] = pmom[(c * probes + pj) * QY + q];
-}
-
-void run_gather_probe(const Launch& L, const double* pmom, int64_t cells, int probes, int QY, int pj,
-                      double* out) {
-  k_gather_probe<<<static_cast<unsigned>(ceil_div(cells * QY, 256)), 256, 0, L.s>>>(pmom, cells, probes, QY, pj, out);
-  L.count();
 }
 
 int64_t finalize_ws_elems(const GridDev& g) {
@@ -893,10 +995,7 @@ int64_t finalize_ws_elems(const GridDev& g) {
     QY *= W;
   }
   const int64_t big = std::max(g.m, g.cells);
-  // bufA: X (QX·cells) + Y (QY·cells); bufB: max(QX·big, 2·QY·big)
-  const int64_t a = (QX + QY) * big;
-  const int64_t b = std::max(QX * big, 2 * QY * big);
-  return 2 * std::max(a, b);
+  return 2 * std::max(QX, QY) * big;  // two ping-pong buffers of the largest intermediate
 }
 
 }  // namespace gsgpc

@@ -34,8 +34,6 @@ void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64
                        int64_t nvalid, const GridDev& g, int probes, double* pmom);
 void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
                   double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems);
-void run_gather_probe(const Launch& L, const double* pmom, int64_t cells, int probes, int QY, int pj,
-                      double* out);
 
 // ---- operators.cu
 // Symmetric half stencil: offsets s = 0..S_min-1 (lexicographically non-negative), per-dim
