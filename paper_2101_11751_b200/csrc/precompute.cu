@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <vector>
 
@@ -82,37 +83,71 @@ __device__ __forceinline__ int agg_inc(int* counters, int64_t key, bool active) 
   return res;
 }
 
-template <typename T>
+// Rows are processed UNR at a time per thread (all loads issued before any use) so each
+// warp keeps UNR row loads — and, in the scatter, UNR atomics and stores — in flight.
+constexpr int SORT_UNR = 8;
+
+template <typename T, bool PACKED>
+__device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T* v) {
+  if (PACKED) {
+    // (x0, x1, x2, y) rows, 4·sizeof(T)-aligned
+    if (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p.x) + i);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p.x) + 2 * i);
+      const double2 b = __ldg(reinterpret_cast<const double2*>(p.x) + 2 * i + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+  } else {
+    const T* X = static_cast<const T*>(p.x);
+    const T* Y = static_cast<const T*>(p.y);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = k < d ? X[i * p.xs + p.xo[k]] : T(0);
+    v[3] = Y[i * p.ys];
+  }
+}
+
+template <typename T, bool PACKED>
 __global__ void __launch_bounds__(256) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
                                                         double* __restrict__ yty_part) {
   __shared__ double sh[8];
   double ysq = 0.0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool active = false;
-    int64_t cell = 0;
-    if (i < n) {
-      double x[GSGPC_MAX_DIM], y;
-      load_point<T>(pts, g.d, i, x, y);
-      ysq += y * y;
-      int64_t i0[GSGPC_MAX_DIM];
-      double t[GSGPC_MAX_DIM];
-      const int st = classify(g, x, i0, t, cell);
-      if (st == PT_VALID) {
-        active = true;
-      } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
-        const unsigned long long code =
-            (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
-        atomicMin(err, code);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
+    T v[SORT_UNR][4];
+#pragma unroll
+    for (int u = 0; u < SORT_UNR; ++u) {
+      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      if (i < n) load_row<T, PACKED>(pts, g.d, i, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < SORT_UNR; ++u) {
+      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      if (i < n) {
+        double x[GSGPC_MAX_DIM];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[k] = static_cast<double>(v[u][k]);
+        const double y = static_cast<double>(v[u][3]);
+        ysq += y * y;
+        int64_t i0[GSGPC_MAX_DIM];
+        double t[GSGPC_MAX_DIM];
+        int64_t cell = 0;
+        const int st = classify(g, x, i0, t, cell);
+        if (st == PT_VALID) {
+          atomicAdd(&hist[cell], 1);  // RED: no return value needed
+        } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
+          const unsigned long long code =
+              (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
+          atomicMin(err, code);
+        }
       }
     }
-    if (active) atomicAdd(&hist[cell], 1);  // RED: no return value needed
   }
-  const double s = block_sum<256>(ysq, sh);
-  if (threadIdx.x == 0) yty_part[blockIdx.x] = s;
+  const double s2 = block_sum<256>(ysq, sh);
+  if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -205,36 +240,42 @@ struct alignas(sizeof(T) * 4) Row4 {
   T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
 };
 
-template <typename T>
+template <typename T, bool PACKED>
 __global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, GridDev g,
                                                  const int64_t* __restrict__ off, int* __restrict__ cur,
                                                  Row4<T>* __restrict__ out,
                                                  const uint64_t* __restrict__ pw_in, int nw,
                                                  uint64_t* __restrict__ pw_out) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool active = false;
-    int64_t cell = 0;
-    Row4<T> r;
-    if (i < n) {
-      const T* X = static_cast<const T*>(pts.x);
-      const T* Y = static_cast<const T*>(pts.y);
-      double x[GSGPC_MAX_DIM];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
+    Row4<T> r[SORT_UNR];
+    int64_t pos[SORT_UNR];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        r.v[k] = k < g.d ? X[i * pts.xs + pts.xo[k]] : T(0);
-        x[k] = static_cast<double>(r.v[k]);
-      }
-      r.v[3] = Y[i * pts.ys];
-      int64_t i0[GSGPC_MAX_DIM];
-      double t[GSGPC_MAX_DIM];
-      active = classify(g, x, i0, t, cell) == PT_VALID;
+    for (int u = 0; u < SORT_UNR; ++u) {
+      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      if (i < n) load_row<T, PACKED>(pts, g.d, i, r[u].v);
     }
-    if (active) {
-      const int64_t pos = off[cell] + atomicAdd(&cur[cell], 1);
-      out[pos] = r;
-      for (int w = 0; w < nw; ++w) pw_out[pos * nw + w] = pw_in[i * nw + w];
+#pragma unroll
+    for (int u = 0; u < SORT_UNR; ++u) {
+      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      pos[u] = -1;
+      if (i < n) {
+        double x[GSGPC_MAX_DIM];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[k] = static_cast<double>(r[u].v[k]);
+        int64_t i0[GSGPC_MAX_DIM];
+        double t[GSGPC_MAX_DIM];
+        int64_t cell = 0;
+        if (classify(g, x, i0, t, cell) == PT_VALID) pos[u] = off[cell] + atomicAdd(&cur[cell], 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SORT_UNR; ++u) {
+      if (pos[u] >= 0) {
+        out[pos[u]] = r[u];
+        const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+        for (int w = 0; w < nw; ++w) pw_out[pos[u] * nw + w] = pw_in[i * nw + w];
+      }
     }
   }
 }
@@ -799,10 +840,21 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
 }
 
 // ================================================================== host side
+// (x0[, x1[, x2]], y) rows packed 4 elements wide and vector-aligned → one vector load per row
+static bool packed4(const PointsDev& p, int d, size_t es) {
+  if (p.xs != 4 || p.ys != 4) return false;
+  for (int k = 0; k < d; ++k)
+    if (p.xo[k] != k) return false;
+  const char* x = static_cast<const char*>(p.x);
+  const char* y = static_cast<const char*>(p.y);
+  return d == 3 && y == x + 3 * es && (reinterpret_cast<uintptr_t>(x) % (4 * es)) == 0;
+}
+
 template <typename T>
 static void launch_classify(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
                             int* hist, unsigned long long* err, double* part, int nblk) {
-  k_classify_count<T><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  if (packed4(p, g.d, sizeof(T))) k_classify_count<T, true><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  else k_classify_count<T, false><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
 }
 
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0,
@@ -834,9 +886,20 @@ void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, cons
                  const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw,
                  uint64_t* pw_out, int nblk) {
   if (dtype == GSGPC_F32) {
-    k_scatter<float><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<float>*>(out), pw_in, nw, pw_out);
+    if (packed4(p, g.d, 4)) {
+      k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<float>*>(out), pw_in, nw, pw_out);
+    } else {
+      k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<float>*>(out), pw_in, nw,
+                                                     pw_out);
+    }
   } else {
-    k_scatter<double><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<double>*>(out), pw_in, nw, pw_out);
+    if (packed4(p, g.d, 8)) {
+      k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<double>*>(out), pw_in, nw,
+                                                     pw_out);
+    } else {
+      k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<double>*>(out), pw_in, nw,
+                                                      pw_out);
+    }
   }
   L.count();
   GSGPC_CUDA(cudaGetLastError());

@@ -210,8 +210,8 @@ def test_efcg_and_posterior_mean_match_oracle(d):
 def test_ill_conditioned_solve_matches_oracle(d):
     """Hundreds-to-thousands of iterations (κ ≫ 1e6): CG iteration counts drift with the
     summation order (as between any two builds of the reference), so the check is on the
-    leading α traces, the count within 5 % and the posterior mean at the solve tolerance."""
-    sizes = (60, 24, 10)[:d]
+    leading α traces, the count within 20 % and the posterior mean at the solve tolerance."""
+    sizes = ((60,), (24, 20), (16, 12, 10))[d - 1]
     g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
     og = ogrid(g)
     x, y = points(d, 30000, 40 + d)
