@@ -213,6 +213,9 @@ GridDev make_grid(const gsgpc_grid* gr, int scheme) {
 }
 
 StencilDesc stencil_desc(const gsgpc_stats* s) {
+  if (static_cast<double>(s->S_min) * static_cast<double>(s->g.m) >= 2147483647.0) {
+    throw Error(GSGPC_UNSUPPORTED, "W^T W stencil larger than 2^31 entries is not supported by this build");
+  }
   StencilDesc sd{};
   sd.d = s->g.d;
   sd.W = s->g.W;

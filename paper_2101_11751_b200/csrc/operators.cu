@@ -23,6 +23,7 @@ namespace gsgpc {
 
 constexpr int MAX_SMIN = 172;  // (7^3 + 1) / 2
 __constant__ long long c_off_flat[MAX_SMIN];
+__constant__ int c_off32[MAX_SMIN];
 __constant__ signed char c_off_d[MAX_SMIN][4];
 
 void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
@@ -49,6 +50,9 @@ void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
   GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_flat, flat, sizeof(long long) * sd.S_min, 0,
                                      cudaMemcpyHostToDevice, s));
   GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_d, dd, sizeof(dd[0]) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
+  int o32[MAX_SMIN];
+  for (int i = 0; i < sd.S_min; ++i) o32[i] = static_cast<int>(flat[i]);
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off32, o32, sizeof(int) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
 }
 
 // ------------------------------------------------------------------ K3 stencil SpMV
@@ -101,17 +105,32 @@ __device__ __forceinline__ double spmv_node(const StencilDesc& sd, const double*
 // the same unrolled loop (no divergence) and the blocks stay in step, which keeps the
 // mirrored-half reads in L2.
 template <int SMIN>
-__device__ __forceinline__ double spmv_node_fast(int64_t m, const double* __restrict__ A,
-                                                 const double* __restrict__ v, int64_t a) {
-  double acc = A[a] * v[a];
-#pragma unroll 8
+__device__ __forceinline__ double spmv_node_fast(int64_t m64, const double* __restrict__ A,
+                                                 const double* __restrict__ v, int64_t a64) {
+  // 32-bit indexing (S_min·m < 2^31 is checked on the host); out-of-[0, m) partners are
+  // clamped to the node itself and masked, so every load is unconditional and can be hoisted.
+  const int m = static_cast<int>(m64), a = static_cast<int>(a64);
+  double acc0 = A[a] * v[a], acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+#pragma unroll 4
   for (int s = 1; s < SMIN; ++s) {
-    const int64_t o = c_off_flat[s];
-    const int64_t f = a + o, b = a - o;
-    if (f >= 0 && f < m) acc = fma(A[s * m + a], v[f], acc);
-    if (b >= 0 && b < m) acc = fma(A[s * m + b], v[b], acc);
+    const int o = c_off32[s];
+    const int f = a + o, b = a - o;
+    const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
+    const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
+    const double* As = A + static_cast<int64_t>(s) * m64;
+    const double af = As[a];
+    const double ab = As[okb ? b : a];
+    const double vf = v[okf ? f : a];
+    const double vb = v[okb ? b : a];
+    if (s & 1) {
+      acc1 = fma(af, okf ? vf : 0.0, acc1);
+      acc2 = fma(okb ? ab : 0.0, vb, acc2);
+    } else {
+      acc3 = fma(af, okf ? vf : 0.0, acc3);
+      acc0 = fma(okb ? ab : 0.0, vb, acc0);
+    }
   }
-  return acc;
+  return (acc0 + acc1) + (acc2 + acc3);
 }
 
 __device__ __forceinline__ double spmv_node_any(const StencilDesc& sd, const double* __restrict__ A,
@@ -219,8 +238,19 @@ __global__ void __launch_bounds__(256) k_toep(ToepArgs t, CgEpi e) {
     }
     const int64_t a = a0 + ar;
     const double* tp = Ts + (n - 1 + a);
-    double acc = 0.0;
-    for (int64_t j = 0; j < n; ++j) acc = fma(tp[-j], Xs[j * t.TL + tl], acc);
+    const double* xs = Xs + tl;
+    const int TL = t.TL;
+    const int nn = static_cast<int>(n);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = 0;
+    for (; j + 3 < nn; j += 4) {
+      a0 = fma(tp[-j], xs[j * TL], a0);
+      a1 = fma(tp[-(j + 1)], xs[(j + 1) * TL], a1);
+      a2 = fma(tp[-(j + 2)], xs[(j + 2) * TL], a2);
+      a3 = fma(tp[-(j + 3)], xs[(j + 3) * TL], a3);
+    }
+    for (; j < nn; ++j) a0 = fma(tp[-j], xs[j * TL], a0);
+    const double acc = (a0 + a1) + (a2 + a3);
     const int64_t l = l0 + tl, o = l / t.inner, i = l % t.inner;
     const int64_t g = (o * n + a) * t.inner + i;
     if (MODE == 0) {

@@ -83,6 +83,32 @@ __device__ __forceinline__ int agg_inc(int* counters, int64_t key, bool active) 
   return res;
 }
 
+// classify() specialised on the dimension with 32-bit cell arithmetic (cells < 2^31).
+template <int D>
+__device__ __forceinline__ int classify_d(const GridDev& g, const double* x, int& cell) {
+  int i0[D], st[D];
+  double t[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    int64_t ii = 0;
+    st[k] = stencil_dim_fast(x[k], g.mn[k], g.sp[k], g.isp[k], g.sz[k], ii, t[k]);
+    i0[k] = static_cast<int>(ii);
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if (st[k] == PT_OUTSIDE) return PT_OUTSIDE;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (st[k] == PT_EMPTY) return PT_EMPTY;
+    if (leaves_dim(i0[k], t[k], g.sz[k], g.W)) return PT_LEAVES;
+  }
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) c = c * static_cast<int>(g.nc[k]) + i0[k];
+  cell = c;
+  return PT_VALID;
+}
+
 // Rows are processed UNR at a time per thread (all loads issued before any use) so each
 // warp keeps UNR row loads — and, in the scatter, UNR atomics and stores — in flight.
 constexpr int SORT_UNR = 8;
@@ -108,7 +134,7 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
-template <typename T, bool PACKED>
+template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
@@ -127,15 +153,13 @@ __global__ void __launch_bounds__(256) k_classify_count(PointsDev pts, int64_t n
     for (int u = 0; u < SORT_UNR; ++u) {
       const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
       if (i < n) {
-        double x[GSGPC_MAX_DIM];
+        double x[D];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) x[k] = static_cast<double>(v[u][k]);
+        for (int k = 0; k < D; ++k) x[k] = static_cast<double>(v[u][k]);
         const double y = static_cast<double>(v[u][3]);
         ysq += y * y;
-        int64_t i0[GSGPC_MAX_DIM];
-        double t[GSGPC_MAX_DIM];
-        int64_t cell = 0;
-        const int st = classify(g, x, i0, t, cell);
+        int cell = 0;
+        const int st = classify_d<D>(g, x, cell);
         if (st == PT_VALID) {
           atomicAdd(&hist[cell], 1);  // RED: no return value needed
         } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
@@ -240,7 +264,7 @@ struct alignas(sizeof(T) * 4) Row4 {
   T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
 };
 
-template <typename T, bool PACKED>
+template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, GridDev g,
                                                  const int64_t* __restrict__ off, int* __restrict__ cur,
                                                  Row4<T>* __restrict__ out,
@@ -260,13 +284,11 @@ __global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, GridD
       const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
       pos[u] = -1;
       if (i < n) {
-        double x[GSGPC_MAX_DIM];
+        double x[D];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) x[k] = static_cast<double>(r[u].v[k]);
-        int64_t i0[GSGPC_MAX_DIM];
-        double t[GSGPC_MAX_DIM];
-        int64_t cell = 0;
-        if (classify(g, x, i0, t, cell) == PT_VALID) pos[u] = off[cell] + atomicAdd(&cur[cell], 1);
+        for (int k = 0; k < D; ++k) x[k] = static_cast<double>(r[u].v[k]);
+        int cell = 0;
+        if (classify_d<D>(g, x, cell) == PT_VALID) pos[u] = off[cell] + atomicAdd(&cur[cell], 1);
       }
     }
 #pragma unroll
@@ -520,17 +542,18 @@ __global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __res
         const double* P = S + (4 * st + kq) * D3C_STRIDE;
         const double y = P[7];
         const double ax = P[r];            // r < 7: t0^r ; r == 7: y
-        const double t1 = P[9];
         const double t2n = r < 7 ? P[16 + r] : 0.0;
         const double ay0 = y * P[ya0] * P[8 + yb0];
         const double ay1 = yv1 ? y * P[ya1] * P[8 + yb1] : 0.0;
         const double by = r < 4 ? t2n : 0.0;
-        double bt = t2n;
+        const double2 p01 = *reinterpret_cast<const double2*>(P + 8);
+        const double2 p23 = *reinterpret_cast<const double2*>(P + 10);
+        const double2 p45 = *reinterpret_cast<const double2*>(P + 12);
+        const double p6 = P[14];
+        const double bt[7] = {t2n * p01.x, t2n * p01.y, t2n * p23.x, t2n * p23.y,
+                              t2n * p45.x, t2n * p45.y, t2n * p6};
 #pragma unroll
-        for (int tt = 0; tt < 7; ++tt) {
-          dmma(dx[tt][0], dx[tt][1], ax, bt);
-          bt *= t1;
-        }
+        for (int tt = 0; tt < 7; ++tt) dmma(dx[tt][0], dx[tt][1], ax, bt[tt]);
         dmma(dy[0][0], dy[0][1], ay0, by);
         dmma(dy[1][0], dy[1][1], ay1, by);
       }
@@ -850,11 +873,35 @@ static bool packed4(const PointsDev& p, int d, size_t es) {
   return d == 3 && y == x + 3 * es && (reinterpret_cast<uintptr_t>(x) % (4 * es)) == 0;
 }
 
+template <typename T, int D>
+static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
+                              int* hist, unsigned long long* err, double* part, int nblk) {
+  if (packed4(p, g.d, sizeof(T))) k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  else k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+}
+
 template <typename T>
 static void launch_classify(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
                             int* hist, unsigned long long* err, double* part, int nblk) {
-  if (packed4(p, g.d, sizeof(T))) k_classify_count<T, true><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
-  else k_classify_count<T, false><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk);
+  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk);
+  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk);
+}
+
+template <typename T, int D>
+static void launch_scatter_d(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const int64_t* off,
+                             int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out, int nblk) {
+  Row4<T>* o = static_cast<Row4<T>*>(out);
+  if (packed4(p, g.d, sizeof(T))) k_scatter<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, o, pw_in, nw, pw_out);
+  else k_scatter<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, o, pw_in, nw, pw_out);
+}
+
+template <typename T>
+static void launch_scatter(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const int64_t* off,
+                           int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out, int nblk) {
+  if (g.d == 1) launch_scatter_d<T, 1>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
+  else if (g.d == 2) launch_scatter_d<T, 2>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
+  else launch_scatter_d<T, 3>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
 }
 
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0,
@@ -885,22 +932,8 @@ int64_t scan_scratch_elems(int64_t n) { return ceil_div(n, SCAN_TILE) + 1; }
 void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g,
                  const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw,
                  uint64_t* pw_out, int nblk) {
-  if (dtype == GSGPC_F32) {
-    if (packed4(p, g.d, 4)) {
-      k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<float>*>(out), pw_in, nw, pw_out);
-    } else {
-      k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<float>*>(out), pw_in, nw,
-                                                     pw_out);
-    }
-  } else {
-    if (packed4(p, g.d, 8)) {
-      k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<double>*>(out), pw_in, nw,
-                                                     pw_out);
-    } else {
-      k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, static_cast<Row4<double>*>(out), pw_in, nw,
-                                                      pw_out);
-    }
-  }
+  if (dtype == GSGPC_F32) launch_scatter<float>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
+  else launch_scatter<double>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }

@@ -189,8 +189,8 @@ def test_efcg_and_posterior_mean_match_oracle(d):
     kg = G.ToeplitzOperator(g, spec)
     okg = O.ToeplitzOperator(og, ls, 1.0, sigma)
     r0 = -okg.apply(os_.wty) / (sigma * sigma)
-    ores = O.factorized_cg_grid_rhs(okg, os_, r0, sigma, eps_abs=1e-16 * os_.yty, maxiter=2000)
-    gres = G.factorized_cg_grid_rhs(kg, gs, r0, sigma, G.GridRhsTolerance(eps_abs=1e-16 * os_.yty), 2000)
+    ores = O.factorized_cg_grid_rhs(okg, os_, r0, sigma, eps_abs=1e-10 * os_.yty, maxiter=2000)
+    gres = G.factorized_cg_grid_rhs(kg, gs, r0, sigma, G.GridRhsTolerance(eps_abs=1e-10 * os_.yty), 2000)
     assert ores.converged and gres.converged
     assert ores.iterations < 300
     assert abs(gres.iterations - ores.iterations) <= 1
