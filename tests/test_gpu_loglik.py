@@ -76,25 +76,28 @@ def test_loglik_matches_oracle():
     acc.add(x, y)
     st = acc.finalize()
     kg = G.ToeplitzOperator(g, spec)
-    opts = G.LoglikOptions(solve_tol=1e-6, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.0), seed=0)
+    # data-fit solve to 1e-9 so the quadratic terms of the two sides agree far below 1e-5
+    opts = G.LoglikOptions(solve_tol=1e-9, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.0), seed=0,
+                           maxiter=5000)
     r = G.log_likelihood_gsgp(st, kg, sigma, opts)
     og = ogrid(g)
     ost = O.sufficient_stats(og, x, y)
     okg = O.ToeplitzOperator(og, ls, 1.0, sigma)
-    ref = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-6, probes=30, max_depth=50,
-                                quad_tol=0.0, seed=0, route="ski-operator")
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-9, probes=30, max_depth=50,
+                                quad_tol=0.0, seed=0, route="ski-operator", maxiter=5000)
     assert abs(r.const_term - ref["const_term"]) <= 1e-12 * abs(ref["const_term"])
     assert abs(r.quad_term - ref["quad_term"]) <= 1e-5 * abs(ref["quad_term"])
     assert abs(r.logdet_term - ref["logdet_term"]) <= 1e-5 * abs(ref["logdet_term"])
     assert abs(r.loglik - ref["loglik"]) <= 1e-5 * abs(ref["loglik"])
-    # ~550-iteration ill-conditioned data-fit solve: count within 2 %
-    assert abs(r.solver_iterations - ref["solver_iterations"]) <= max(1, 0.02 * ref["solver_iterations"])
+    # ill-conditioned data-fit solve (hundreds of iterations): count within 5 %
+    assert abs(r.solver_iterations - ref["solver_iterations"]) <= max(1, 0.05 * ref["solver_iterations"])
     assert r.probes_used == 30
     # default quad_tol (0.01) early-stop path
-    opts2 = G.LoglikOptions(solve_tol=1e-6, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.01), seed=0)
+    opts2 = G.LoglikOptions(solve_tol=1e-9, probes=30, slq=G.SlqOptions(max_depth=50, quad_tol=0.01), seed=0,
+                            maxiter=5000)
     r2 = G.log_likelihood_gsgp(st, kg, sigma, opts2)
-    ref2 = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-6, probes=30, max_depth=50,
-                                 quad_tol=0.01, seed=0, route="ski-operator")
+    ref2 = O.log_likelihood_gsgp(ost, okg, sigma, grid=og, x=x, solve_tol=1e-9, probes=30, max_depth=50,
+                                 quad_tol=0.01, seed=0, route="ski-operator", maxiter=5000)
     assert abs(r2.loglik - ref2["loglik"]) <= 1e-5 * abs(ref2["loglik"])
 
 
