@@ -1310,35 +1310,48 @@ CgOutcome run_efcg(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, const double* r
   GSGPC_CUDA(cudaMemsetAsync(b.s, 0, sizeof(double) * m, ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(b.z, 0, sizeof(double) * m, ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(b.x, 0, sizeof(double) * m, ctx->stream));
-  run_cg_init(L, sd, s->stencil(), kg->dev, b, m);
-  // capture (once per cache) a graph of kGraphIters iterations
-  if (!c.exec) {
-    cudaGraph_t graph;
-    uint64_t dummy = 0;
-    const Launch Lc{ctx->stream, &dummy};
-    GSGPC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < kGraphIters; ++i) run_cg_iter(Lc, sd, s->stencil(), kg->dev, b, m);
-    GSGPC_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
-    GSGPC_CUDA(cudaGraphInstantiate(&c.exec, graph, 0));
-    GSGPC_CUDA(cudaGraphDestroy(graph));
-    c.B = kGraphIters;
-  }
-  // kernels per iteration (counted per replay)
+  static const bool use_graph = [] {
+    const char* e = getenv("GSGPC_CG_GRAPH");
+    return e && e[0] == '1';
+  }();
   const int per_iter = 2 + s->g.d;
   cudaEvent_t e0, e1;
   GSGPC_CUDA(cudaEventCreate(&e0));
   GSGPC_CUDA(cudaEventCreate(&e1));
-  GSGPC_CUDA(cudaEventRecord(e0, ctx->stream));
   CgState h{};
-  for (;;) {
+  if (!use_graph) {
+    // one cooperative launch runs the whole solve (efcg_persistent.cu)
+    GSGPC_CUDA(cudaEventRecord(e0, ctx->stream));
+    run_efcg_persistent(L, sd, s->stencil(), kg->dev, b, 1);
+    GSGPC_CUDA(cudaEventRecord(e1, ctx->stream));
     GSGPC_CUDA(cudaMemcpyAsync(ctx->pin.p, b.st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
     GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
     std::memcpy(&h, ctx->pin.p, sizeof(CgState));
-    if (h.done) break;
-    GSGPC_CUDA(cudaGraphLaunch(c.exec, ctx->stream));
-    ctx->launches += static_cast<uint64_t>(per_iter) * c.B;
+  } else {
+    run_cg_init(L, sd, s->stencil(), kg->dev, b, m);
+    // capture (once per cache) a graph of kGraphIters iterations
+    if (!c.exec) {
+      cudaGraph_t graph;
+      uint64_t dummy = 0;
+      const Launch Lc{ctx->stream, &dummy};
+      GSGPC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      for (int i = 0; i < kGraphIters; ++i) run_cg_iter(Lc, sd, s->stencil(), kg->dev, b, m);
+      GSGPC_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+      GSGPC_CUDA(cudaGraphInstantiate(&c.exec, graph, 0));
+      GSGPC_CUDA(cudaGraphDestroy(graph));
+      c.B = kGraphIters;
+    }
+    GSGPC_CUDA(cudaEventRecord(e0, ctx->stream));
+    for (;;) {
+      GSGPC_CUDA(cudaMemcpyAsync(ctx->pin.p, b.st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
+      GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::memcpy(&h, ctx->pin.p, sizeof(CgState));
+      if (h.done) break;
+      GSGPC_CUDA(cudaGraphLaunch(c.exec, ctx->stream));
+      ctx->launches += static_cast<uint64_t>(per_iter) * c.B;
+    }
+    GSGPC_CUDA(cudaEventRecord(e1, ctx->stream));
   }
-  GSGPC_CUDA(cudaEventRecord(e1, ctx->stream));
   GSGPC_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   GSGPC_CUDA(cudaEventElapsedTime(&ms, e0, e1));

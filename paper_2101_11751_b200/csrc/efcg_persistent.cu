@@ -1,0 +1,354 @@
+// efcg_persistent.cu — the whole factorized_cg_grid_rhs loop (solvers.cpp:271-336) as ONE
+// cooperative kernel: update → stencil SpMV + ρ → d Toeplitz mode products → fused
+// epilogue + pap, separated by grid-wide barriers.  α, β, ρ, pap never leave the device;
+// every block reduces the per-block partials itself in the same fixed order, so all blocks
+// hold bit-identical scalars without an extra barrier.  Replaces the per-iteration chain of
+// 2 + d kernel launches (launch gaps dominated the m ≈ 1e5 iteration).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+#include "precompute.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace gsgpc {
+
+constexpr int PCG_NT = 256;
+
+__constant__ int c_pcg_off[172];
+
+struct PcgMode {
+  int64_t n, inner, L;
+  int TL, TA;
+  int64_t tiles, chunks;
+  const double* gen;
+};
+
+struct PcgArgs {
+  int m;
+  int d;
+  const double* A;
+  double *r, *u, *s, *z, *x, *t0, *t1;
+  double *part_a, *part_b;
+  double *trace, *alphas, *betas;
+  CgState* st;
+  PcgMode mode[3];
+  int init;
+};
+
+// Sum of the per-block partials, identical in every block (fixed order, one warp).
+__device__ __forceinline__ double grid_reduce(const double* part, int np, double* sh1) {
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < np; i += 32) v += __ldcg(part + i);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *sh1 = v;
+  }
+  __syncthreads();
+  const double r = *sh1;
+  __syncthreads();
+  return r;
+}
+
+template <int SMIN>
+__device__ __forceinline__ double pcg_spmv_node(int m, const double* __restrict__ A, const double* __restrict__ v,
+                                                int a) {
+  double acc0 = A[a] * __ldcg(v + a), acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+#pragma unroll 4
+  for (int s = 1; s < SMIN; ++s) {
+    const int o = c_pcg_off[s];
+    const int f = a + o, b = a - o;
+    const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
+    const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
+    const double* As = A + static_cast<int64_t>(s) * m;
+    const double af = As[a];
+    const double ab = As[okb ? b : a];
+    const double vf = __ldcg(v + (okf ? f : a));
+    const double vb = __ldcg(v + (okb ? b : a));
+    if (s & 1) {
+      acc1 = fma(af, okf ? vf : 0.0, acc1);
+      acc2 = fma(okb ? ab : 0.0, vb, acc2);
+    } else {
+      acc3 = fma(af, okf ? vf : 0.0, acc3);
+      acc0 = fma(okb ? ab : 0.0, vb, acc0);
+    }
+  }
+  return (acc0 + acc1) + (acc2 + acc3);
+}
+
+// One Toeplitz mode product (grid-stride over line tiles × output chunks).  EPI: fused
+// v̂ = (K û) + σ² r̂, ŝ = û + β ŝ, z̄ = v̂ + β z̄ and the ŝ·z̄ partial.
+template <bool EPI>
+__device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, double* Y, double* smem,
+                                         const PcgArgs& a, double beta, double s2, double& dot) {
+  const int64_t n = c.n;
+  double* Ts = smem;
+  double* Xs = smem + 2 * n - 1;
+  const int64_t nwork = c.tiles * c.chunks;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t tile = w % c.tiles, chunk = w / c.tiles;
+    const int64_t l0 = tile * c.TL;
+    const int nl = static_cast<int>(imin64(c.TL, c.L - l0));
+    const int64_t a0 = chunk * c.TA;
+    const int na = static_cast<int>(imin64(c.TA, n - a0));
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < 2 * n - 1; q += PCG_NT) {
+      const int64_t dd = q - (n - 1);
+      Ts[q] = c.gen[dd < 0 ? -dd : dd];
+    }
+    if (c.inner == 1) {
+      for (int64_t q = threadIdx.x; q < static_cast<int64_t>(nl) * n; q += PCG_NT) {
+        const int64_t tl = q / n, j = q % n;
+        Xs[j * c.TL + tl] = __ldcg(X + (l0 + tl) * n + j);
+      }
+    } else {
+      for (int64_t q = threadIdx.x; q < static_cast<int64_t>(c.TL) * n; q += PCG_NT) {
+        const int tl = static_cast<int>(q % c.TL);
+        const int64_t j = q / c.TL;
+        if (tl < nl) {
+          const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
+          Xs[j * c.TL + tl] = __ldcg(X + (o * n + j) * c.inner + i);
+        }
+      }
+    }
+    __syncthreads();
+    const int total = nl * na;
+    for (int uu = threadIdx.x; uu < total; uu += PCG_NT) {
+      int tl, ar;
+      if (c.inner == 1) {
+        ar = uu % na;
+        tl = uu / na;
+      } else {
+        tl = uu % nl;
+        ar = uu / nl;
+      }
+      const int64_t aa = a0 + ar;
+      const double* tp = Ts + (n - 1 + aa);
+      const double* xs = Xs + tl;
+      const int TL = c.TL;
+      const int nn = static_cast<int>(n);
+      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+      int j = 0;
+      for (; j + 3 < nn; j += 4) {
+        b0 = fma(tp[-j], xs[j * TL], b0);
+        b1 = fma(tp[-(j + 1)], xs[(j + 1) * TL], b1);
+        b2 = fma(tp[-(j + 2)], xs[(j + 2) * TL], b2);
+        b3 = fma(tp[-(j + 3)], xs[(j + 3) * TL], b3);
+      }
+      for (; j < nn; ++j) b0 = fma(tp[-j], xs[j * TL], b0);
+      const double acc = (b0 + b1) + (b2 + b3);
+      const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
+      const int64_t g = (o * n + aa) * c.inner + i;
+      if (!EPI) {
+        Y[g] = acc;
+      } else {
+        const double v = acc + s2 * __ldcg(a.r + g);
+        const double sn = __ldcg(a.u + g) + beta * a.s[g];
+        const double zn = v + beta * a.z[g];
+        a.s[g] = sn;
+        a.z[g] = zn;
+        dot = fma(sn, zn, dot);
+      }
+    }
+  }
+}
+
+template <int SMIN>
+__global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
+  extern __shared__ double smem[];
+  __shared__ double sh[8];
+  __shared__ double sh1;
+  cg::grid_group grid = cg::this_grid();
+  CgState* st = a.st;
+  const double s2 = st->sigma_sq;
+  const int maxiter = st->maxiter;
+  double rho = st->rho, pap = st->pap, eps = st->eps;
+  int iter = st->iter;
+  int converged = 0, breakdown = 0;
+  const int m = a.m;
+  const int tid = blockIdx.x * PCG_NT + threadIdx.x;
+  const int nthr = gridDim.x * PCG_NT;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+
+  auto spmv_phase = [&]() {
+    double dot = 0.0;
+    for (int node = tid; node < m; node += nthr) {
+      const double u = pcg_spmv_node<SMIN>(m, a.A, a.r, node);
+      a.u[node] = u;
+      dot = fma(u, __ldcg(a.r + node), dot);
+    }
+    const double bs = block_sum<PCG_NT>(dot, sh);
+    if (threadIdx.x == 0) a.part_a[blockIdx.x] = bs;
+  };
+  auto kg_phase = [&](double beta) {
+    double dot = 0.0;
+    const double* src = a.u;
+    for (int k = a.d - 1; k >= 1; --k) {
+      double* dst = (src == a.t0) ? a.t1 : a.t0;
+      pcg_mode<false>(a.mode[k], src, dst, smem, a, beta, s2, dot);
+      grid.sync();
+      src = dst;
+    }
+    pcg_mode<true>(a.mode[0], src, nullptr, smem, a, beta, s2, dot);
+    const double bs = block_sum<PCG_NT>(dot, sh);
+    if (threadIdx.x == 0) a.part_b[blockIdx.x] = bs;
+  };
+
+  if (a.init) {
+    spmv_phase();
+    grid.sync();
+    rho = grid_reduce(a.part_a, gridDim.x, &sh1);
+    eps = st->eps_abs >= 0.0 ? st->eps_abs : st->rel_tol * st->rel_tol * rho;
+    if (leader) a.trace[0] = rho;
+    if (rho <= eps) {
+      converged = 1;
+    } else {
+      kg_phase(0.0);
+      grid.sync();
+      pap = grid_reduce(a.part_b, gridDim.x, &sh1);
+    }
+  }
+  while (!converged) {
+    if (iter >= maxiter) break;
+    if (pap <= 0.0) {
+      breakdown = 1;
+      break;
+    }
+    const double alpha = rho / pap;
+    for (int i = tid; i < m; i += nthr) {
+      a.x[i] += alpha * __ldcg(a.s + i);  // ŝ, z̄ were written by other blocks
+      a.r[i] -= alpha * __ldcg(a.z + i);
+    }
+    if (leader) a.alphas[iter] = alpha;
+    grid.sync();
+    spmv_phase();
+    grid.sync();
+    const double rho_new = grid_reduce(a.part_a, gridDim.x, &sh1);
+    ++iter;
+    if (leader) a.trace[iter] = rho_new;
+    if (rho_new <= eps) {
+      converged = 1;
+      rho = rho_new;
+      break;
+    }
+    const double beta = rho_new / rho;
+    if (leader) a.betas[iter - 1] = beta;
+    rho = rho_new;
+    kg_phase(beta);
+    grid.sync();
+    pap = grid_reduce(a.part_b, gridDim.x, &sh1);
+  }
+  if (leader) {
+    st->rho = rho;
+    st->pap = pap;
+    st->eps = eps;
+    st->iter = iter;
+    st->converged = converged;
+    st->breakdown = breakdown;
+    st->done = 1;
+  }
+}
+
+static PcgMode mode_cfg(const KgDev& kg, int k) {
+  PcgMode c{};
+  int64_t inner = 1, outer = 1;
+  for (int j = k + 1; j < kg.d; ++j) inner *= kg.sz[j];
+  for (int j = 0; j < k; ++j) outer *= kg.sz[j];
+  const int64_t n = kg.sz[k];
+  c.n = n;
+  c.inner = inner;
+  c.L = inner * outer;
+  const int64_t cap = 6144;  // doubles of dynamic smem per block (48 KB)
+  if (3 * n > cap) throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2048 nodes is not supported");
+  int64_t TL = std::min<int64_t>(32, (cap - 2 * n) / n);
+  TL = std::max<int64_t>(1, std::min<int64_t>(TL, c.L));
+  c.TL = static_cast<int>(TL);
+  c.tiles = ceil_div(c.L, TL);
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(1184, c.tiles), ceil_div(n, 32)));
+  c.TA = static_cast<int>(ceil_div(n, chunks));
+  c.chunks = ceil_div(n, c.TA);
+  c.gen = kg.gen[k];
+  return c;
+}
+
+template <int SMIN>
+static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
+  static int grid = 0;
+  static size_t grid_smem = 0;
+  if (grid == 0 || grid_smem != smem) {
+    int dev = 0, sms = 0, per_sm = 0;
+    GSGPC_CUDA(cudaGetDevice(&dev));
+    GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
+    if (per_sm < 1) throw Error(GSGPC_CUDA_ERROR, "persistent EFCG kernel cannot be resident");
+    grid = sms * std::min(per_sm, 4);
+    grid_smem = smem;
+  }
+  PcgArgs aa = a;
+  void* params[] = {&aa};
+  GSGPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_efcg_persistent<SMIN>), dim3(grid), dim3(PCG_NT),
+                                         params, smem, L.s));
+  L.count();
+}
+
+int pcg_max_blocks() { return 148 * 4 + 64; }
+
+void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
+                         int init) {
+  int o32[172];
+  {
+    const int E = 2 * sd.W - 1;
+    int S = 1;
+    for (int k = 0; k < sd.d; ++k) S *= E;
+    const int c0 = (S - 1) / 2;
+    for (int s2 = 0; s2 < sd.S_min; ++s2) {
+      int q = c0 + s2;
+      int dig[3] = {0, 0, 0};
+      for (int k = sd.d - 1; k >= 0; --k) {
+        dig[k] = q % E - (sd.W - 1);
+        q /= E;
+      }
+      long long f = 0;
+      for (int k = 0; k < sd.d; ++k) f = f * sd.sz[k] + dig[k];
+      o32[s2] = static_cast<int>(f);
+    }
+  }
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pcg_off, o32, sizeof(int) * sd.S_min, 0, cudaMemcpyHostToDevice, L.s));
+  PcgArgs a{};
+  a.m = static_cast<int>(sd.m);
+  a.d = sd.d;
+  a.A = A;
+  a.r = b.r;
+  a.u = b.u;
+  a.s = b.s;
+  a.z = b.z;
+  a.x = b.x;
+  a.t0 = b.kt0;
+  a.t1 = b.kt1;
+  a.part_a = b.part_a;
+  a.part_b = b.part_b;
+  a.trace = b.trace;
+  a.alphas = b.alphas;
+  a.betas = b.betas;
+  a.st = b.st;
+  a.init = init;
+  size_t smem = 0;
+  for (int k = 0; k < kg.d; ++k) {
+    a.mode[k] = mode_cfg(kg, k);
+    smem = std::max(smem, sizeof(double) * (2 * a.mode[k].n - 1 + a.mode[k].TL * a.mode[k].n));
+  }
+  switch (sd.S_min) {
+    case 172: launch_pcg<172>(L, a, smem); break;
+    case 25: launch_pcg<25>(L, a, smem); break;
+    case 4: launch_pcg<4>(L, a, smem); break;
+    case 14: launch_pcg<14>(L, a, smem); break;
+    case 5: launch_pcg<5>(L, a, smem); break;
+    default: launch_pcg<2>(L, a, smem); break;
+  }
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+}  // namespace gsgpc

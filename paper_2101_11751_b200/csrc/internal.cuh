@@ -94,18 +94,26 @@ __device__ __forceinline__ int stencil_dim(double x, double mn, double sp, int64
   return PT_VALID;
 }
 
-// Same result as stencil_dim for the cell index i0 and the status, with t to within a few
-// ulp: u ≈ (x - min)·(1/spacing) differs from the correctly rounded quotient by ≤ 2 ulp
-// (≤ 5e-13 for u < 2^11), so whenever u is more than 4e-9 from every integer the snap rule
-// cannot fire, floor(u) and the range tests agree with the exact path; otherwise (snap zone,
-// cell boundaries, range ends, NaN, inf) fall back to the exact division.  Used by the
-// precompute (cell binning + moments, tolerance 1e-10), never for reported weights.
+// Same result as stencil_dim (status, cell index i0; t to within a few ulp) without the
+// IEEE division on all but a measure-zero set of inputs.  u ≈ (x - min)·(1/spacing)
+// differs from the correctly rounded quotient u* by ≤ 2 ulp(u) ≤ |u|·2^-51.  With
+// d = |u - round(u)| and margin e = 1e-12 + |u|·2^-48:
+//   d < 1e-9 - e  → |u* - round(u*)| < 1e-9: the reference snaps, u = round(u) exactly;
+//   d > 1e-9 + e  → it does not snap, and floor(u) = floor(u*) (no integer in between) and
+//                   the range tests agree;
+//   otherwise (|d - 1e-9| ≤ e) → fall back to the exact division.
+// NaN / ±inf take the first branch with u = NaN / ±inf and classify like stencil_dim.
+// Used by the precompute (cell binning + moments, tolerance 1e-10), never for reported weights.
 __device__ __forceinline__ int stencil_dim_fast(double x, double mn, double sp, double isp, int64_t size,
                                                 int64_t& i0, double& t) {
-  const double u = __dsub_rn(x, mn) * isp;
+  double u = __dsub_rn(x, mn) * isp;
   const double r = round(u);
-  if (!(fabs(u - r) > 4e-9)) return stencil_dim(x, mn, sp, size, i0, t);
+  const double dd = fabs(u - r);
+  const double e = 1e-12 + fabs(u) * 3.552713678800501e-15;
+  if (dd >= 1e-9 - e && dd <= 1e-9 + e) return stencil_dim(x, mn, sp, size, i0, t);
+  if (dd < 1e-9) u = r;
   if (u < 0.0 || u > static_cast<double>(size - 1)) return PT_OUTSIDE;
+  if (u != u) return PT_EMPTY;
   int64_t i = static_cast<int64_t>(floor(u));
   if (i > size - 2) i = size - 2;
   i0 = i;

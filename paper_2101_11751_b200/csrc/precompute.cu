@@ -135,7 +135,7 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
 }
 
 template <typename T, bool PACKED, int D>
-__global__ void __launch_bounds__(256) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
+__global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
                                                         double* __restrict__ yty_part) {
@@ -265,7 +265,7 @@ struct alignas(sizeof(T) * 4) Row4 {
 };
 
 template <typename T, bool PACKED, int D>
-__global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, GridDev g,
+__global__ void __launch_bounds__(256, 3) k_scatter(PointsDev pts, int64_t n, GridDev g,
                                                  const int64_t* __restrict__ off, int* __restrict__ cur,
                                                  Row4<T>* __restrict__ out,
                                                  const uint64_t* __restrict__ pw_in, int nw,
