@@ -100,7 +100,17 @@ struct gsgpc_ctx {
   std::map<std::string, std::unique_ptr<DBuf>> bufs;
   PinnedBuf pin;
   std::unique_ptr<CgCache> cg;
+  cudaStream_t copy = nullptr;   // H2D staging stream (overlaps the next batch's copy with compute)
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   Launch L() { return Launch{stream, &launches}; }
+  void ensure_copy_stream() {
+    if (copy) return;
+    GSGPC_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      GSGPC_CUDA(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
+      GSGPC_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
+  }
   DBuf& buf(const std::string& name) {
     auto& b = bufs[name];
     if (!b) b.reset(new DBuf());
@@ -337,7 +347,8 @@ void check_points(const gsgpc_points* p, int64_t n, bool need_y) {
 // Stage rows [r0, r1) of a host-resident point set into device memory; returns the device
 // descriptor for that chunk (row 0 = r0).
 PointsDev stage_points(gsgpc_ctx* ctx, const gsgpc_points* p, int d, int64_t r0, int64_t r1, bool need_y,
-                       const char* slot) {
+                       const char* slot, cudaStream_t strm = nullptr) {
+  if (!strm) strm = ctx->stream;
   const size_t es = dtype_size(p->dtype);
   const int64_t rows = r1 - r0;
   PointsDev q{};
@@ -358,7 +369,7 @@ PointsDev stage_points(gsgpc_ctx* ctx, const gsgpc_points* p, int d, int64_t r0,
   if (columns) {
     for (int k = 0; k < d; ++k) {
       GSGPC_CUDA(cudaMemcpyAsync(dx + es * k * rows, hx + es * (p->x_col_offset[k] + r0), es * rows,
-                                 cudaMemcpyHostToDevice, ctx->stream));
+                                 cudaMemcpyHostToDevice, strm));
       q.xo[k] = k * rows;
     }
     q.xs = 1;
@@ -367,7 +378,7 @@ PointsDev stage_points(gsgpc_ctx* ctx, const gsgpc_points* p, int d, int64_t r0,
       throw Error(GSGPC_UNSUPPORTED, "host points: column offset beyond the row stride");
     }
     const int64_t span = (rows - 1) * p->x_row_stride + std::max(maxo, y_in_x ? yoff : 0) + 1;
-    GSGPC_CUDA(cudaMemcpyAsync(dx, hx + es * r0 * p->x_row_stride, es * span, cudaMemcpyHostToDevice, ctx->stream));
+    GSGPC_CUDA(cudaMemcpyAsync(dx, hx + es * r0 * p->x_row_stride, es * span, cudaMemcpyHostToDevice, strm));
     q.xs = p->x_row_stride;
     for (int k = 0; k < d; ++k) q.xo[k] = p->x_col_offset[k];
   }
@@ -381,7 +392,7 @@ PointsDev stage_points(gsgpc_ctx* ctx, const gsgpc_points* p, int d, int64_t r0,
   } else {
     char* dy = dx + es * xelems;
     const int64_t span = (rows - 1) * p->y_stride + 1;
-    GSGPC_CUDA(cudaMemcpyAsync(dy, hy + es * r0 * p->y_stride, es * span, cudaMemcpyHostToDevice, ctx->stream));
+    GSGPC_CUDA(cudaMemcpyAsync(dy, hy + es * r0 * p->y_stride, es * span, cudaMemcpyHostToDevice, strm));
     q.y = dy;
     q.ys = p->y_stride;
   }
@@ -586,6 +597,14 @@ void gsgpc_ctx_destroy(gsgpc_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->cg.reset();
   ctx->bufs.clear();
+  if (ctx->copy) {
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamDestroy(ctx->copy);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(ctx->ev_copied[i]);
+      cudaEventDestroy(ctx->ev_free[i]);
+    }
+  }
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -740,38 +759,90 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
     const std::vector<std::mt19937_64> gens_backup = s->gens;  // restored if a batch fails
     const bool pw_dev = nw ? is_device_ptr(probe_words) : true;
     const int64_t CH = dev ? (int64_t{1} << 27) : (int64_t{1} << 24);
-    for (int64_t r0 = 0; r0 < n; r0 += CH) {
-      const int64_t r1 = std::min(n, r0 + CH);
-      PointsDev P;
-      if (dev) {
-        P = points_dev(pts, s->g.d, r0);
-      } else {
-        PhaseTimer pt(ctx);
-        const int h = pt.begin(5);
-        P = stage_points(ctx, pts, s->g.d, r0, r1, true, "stage");
-        pt.end(h);
+    const int64_t nchunks = ceil_div(n, CH);
+    // A batch larger than one chunk commits chunk by chunk; snapshot the accumulator so a
+    // failing later chunk still leaves it unchanged (the reference's single pass throws
+    // before returning any statistics).
+    const int64_t n_before = s->n;
+    if (nchunks > 1) {
+      DBuf& bm = ctx->buf("bk_mom");
+      bm.ensure(sizeof(double) * s->g.cells * s->Q + 8);
+      GSGPC_CUDA(cudaMemcpyAsync(bm.p, s->mom.p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      DBuf& by = ctx->buf("bk_yty");
+      by.ensure(sizeof(double));
+      GSGPC_CUDA(cudaMemcpyAsync(by.p, s->yty.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      if (s->probes) {
+        DBuf& bp = ctx->buf("bk_pmom");
+        bp.ensure(sizeof(double) * s->g.cells * s->probes * s->QY);
+        GSGPC_CUDA(cudaMemcpyAsync(bp.p, s->pmom.p, sizeof(double) * s->g.cells * s->probes * s->QY,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
       }
-      const uint64_t* pw = nullptr;
-      if (s->probe_seeded && !probe_words) {
-        gen_probe_words(ctx, s, r1 - r0);
-        pw = ctx->buf("probe_stage").as<uint64_t>();
-      } else if (nw) {
-        if (pw_dev) {
-          pw = probe_words + r0 * nw;
-        } else {
-          DBuf& b = ctx->buf("probe_stage");
-          b.ensure(sizeof(uint64_t) * nw * (r1 - r0));
-          GSGPC_CUDA(cudaMemcpyAsync(b.p, probe_words + r0 * nw, sizeof(uint64_t) * nw * (r1 - r0),
-                                     cudaMemcpyHostToDevice, ctx->stream));
-          pw = b.as<uint64_t>();
+    }
+    auto rollback = [&] {
+      s->gens = gens_backup;
+      if (nchunks > 1) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
+        cudaMemcpy(s->yty.p, ctx->buf("bk_yty").p, sizeof(double), cudaMemcpyDeviceToDevice);
+        if (s->probes) {
+          cudaMemcpy(s->pmom.p, ctx->buf("bk_pmom").p, sizeof(double) * s->g.cells * s->probes * s->QY,
+                     cudaMemcpyDeviceToDevice);
         }
+        s->n = n_before;
+        s->finalized = false;
       }
-      try {
+    };
+    // host rows: double-buffered staging, the copy of chunk k+1 overlaps the compute of chunk k
+    static const char* kSlot[2] = {"stage0", "stage1"};
+    PointsDev staged[2];
+    auto stage = [&](int64_t k) {
+      const int sl = static_cast<int>(k & 1);
+      const int64_t a0 = k * CH, a1 = std::min(n, a0 + CH);
+      if (k >= 2) GSGPC_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_free[sl], 0));
+      staged[sl] = stage_points(ctx, pts, s->g.d, a0, a1, true, kSlot[sl], ctx->copy);
+      GSGPC_CUDA(cudaEventRecord(ctx->ev_copied[sl], ctx->copy));
+    };
+    try {
+      if (!dev) {
+        ctx->ensure_copy_stream();
+        // the staging buffers may still be read by earlier work on the compute stream
+        GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+        stage(0);
+      }
+      for (int64_t k = 0; k < nchunks; ++k) {
+        const int64_t r0 = k * CH, r1 = std::min(n, r0 + CH);
+        PointsDev P;
+        if (dev) {
+          P = points_dev(pts, s->g.d, r0);
+        } else {
+          if (k + 1 < nchunks) stage(k + 1);
+          GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[k & 1], 0));
+          P = staged[k & 1];
+        }
+        const uint64_t* pw = nullptr;
+        if (s->probe_seeded && !probe_words) {
+          gen_probe_words(ctx, s, r1 - r0);
+          pw = ctx->buf("probe_stage").as<uint64_t>();
+        } else if (nw) {
+          if (pw_dev) {
+            pw = probe_words + r0 * nw;
+          } else {
+            DBuf& b = ctx->buf("probe_stage");
+            b.ensure(sizeof(uint64_t) * nw * (r1 - r0));
+            GSGPC_CUDA(cudaMemcpyAsync(b.p, probe_words + r0 * nw, sizeof(uint64_t) * nw * (r1 - r0),
+                                       cudaMemcpyHostToDevice, ctx->stream));
+            pw = b.as<uint64_t>();
+          }
+        }
         add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
-      } catch (...) {
-        s->gens = gens_backup;
-        throw;
+        if (!dev) GSGPC_CUDA(cudaEventRecord(ctx->ev_free[k & 1], ctx->stream));
       }
+      if (!dev) GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
+    } catch (...) {
+      if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+      rollback();
+      throw;
     }
   });
 }

@@ -83,30 +83,59 @@ __device__ __forceinline__ int agg_inc(int* counters, int64_t key, bool active) 
   return res;
 }
 
-// classify() specialised on the dimension with 32-bit cell arithmetic (cells < 2^31).
+// classify() specialised on the dimension, branch-light, 32-bit cell arithmetic
+// (cells < 2^31).  Same decisions as the reference (see stencil_dim_fast for the snap
+// argument).  Non-snapped offsets satisfy t ∈ [1e-9, 1 - 1e-9], where every Keys slot is
+// nonzero (the pieces vanish only at integer arguments), so "stencil leaves the grid" is
+// exactly (i0 == 0 || i0 + 2 >= size) && t ∉ {0, 1} for cubic and never for linear.
+// Rows whose |u - round(u)| lies within a few ulp of the 1e-9 snap tolerance take the
+// exact-division path.
+template <int D>
+__device__ __noinline__ int classify_exact(const GridDev& g, const double* x, int& cell) {
+  int64_t i0[GSGPC_MAX_DIM];
+  double t[GSGPC_MAX_DIM];
+  double xx[GSGPC_MAX_DIM] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < D; ++k) xx[k] = x[k];
+  int64_t c = 0;
+  GridDev gd = g;
+  gd.d = D;
+  const int st = classify(gd, xx, i0, t, c);
+  cell = static_cast<int>(c);
+  return st;
+}
+
 template <int D>
 __device__ __forceinline__ int classify_d(const GridDev& g, const double* x, int& cell) {
-  int i0[D], st[D];
-  double t[D];
+  double u[D];
+  bool band = false;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    int64_t ii = 0;
-    st[k] = stencil_dim_fast(x[k], g.mn[k], g.sp[k], g.isp[k], g.sz[k], ii, t[k]);
-    i0[k] = static_cast<int>(ii);
+    const double uu = __dsub_rn(x[k], g.mn[k]) * g.isp[k];
+    const double r = rint(uu);
+    const double dd = fabs(uu - r);
+    const double e = 1e-12 + fabs(uu) * 3.552713678800501e-15;
+    band = band || (dd >= 1e-9 - e && dd <= 1e-9 + e);
+    u[k] = dd < 1e-9 ? r : uu;
   }
+  if (band) return classify_exact<D>(g, x, cell);
+  bool outside = false;
 #pragma unroll
-  for (int k = 0; k < D; ++k)
-    if (st[k] == PT_OUTSIDE) return PT_OUTSIDE;
+  for (int k = 0; k < D; ++k) outside = outside || u[k] < 0.0 || u[k] > static_cast<double>(g.sz[k] - 1);
+  if (outside) return PT_OUTSIDE;
+  int c = 0, st = PT_VALID;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    if (st[k] == PT_EMPTY) return PT_EMPTY;
-    if (leaves_dim(i0[k], t[k], g.sz[k], g.W)) return PT_LEAVES;
+    const bool isnan_k = u[k] != u[k];
+    const int sz = static_cast<int>(g.sz[k]);
+    int i0 = isnan_k ? 0 : static_cast<int>(floor(u[k]));
+    i0 = min(i0, sz - 2);
+    const double t = u[k] - static_cast<double>(i0);
+    const bool leaves = g.W == 4 && (i0 == 0 || i0 + 2 >= sz) && t != 0.0 && t != 1.0;
+    if (st == PT_VALID) st = isnan_k ? PT_EMPTY : (leaves ? PT_LEAVES : PT_VALID);
+    c = c * static_cast<int>(g.nc[k]) + i0;
   }
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) c = c * static_cast<int>(g.nc[k]) + i0[k];
   cell = c;
-  return PT_VALID;
+  return st;
 }
 
 // Rows are processed UNR at a time per thread (all loads issued before any use) so each
@@ -312,15 +341,26 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t* __restrict__ a
   return lo;
 }
 
-// Recompute (t_0..t_{d-1}) of a sorted row (same arithmetic as classify → same t).
+// Recompute (t_0..t_{d-1}) of a sorted (valid) row: same snap decision as classify_d, t to
+// within a few ulp of the reference's (exact division in the rare snap band).
 template <typename T>
 __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double* t, double& y) {
 #pragma unroll
   for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
     if (k < g.d) {
-      int64_t i0;
-      t[k] = 0.0;
-      stencil_dim_fast(static_cast<double>(r.v[k]), g.mn[k], g.sp[k], g.isp[k], g.sz[k], i0, t[k]);
+      const double x = static_cast<double>(r.v[k]);
+      double uu = __dsub_rn(x, g.mn[k]) * g.isp[k];
+      const double rr = rint(uu);
+      const double dd = fabs(uu - rr);
+      const double e = 1e-12 + fabs(uu) * 3.552713678800501e-15;
+      if (dd >= 1e-9 - e && dd <= 1e-9 + e) {
+        int64_t i0;
+        stencil_dim(x, g.mn[k], g.sp[k], g.sz[k], i0, t[k]);
+      } else {
+        if (dd < 1e-9) uu = rr;
+        const double i0 = fmin(floor(uu), static_cast<double>(g.sz[k] - 2));
+        t[k] = uu - i0;
+      }
     }
   }
   y = static_cast<double>(r.v[3]);
