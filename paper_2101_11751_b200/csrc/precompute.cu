@@ -163,11 +163,14 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
-template <typename T, bool PACKED, int D>
+// DIAG (diagnostics only, GSGPC_DIAG_BIN): 1 = no histogram atomics, 2 = contention-free
+// atomics (row-indexed bins) — the histogram is then invalid; used to attribute the cost.
+template <typename T, bool PACKED, int D, int DIAG = 0>
 __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
                                                         double* __restrict__ yty_part) {
+  int sink = 0;
   __shared__ double sh[8];
   double ysq = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
@@ -190,7 +193,9 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
         int cell = 0;
         const int st = classify_d<D>(g, x, cell);
         if (st == PT_VALID) {
-          atomicAdd(&hist[cell], 1);  // RED: no return value needed
+          if (DIAG == 0) atomicAdd(&hist[cell], 1);  // RED: no return value needed
+          else if (DIAG == 1) sink += cell;
+          else atomicAdd(&hist[i % g.cells], 1);
         } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
           const unsigned long long code =
               (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
@@ -201,6 +206,7 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
   }
   const double s2 = block_sum<256>(ysq, sh);
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
+  if (DIAG == 1 && sink == 0x7fffffff) hist[0] = sink;
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -916,8 +922,17 @@ static bool packed4(const PointsDev& p, int d, size_t es) {
 template <typename T, int D>
 static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
                               int* hist, unsigned long long* err, double* part, int nblk) {
-  if (packed4(p, g.d, sizeof(T))) k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
-  else k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  static const int diag = [] {
+    const char* e = getenv("GSGPC_DIAG_BIN");
+    return e ? atoi(e) : 0;
+  }();
+  if (packed4(p, g.d, sizeof(T))) {
+    if (diag == 1) k_classify_count<T, true, D, 1><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+    else if (diag == 2) k_classify_count<T, true, D, 2><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+    else k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  } else {
+    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+  }
 }
 
 template <typename T>
