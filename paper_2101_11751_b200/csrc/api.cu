@@ -459,29 +459,37 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   const Launch L = ctx->L();
   const GridDev& g = s->g;
   PhaseTimer pt(ctx);
+  const int K = bin_k();
+  const int64_t nb = g.cells * K;  // spread buckets
   DBuf& hist = ctx->buf("hist");
-  hist.ensure(sizeof(int) * (g.cells + 1));
+  hist.ensure(sizeof(int) * (nb + 1));
+  DBuf& boff = ctx->buf("boff");
+  boff.ensure(sizeof(int64_t) * (nb + 2));
   DBuf& off = ctx->buf("off");
   off.ensure(sizeof(int64_t) * (g.cells + 2));
   DBuf& bsum = ctx->buf("scan_bs");
-  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(g.cells) + 1));
+  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(nb) + 1));
+  DBuf& code = ctx->buf("bin_code");
+  code.ensure(sizeof(unsigned long long) * n);
   DBuf& err = ctx->buf("err");
   err.ensure(sizeof(unsigned long long) * 2);
-  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)));
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 8), 148 * 6)));
   DBuf& part = ctx->buf("yty_part");
   part.ensure(sizeof(double) * nblk);
   DBuf& ychunk = ctx->buf("yty_chunk");
   ychunk.ensure(sizeof(double));
 
   int h = pt.begin(0);
-  GSGPC_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * (nb + 1), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
-  run_classify(L, dtype, P, n, row0, g, hist.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk);
+  run_classify(L, dtype, P, n, row0, g, hist.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
+               code.as<unsigned long long>());
   run_sum_partials(L, part.as<double>(), nblk, ychunk.as<double>());
   pt.end(h);
   h = pt.begin(1);
-  run_scan(L, hist.as<int>(), g.cells, off.as<int64_t>(), bsum.as<int64_t>());
+  run_scan(L, hist.as<int>(), nb, boff.as<int64_t>(), bsum.as<int64_t>());
+  run_cell_offsets(L, boff.as<int64_t>(), g.cells, off.as<int64_t>());
   pt.end(h);
   // one sync: error row + number of valid rows
   struct {
@@ -511,14 +519,11 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     const size_t es = dtype_size(dtype);
     DBuf& pay = ctx->buf("payload");
     pay.ensure(es * 4 * nvalid);
-    DBuf& cur = ctx->buf("cursor");
-    cur.ensure(sizeof(int) * (g.cells + 1));
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
     DBuf& pws = ctx->buf("probe_sorted");
     if (nw) pws.ensure(sizeof(uint64_t) * nw * nvalid);
     h = pt.begin(2);
-    GSGPC_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
-    run_scatter(L, dtype, P, n, g, off.as<int64_t>(), cur.as<int>(), pay.p, pw_dev, nw,
+    run_scatter(L, dtype, P, n, g, code.as<unsigned long long>(), boff.as<int64_t>(), pay.p, pw_dev, nw,
                 nw ? pws.as<uint64_t>() : nullptr, nblk);
     pt.end(h);
     h = pt.begin(3);

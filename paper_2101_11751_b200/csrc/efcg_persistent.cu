@@ -157,7 +157,7 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
 }
 
 template <int SMIN>
-__global__ void __launch_bounds__(PCG_NT, 4) k_efcg_persistent(PcgArgs a) {
+__global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
   extern __shared__ double smem[];
   __shared__ double sh[8];
   __shared__ double sh1;

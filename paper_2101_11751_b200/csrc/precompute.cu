@@ -163,14 +163,20 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
-// DIAG (diagnostics only, GSGPC_DIAG_BIN): 1 = no histogram atomics, 2 = contention-free
-// atomics (row-indexed bins) — the histogram is then invalid; used to attribute the cost.
-template <typename T, bool PACKED, int D, int DIAG = 0>
+// Binning with spread counters: each cell owns BIN_K sub-counters and row i uses sub-counter
+// (i >> 8) & (BIN_K-1), so the rows a whole GPU processes at one instant hit BIN_K different
+// addresses of a hot cell instead of one (atomic contention on clustered data was the cost).
+// The atomic returns the row's rank inside its (cell, sub) bucket; the packed code
+// (bucket << 32 | rank) lets the scatter place the row without classifying it again and
+// without atomics.  Invalid rows get code ~0.
+constexpr int BIN_K = 16;
+
+template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
-                                                        double* __restrict__ yty_part) {
-  int sink = 0;
+                                                        double* __restrict__ yty_part,
+                                                        unsigned long long* __restrict__ code) {
   __shared__ double sh[8];
   double ysq = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
@@ -192,21 +198,28 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
         ysq += y * y;
         int cell = 0;
         const int st = classify_d<D>(g, x, cell);
+        unsigned long long c = ~0ull;
         if (st == PT_VALID) {
-          if (DIAG == 0) atomicAdd(&hist[cell], 1);  // RED: no return value needed
-          else if (DIAG == 1) sink += cell;
-          else atomicAdd(&hist[i % g.cells], 1);
+          const unsigned bucket = static_cast<unsigned>(cell) * BIN_K + static_cast<unsigned>((i >> 8) & (BIN_K - 1));
+          const unsigned rank = static_cast<unsigned>(atomicAdd(&hist[bucket], 1));
+          c = (static_cast<unsigned long long>(bucket) << 32) | rank;
         } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
-          const unsigned long long code =
+          const unsigned long long ecode =
               (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
-          atomicMin(err, code);
+          atomicMin(err, ecode);
         }
+        code[i] = c;
       }
     }
   }
   const double s2 = block_sum<256>(ysq, sh);
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
-  if (DIAG == 1 && sink == 0x7fffffff) hist[0] = sink;
+}
+
+// cell offsets for K1 from the bucket offsets: off[c] = boff[c·BIN_K] (c ≤ cells)
+__global__ void k_cell_offsets(const int64_t* __restrict__ boff, int64_t cells, int64_t* __restrict__ off) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c <= cells) off[c] = boff[c * BIN_K];
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -299,39 +312,32 @@ struct alignas(sizeof(T) * 4) Row4 {
   T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
 };
 
-template <typename T, bool PACKED, int D>
-__global__ void __launch_bounds__(256, 3) k_scatter(PointsDev pts, int64_t n, GridDev g,
-                                                 const int64_t* __restrict__ off, int* __restrict__ cur,
-                                                 Row4<T>* __restrict__ out,
+template <typename T, bool PACKED>
+__global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, int d,
+                                                 const unsigned long long* __restrict__ code,
+                                                 const int64_t* __restrict__ boff, Row4<T>* __restrict__ out,
                                                  const uint64_t* __restrict__ pw_in, int nw,
                                                  uint64_t* __restrict__ pw_out) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
     Row4<T> r[SORT_UNR];
-    int64_t pos[SORT_UNR];
+    unsigned long long c[SORT_UNR];
 #pragma unroll
     for (int u = 0; u < SORT_UNR; ++u) {
       const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      if (i < n) load_row<T, PACKED>(pts, g.d, i, r[u].v);
-    }
-#pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) {
-      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      pos[u] = -1;
+      c[u] = ~0ull;
       if (i < n) {
-        double x[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = static_cast<double>(r[u].v[k]);
-        int cell = 0;
-        if (classify_d<D>(g, x, cell) == PT_VALID) pos[u] = off[cell] + atomicAdd(&cur[cell], 1);
+        c[u] = __ldcs(code + i);
+        load_row<T, PACKED>(pts, d, i, r[u].v);
       }
     }
 #pragma unroll
     for (int u = 0; u < SORT_UNR; ++u) {
-      if (pos[u] >= 0) {
-        out[pos[u]] = r[u];
+      if (c[u] != ~0ull) {
+        const int64_t pos = boff[c[u] >> 32] + static_cast<int64_t>(c[u] & 0xffffffffull);
+        out[pos] = r[u];
         const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-        for (int w = 0; w < nw; ++w) pw_out[pos[u] * nw + w] = pw_in[i * nw + w];
+        for (int w = 0; w < nw; ++w) pw_out[pos * nw + w] = pw_in[i * nw + w];
       }
     }
   }
@@ -921,48 +927,35 @@ static bool packed4(const PointsDev& p, int d, size_t es) {
 
 template <typename T, int D>
 static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                              int* hist, unsigned long long* err, double* part, int nblk) {
-  static const int diag = [] {
-    const char* e = getenv("GSGPC_DIAG_BIN");
-    return e ? atoi(e) : 0;
-  }();
+                              int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code) {
   if (packed4(p, g.d, sizeof(T))) {
-    if (diag == 1) k_classify_count<T, true, D, 1><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
-    else if (diag == 2) k_classify_count<T, true, D, 2><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
-    else k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code);
   } else {
-    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part);
+    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code);
   }
 }
 
 template <typename T>
 static void launch_classify(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                            int* hist, unsigned long long* err, double* part, int nblk) {
-  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk);
-  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk);
-  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk);
-}
-
-template <typename T, int D>
-static void launch_scatter_d(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const int64_t* off,
-                             int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out, int nblk) {
-  Row4<T>* o = static_cast<Row4<T>*>(out);
-  if (packed4(p, g.d, sizeof(T))) k_scatter<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, o, pw_in, nw, pw_out);
-  else k_scatter<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, g, off, cur, o, pw_in, nw, pw_out);
-}
-
-template <typename T>
-static void launch_scatter(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const int64_t* off,
-                           int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out, int nblk) {
-  if (g.d == 1) launch_scatter_d<T, 1>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
-  else if (g.d == 2) launch_scatter_d<T, 2>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
-  else launch_scatter_d<T, 3>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
+                            int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code) {
+  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk, code);
+  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk, code);
+  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk, code);
 }
 
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0,
-                  const GridDev& g, int* hist, unsigned long long* err, double* part, int nblk) {
-  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, hist, err, part, nblk);
-  else launch_classify<double>(L, p, n, row0, g, hist, err, part, nblk);
+                  const GridDev& g, int* hist, unsigned long long* err, double* part, int nblk,
+                  unsigned long long* code) {
+  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, hist, err, part, nblk, code);
+  else launch_classify<double>(L, p, n, row0, g, hist, err, part, nblk, code);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+int bin_k() { return BIN_K; }
+
+void run_cell_offsets(const Launch& L, const int64_t* boff, int64_t cells, int64_t* off) {
+  k_cell_offsets<<<static_cast<unsigned>(ceil_div(cells + 1, 256)), 256, 0, L.s>>>(boff, cells, off);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -985,10 +978,17 @@ void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* 
 int64_t scan_scratch_elems(int64_t n) { return ceil_div(n, SCAN_TILE) + 1; }
 
 void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g,
-                 const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw,
+                 const unsigned long long* code, const int64_t* boff, void* out, const uint64_t* pw_in, int nw,
                  uint64_t* pw_out, int nblk) {
-  if (dtype == GSGPC_F32) launch_scatter<float>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
-  else launch_scatter<double>(L, p, n, g, off, cur, out, pw_in, nw, pw_out, nblk);
+  if (dtype == GSGPC_F32) {
+    Row4<float>* o = static_cast<Row4<float>*>(out);
+    if (packed4(p, g.d, 4)) k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+    else k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+  } else {
+    Row4<double>* o = static_cast<Row4<double>*>(out);
+    if (packed4(p, g.d, 8)) k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+    else k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+  }
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
