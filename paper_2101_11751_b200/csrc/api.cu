@@ -1397,9 +1397,47 @@ CgOutcome run_efcg(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, const double* r
   CgState h{};
   if (!use_graph) {
     // one cooperative launch runs the whole solve (efcg_persistent.cu)
+    static const bool trace = [] {
+      const char* e = getenv("GSGPC_CG_TRACE");
+      return e && e[0] == '1';
+    }();
+    DBuf& tb = ctx->buf("cg_trace");
+    if (trace) {
+      tb.ensure(sizeof(unsigned long long) * 64 * 8);
+      GSGPC_CUDA(cudaMemsetAsync(tb.p, 0, sizeof(unsigned long long) * 64 * 8, ctx->stream));
+    }
     GSGPC_CUDA(cudaEventRecord(e0, ctx->stream));
-    run_efcg_persistent(L, sd, s->stencil(), kg->dev, b, 1);
+    run_efcg_persistent(L, sd, s->stencil(), kg->dev, b, 1, trace ? tb.as<unsigned long long>() : nullptr);
     GSGPC_CUDA(cudaEventRecord(e1, ctx->stream));
+    if (trace) {  // diagnostics: mean per-phase time over iterations 2..63
+      std::vector<unsigned long long> t(64 * 8);
+      GSGPC_CUDA(cudaMemcpyAsync(t.data(), tb.p, sizeof(unsigned long long) * 64 * 8, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+      double acc[8] = {0};
+      int cnt = 0;
+      for (int it = 2; it < 63; ++it) {
+        const unsigned long long* r = &t[it * 8];
+        if (!r[0] || !r[6] || !t[(it + 1) * 8]) continue;
+        acc[0] += r[1] - r[0];              // update + sync
+        acc[1] += r[2] - r[1];              // SpMV + sync
+        unsigned long long prev = r[2];
+        for (int ph = 3; ph <= 5; ++ph) {
+          if (r[ph]) {
+            acc[ph - 1] += r[ph] - prev;    // Toeplitz modes
+            prev = r[ph];
+          }
+        }
+        acc[5] += r[6] - prev;              // last mode + epilogue + sync
+        acc[6] += t[(it + 1) * 8] - r[6];   // reduce, scalars
+        ++cnt;
+      }
+      if (cnt) {
+        std::fprintf(stderr, "[gsgpc cg trace] us/iter: update %.1f spmv %.1f mode2 %.1f mode1 %.1f mode0+epi %.1f "
+                     "tail %.1f (n=%d)\n", acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3,
+                     acc[3] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, cnt);
+      }
+    }
     GSGPC_CUDA(cudaMemcpyAsync(ctx->pin.p, b.st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
     GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
     std::memcpy(&h, ctx->pin.p, sizeof(CgState));

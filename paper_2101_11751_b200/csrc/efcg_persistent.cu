@@ -37,7 +37,14 @@ struct PcgArgs {
   CgState* st;
   PcgMode mode[3];
   int init;
+  unsigned long long* tbuf;  // optional phase trace: tbuf[iter * 8 + phase] = %globaltimer (ns)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Sum of the per-block partials, identical in every block (fixed order, one warp).
 __device__ __forceinline__ double grid_reduce(const double* part, int np, double* sh1) {
@@ -183,6 +190,9 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
     const double bs = block_sum<PCG_NT>(dot, sh);
     if (threadIdx.x == 0) a.part_a[blockIdx.x] = bs;
   };
+  auto stamp = [&](int phase) {
+    if (a.tbuf && leader && iter < 64) a.tbuf[iter * 8 + phase] = gtimer();
+  };
   auto kg_phase = [&](double beta) {
     double dot = 0.0;
     const double* src = a.u;
@@ -190,6 +200,7 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
       double* dst = (src == a.t0) ? a.t1 : a.t0;
       pcg_mode<false>(a.mode[k], src, dst, smem, a, beta, s2, dot);
       grid.sync();
+      stamp(5 - k);
       src = dst;
     }
     pcg_mode<true>(a.mode[0], src, nullptr, smem, a, beta, s2, dot);
@@ -218,14 +229,17 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
       break;
     }
     const double alpha = rho / pap;
+    stamp(0);
     for (int i = tid; i < m; i += nthr) {
       a.x[i] += alpha * __ldcg(a.s + i);  // ŝ, z̄ were written by other blocks
       a.r[i] -= alpha * __ldcg(a.z + i);
     }
     if (leader) a.alphas[iter] = alpha;
     grid.sync();
+    stamp(1);
     spmv_phase();
     grid.sync();
+    stamp(2);
     const double rho_new = grid_reduce(a.part_a, gridDim.x, &sh1);
     ++iter;
     if (leader) a.trace[iter] = rho_new;
@@ -237,8 +251,11 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
     const double beta = rho_new / rho;
     if (leader) a.betas[iter - 1] = beta;
     rho = rho_new;
+    --iter;
     kg_phase(beta);
     grid.sync();
+    stamp(6);
+    ++iter;
     pap = grid_reduce(a.part_b, gridDim.x, &sh1);
   }
   if (leader) {
@@ -297,7 +314,7 @@ static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
 int pcg_max_blocks() { return 148 * 4 + 64; }
 
 void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
-                         int init) {
+                         int init, unsigned long long* tbuf) {
   int o32[172];
   {
     const int E = 2 * sd.W - 1;
@@ -335,6 +352,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
   a.betas = b.betas;
   a.st = b.st;
   a.init = init;
+  a.tbuf = tbuf;
   size_t smem = 0;
   for (int k = 0; k < kg.d; ++k) {
     a.mode[k] = mode_cfg(kg, k);

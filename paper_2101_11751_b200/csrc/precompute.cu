@@ -169,14 +169,15 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
 // The atomic returns the row's rank inside its (cell, sub) bucket; the packed code
 // (bucket << 32 | rank) lets the scatter place the row without classifying it again and
 // without atomics.  Invalid rows get code ~0.
-constexpr int BIN_K = 16;
+constexpr int BIN_K = 16;  // maximum spread; the active spread (bin_k()) is a power of two ≤ BIN_K
 
 template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
                                                         double* __restrict__ yty_part,
-                                                        unsigned long long* __restrict__ code) {
+                                                        unsigned long long* __restrict__ code, int kshift) {
+  const unsigned kmask = (1u << kshift) - 1u;
   __shared__ double sh[8];
   double ysq = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
         const int st = classify_d<D>(g, x, cell);
         unsigned long long c = ~0ull;
         if (st == PT_VALID) {
-          const unsigned bucket = static_cast<unsigned>(cell) * BIN_K + static_cast<unsigned>((i >> 8) & (BIN_K - 1));
+          const unsigned bucket = (static_cast<unsigned>(cell) << kshift) + (static_cast<unsigned>(i >> 8) & kmask);
           const unsigned rank = static_cast<unsigned>(atomicAdd(&hist[bucket], 1));
           c = (static_cast<unsigned long long>(bucket) << 32) | rank;
         } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
@@ -216,10 +217,21 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
 }
 
-// cell offsets for K1 from the bucket offsets: off[c] = boff[c·BIN_K] (c ≤ cells)
-__global__ void k_cell_offsets(const int64_t* __restrict__ boff, int64_t cells, int64_t* __restrict__ off) {
+// cell offsets for K1 from the bucket offsets: off[c] = boff[c·K] (c ≤ cells)
+__global__ void k_cell_offsets(const int64_t* __restrict__ boff, int64_t cells, int64_t* __restrict__ off, int kshift) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c <= cells) off[c] = boff[c * BIN_K];
+  if (c <= cells) off[c] = boff[c << kshift];
+}
+
+static int bin_shift() {
+  static const int sh = [] {
+    const char* e = getenv("GSGPC_BIN_K");
+    const int k = e ? atoi(e) : 1;
+    int s2 = 0;
+    while ((1 << (s2 + 1)) <= k && (1 << (s2 + 1)) <= BIN_K) ++s2;
+    return s2;
+  }();
+  return sh;
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -929,9 +941,9 @@ template <typename T, int D>
 static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
                               int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code) {
   if (packed4(p, g.d, sizeof(T))) {
-    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code);
+    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code, bin_shift());
   } else {
-    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code);
+    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code, bin_shift());
   }
 }
 
@@ -952,10 +964,10 @@ void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int
   GSGPC_CUDA(cudaGetLastError());
 }
 
-int bin_k() { return BIN_K; }
+int bin_k() { return 1 << bin_shift(); }
 
 void run_cell_offsets(const Launch& L, const int64_t* boff, int64_t cells, int64_t* off) {
-  k_cell_offsets<<<static_cast<unsigned>(ceil_div(cells + 1, 256)), 256, 0, L.s>>>(boff, cells, off);
+  k_cell_offsets<<<static_cast<unsigned>(ceil_div(cells + 1, 256)), 256, 0, L.s>>>(boff, cells, off, bin_shift());
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }

@@ -80,7 +80,7 @@ void run_cg_iter(const Launch& L, const StencilDesc& sd, const double* A, const 
 int cg_partials_needed(int64_t m);
 // efcg_persistent.cu: the whole solve in one cooperative launch (init = run the r̂0 setup first)
 void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
-                         int init);
+                         int init, unsigned long long* tbuf = nullptr);
 
 // Vector helpers
 void run_axpby(const Launch& L, int64_t n, double a, const double* x, double b, const double* y, double* out);
