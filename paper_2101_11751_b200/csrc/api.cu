@@ -460,17 +460,17 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   const GridDev& g = s->g;
   PhaseTimer pt(ctx);
   const int K = bin_k();
-  const int64_t nb = g.cells * K;  // spread buckets
+  const int64_t nb = g.cells * K;  // spread histogram buckets
   DBuf& hist = ctx->buf("hist");
   hist.ensure(sizeof(int) * (nb + 1));
-  DBuf& boff = ctx->buf("boff");
-  boff.ensure(sizeof(int64_t) * (nb + 2));
+  DBuf& counts = ctx->buf("counts");
+  counts.ensure(sizeof(int) * (g.cells + 1));
   DBuf& off = ctx->buf("off");
   off.ensure(sizeof(int64_t) * (g.cells + 2));
   DBuf& bsum = ctx->buf("scan_bs");
-  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(nb) + 1));
-  DBuf& code = ctx->buf("bin_code");
-  code.ensure(sizeof(unsigned long long) * n);
+  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(g.cells) + 1));
+  DBuf& cellid = ctx->buf("cellid");
+  cellid.ensure(sizeof(int) * n);
   DBuf& err = ctx->buf("err");
   err.ensure(sizeof(unsigned long long) * 2);
   const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 8), 148 * 6)));
@@ -484,12 +484,12 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
   run_classify(L, dtype, P, n, row0, g, hist.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
-               code.as<unsigned long long>());
+               cellid.as<int>());
   run_sum_partials(L, part.as<double>(), nblk, ychunk.as<double>());
   pt.end(h);
   h = pt.begin(1);
-  run_scan(L, hist.as<int>(), nb, boff.as<int64_t>(), bsum.as<int64_t>());
-  run_cell_offsets(L, boff.as<int64_t>(), g.cells, off.as<int64_t>());
+  run_cell_counts(L, hist.as<int>(), g.cells, counts.as<int>());
+  run_scan(L, counts.as<int>(), g.cells, off.as<int64_t>(), bsum.as<int64_t>());
   pt.end(h);
   // one sync: error row + number of valid rows
   struct {
@@ -522,8 +522,11 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
     DBuf& pws = ctx->buf("probe_sorted");
     if (nw) pws.ensure(sizeof(uint64_t) * nw * nvalid);
+    DBuf& cur = ctx->buf("cursor");
+    cur.ensure(sizeof(int) * (g.cells + 1));
     h = pt.begin(2);
-    run_scatter(L, dtype, P, n, g, code.as<unsigned long long>(), boff.as<int64_t>(), pay.p, pw_dev, nw,
+    GSGPC_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
+    run_scatter(L, dtype, P, n, g, cellid.as<int>(), off.as<int64_t>(), cur.as<int>(), pay.p, pw_dev, nw,
                 nw ? pws.as<uint64_t>() : nullptr, nblk);
     pt.end(h);
     h = pt.begin(3);

@@ -11,6 +11,7 @@
 
 #include "internal.cuh"
 #include "precompute.cuh"
+#include "toeplitz.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -93,7 +94,7 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
                                          const PcgArgs& a, double beta, double s2, double& dot) {
   const int64_t n = c.n;
   double* Ts = smem;
-  double* Xs = smem + 2 * n - 1;
+  double* Xs = smem + toep_ts_doubles(n);
   const int64_t nwork = c.tiles * c.chunks;
   for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
     const int64_t tile = w % c.tiles, chunk = w / c.tiles;
@@ -102,62 +103,29 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
     const int64_t a0 = chunk * c.TA;
     const int na = static_cast<int>(imin64(c.TA, n - a0));
     __syncthreads();
-    for (int64_t q = threadIdx.x; q < 2 * n - 1; q += PCG_NT) {
-      const int64_t dd = q - (n - 1);
-      Ts[q] = c.gen[dd < 0 ? -dd : dd];
-    }
-    if (c.inner == 1) {
-      for (int64_t q = threadIdx.x; q < static_cast<int64_t>(nl) * n; q += PCG_NT) {
-        const int64_t tl = q / n, j = q % n;
-        Xs[j * c.TL + tl] = __ldcg(X + (l0 + tl) * n + j);
-      }
-    } else {
-      for (int64_t q = threadIdx.x; q < static_cast<int64_t>(c.TL) * n; q += PCG_NT) {
-        const int tl = static_cast<int>(q % c.TL);
-        const int64_t j = q / c.TL;
-        if (tl < nl) {
-          const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
-          Xs[j * c.TL + tl] = __ldcg(X + (o * n + j) * c.inner + i);
-        }
-      }
-    }
+    toep_load_tile(X, c.gen, n, c.inner, c.TL, l0, nl, Ts, Xs, PCG_NT);
     __syncthreads();
-    const int total = nl * na;
-    for (int uu = threadIdx.x; uu < total; uu += PCG_NT) {
+    const int ngroups = nl * ((na + TOEP_RB - 1) / TOEP_RB);
+    for (int uu = threadIdx.x; uu < ngroups; uu += PCG_NT) {
       int tl, ar;
-      if (c.inner == 1) {
-        ar = uu % na;
-        tl = uu / na;
-      } else {
-        tl = uu % nl;
-        ar = uu / nl;
-      }
-      const int64_t aa = a0 + ar;
-      const double* tp = Ts + (n - 1 + aa);
-      const double* xs = Xs + tl;
-      const int TL = c.TL;
-      const int nn = static_cast<int>(n);
-      double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-      int j = 0;
-      for (; j + 3 < nn; j += 4) {
-        b0 = fma(tp[-j], xs[j * TL], b0);
-        b1 = fma(tp[-(j + 1)], xs[(j + 1) * TL], b1);
-        b2 = fma(tp[-(j + 2)], xs[(j + 2) * TL], b2);
-        b3 = fma(tp[-(j + 3)], xs[(j + 3) * TL], b3);
-      }
-      for (; j < nn; ++j) b0 = fma(tp[-j], xs[j * TL], b0);
-      const double acc = (b0 + b1) + (b2 + b3);
+      toep_group(uu, nl, na, c.inner == 1, tl, ar);
+      double acc[TOEP_RB];
+      toep_dot4(Ts, Xs, n, c.TL, tl, a0 + ar, acc);
       const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
-      const int64_t g = (o * n + aa) * c.inner + i;
-      if (!EPI) {
-        Y[g] = acc;
-      } else {
-        const double v = acc + s2 * __ldcg(a.r + g);
-        const double sn = __ldcg(a.u + g) + beta * a.s[g];
-        const double zn = v + beta * a.z[g];
-        a.s[g] = sn;
-        a.z[g] = zn;
-        dot = fma(sn, zn, dot);
+#pragma unroll
+      for (int r = 0; r < TOEP_RB; ++r) {
+        if (ar + r >= na) break;
+        const int64_t g = (o * n + a0 + ar + r) * c.inner + i;
+        if (!EPI) {
+          Y[g] = acc[r];
+        } else {
+          const double v = acc[r] + s2 * __ldcg(a.r + g);
+          const double sn = __ldcg(a.u + g) + beta * a.s[g];
+          const double zn = v + beta * a.z[g];
+          a.s[g] = sn;
+          a.z[g] = zn;
+          dot = fma(sn, zn, dot);
+        }
       }
     }
   }
@@ -279,8 +247,10 @@ static PcgMode mode_cfg(const KgDev& kg, int k) {
   c.inner = inner;
   c.L = inner * outer;
   const int64_t cap = 6144;  // doubles of dynamic smem per block (48 KB)
-  if (3 * n > cap) throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2048 nodes is not supported");
-  int64_t TL = std::min<int64_t>(32, (cap - 2 * n) / n);
+  if (toep_smem_doubles(n, 1) > cap) {
+    throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2040 nodes is not supported");
+  }
+  int64_t TL = std::min<int64_t>(32, (cap - toep_ts_doubles(n)) / n);
   TL = std::max<int64_t>(1, std::min<int64_t>(TL, c.L));
   c.TL = static_cast<int>(TL);
   c.tiles = ceil_div(c.L, TL);
@@ -356,7 +326,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
   size_t smem = 0;
   for (int k = 0; k < kg.d; ++k) {
     a.mode[k] = mode_cfg(kg, k);
-    smem = std::max(smem, sizeof(double) * (2 * a.mode[k].n - 1 + a.mode[k].TL * a.mode[k].n));
+    smem = std::max(smem, sizeof(double) * static_cast<size_t>(toep_smem_doubles(a.mode[k].n, a.mode[k].TL)));
   }
   switch (sd.S_min) {
     case 172: launch_pcg<172>(L, a, smem); break;

@@ -18,6 +18,7 @@
 
 #include "internal.cuh"
 #include "precompute.cuh"
+#include "toeplitz.cuh"
 
 namespace gsgpc {
 
@@ -199,70 +200,37 @@ __global__ void __launch_bounds__(256) k_toep(ToepArgs t, CgEpi e) {
   extern __shared__ double smem[];
   if (e.st != nullptr && e.st->done) return;
   const int64_t n = t.n;
-  double* Ts = smem;              // 2n-1 symmetric generator
-  double* Xs = smem + 2 * n - 1;  // [n][TL]
+  double* Ts = smem;
+  double* Xs = smem + toep_ts_doubles(n);
   const int64_t l0 = static_cast<int64_t>(blockIdx.x) * t.TL;
   const int nl = static_cast<int>(imin64(t.TL, t.L - l0));
   const int64_t a0 = static_cast<int64_t>(blockIdx.y) * t.TA;
   const int na = static_cast<int>(imin64(t.TA, n - a0));
-  for (int64_t q = threadIdx.x; q < 2 * n - 1; q += blockDim.x) {
-    const int64_t dd = q - (n - 1);
-    Ts[q] = t.gen[dd < 0 ? -dd : dd];
-  }
-  if (t.inner == 1) {
-    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(nl) * n; q += blockDim.x) {
-      const int64_t tl = q / n, j = q % n;
-      Xs[j * t.TL + tl] = t.X[(l0 + tl) * n + j];
-    }
-  } else {
-    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(t.TL) * n; q += blockDim.x) {
-      const int tl = static_cast<int>(q % t.TL);
-      const int64_t j = q / t.TL;
-      if (tl < nl) {
-        const int64_t l = l0 + tl, o = l / t.inner, i = l % t.inner;
-        Xs[j * t.TL + tl] = t.X[(o * n + j) * t.inner + i];
-      }
-    }
-  }
+  toep_load_tile(t.X, t.gen, n, t.inner, t.TL, l0, nl, Ts, Xs, blockDim.x);
   __syncthreads();
   double dot = 0.0;
-  const int total = nl * na;
-  for (int u = threadIdx.x; u < total; u += blockDim.x) {
+  const int ngroups = nl * ((na + TOEP_RB - 1) / TOEP_RB);
+  for (int uu = threadIdx.x; uu < ngroups; uu += blockDim.x) {
     int tl, ar;
-    if (t.inner == 1) {
-      ar = u % na;
-      tl = u / na;
-    } else {
-      tl = u % nl;
-      ar = u / nl;
-    }
-    const int64_t a = a0 + ar;
-    const double* tp = Ts + (n - 1 + a);
-    const double* xs = Xs + tl;
-    const int TL = t.TL;
-    const int nn = static_cast<int>(n);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int j = 0;
-    for (; j + 3 < nn; j += 4) {
-      a0 = fma(tp[-j], xs[j * TL], a0);
-      a1 = fma(tp[-(j + 1)], xs[(j + 1) * TL], a1);
-      a2 = fma(tp[-(j + 2)], xs[(j + 2) * TL], a2);
-      a3 = fma(tp[-(j + 3)], xs[(j + 3) * TL], a3);
-    }
-    for (; j < nn; ++j) a0 = fma(tp[-j], xs[j * TL], a0);
-    const double acc = (a0 + a1) + (a2 + a3);
+    toep_group(uu, nl, na, t.inner == 1, tl, ar);
+    double acc[TOEP_RB];
+    toep_dot4(Ts, Xs, n, t.TL, tl, a0 + ar, acc);
     const int64_t l = l0 + tl, o = l / t.inner, i = l % t.inner;
-    const int64_t g = (o * n + a) * t.inner + i;
-    if (MODE == 0) {
-      t.Y[g] = acc;
-    } else {
-      const double beta = e.st->beta;
-      const double v = acc + e.st->sigma_sq * e.r[g];
-      const double s = e.u[g] + beta * e.s[g];
-      const double z = v + beta * e.z[g];
-      e.s[g] = s;
-      e.z[g] = z;
-      dot = fma(s, z, dot);
+#pragma unroll
+    for (int r = 0; r < TOEP_RB; ++r) {
+      if (ar + r >= na) break;
+      const int64_t g = (o * n + a0 + ar + r) * t.inner + i;
+      if (MODE == 0) {
+        t.Y[g] = acc[r];
+      } else {
+        const double beta = e.st->beta;
+        const double v = acc[r] + e.st->sigma_sq * e.r[g];
+        const double s = e.u[g] + beta * e.s[g];
+        const double z = v + beta * e.z[g];
+        e.s[g] = s;
+        e.z[g] = z;
+        dot = fma(s, z, dot);
+      }
     }
   }
   if (MODE == 1) {
@@ -285,8 +253,10 @@ static void toep_config(int64_t n, int64_t inner, int64_t outer, ToepArgs& t, di
   t.outer = outer;
   t.L = inner * outer;
   const int64_t cap = 8192;  // doubles of dynamic smem (64 KB)
-  if (3 * n > cap) throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2730 nodes is not supported");
-  int64_t TL = std::min<int64_t>(32, (cap - 2 * n) / n);
+  if (toep_smem_doubles(n, 1) > cap) {
+    throw Error(GSGPC_UNSUPPORTED, "K_G: grid dimension larger than 2730 nodes is not supported");
+  }
+  int64_t TL = std::min<int64_t>(32, (cap - toep_ts_doubles(n)) / n);
   TL = std::max<int64_t>(1, std::min<int64_t>(TL, t.L));
   t.TL = static_cast<int>(TL);
   const int64_t tiles = ceil_div(t.L, TL);
@@ -294,7 +264,7 @@ static void toep_config(int64_t n, int64_t inner, int64_t outer, ToepArgs& t, di
   t.TA = static_cast<int>(ceil_div(n, chunks));
   chunks = ceil_div(n, t.TA);
   grid = dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
-  smem = sizeof(double) * (2 * n - 1 + TL * n);
+  smem = sizeof(double) * toep_smem_doubles(n, TL);
 }
 
 static void launch_toep(const Launch& L, int mode, ToepArgs t, dim3 grid, size_t smem, CgEpi e) {

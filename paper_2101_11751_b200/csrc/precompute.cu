@@ -163,22 +163,35 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
-// Binning with spread counters: each cell owns BIN_K sub-counters and row i uses sub-counter
-// (i >> 8) & (BIN_K-1), so the rows a whole GPU processes at one instant hit BIN_K different
-// addresses of a hot cell instead of one (atomic contention on clustered data was the cost).
-// The atomic returns the row's rank inside its (cell, sub) bucket; the packed code
-// (bucket << 32 | rank) lets the scatter place the row without classifying it again and
-// without atomics.  Invalid rows get code ~0.
-constexpr int BIN_K = 16;  // maximum spread; the active spread (bin_k()) is a power of two ≤ BIN_K
+// Binning.  The histogram uses spread sub-counters per cell — row i adds to sub-counter
+// (i >> 8) & (K-1) — so the rows the GPU processes at one instant hit K addresses of a hot
+// cell instead of one (RED contention on clustered data was the cost); k_cell_counts folds
+// them.  Classify also stores each row's cell id (-1: not interpolated), so the scatter
+// neither re-classifies nor repeats the exact arithmetic.  The scatter takes its slot from a
+// per-cell cursor atomic in its own processing order, which keeps each cell's writes
+// sequential in time (sectors complete in L2; slots assigned by another pass's order left
+// half-written sectors to be evicted).
+constexpr int BIN_K = 16;  // maximum spread; the active spread is 1 << bin_shift()
+
+static int bin_shift() {  // GSGPC_BIN_K overrides the spread (diagnostics); default BIN_K
+  static const int sh = [] {
+    const char* e = getenv("GSGPC_BIN_K");
+    const int k = e ? atoi(e) : BIN_K;
+    int s2 = 0;
+    while ((1 << (s2 + 1)) <= k && (1 << (s2 + 1)) <= BIN_K) ++s2;
+    return s2;
+  }();
+  return sh;
+}
 
 template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
                                                         int* __restrict__ hist,
                                                         unsigned long long* __restrict__ err,
                                                         double* __restrict__ yty_part,
-                                                        unsigned long long* __restrict__ code, int kshift) {
-  const unsigned kmask = (1u << kshift) - 1u;
+                                                        int* __restrict__ cellid, int kshift) {
   __shared__ double sh[8];
+  const unsigned kmask = (1u << kshift) - 1u;
   double ysq = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
@@ -199,17 +212,17 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
         ysq += y * y;
         int cell = 0;
         const int st = classify_d<D>(g, x, cell);
-        unsigned long long c = ~0ull;
         if (st == PT_VALID) {
-          const unsigned bucket = (static_cast<unsigned>(cell) << kshift) + (static_cast<unsigned>(i >> 8) & kmask);
-          const unsigned rank = static_cast<unsigned>(atomicAdd(&hist[bucket], 1));
-          c = (static_cast<unsigned long long>(bucket) << 32) | rank;
-        } else if (st == PT_OUTSIDE || st == PT_LEAVES) {
-          const unsigned long long ecode =
-              (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
-          atomicMin(err, ecode);
+          atomicAdd(&hist[(static_cast<unsigned>(cell) << kshift) + (static_cast<unsigned>(i >> 8) & kmask)], 1);
+        } else {
+          cell = -1;
+          if (st == PT_OUTSIDE || st == PT_LEAVES) {
+            const unsigned long long ecode =
+                (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
+            atomicMin(err, ecode);
+          }
         }
-        code[i] = c;
+        __stcs(cellid + i, cell);
       }
     }
   }
@@ -217,21 +230,13 @@ __global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
 }
 
-// cell offsets for K1 from the bucket offsets: off[c] = boff[c·K] (c ≤ cells)
-__global__ void k_cell_offsets(const int64_t* __restrict__ boff, int64_t cells, int64_t* __restrict__ off, int kshift) {
+// counts[c] = Σ_k hist[c·K + k]
+__global__ void k_cell_counts(const int* __restrict__ hist, int64_t cells, int kshift, int* __restrict__ counts) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c <= cells) off[c] = boff[c << kshift];
-}
-
-static int bin_shift() {
-  static const int sh = [] {
-    const char* e = getenv("GSGPC_BIN_K");
-    const int k = e ? atoi(e) : 1;
-    int s2 = 0;
-    while ((1 << (s2 + 1)) <= k && (1 << (s2 + 1)) <= BIN_K) ++s2;
-    return s2;
-  }();
-  return sh;
+  if (c >= cells) return;
+  int s2 = 0;
+  for (int k = 0; k < (1 << kshift); ++k) s2 += hist[(c << kshift) + k];
+  counts[c] = s2;
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -325,31 +330,32 @@ struct alignas(sizeof(T) * 4) Row4 {
 };
 
 template <typename T, bool PACKED>
-__global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, int d,
-                                                 const unsigned long long* __restrict__ code,
-                                                 const int64_t* __restrict__ boff, Row4<T>* __restrict__ out,
-                                                 const uint64_t* __restrict__ pw_in, int nw,
-                                                 uint64_t* __restrict__ pw_out) {
+__global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, int d, const int* __restrict__ cellid,
+                                                 const int64_t* __restrict__ off, int* __restrict__ cur,
+                                                 Row4<T>* __restrict__ out, const uint64_t* __restrict__ pw_in,
+                                                 int nw, uint64_t* __restrict__ pw_out) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
     Row4<T> r[SORT_UNR];
-    unsigned long long c[SORT_UNR];
+    int c[SORT_UNR];
 #pragma unroll
     for (int u = 0; u < SORT_UNR; ++u) {
       const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      c[u] = ~0ull;
+      c[u] = -1;
       if (i < n) {
-        c[u] = __ldcs(code + i);
+        c[u] = __ldcs(cellid + i);
         load_row<T, PACKED>(pts, d, i, r[u].v);
       }
     }
+    int64_t pos[SORT_UNR];
+#pragma unroll
+    for (int u = 0; u < SORT_UNR; ++u) pos[u] = c[u] >= 0 ? off[c[u]] + atomicAdd(&cur[c[u]], 1) : -1;
 #pragma unroll
     for (int u = 0; u < SORT_UNR; ++u) {
-      if (c[u] != ~0ull) {
-        const int64_t pos = boff[c[u] >> 32] + static_cast<int64_t>(c[u] & 0xffffffffull);
-        out[pos] = r[u];
+      if (pos[u] >= 0) {
+        out[pos[u]] = r[u];
         const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-        for (int w = 0; w < nw; ++w) pw_out[pos * nw + w] = pw_in[i * nw + w];
+        for (int w = 0; w < nw; ++w) pw_out[pos[u] * nw + w] = pw_in[i * nw + w];
       }
     }
   }
@@ -939,35 +945,34 @@ static bool packed4(const PointsDev& p, int d, size_t es) {
 
 template <typename T, int D>
 static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                              int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code) {
+                              int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
   if (packed4(p, g.d, sizeof(T))) {
-    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code, bin_shift());
+    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, cellid, bin_shift());
   } else {
-    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, code, bin_shift());
+    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, cellid, bin_shift());
   }
 }
 
 template <typename T>
 static void launch_classify(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                            int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code) {
-  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk, code);
-  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk, code);
-  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk, code);
+                            int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
+  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk, cellid);
+  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk, cellid);
+  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk, cellid);
 }
 
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0,
-                  const GridDev& g, int* hist, unsigned long long* err, double* part, int nblk,
-                  unsigned long long* code) {
-  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, hist, err, part, nblk, code);
-  else launch_classify<double>(L, p, n, row0, g, hist, err, part, nblk, code);
+                  const GridDev& g, int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
+  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, hist, err, part, nblk, cellid);
+  else launch_classify<double>(L, p, n, row0, g, hist, err, part, nblk, cellid);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
 
 int bin_k() { return 1 << bin_shift(); }
 
-void run_cell_offsets(const Launch& L, const int64_t* boff, int64_t cells, int64_t* off) {
-  k_cell_offsets<<<static_cast<unsigned>(ceil_div(cells + 1, 256)), 256, 0, L.s>>>(boff, cells, off, bin_shift());
+void run_cell_counts(const Launch& L, const int* hist, int64_t cells, int* counts) {
+  k_cell_counts<<<static_cast<unsigned>(ceil_div(cells, 256)), 256, 0, L.s>>>(hist, cells, bin_shift(), counts);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -989,17 +994,17 @@ void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* 
 
 int64_t scan_scratch_elems(int64_t n) { return ceil_div(n, SCAN_TILE) + 1; }
 
-void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g,
-                 const unsigned long long* code, const int64_t* boff, void* out, const uint64_t* pw_in, int nw,
-                 uint64_t* pw_out, int nblk) {
+void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const int* cellid,
+                 const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out,
+                 int nblk) {
   if (dtype == GSGPC_F32) {
     Row4<float>* o = static_cast<Row4<float>*>(out);
-    if (packed4(p, g.d, 4)) k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
-    else k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+    if (packed4(p, g.d, 4)) k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
+    else k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
   } else {
     Row4<double>* o = static_cast<Row4<double>*>(out);
-    if (packed4(p, g.d, 8)) k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
-    else k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, code, boff, o, pw_in, nw, pw_out);
+    if (packed4(p, g.d, 8)) k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
+    else k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
   }
   L.count();
   GSGPC_CUDA(cudaGetLastError());

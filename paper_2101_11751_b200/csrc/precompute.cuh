@@ -22,16 +22,16 @@ struct Launch {
 int moments_per_cell(int d, int W);
 int64_t scan_scratch_elems(int64_t n);
 int64_t finalize_ws_elems(const GridDev& g);
-// Binning: BIN_K spread sub-counters per cell; classify writes a (bucket, rank) code per row.
+// Binning: spread histogram sub-counters per cell (bin_k()); classify writes a cell id per row.
 int bin_k();
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                  int* hist, unsigned long long* err, double* part, int nblk, unsigned long long* code);
-void run_cell_offsets(const Launch& L, const int64_t* boff, int64_t cells, int64_t* off);
+                  int* hist, unsigned long long* err, double* part, int nblk, int* cellid);
+void run_cell_counts(const Launch& L, const int* hist, int64_t cells, int* counts);
 void run_sum_partials(const Launch& L, const double* part, int np, double* acc);
 void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* block_sums);
-void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g,
-                 const unsigned long long* code, const int64_t* boff, void* out, const uint64_t* pw_in, int nw,
-                 uint64_t* pw_out, int nblk);
+void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const int* cellid,
+                 const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out,
+                 int nblk);
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t nvalid,
                  const GridDev& g, double* mom);
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
