@@ -932,85 +932,6 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
   }
 }
 
-// First transform (dimension d-1) from the cell-major moments, one CTA per cell line
-// (fixed c_0..c_{d-2}): the line's cells are contiguous in the cell-major array, so the CTA
-// stages their moment slices in shared memory with coalesced loads and every output reads
-// shared memory (the generic k_xform gathered them with a Q·8-byte stride between lanes).
-struct XformLine {
-  int W, shift, ymode, half;
-  int64_t nc, sz;          // cells / nodes along dimension d-1
-  int64_t lines;           // Π_{k<d-1} nc_k
-  int64_t qrest;           // index combinations of dimensions 0..d-2
-  int E_in, E_out;         // exponent extent in, index extent out along d-1
-  int64_t cstride, qoff;   // cell-major addressing of the input
-  int64_t qcount;          // moments used per cell (qrest · E_in)
-  int64_t sp_out;          // lines · sz
-  int64_t c0;              // half-stencil offset (d == 1, x-moments)
-};
-
-__global__ void __launch_bounds__(256) k_xform_line(const double* __restrict__ in, double* __restrict__ out,
-                                                    XformLine x) {
-  extern __shared__ double sm_line[];  // [nc][qcount]
-  const int64_t line = blockIdx.x;
-  const double* src = in + line * x.nc * x.cstride + x.qoff;
-  const int64_t tot = x.nc * x.qcount;
-  for (int64_t q = threadIdx.x; q < tot; q += blockDim.x) {
-    const int64_t c = q / x.qcount, e = q % x.qcount;
-    sm_line[q] = src[c * x.cstride + e];
-  }
-  __syncthreads();
-  const int W = x.W;
-  const int64_t items = x.qrest * x.sz;
-  for (int64_t it = threadIdx.x; it < items; it += blockDim.x) {
-    const int64_t a = it % x.sz, qr = it / x.sz;
-    double v[4][7];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-#pragma unroll
-      for (int e = 0; e < 7; ++e) v[i][e] = 0.0;
-      if (i < W) {
-        const int64_t c = a + x.shift - i;
-        if (c >= 0 && c < x.nc) {
-          const double* row = sm_line + c * x.qcount + qr * x.E_in;
-#pragma unroll
-          for (int e = 0; e < 7; ++e)
-            if (e < x.E_in) v[i][e] = row[e];
-        }
-      }
-    }
-    const int64_t spo = line * x.sz + a;
-    if (x.ymode) {
-      double acc = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (i < W && e < x.E_in) acc = fma(v[i][e], c_P[i * 4 + e], acc);
-      out[qr * x.sp_out + spo] = acc;
-      continue;
-    }
-#pragma unroll
-    for (int dq = 0; dq < 7; ++dq) {
-      if (dq >= x.E_out) break;
-      const int delta = dq - (W - 1);
-      const int64_t qo = qr * x.E_out + dq;
-      if (x.half && qo < x.c0) continue;
-      double acc = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = i + delta;
-        if (i < W && j >= 0 && j < W) {
-          const double* coef = c_C + (i * 4 + j) * 7;
-#pragma unroll
-          for (int e = 0; e < 7; ++e)
-            if (e < x.E_in) acc = fma(v[i][e], coef[e], acc);
-        }
-      }
-      out[(x.half ? qo - x.c0 : qo) * x.sp_out + spo] = acc;
-    }
-  }
-}
-
 // ================================================================== host side
 // (x0[, x1[, x2]], y) rows packed 4 elements wide and vector-aligned → one vector load per row
 static bool packed4(const PointsDev& p, int d, size_t es) {
@@ -1215,33 +1136,7 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
       for (int j = 0; j < d; ++j)
         if (j != k) qrest *= x.qext_out[j];
       const int64_t total = qrest * x.sp_out;
-      const int64_t qcount = qrest * x.qext_in[k];
-      const size_t line_smem = sizeof(double) * static_cast<size_t>(g.nc[k] * qcount);
-      if (first && k == d - 1 && line_smem <= 200 * 1024) {
-        XformLine xl{};
-        xl.W = W;
-        xl.shift = x.shift;
-        xl.ymode = x.ymode;
-        xl.half = x.half;
-        xl.nc = g.nc[k];
-        xl.sz = g.sz[k];
-        xl.lines = x.sp_in / g.nc[k];
-        xl.qrest = qrest;
-        xl.E_in = static_cast<int>(x.qext_in[k]);
-        xl.E_out = static_cast<int>(x.qext_out[k]);
-        xl.cstride = cstride;
-        xl.qoff = qoff;
-        xl.qcount = qcount;
-        xl.sp_out = x.sp_out;
-        xl.c0 = c0;
-        if (line_smem > 48 * 1024) {
-          GSGPC_CUDA(cudaFuncSetAttribute(k_xform_line, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(line_smem)));
-        }
-        k_xform_line<<<static_cast<unsigned>(xl.lines), 256, line_smem, L.s>>>(cur, dst, xl);
-      } else {
-        k_xform<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, L.s>>>(cur, dst, x);
-      }
+      k_xform<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, L.s>>>(cur, dst, x);
       L.count();
       cur = dst;
       first = false;
