@@ -11,6 +11,7 @@
 
 #include "internal.cuh"
 #include "precompute.cuh"
+#include "stencil_spmv.cuh"
 #include "toeplitz.cuh"
 
 namespace cg = cooperative_groups;
@@ -61,30 +62,14 @@ __device__ __forceinline__ double grid_reduce(const double* part, int np, double
   return r;
 }
 
+struct PcgOff {
+  __device__ __forceinline__ int operator()(int s) const { return c_pcg_off[s]; }
+};
+
 template <int SMIN>
 __device__ __forceinline__ double pcg_spmv_node(int m, const double* __restrict__ A, const double* __restrict__ v,
                                                 int a) {
-  double acc0 = A[a] * __ldcg(v + a), acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-#pragma unroll 4
-  for (int s = 1; s < SMIN; ++s) {
-    const int o = c_pcg_off[s];
-    const int f = a + o, b = a - o;
-    const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
-    const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
-    const double* As = A + static_cast<int64_t>(s) * m;
-    const double af = As[a];
-    const double ab = As[okb ? b : a];
-    const double vf = __ldcg(v + (okf ? f : a));
-    const double vb = __ldcg(v + (okb ? b : a));
-    if (s & 1) {
-      acc1 = fma(af, okf ? vf : 0.0, acc1);
-      acc2 = fma(okb ? ab : 0.0, vb, acc2);
-    } else {
-      acc3 = fma(af, okf ? vf : 0.0, acc3);
-      acc0 = fma(okb ? ab : 0.0, vb, acc0);
-    }
-  }
-  return (acc0 + acc1) + (acc2 + acc3);
+  return stencil_row_dot<SMIN>(m, A, v, a, PcgOff{});
 }
 
 // One Toeplitz mode product (grid-stride over line tiles × output chunks).  EPI: fused

@@ -18,6 +18,7 @@
 
 #include "internal.cuh"
 #include "precompute.cuh"
+#include "stencil_spmv.cuh"
 #include "toeplitz.cuh"
 
 namespace gsgpc {
@@ -105,33 +106,15 @@ __device__ __forceinline__ double spmv_node(const StencilDesc& sd, const double*
 // whose own partner b'+δ is off-grid (else b' = a-δ would be on-grid).  So every thread runs
 // the same unrolled loop (no divergence) and the blocks stay in step, which keeps the
 // mirrored-half reads in L2.
+struct OpOff {
+  __device__ __forceinline__ int operator()(int s) const { return c_off32[s]; }
+};
+
 template <int SMIN>
 __device__ __forceinline__ double spmv_node_fast(int64_t m64, const double* __restrict__ A,
                                                  const double* __restrict__ v, int64_t a64) {
-  // 32-bit indexing (S_min·m < 2^31 is checked on the host); out-of-[0, m) partners are
-  // clamped to the node itself and masked, so every load is unconditional and can be hoisted.
-  const int m = static_cast<int>(m64), a = static_cast<int>(a64);
-  double acc0 = A[a] * v[a], acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-#pragma unroll 4
-  for (int s = 1; s < SMIN; ++s) {
-    const int o = c_off32[s];
-    const int f = a + o, b = a - o;
-    const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
-    const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
-    const double* As = A + static_cast<int64_t>(s) * m64;
-    const double af = As[a];
-    const double ab = As[okb ? b : a];
-    const double vf = v[okf ? f : a];
-    const double vb = v[okb ? b : a];
-    if (s & 1) {
-      acc1 = fma(af, okf ? vf : 0.0, acc1);
-      acc2 = fma(okb ? ab : 0.0, vb, acc2);
-    } else {
-      acc3 = fma(af, okf ? vf : 0.0, acc3);
-      acc0 = fma(okb ? ab : 0.0, vb, acc0);
-    }
-  }
-  return (acc0 + acc1) + (acc2 + acc3);
+  // 32-bit indexing: S_min·m < 2^31 is checked on the host
+  return stencil_row_dot<SMIN>(static_cast<int>(m64), A, v, static_cast<int>(a64), OpOff{});
 }
 
 __device__ __forceinline__ double spmv_node_any(const StencilDesc& sd, const double* __restrict__ A,

@@ -544,9 +544,10 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
 // One warp runs mma.sync.m8n8k4.f64 (D 8×8 += A 8×4 · B 4×8, k = 4 points per step):
 //   x tiles t = 0..6 : A rows e0 = 0..6 plus row 7 = y  (row 7 yields Y[0][t][c]),
 //                      B[k][n] = t1^t · t2^n  (n = 0..6, column 7 zero);
-//   y tiles j = 0..1 : A rows ρ = 8j + r → (a, b) = (1 + ρ/4, ρ%4), value y t0^a t1^b (ρ < 12),
-//                      B[k][n] = t2^n for n < 4.
-// Accumulators stay in the MMA fragments (18 doubles per lane); at a cell boundary every
+//   y tile (a = 1..3): A rows r < 6 → y t0^(1 + r/2) t1^(2 (r&1)),
+//                      B[k][n] = t1^(n>>2) t2^(n&3)  → D[r][n] = Y[1 + r/2][2 (r&1) + (n>>2)][n&3]
+//                      (48 of the 64 entries used; 8 MMAs per step for 407 moments).
+// Accumulators stay in the MMA fragments (16 doubles per lane); at a cell boundary every
 // lane writes its own fragment entries — no cross-lane reduction.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -554,8 +555,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
                                                             int64_t nvalid, GridDev g, double* __restrict__ mom,
                                                             int64_t range) {
@@ -569,16 +570,15 @@ __global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __res
   const int r = lane >> 2;   // A row / B column / D row
   const int kq = lane & 3;   // A column / B row: the point of the 4-point step
   const int cb = 2 * (lane & 3);  // D columns cb, cb+1
-  // y-tile row meaning for this lane
-  const int rho0 = r, rho1 = 8 + r;
-  const int ya0 = 1 + rho0 / 4, yb0 = rho0 % 4;
-  const int ya1 = 1 + rho1 / 4, yb1 = rho1 % 4;
-  const bool yv1 = rho1 < 12;
+  // y-tile: A row r → (a, b_hi), B column r → (b_lo, c)
+  const bool yrow = r < 6;
+  const int ya = 1 + r / 2, ybh = 2 * (r & 1);
+  const int ybl = r >> 2, yc = r & 3;
 
-  double dx[7][2], dy[2][2];
+  double dx[7][2], dy[2];
 #pragma unroll
   for (int t = 0; t < 7; ++t) dx[t][0] = dx[t][1] = 0.0;
-  dy[0][0] = dy[0][1] = dy[1][0] = dy[1][1] = 0.0;
+  dy[0] = dy[1] = 0.0;
 
   int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
   int64_t p = r0;
@@ -613,9 +613,8 @@ __global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __res
         const double y = P[7];
         const double ax = P[r];            // r < 7: t0^r ; r == 7: y
         const double t2n = r < 7 ? P[16 + r] : 0.0;
-        const double ay0 = y * P[ya0] * P[8 + yb0];
-        const double ay1 = yv1 ? y * P[ya1] * P[8 + yb1] : 0.0;
-        const double by = r < 4 ? t2n : 0.0;
+        const double ay = yrow ? y * P[ya] * P[8 + ybh] : 0.0;
+        const double by = P[8 + ybl] * P[16 + yc];
         const double2 p01 = *reinterpret_cast<const double2*>(P + 8);
         const double2 p23 = *reinterpret_cast<const double2*>(P + 10);
         const double2 p45 = *reinterpret_cast<const double2*>(P + 12);
@@ -624,8 +623,7 @@ __global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __res
                               t2n * p45.x, t2n * p45.y, t2n * p6};
 #pragma unroll
         for (int tt = 0; tt < 7; ++tt) dmma(dx[tt][0], dx[tt][1], ax, bt[tt]);
-        dmma(dy[0][0], dy[0][1], ay0, by);
-        dmma(dy[1][0], dy[1][1], ay1, by);
+        dmma(dy[0], dy[1], ay, by);
       }
       __syncwarp();
     }
@@ -649,11 +647,8 @@ __global__ void __launch_bounds__(128, 4) k_moments_d3c_mma(const Row4<T>* __res
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int col = cb + i;
-      if (col < 4) {
-        flush_val(M + D3C_QX + ya0 * 16 + yb0 * 4 + col, dy[0][i], owned);
-        if (yv1) flush_val(M + D3C_QX + ya1 * 16 + yb1 * 4 + col, dy[1][i], owned);
-      }
-      dy[0][i] = dy[1][i] = 0.0;
+      if (yrow) flush_val(M + D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i], owned);
+      dy[i] = 0.0;
     }
     p = seg_end;
   }
@@ -1032,11 +1027,23 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
       const char* e = getenv("GSGPC_K1_DFMA");
       return e && e[0] == '1';
     }();
+    static const int minb = [] {
+      const char* e = getenv("GSGPC_K1_MINB");
+      return e ? atoi(e) : 6;  // resident blocks/SM; B200: 4 → 6.39 ms, 5 → 5.76, 6 → 5.52 (config 3)
+    }();
+    const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
     if (use_dfma) {
-      k_moments_d3c<T><<<static_cast<unsigned>(ceil_div(warps, 4)), 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    } else if (minb == 8) {
+      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    } else if (minb == 7) {
+      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    } else if (minb == 6) {
+      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+    } else if (minb == 5) {
+      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
     } else {
-      k_moments_d3c_mma<T><<<static_cast<unsigned>(ceil_div(warps, 4)), 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom,
-                                                                                       range);
+      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
     }
   } else {
     const int64_t range = 1024;
