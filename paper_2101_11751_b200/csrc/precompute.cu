@@ -833,14 +833,12 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
 // W^T v_p).  A thread owns one (line, node): it loads the W·E moments of the W cells whose
 // 4^d block contains the node once and produces every output offset from them.
 struct XformDims {
-  int d, W, k;
-  int shift;               // cell of node a at slot i: c = a + shift - i (cubic 1, linear 0)
-  int ymode;               // 1: exponent digit collapses to one output (no offset)
-  int64_t ext_in[3], ext_out[3];   // spatial extents (cells / nodes)
-  int64_t qext_in[3], qext_out[3]; // index extents
-  int64_t sp_in, sp_out;           // Π spatial extents
-  int64_t nc_k;
-  // input addressing: moment-major In[q * sp_in + sp]  or cell-major In[sp * cstride + qoff + q]
+  int sp_in, sp_out;   // Π spatial extents of input / output (< 2^31)
+  int inner_sp;        // Π spatial extents of dims after k (already transformed, same in/out)
+  int ext_in_k, ext_out_k;  // cells / nodes along k
+  int inner_q;         // Π index extents of digits after k (same in/out)
+  int shift;           // cell of node a at slot i: c = a + shift - i (cubic 1, linear 0)
+  // input addressing: moment-major In[q * sp_in + sp] or cell-major In[sp * cstride + qoff + q]
   int cell_major;
   int64_t cstride, qoff;
   // output: moment-major Out[q * sp_out + sp], or the half stencil (last x pass): q >= c0 only
@@ -848,82 +846,61 @@ struct XformDims {
   int64_t c0;
 };
 
+// Thread = (output spatial index sp: blockIdx.x/threadIdx.x, remaining index digits:
+// blockIdx.y).  W (4 cubic / 2 linear) and the y/x mode are template parameters so the
+// 4 × 7 load window and the coefficient loops unroll without guards; all index math is
+// 32-bit (the launch is issue-bound otherwise).
+template <int W, bool YM>
 __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, double* __restrict__ out, XformDims x) {
-  int64_t qrest_total = 1;
-  for (int j = 0; j < x.d; ++j)
-    if (j != x.k) qrest_total *= x.qext_out[j];
-  const int64_t total = qrest_total * x.sp_out;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int64_t sp = idx % x.sp_out;
-  const int64_t qrest = idx / x.sp_out;
-  int64_t inner_sp = 1;
-  for (int j = x.k + 1; j < x.d; ++j) inner_sp *= x.ext_out[j];
-  const int64_t sp_lo = sp % inner_sp;
-  const int64_t a = (sp / inner_sp) % x.ext_out[x.k];
-  const int64_t sp_hi = sp / (inner_sp * x.ext_out[x.k]);
-  // index digits: qrest enumerates digits j != k (row-major)
-  int64_t inner_q_in = 1, inner_q_out = 1;
-  for (int j = x.k + 1; j < x.d; ++j) {
-    inner_q_in *= x.qext_in[j];
-    inner_q_out *= x.qext_out[j];
-  }
-  const int64_t q_lo = qrest % inner_q_out;  // digits after k (same extents in and out)
-  const int64_t q_hi = qrest / inner_q_out;
-  const int W = x.W;
-  const int E_in = static_cast<int>(x.qext_in[x.k]);
-  double v[4][7];
+  constexpr int E = 2 * W - 1;
+  constexpr int EIN = YM ? W : E;
+  const int sp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sp >= x.sp_out) return;
+  const int qrest = blockIdx.y;
+  const int q_hi = qrest / x.inner_q, q_lo = qrest - q_hi * x.inner_q;
+  const int t = sp / x.inner_sp;
+  const int sp_lo = sp - t * x.inner_sp;
+  const int sp_hi = t / x.ext_out_k;
+  const int a = t - sp_hi * x.ext_out_k;
+  double v[W][EIN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < W; ++i) {
+    const int c = a + x.shift - i;
+    const bool ok = c >= 0 && c < x.ext_in_k;
+    const int spi = (sp_hi * x.ext_in_k + c) * x.inner_sp + sp_lo;
 #pragma unroll
-    for (int e = 0; e < 7; ++e) v[i][e] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i < W) {
-      const int64_t c = a + x.shift - i;
-      if (c >= 0 && c < x.nc_k) {
-        const int64_t spi = (sp_hi * x.ext_in[x.k] + c) * inner_sp + sp_lo;
-#pragma unroll
-        for (int e = 0; e < 7; ++e) {
-          if (e < E_in) {
-            const int64_t qi = (q_hi * E_in + e) * inner_q_in + q_lo;
-            v[i][e] = x.cell_major ? in[spi * x.cstride + x.qoff + qi] : in[qi * x.sp_in + spi];
-          }
-        }
-      }
+    for (int e = 0; e < EIN; ++e) {
+      const int qi = (q_hi * EIN + e) * x.inner_q + q_lo;
+      const int64_t addr = x.cell_major ? static_cast<int64_t>(spi) * x.cstride + x.qoff + qi
+                                        : static_cast<int64_t>(qi) * x.sp_in + spi;
+      v[i][e] = ok ? __ldg(in + addr) : 0.0;
     }
   }
-  if (x.ymode) {
+  if (YM) {
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < W; ++i)
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (i < W && e < E_in) acc = fma(v[i][e], c_P[i * 4 + e], acc);
-    const int64_t qo = q_hi * inner_q_out + q_lo;  // digit k collapsed to extent 1
-    out[qo * x.sp_out + sp] = acc;
+      for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_P[i * 4 + e], acc);
+    const int qo = q_hi * x.inner_q + q_lo;  // digit k collapsed to extent 1
+    out[static_cast<int64_t>(qo) * x.sp_out + sp] = acc;
     return;
   }
-  const int E = 2 * W - 1;
 #pragma unroll
-  for (int dq = 0; dq < 7; ++dq) {
-    if (dq >= E) break;
+  for (int dq = 0; dq < E; ++dq) {
     const int delta = dq - (W - 1);
-    const int64_t qo = (q_hi * E + dq) * inner_q_out + q_lo;
+    const int64_t qo = static_cast<int64_t>(q_hi * E + dq) * x.inner_q + q_lo;
     if (x.half && qo < x.c0) continue;
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < W; ++i) {
       const int j = i + delta;
-      if (i < W && j >= 0 && j < W) {
-        const double* coef = c_C + (i * 4 + j) * 7;
+      if (j >= 0 && j < W) {
 #pragma unroll
-        for (int e = 0; e < 7; ++e)
-          if (e < E_in) acc = fma(v[i][e], coef[e], acc);
+        for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_C[(i * 4 + j) * 7 + e], acc);
       }
     }
-    if (x.half) out[(qo - x.c0) * x.sp_out + sp] = acc;
-    else out[qo * x.sp_out + sp] = acc;
+    out[(x.half ? qo - x.c0 : qo) * x.sp_out + sp] = acc;
   }
 }
 
@@ -1108,11 +1085,6 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
   // chain over k = d-1 .. 0; the first pass reads the cell-major moments directly
   auto chain = [&](bool ymode, const double* src, int64_t cstride, int64_t qoff, int qk0, double* final_out,
                    int64_t c0) {
-    XformDims x{};
-    x.d = d;
-    x.W = W;
-    x.shift = W == 4 ? 1 : 0;
-    x.ymode = ymode ? 1 : 0;
     int64_t ext[3], qext[3];
     for (int k = 0; k < d; ++k) {
       ext[k] = g.nc[k];
@@ -1121,17 +1093,26 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
     const double* cur = src;
     bool first = true;
     for (int k = d - 1; k >= 0; --k) {
-      x.k = k;
-      x.nc_k = g.nc[k];
-      x.sp_in = x.sp_out = 1;
+      XformDims x{};
+      int64_t ext_out[3], qext_out[3], sp_in = 1, sp_out = 1, inner_sp = 1, inner_q = 1, qrest = 1;
       for (int j = 0; j < d; ++j) {
-        x.ext_in[j] = ext[j];
-        x.ext_out[j] = j == k ? g.sz[k] : ext[j];
-        x.qext_in[j] = qext[j];
-        x.qext_out[j] = j == k ? (ymode ? 1 : E) : qext[j];
-        x.sp_in *= x.ext_in[j];
-        x.sp_out *= x.ext_out[j];
+        ext_out[j] = j == k ? g.sz[k] : ext[j];
+        qext_out[j] = j == k ? (ymode ? 1 : E) : qext[j];
+        sp_in *= ext[j];
+        sp_out *= ext_out[j];
+        if (j > k) {
+          inner_sp *= ext[j];
+          inner_q *= qext[j];
+        }
+        if (j != k) qrest *= qext_out[j];
       }
+      x.sp_in = static_cast<int>(sp_in);
+      x.sp_out = static_cast<int>(sp_out);
+      x.inner_sp = static_cast<int>(inner_sp);
+      x.ext_in_k = static_cast<int>(ext[k]);
+      x.ext_out_k = static_cast<int>(g.sz[k]);
+      x.inner_q = static_cast<int>(inner_q);
+      x.shift = W == 4 ? 1 : 0;
       x.cell_major = first ? 1 : 0;
       x.cstride = cstride;
       x.qoff = qoff;
@@ -1139,17 +1120,20 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
       x.half = (last && !ymode) ? 1 : 0;
       x.c0 = c0;
       double* dst = last ? final_out : (cur == bufA ? bufB : bufA);
-      int64_t qrest = 1;
-      for (int j = 0; j < d; ++j)
-        if (j != k) qrest *= x.qext_out[j];
-      const int64_t total = qrest * x.sp_out;
-      k_xform<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, L.s>>>(cur, dst, x);
+      const dim3 grid(static_cast<unsigned>(ceil_div(sp_out, 256)), static_cast<unsigned>(qrest));
+      if (W == 4) {
+        if (ymode) k_xform<4, true><<<grid, 256, 0, L.s>>>(cur, dst, x);
+        else k_xform<4, false><<<grid, 256, 0, L.s>>>(cur, dst, x);
+      } else {
+        if (ymode) k_xform<2, true><<<grid, 256, 0, L.s>>>(cur, dst, x);
+        else k_xform<2, false><<<grid, 256, 0, L.s>>>(cur, dst, x);
+      }
       L.count();
       cur = dst;
       first = false;
       for (int j = 0; j < d; ++j) {
-        ext[j] = x.ext_out[j];
-        qext[j] = x.qext_out[j];
+        ext[j] = ext_out[j];
+        qext[j] = qext_out[j];
       }
     }
   };
