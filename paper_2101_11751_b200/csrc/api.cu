@@ -459,50 +459,53 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   const Launch L = ctx->L();
   const GridDev& g = s->g;
   PhaseTimer pt(ctx);
-  const int K = bin_k();
-  const int64_t nb = g.cells * K;  // spread histogram buckets
-  DBuf& hist = ctx->buf("hist");
-  hist.ensure(sizeof(int) * (nb + 1));
-  DBuf& counts = ctx->buf("counts");
-  counts.ensure(sizeof(int) * (g.cells + 1));
+  if (n >= (int64_t{1} << 31)) throw Error(GSGPC_INVALID_ARGUMENT, "sufficient_stats: batch too large");
+  const BinDesc bd = bin_desc(g.cells);
+  const int64_t ntiles = bin_tiles(n);
+  DBuf& tcnt = ctx->buf("bin_tcnt");
+  tcnt.ensure(sizeof(int) * ntiles * bd.nb);
+  DBuf& gsum = ctx->buf("bin_gsum");
+  gsum.ensure(sizeof(int) * bin_groups(n) * bd.nb);
+  DBuf& bbase = ctx->buf("bin_base");
+  bbase.ensure(sizeof(int64_t) * (bd.nb + 1));
+  DBuf& sbase = ctx->buf("bin_sbase");
+  sbase.ensure(sizeof(int64_t) * (bd.nb + 1));
   DBuf& off = ctx->buf("off");
   off.ensure(sizeof(int64_t) * (g.cells + 2));
-  DBuf& bsum = ctx->buf("scan_bs");
-  bsum.ensure(sizeof(int64_t) * (scan_scratch_elems(g.cells) + 1));
   DBuf& cellid = ctx->buf("cellid");
   cellid.ensure(sizeof(int) * n);
   DBuf& err = ctx->buf("err");
   err.ensure(sizeof(unsigned long long) * 2);
-  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256 * 8), 148 * 6)));
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 148 * 6)));
   DBuf& part = ctx->buf("yty_part");
   part.ensure(sizeof(double) * nblk);
   DBuf& ychunk = ctx->buf("yty_chunk");
   ychunk.ensure(sizeof(double));
 
   int h = pt.begin(0);
-  GSGPC_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * (nb + 1), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
-  run_classify(L, dtype, P, n, row0, g, hist.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
+  run_classify(L, dtype, P, n, row0, g, bd, tcnt.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
                cellid.as<int>());
   run_sum_partials(L, part.as<double>(), nblk, ychunk.as<double>());
   pt.end(h);
   h = pt.begin(1);
-  run_cell_counts(L, hist.as<int>(), g.cells, counts.as<int>());
-  run_scan(L, counts.as<int>(), g.cells, off.as<int64_t>(), bsum.as<int64_t>());
+  run_bucket_totals(L, bd, n, tcnt.as<int>(), gsum.as<int>(), bbase.as<int64_t>(), sbase.as<int64_t>());
   pt.end(h);
   // one sync: error row + number of valid rows
   struct {
     unsigned long long err;
-    int64_t nvalid;
+    int64_t nvalid, nslices;
   } hs{};
   ctx->pin.ensure(64);
   char* pin = static_cast<char*>(ctx->pin.p);
   GSGPC_CUDA(cudaMemcpyAsync(pin, err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaMemcpyAsync(pin + 8, off.as<int64_t>() + g.cells, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(pin + 8, bbase.as<int64_t>() + bd.nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(pin + 16, sbase.as<int64_t>() + bd.nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
   GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
   std::memcpy(&hs.err, pin, 8);
   std::memcpy(&hs.nvalid, pin + 8, 8);
+  std::memcpy(&hs.nslices, pin + 16, 8);
   if (hs.err != ~0ull) {
     const int64_t row = static_cast<int64_t>(hs.err >> 2);
     const int kind = static_cast<int>(hs.err & 3);
@@ -522,12 +525,23 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
     DBuf& pws = ctx->buf("probe_sorted");
     if (nw) pws.ensure(sizeof(uint64_t) * nw * nvalid);
-    DBuf& cur = ctx->buf("cursor");
-    cur.ensure(sizeof(int) * (g.cells + 1));
+    DBuf& rows1 = ctx->buf("bin_rows");
+    rows1.ensure(es * 4 * nvalid);
+    DBuf& cid1 = ctx->buf("bin_cid");
+    cid1.ensure(sizeof(int) * nvalid);
+    DBuf& pw1 = ctx->buf("bin_probe");
+    if (nw) pw1.ensure(sizeof(uint64_t) * nw * nvalid);
+    DBuf& gcur = ctx->buf("bin_cursor");
+    gcur.ensure(sizeof(int) * bd.nb);
+    DBuf& scnt = ctx->buf("bin_scnt");
+    scnt.ensure(sizeof(int) * std::max<int64_t>(1, hs.nslices) * (int64_t{1} << bd.bsh));
     h = pt.begin(2);
-    GSGPC_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int) * (g.cells + 1), ctx->stream));
-    run_scatter(L, dtype, P, n, g, cellid.as<int>(), off.as<int64_t>(), cur.as<int>(), pay.p, pw_dev, nw,
-                nw ? pws.as<uint64_t>() : nullptr, nblk);
+    GSGPC_CUDA(cudaMemsetAsync(gcur.p, 0, sizeof(int) * bd.nb, ctx->stream));
+    run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), bbase.as<int64_t>(), gcur.as<int>(), rows1.p,
+                  cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr);
+    run_slice_sort(L, dtype, bd, g.cells, hs.nslices, rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
+                   sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p, nw ? pw1.as<uint64_t>() : nullptr,
+                   nw, nw ? pws.as<uint64_t>() : nullptr);
     pt.end(h);
     h = pt.begin(3);
     run_moments(L, dtype, pay.p, off.as<int64_t>(), nvalid, g, s->mom.as<double>());

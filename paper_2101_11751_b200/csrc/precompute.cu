@@ -67,22 +67,6 @@ void upload_poly_tables(int W, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ K2a classify + count
-__device__ __forceinline__ int agg_inc(int* counters, int64_t key, bool active) {
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned mask = __ballot_sync(0xffffffffu, active);
-  int res = 0;
-  if (active) {
-    const unsigned peers = __match_any_sync(mask, static_cast<unsigned long long>(key));
-    const int leader = __ffs(peers) - 1;
-    const int rank = __popc(peers & ((1u << lane) - 1u));
-    int base = 0;
-    if (static_cast<int>(lane) == leader) base = atomicAdd(&counters[key], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    res = base + rank;
-  }
-  return res;
-}
-
 // classify() specialised on the dimension, branch-light, 32-bit cell arithmetic
 // (cells < 2^31).  Same decisions as the reference (see stencil_dim_fast for the snap
 // argument).  Non-snapped offsets satisfy t ∈ [1e-9, 1 - 1e-9], where every Keys slot is
@@ -163,80 +147,400 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
-// Binning.  The histogram uses spread sub-counters per cell — row i adds to sub-counter
-// (i >> 8) & (K-1) — so the rows the GPU processes at one instant hit K addresses of a hot
-// cell instead of one (RED contention on clustered data was the cost); k_cell_counts folds
-// them.  Classify also stores each row's cell id (-1: not interpolated), so the scatter
-// neither re-classifies nor repeats the exact arithmetic.  The scatter takes its slot from a
-// per-cell cursor atomic in its own processing order, which keeps each cell's writes
-// sequential in time (sectors complete in L2; slots assigned by another pass's order left
-// half-written sectors to be evicted).
-constexpr int BIN_K = 16;  // maximum spread; the active spread is 1 << bin_shift()
+// ------------------------------------------------------------------ K2 binning
+// Two-level counting sort, no per-row global atomics.  Rows are cut into tiles of
+// TILE_ROWS; cells into buckets of 2^bsh consecutive (row-major) cells, nb ≤ ~1024 buckets.
+//   K2a classify : exact cell of every row → cellid[i] (-1: not interpolated); per-tile
+//                  bucket histogram from shared-memory atomics → tcnt[tile][bucket]; error
+//                  row (atomicMin); Σy² partials.
+//   K2b totals   : bucket sizes → bbase (row offsets), sbase (slice offsets).
+//   K2c partition: each tile claims one run per bucket from the bucket's cursor and writes
+//                  its rows there (shared-memory cursors) → bucket-contiguous rows + cell ids.
+//   K2d slices   : per-bucket counting sort by cell in SLICE_ROWS slices (count, scan,
+//                  scatter with shared-memory cursors) → cell-sorted rows, off[cells + 1].
+// A direct counting sort (one global cursor atomic per row on 1.3e5 hot counters) was
+// latency-bound at ~1.7 TB/s; this pays one extra pass over the rows for no per-row global
+// atomics and at most nb + slices write frontiers.
+template <typename T>
+struct alignas(sizeof(T) * 4) Row4 {
+  T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
+};
 
-static int bin_shift() {  // GSGPC_BIN_K overrides the spread (diagnostics); default BIN_K
-  static const int sh = [] {
-    const char* e = getenv("GSGPC_BIN_K");
-    const int k = e ? atoi(e) : BIN_K;
-    int s2 = 0;
-    while ((1 << (s2 + 1)) <= k && (1 << (s2 + 1)) <= BIN_K) ++s2;
-    return s2;
-  }();
-  return sh;
-}
+constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threads × SORT_UNR × 16
+constexpr int PART_NT = 1024;     // partition: one 1024-thread block per SM
+constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints
 
 template <typename T, bool PACKED, int D>
-__global__ void __launch_bounds__(256, 3) k_classify_count(PointsDev pts, int64_t n, int64_t row0, GridDev g,
-                                                        int* __restrict__ hist,
-                                                        unsigned long long* __restrict__ err,
-                                                        double* __restrict__ yty_part,
-                                                        int* __restrict__ cellid, int kshift) {
+__global__ void __launch_bounds__(256, 3) k_classify_tiles(PointsDev pts, int64_t n, int64_t row0, GridDev g,
+                                                         int bsh, int nb, int* __restrict__ tcnt,
+                                                         unsigned long long* __restrict__ err,
+                                                         double* __restrict__ yty_part,
+                                                         int* __restrict__ cellid) {
+  extern __shared__ int hist[];
   __shared__ double sh[8];
-  const unsigned kmask = (1u << kshift) - 1u;
   double ysq = 0.0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
-    T v[SORT_UNR][4];
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) hist[j] = 0;
+    __syncthreads();
+    for (int sub = 0; sub < TILE_ROWS / (256 * SORT_UNR); ++sub) {
+      const int64_t base = tile * TILE_ROWS + static_cast<int64_t>(sub) * 256 * SORT_UNR;
+      T v[SORT_UNR][4];
 #pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) {
-      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      if (i < n) load_row<T, PACKED>(pts, g.d, i, v[u]);
-    }
+      for (int u = 0; u < SORT_UNR; ++u) {
+        const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * 256;
+        if (i < n) load_row<T, PACKED>(pts, g.d, i, v[u]);
+      }
 #pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) {
-      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      if (i < n) {
-        double x[D];
+      for (int u = 0; u < SORT_UNR; ++u) {
+        const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * 256;
+        if (i < n) {
+          double x[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = static_cast<double>(v[u][k]);
-        const double y = static_cast<double>(v[u][3]);
-        ysq += y * y;
-        int cell = 0;
-        const int st = classify_d<D>(g, x, cell);
-        if (st == PT_VALID) {
-          atomicAdd(&hist[(static_cast<unsigned>(cell) << kshift) + (static_cast<unsigned>(i >> 8) & kmask)], 1);
-        } else {
-          cell = -1;
-          if (st == PT_OUTSIDE || st == PT_LEAVES) {
-            const unsigned long long ecode =
-                (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
-            atomicMin(err, ecode);
+          for (int k = 0; k < D; ++k) x[k] = static_cast<double>(v[u][k]);
+          const double y = static_cast<double>(v[u][3]);
+          ysq += y * y;
+          int cell = 0;
+          const int st = classify_d<D>(g, x, cell);
+          if (st == PT_VALID) {
+            atomicAdd(&hist[cell >> bsh], 1);
+          } else {
+            cell = -1;
+            if (st == PT_OUTSIDE || st == PT_LEAVES) {
+              const unsigned long long ecode =
+                  (static_cast<unsigned long long>(row0 + i + 1) << 2) | static_cast<unsigned long long>(st);
+              atomicMin(err, ecode);
+            }
           }
+          __stcs(cellid + i, cell);
         }
-        __stcs(cellid + i, cell);
       }
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) tcnt[tile * nb + j] = hist[j];
+    __syncthreads();
   }
   const double s2 = block_sum<256>(ysq, sh);
   if (threadIdx.x == 0) yty_part[blockIdx.x] = s2;
 }
 
-// counts[c] = Σ_k hist[c·K + k]
-__global__ void k_cell_counts(const int* __restrict__ hist, int64_t cells, int kshift, int* __restrict__ counts) {
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= cells) return;
+// K2b.  Bucket totals: tiles are grouped TSCAN_G at a time (group sums), then one block sums
+// the groups per bucket and scans: bbase[b] (first row of bucket b, bbase[nb] = rows
+// binned) and sbase[b] (first slice of bucket b, sbase[nb] = slices).
+constexpr int TSCAN_G = 64;
+constexpr int SLICE_ROWS = 8192;  // K2d work unit
+
+__global__ void k_tscan_groups(const int* __restrict__ tcnt, int64_t ntiles, int nb, int* __restrict__ gsum) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ngroups = (ntiles + TSCAN_G - 1) / TSCAN_G;
+  if (idx >= ngroups * nb) return;
+  const int64_t gi = idx / nb;
+  const int b = static_cast<int>(idx - gi * nb);
+  const int64_t t1 = imin64((gi + 1) * TSCAN_G, ntiles);
   int s2 = 0;
-  for (int k = 0; k < (1 << kshift); ++k) s2 += hist[(c << kshift) + k];
-  counts[c] = s2;
+  const int64_t t0 = gi * TSCAN_G;
+#pragma unroll 16
+  for (int q = 0; q < TSCAN_G; ++q) s2 += t0 + q < t1 ? tcnt[(t0 + q) * nb + b] : 0;
+  gsum[idx] = s2;
+}
+
+// Exclusive scan of one int64 per thread over a 1024-thread block; *total = Σ.
+__device__ __forceinline__ int64_t block_exscan_1024(int64_t v, int64_t* wsum, int64_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t x = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    wsum[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  *total = wsum[31];
+  return incl - v + (w > 0 ? wsum[w - 1] : 0);
+}
+
+// One block (1024 threads), nb ≤ 8 · 1024.
+__global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ gsum, int64_t ngroups, int nb,
+                                                        int64_t* __restrict__ bbase, int64_t* __restrict__ sbase) {
+  __shared__ int64_t wsum[32];
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  int64_t tots[8], rows_local = 0, slices_local = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    tots[q] = 0;
+    const int b = b0 + q;
+    if (q < per && b < nb) {
+      int64_t run = 0;
+      for (int64_t gi = 0; gi < ngroups; ++gi) run += gsum[gi * nb + b];
+      tots[q] = run;
+      rows_local += run;
+      slices_local += (run + SLICE_ROWS - 1) / SLICE_ROWS;
+    }
+  }
+  int64_t rows_total = 0, slices_total = 0;
+  int64_t rrun = block_exscan_1024(rows_local, wsum, &rows_total);
+  int64_t srun = block_exscan_1024(slices_local, wsum, &slices_total);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int b = b0 + q;
+    if (q < per && b < nb) {
+      bbase[b] = rrun;
+      sbase[b] = srun;
+      rrun += tots[q];
+      srun += (tots[q] + SLICE_ROWS - 1) / SLICE_ROWS;
+    }
+  }
+  if (threadIdx.x == 0) {
+    bbase[nb] = rows_total;
+    sbase[nb] = slices_total;
+  }
+}
+
+// K2c.  Rows are taken in sub-tiles of R rows (R = rows_per_thread · PART_NT): each
+// sub-tile is counting-sorted by bucket in shared memory, claims one run per bucket from
+// the bucket's global cursor (one atomic per (sub-tile, bucket)), and is written out
+// linearly — consecutive lanes store consecutive rows of a run.  Rows stored straight from
+// registers (every lane of a warp in a different bucket, 1e3 buckets spread over 2 GB)
+// ran at ~1.1 TB/s whatever the DRAM traffic: the stores' address spread, not the bytes,
+// was the limit.
+template <typename T, bool PACKED, int RPT>
+__global__ void __launch_bounds__(PART_NT, 1) k_partition(PointsDev pts, int64_t n, int d,
+                                                          const int* __restrict__ cellid, int bsh, int nb,
+                                                          const int64_t* __restrict__ bbase, int* __restrict__ gcur,
+                                                          Row4<T>* __restrict__ rows1, int* __restrict__ cid1,
+                                                          const uint64_t* __restrict__ pw_in, int nw,
+                                                          uint64_t* __restrict__ pw1) {
+  constexpr int R = RPT * PART_NT;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
+  int* stage_c = reinterpret_cast<int*>(stage + R);
+  int* cnt = stage_c + R;   // per-bucket count, then cursor
+  int* goff = cnt + nb;     // global slot of stage row j = goff[bucket] + j
+  __shared__ int wsum[32];
+  __shared__ int total_s;
+  const int64_t nsub = (n + R - 1) / R;
+  for (int64_t sub = blockIdx.x; sub < nsub; sub += gridDim.x) {
+    const int64_t base = sub * R;
+    for (int j = threadIdx.x; j < nb; j += PART_NT) cnt[j] = 0;
+    __syncthreads();
+    Row4<T> r[RPT];
+    int c[RPT], rank[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
+      c[u] = -1;
+      if (i < n) {
+        c[u] = __ldcs(cellid + i);
+        load_row<T, PACKED>(pts, d, i, r[u].v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) rank[u] = c[u] >= 0 ? atomicAdd(&cnt[c[u] >> bsh], 1) : 0;
+    __syncthreads();
+    // exclusive scan of cnt over the buckets (each thread a contiguous segment)
+    const int per = (nb + PART_NT - 1) / PART_NT;
+    const int j0 = threadIdx.x * per;
+    int local = 0;
+    for (int q = 0; q < per; ++q)
+      if (j0 + q < nb) local += cnt[j0 + q];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int x = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      wsum[lane] = x;
+      if (lane == 31) total_s = x;
+    }
+    __syncthreads();
+    int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+    for (int q = 0; q < per; ++q) {
+      const int j = j0 + q;
+      if (j < nb) {
+        const int k = cnt[j];
+        goff[j] = k > 0 ? static_cast<int>(bbase[j]) + atomicAdd(&gcur[j], k) - run : 0;
+        cnt[j] = run;  // local start
+        run += k;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (c[u] >= 0) {
+        const int bk = c[u] >> bsh;
+        const int lp = cnt[bk] + rank[u];
+        stage[lp] = r[u];
+        stage_c[lp] = c[u];
+        if (nw) {
+          const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
+          const int64_t gp = goff[bk] + lp;
+          for (int q = 0; q < nw; ++q) pw1[gp * nw + q] = pw_in[i * nw + q];
+        }
+      }
+    }
+    __syncthreads();
+    const int tot = total_s;
+    for (int j = threadIdx.x; j < tot; j += PART_NT) {
+      const int cc = stage_c[j];
+      const int64_t gp = goff[cc >> bsh] + j;
+      rows1[gp] = stage[j];
+      cid1[gp] = cc;
+    }
+    __syncthreads();
+  }
+}
+
+// K2d.  Per-bucket counting sort by cell, in slices of SLICE_ROWS rows so the work is
+// uniform whatever the bucket sizes:
+//   slice_count : per slice, cell histogram (shared atomics) → scnt[slice][2^bsh]
+//   slice_scan  : per bucket, per cell: exclusive over the bucket's slices (in place), then
+//                 over the bucket's cells → off[c]
+//   slice_scatter: per slice, shared cursors off[c] + scnt[slice][c] → sorted rows.
+__device__ __forceinline__ int slice_bucket(const int64_t* __restrict__ sbase, int nb, int64_t sl) {
+  int lo = 0, hi = nb;  // last b with sbase[b] <= sl
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (sbase[mid] <= sl) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_slice_count(const int* __restrict__ cid1, const int64_t* __restrict__ bbase,
+                                                     const int64_t* __restrict__ sbase, int bsh, int nb,
+                                                     int* __restrict__ scnt) {
+  extern __shared__ int cnt[];
+  const int64_t sl = blockIdx.x;
+  const int b = slice_bucket(sbase, nb, sl);
+  const int nbin = 1 << bsh;
+  const int64_t c0 = static_cast<int64_t>(b) << bsh;
+  const int64_t r0 = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
+  const int64_t r1 = imin64(r0 + SLICE_ROWS, bbase[b + 1]);
+  for (int j = threadIdx.x; j < nbin; j += blockDim.x) cnt[j] = 0;
+  __syncthreads();
+  for (int64_t i0 = r0 + threadIdx.x; i0 < r1; i0 += 256 * 8) {
+    int cc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + u * 256;
+      cc[u] = i < r1 ? __ldcg(cid1 + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (cc[u] >= 0) atomicAdd(&cnt[cc[u] - c0], 1);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nbin; j += blockDim.x) scnt[sl * nbin + j] = cnt[j];
+}
+
+// One block per bucket (1024 threads; 2^bsh ≤ 16384 cells → ≤ 16 per thread).
+__global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, const int64_t* __restrict__ bbase,
+                                                     const int64_t* __restrict__ sbase, int bsh, int nb,
+                                                     int64_t cells, int64_t* __restrict__ off) {
+  __shared__ int64_t wsum[32];
+  const int b = blockIdx.x;
+  const int nbin = 1 << bsh;
+  const int64_t c0 = static_cast<int64_t>(b) << bsh;
+  const int ncell = static_cast<int>(imin64(nbin, cells - c0));
+  const int64_t s0 = sbase[b], s1 = sbase[b + 1];
+  const int per = (nbin + 1023) / 1024;
+  const int j0 = threadIdx.x * per;
+  int tot[16];
+  int64_t local = 0;
+  for (int q = 0; q < 16; ++q) {
+    tot[q] = 0;
+    const int j = j0 + q;
+    if (q < per && j < ncell) {
+      int run = 0;
+      for (int64_t sb = s0; sb < s1; sb += 8) {  // batched: in-place stores alias the loads
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = sb + u < s1 ? scnt[(sb + u) * nbin + j] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (sb + u < s1) scnt[(sb + u) * nbin + j] = run;
+          run += v[u];
+        }
+      }
+      tot[q] = run;
+      local += run;
+    }
+  }
+  int64_t total = 0;
+  int64_t run = bbase[b] + block_exscan_1024(local, wsum, &total);
+  for (int q = 0; q < 16; ++q) {
+    const int j = j0 + q;
+    if (q < per && j < ncell) {
+      off[c0 + j] = run;
+      run += tot[q];
+    }
+  }
+  if (b == nb - 1 && threadIdx.x == 0) off[cells] = bbase[nb];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
+                                                       const int64_t* __restrict__ bbase,
+                                                       const int64_t* __restrict__ sbase, int bsh, int nb,
+                                                       int64_t cells, const int* __restrict__ scnt,
+                                                       const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
+                                                       const uint64_t* __restrict__ pw1, int nw,
+                                                       uint64_t* __restrict__ pws) {
+  constexpr int UNR = sizeof(T) == 4 ? 8 : 4;
+  extern __shared__ int cur[];
+  const int64_t sl = blockIdx.x;
+  const int b = slice_bucket(sbase, nb, sl);
+  const int nbin = 1 << bsh;
+  const int64_t c0 = static_cast<int64_t>(b) << bsh;
+  const int ncell = static_cast<int>(imin64(nbin, cells - c0));
+  const int64_t r0 = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
+  const int64_t r1 = imin64(r0 + SLICE_ROWS, bbase[b + 1]);
+  for (int j = threadIdx.x; j < ncell; j += blockDim.x)
+    cur[j] = static_cast<int>(off[c0 + j]) + scnt[sl * nbin + j];  // rows per add < 2^31
+  __syncthreads();
+  for (int64_t i0 = r0 + threadIdx.x; i0 < r1; i0 += 256 * UNR) {
+    int cc[UNR];
+    Row4<T> rr[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t i = i0 + u * 256;
+      cc[u] = -1;
+      if (i < r1) {
+        cc[u] = __ldcs(cid1 + i);
+        rr[u] = rows1[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (cc[u] >= 0) {
+        const int64_t pos = atomicAdd(&cur[cc[u] - c0], 1);
+        out[pos] = rr[u];
+        const int64_t i = i0 + u * 256;
+        for (int w2 = 0; w2 < nw; ++w2) pws[pos * nw + w2] = pw1[i * nw + w2];
+      }
+    }
+  }
 }
 
 // Deterministic Σ of the per-block y² partials into the running yty.
@@ -246,119 +550,6 @@ __global__ void k_sum_partials(const double* __restrict__ part, int np, double* 
   for (int i = threadIdx.x; i < np; i += blockDim.x) v += part[i];
   const double s = block_sum<256>(v, sh);
   if (threadIdx.x == 0) *acc += s;
-}
-
-// ------------------------------------------------------------------ K2b scan (int → int64)
-constexpr int SCAN_TILE = 2048;  // 256 threads × 8
-
-__global__ void __launch_bounds__(256) k_scan_reduce(const int* __restrict__ in, int64_t n,
-                                                     int64_t* __restrict__ block_sums) {
-  __shared__ int64_t sh[256];
-  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * SCAN_TILE;
-  int64_t s = 0;
-  for (int k = 0; k < 8; ++k) {
-    const int64_t i = b0 + threadIdx.x + k * 256;
-    if (i < n) s += in[i];
-  }
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = sh[0];
-}
-
-// Exclusive scan of the block sums in place (single block, sequential chunks).
-__global__ void __launch_bounds__(1024) k_scan_top(int64_t* __restrict__ bs, int64_t nb) {
-  __shared__ int64_t sh[1024];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nb; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < nb ? bs[i] : 0;
-    sh[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const int64_t a = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
-      __syncthreads();
-      sh[threadIdx.x] += a;
-      __syncthreads();
-    }
-    if (i < nb) bs[i] = carry + sh[threadIdx.x] - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry += sh[1023];
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) k_scan_down(const int* __restrict__ in, int64_t n,
-                                                   const int64_t* __restrict__ block_sums,
-                                                   int64_t* __restrict__ out) {
-  __shared__ int64_t sh[256];
-  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * SCAN_TILE + threadIdx.x * 8;
-  int64_t v[8];
-  int64_t s = 0;
-  for (int k = 0; k < 8; ++k) {
-    const int64_t i = b0 + k;
-    v[k] = i < n ? in[i] : 0;
-    s += v[k];
-  }
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const int64_t a = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
-    __syncthreads();
-    sh[threadIdx.x] += a;
-    __syncthreads();
-  }
-  int64_t run = block_sums[blockIdx.x] + sh[threadIdx.x] - s;
-  for (int k = 0; k < 8; ++k) {
-    const int64_t i = b0 + k;
-    if (i < n) out[i] = run;
-    run += v[k];
-  }
-  // the total lands in out[n] (the caller allocates n+1)
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 255) out[n] = run;
-}
-
-// ------------------------------------------------------------------ K2c scatter
-template <typename T>
-struct alignas(sizeof(T) * 4) Row4 {
-  T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
-};
-
-template <typename T, bool PACKED>
-__global__ void __launch_bounds__(256) k_scatter(PointsDev pts, int64_t n, int d, const int* __restrict__ cellid,
-                                                 const int64_t* __restrict__ off, int* __restrict__ cur,
-                                                 Row4<T>* __restrict__ out, const uint64_t* __restrict__ pw_in,
-                                                 int nw, uint64_t* __restrict__ pw_out) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * SORT_UNR;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * SORT_UNR; base < n; base += stride) {
-    Row4<T> r[SORT_UNR];
-    int c[SORT_UNR];
-#pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) {
-      const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-      c[u] = -1;
-      if (i < n) {
-        c[u] = __ldcs(cellid + i);
-        load_row<T, PACKED>(pts, d, i, r[u].v);
-      }
-    }
-    int64_t pos[SORT_UNR];
-#pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) pos[u] = c[u] >= 0 ? off[c[u]] + atomicAdd(&cur[c[u]], 1) : -1;
-#pragma unroll
-    for (int u = 0; u < SORT_UNR; ++u) {
-      if (pos[u] >= 0) {
-        out[pos[u]] = r[u];
-        const int64_t i = base + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
-        for (int w = 0; w < nw; ++w) pw_out[pos[u] * nw + w] = pw_in[i * nw + w];
-      }
-    }
-  }
 }
 
 // ------------------------------------------------------------------ K1 helpers
@@ -915,36 +1106,46 @@ static bool packed4(const PointsDev& p, int d, size_t es) {
   return d == 3 && y == x + 3 * es && (reinterpret_cast<uintptr_t>(x) % (4 * es)) == 0;
 }
 
+BinDesc bin_desc(int64_t cells) {
+  BinDesc bd{};
+  static const int64_t target = [] {  // GSGPC_BIN_BUCKETS: diagnostics override
+    const char* e = getenv("GSGPC_BIN_BUCKETS");
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t{1024};
+  }();
+  bd.bsh = 0;
+  while (((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh) > target && bd.bsh < BIN_MAX_BSH) ++bd.bsh;
+  bd.nb = static_cast<int>((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh);
+  return bd;
+}
+
+int64_t bin_tiles(int64_t n) { return ceil_div(n, TILE_ROWS); }
+int64_t bin_groups(int64_t n) { return ceil_div(bin_tiles(n), TSCAN_G); }
+
 template <typename T, int D>
 static void launch_classify_d(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                              int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
+                              const BinDesc& bd, int* tcnt, unsigned long long* err, double* part, int nblk,
+                              int* cellid) {
+  const size_t sm = sizeof(int) * bd.nb;
   if (packed4(p, g.d, sizeof(T))) {
-    k_classify_count<T, true, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, cellid, bin_shift());
+    k_classify_tiles<T, true, D><<<nblk, 256, sm, L.s>>>(p, n, row0, g, bd.bsh, bd.nb, tcnt, err, part, cellid);
   } else {
-    k_classify_count<T, false, D><<<nblk, 256, 0, L.s>>>(p, n, row0, g, hist, err, part, cellid, bin_shift());
+    k_classify_tiles<T, false, D><<<nblk, 256, sm, L.s>>>(p, n, row0, g, bd.bsh, bd.nb, tcnt, err, part, cellid);
   }
 }
 
 template <typename T>
 static void launch_classify(const Launch& L, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                            int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
-  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, hist, err, part, nblk, cellid);
-  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, hist, err, part, nblk, cellid);
-  else launch_classify_d<T, 3>(L, p, n, row0, g, hist, err, part, nblk, cellid);
+                            const BinDesc& bd, int* tcnt, unsigned long long* err, double* part, int nblk,
+                            int* cellid) {
+  if (g.d == 1) launch_classify_d<T, 1>(L, p, n, row0, g, bd, tcnt, err, part, nblk, cellid);
+  else if (g.d == 2) launch_classify_d<T, 2>(L, p, n, row0, g, bd, tcnt, err, part, nblk, cellid);
+  else launch_classify_d<T, 3>(L, p, n, row0, g, bd, tcnt, err, part, nblk, cellid);
 }
 
-void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0,
-                  const GridDev& g, int* hist, unsigned long long* err, double* part, int nblk, int* cellid) {
-  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, hist, err, part, nblk, cellid);
-  else launch_classify<double>(L, p, n, row0, g, hist, err, part, nblk, cellid);
-  L.count();
-  GSGPC_CUDA(cudaGetLastError());
-}
-
-int bin_k() { return 1 << bin_shift(); }
-
-void run_cell_counts(const Launch& L, const int* hist, int64_t cells, int* counts) {
-  k_cell_counts<<<static_cast<unsigned>(ceil_div(cells, 256)), 256, 0, L.s>>>(hist, cells, bin_shift(), counts);
+void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
+                  const BinDesc& bd, int* tcnt, unsigned long long* err, double* part, int nblk, int* cellid) {
+  if (dtype == GSGPC_F32) launch_classify<float>(L, p, n, row0, g, bd, tcnt, err, part, nblk, cellid);
+  else launch_classify<double>(L, p, n, row0, g, bd, tcnt, err, part, nblk, cellid);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -955,30 +1156,76 @@ void run_sum_partials(const Launch& L, const double* part, int np, double* acc) 
   GSGPC_CUDA(cudaGetLastError());
 }
 
-void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* block_sums) {
-  const int64_t nb = ceil_div(n, SCAN_TILE);
-  k_scan_reduce<<<static_cast<unsigned>(nb), 256, 0, L.s>>>(in, n, block_sums);
-  k_scan_top<<<1, 1024, 0, L.s>>>(block_sums, nb);
-  k_scan_down<<<static_cast<unsigned>(nb), 256, 0, L.s>>>(in, n, block_sums, out);
-  L.count(3);
+void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, const int* tcnt, int* gsum, int64_t* bbase,
+                       int64_t* sbase) {
+  const int64_t nt = bin_tiles(n), ng = bin_groups(n);
+  k_tscan_groups<<<static_cast<unsigned>(ceil_div(ng * bd.nb, 256)), 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum);
+  k_tscan_buckets<<<1, 1024, 0, L.s>>>(gsum, ng, bd.nb, bbase, sbase);
+  L.count(2);
   GSGPC_CUDA(cudaGetLastError());
 }
 
-int64_t scan_scratch_elems(int64_t n) { return ceil_div(n, SCAN_TILE) + 1; }
+int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd) { return ceil_div(nvalid, SLICE_ROWS) + bd.nb; }
 
-void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const int* cellid,
-                 const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out,
-                 int nblk) {
-  if (dtype == GSGPC_F32) {
-    Row4<float>* o = static_cast<Row4<float>*>(out);
-    if (packed4(p, g.d, 4)) k_scatter<float, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
-    else k_scatter<float, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
-  } else {
-    Row4<double>* o = static_cast<Row4<double>*>(out);
-    if (packed4(p, g.d, 8)) k_scatter<double, true><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
-    else k_scatter<double, false><<<nblk, 256, 0, L.s>>>(p, n, g.d, cellid, off, cur, o, pw_in, nw, pw_out);
-  }
+template <typename T, int RPT>
+static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                               const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
+                               const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk) {
+  Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
+  const size_t sm = static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 2 * sizeof(int) * bd.nb;
+  auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT> : k_partition<T, false, RPT>;
+  GSGPC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, bbase, gcur, r1, cid1, pw_in, nw, pw1);
+}
+
+// rows per thread so that the staged sub-tile + 2 nb counters fit the shared memory
+template <typename T>
+static void launch_partition(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                             const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
+                             const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk) {
+  const size_t budget = 200 * 1024 - 2 * sizeof(int) * bd.nb;
+  const size_t per_rpt = PART_NT * (sizeof(Row4<T>) + sizeof(int));
+  if (budget >= 8 * per_rpt)
+    launch_partition_r<T, 8>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+  else if (budget >= 4 * per_rpt)
+    launch_partition_r<T, 4>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+  else if (budget >= 2 * per_rpt)
+    launch_partition_r<T, 2>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+  else
+    launch_partition_r<T, 1>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+}
+
+void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                   const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
+                   const uint64_t* pw_in, int nw, uint64_t* pw1) {
+  int dev = 0, sms = 148;
+  GSGPC_CUDA(cudaGetDevice(&dev));
+  GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, PART_NT), sms)));
+  if (dtype == GSGPC_F32) launch_partition<float>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+  else launch_partition<double>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
   L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int64_t nslices, const void* rows1,
+                    const int* cid1, const int64_t* bbase, const int64_t* sbase, int* scnt, int64_t* off, void* out,
+                    const uint64_t* pw1, int nw, uint64_t* pws) {
+  const size_t sm = sizeof(int) * (size_t{1} << bd.bsh);
+  if (nslices > 0)
+    k_slice_count<<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt);
+  k_slice_scan<<<static_cast<unsigned>(bd.nb), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off);
+  if (nslices > 0) {
+    if (dtype == GSGPC_F32)
+      k_slice_scatter<float><<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(
+          static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+          static_cast<Row4<float>*>(out), pw1, nw, pws);
+    else
+      k_slice_scatter<double><<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(
+          static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+          static_cast<Row4<double>*>(out), pw1, nw, pws);
+  }
+  L.count(3);
   GSGPC_CUDA(cudaGetLastError());
 }
 

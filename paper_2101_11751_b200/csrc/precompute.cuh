@@ -20,18 +20,29 @@ struct Launch {
 
 // ---- precompute.cu
 int moments_per_cell(int d, int W);
-int64_t scan_scratch_elems(int64_t n);
 int64_t finalize_ws_elems(const GridDev& g);
-// Binning: spread histogram sub-counters per cell (bin_k()); classify writes a cell id per row.
-int bin_k();
+// Binning (two-level counting sort, see precompute.cu K2): bucket = cell >> bsh.
+struct BinDesc {
+  int bsh, nb;
+};
+BinDesc bin_desc(int64_t cells);
+int64_t bin_tiles(int64_t n);   // rows per tile: TILE_ROWS
+int64_t bin_groups(int64_t n);  // tile groups of the tile scan
 void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int64_t row0, const GridDev& g,
-                  int* hist, unsigned long long* err, double* part, int nblk, int* cellid);
-void run_cell_counts(const Launch& L, const int* hist, int64_t cells, int* counts);
+                  const BinDesc& bd, int* tcnt, unsigned long long* err, double* part, int nblk, int* cellid);
 void run_sum_partials(const Launch& L, const double* part, int np, double* acc);
-void run_scan(const Launch& L, const int* in, int64_t n, int64_t* out, int64_t* block_sums);
-void run_scatter(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const int* cellid,
-                 const int64_t* off, int* cur, void* out, const uint64_t* pw_in, int nw, uint64_t* pw_out,
-                 int nblk);
+// bucket sizes: bbase[nb + 1] (row offsets), sbase[nb + 1] (slice offsets); gsum scratch [groups][nb]
+void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, const int* tcnt, int* gsum, int64_t* bbase,
+                       int64_t* sbase);
+int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd);
+// rows → bucket-contiguous rows1 / cid1 / pw1 (gcur: nb zeroed cursors)
+void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                   const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
+                   const uint64_t* pw_in, int nw, uint64_t* pw1);
+// bucket-contiguous → cell-sorted rows (out, pws) and off[cells + 1]; scnt: nslices × 2^bsh
+void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int64_t nslices, const void* rows1,
+                    const int* cid1, const int64_t* bbase, const int64_t* sbase, int* scnt, int64_t* off, void* out,
+                    const uint64_t* pw1, int nw, uint64_t* pws);
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t nvalid,
                  const GridDev& g, double* mom);
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
