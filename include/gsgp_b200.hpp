@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -299,6 +301,48 @@ class RowStream {
   virtual bool next(std::vector<double>& x, double& y) = 0;
 };
 
+// GSGPDAT1 dataset file (io.hpp:31-45): 8-byte magic "GSGPDAT1", u64 n, u64 d, then n rows
+// of (d+1) little-endian doubles.  The constructor validates the header (io.cpp:103-113);
+// sufficient_stats() hands the whole file to the library (gsgpc_stats_add_file: reader
+// thread + pinned double buffers overlapped with the precompute); next() also works.
+class BinaryRowStream : public RowStream {
+ public:
+  explicit BinaryRowStream(const std::string& path) : path_(path), file_(path, std::ios::binary) {
+    if (!file_) throw std::invalid_argument("cannot open binary dataset: " + path);
+    char magic[8];
+    if (!file_.read(magic, 8) || std::memcmp(magic, "GSGPDAT1", 8) != 0) {
+      throw std::invalid_argument("bad magic in binary dataset: " + path);
+    }
+    uint64_t v = 0;
+    if (!file_.read(reinterpret_cast<char*>(&v), 8)) throw std::invalid_argument("truncated file while reading row count");
+    n_ = static_cast<int64_t>(v);
+    if (!file_.read(reinterpret_cast<char*>(&v), 8)) throw std::invalid_argument("truncated file while reading dimension");
+    dim_ = static_cast<int>(v);
+    if (v < 1 || v > 64) throw std::invalid_argument("binary dataset: bad dimension");
+  }
+  int dim() const override { return dim_; }
+  int64_t rows() const { return n_; }
+  const std::string& path() const { return path_; }
+  int64_t rows_read() const { return read_; }
+  bool next(std::vector<double>& x, double& y) override {
+    if (read_ >= n_) return false;
+    x.resize(dim_);
+    for (int k = 0; k < dim_; ++k) {
+      if (!file_.read(reinterpret_cast<char*>(&x[k]), 8)) throw std::invalid_argument("truncated file while reading coordinate");
+    }
+    if (!file_.read(reinterpret_cast<char*>(&y), 8)) throw std::invalid_argument("truncated file while reading response");
+    ++read_;
+    return true;
+  }
+
+ private:
+  std::string path_;
+  std::ifstream file_;
+  int dim_ = 0;
+  int64_t n_ = 0;
+  int64_t read_ = 0;
+};
+
 class SufficientStatsAccumulator {
  public:
   SufficientStatsAccumulator(Grid grid, InterpScheme scheme, Context ctx = Context::default_context())
@@ -325,6 +369,13 @@ class SufficientStatsAccumulator {
   void add_points(const gsgpc_points& p, int64_t n) {
     ctx_.check(gsgpc_stats_add(ctx_.get(), h_.get(), &p, n, nullptr, 0));
     rows_ += n;
+  }
+  // every row of a GSGPDAT1 file; returns the rows added
+  int64_t add_file(const std::string& path) {
+    int64_t rows = 0;
+    ctx_.check(gsgpc_stats_add_file(ctx_.get(), h_.get(), path.c_str(), &rows));
+    rows_ += rows;
+    return rows;
   }
   void enable_probes(int probes, uint64_t seed) {
     ctx_.check(gsgpc_stats_enable_probes(ctx_.get(), h_.get(), probes, seed));
@@ -354,6 +405,12 @@ inline SufficientStats sufficient_stats(const Grid& grid, InterpScheme scheme, R
     throw std::invalid_argument("sufficient_stats: stream/grid dimension mismatch");
   }
   SufficientStatsAccumulator acc(grid, scheme, ctx);
+  if (auto* bin = dynamic_cast<BinaryRowStream*>(&stream)) {
+    if (bin->rows_read() == 0) {  // whole file through the library's overlapped reader
+      acc.add_file(bin->path());
+      return acc.finalize();
+    }
+  }
   const int d = grid.dim();
   const int64_t batch = int64_t{1} << 20;
   std::vector<double> xs, ys, x(d);

@@ -124,6 +124,16 @@ void gsgpc_stats_destroy(gsgpc_stats* stats);
  * used by the factorized SLQ (gp.cpp:97-99); pass NULL / 0 otherwise. */
 gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* stats, const gsgpc_points* pts,
                              int64_t n, const uint64_t* probe_words, int probes);
+/* Accumulate every row of a GSGPDAT1 dataset file (BinaryRowStream, io.hpp:31-45,
+ * io.cpp:103-122: magic "GSGPDAT1", u64 n, u64 d, n rows of (d+1) little-endian f64) —
+ * sufficient_stats(grid, scheme, BinaryRowStream(path)) (interp.cpp:244-263) when stats is
+ * fresh.  Reading, host-to-device copies and the precompute overlap (pinned double buffers).
+ * Errors as the reference: "cannot open binary dataset", "bad magic in binary dataset",
+ * "truncated file while reading row count|dimension|coordinate|response", "binary dataset:
+ * bad dimension", "sufficient_stats: stream/grid dimension mismatch", and
+ * GSGPC_OUT_OF_GRID "sufficient_stats: stream row N: ..." with N counted from the file's
+ * first row.  On error the accumulator is unchanged.  rows_added may be NULL. */
+gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* stats, const char* path, int64_t* rows_added);
 /* Accumulate probe images of the reference's Rademacher probes (rademacher_probe,
  * gp.cpp:16-25: std::seed_seq{seed_lo, seed_hi, p_lo, p_hi} + std::mt19937_64, one draw per
  * row in stream order) for p = 0..probes-1 in every following gsgpc_stats_add; the library

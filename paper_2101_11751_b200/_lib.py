@@ -66,6 +66,7 @@ SIGNATURES = {
     "gsgpc_stats_create": (_i, [_vp, _P(Grid_t), _i, _P(_vp)]),
     "gsgpc_stats_destroy": (None, [_vp]),
     "gsgpc_stats_add": (_i, [_vp, _vp, _P(Points_t), _i64, _vp, _i]),
+    "gsgpc_stats_add_file": (_i, [_vp, _vp, C.c_char_p, _P(_i64)]),
     "gsgpc_stats_merge": (_i, [_vp, _vp, _vp]),
     "gsgpc_stats_reset": (_i, [_vp, _vp]),
     "gsgpc_stats_enable_probes": (_i, [_vp, _vp, _i, C.c_uint64]),

@@ -102,6 +102,8 @@ struct gsgpc_ctx {
   std::unique_ptr<CgCache> cg;
   cudaStream_t copy = nullptr;   // H2D staging stream (overlaps the next batch's copy with compute)
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  PinnedBuf file_pin[2];         // GSGPDAT1 ingest: host read buffers (reader thread fills one while
+                                 // the other is copied to the device)
   Launch L() { return Launch{stream, &launches}; }
   void ensure_copy_stream() {
     if (copy) return;
@@ -751,6 +753,46 @@ void gsgpc_stats_destroy(gsgpc_stats* s) {
   delete s;
 }
 
+// A batch committed in several chunks snapshots the accumulator first, so a failing later
+// chunk leaves it unchanged (the reference's single pass throws before returning any
+// statistics).
+struct StatsSnapshot {
+  gsgpc_ctx* ctx;
+  gsgpc_stats* s;
+  bool active = false;
+  int64_t n_before = 0;
+  std::vector<std::mt19937_64> gens;
+  StatsSnapshot(gsgpc_ctx* c, gsgpc_stats* st, bool take) : ctx(c), s(st), active(take), n_before(st->n), gens(st->gens) {
+    if (!active) return;
+    DBuf& bm = ctx->buf("bk_mom");
+    bm.ensure(sizeof(double) * s->g.cells * s->Q + 8);
+    GSGPC_CUDA(cudaMemcpyAsync(bm.p, s->mom.p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    DBuf& by = ctx->buf("bk_yty");
+    by.ensure(sizeof(double));
+    GSGPC_CUDA(cudaMemcpyAsync(by.p, s->yty.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (s->probes) {
+      DBuf& bp = ctx->buf("bk_pmom");
+      bp.ensure(sizeof(double) * s->g.cells * s->probes * s->QY);
+      GSGPC_CUDA(cudaMemcpyAsync(bp.p, s->pmom.p, sizeof(double) * s->g.cells * s->probes * s->QY,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  void restore() {
+    s->gens = gens;
+    if (!active) return;
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
+    cudaMemcpy(s->yty.p, ctx->buf("bk_yty").p, sizeof(double), cudaMemcpyDeviceToDevice);
+    if (s->probes) {
+      cudaMemcpy(s->pmom.p, ctx->buf("bk_pmom").p, sizeof(double) * s->g.cells * s->probes * s->QY,
+                 cudaMemcpyDeviceToDevice);
+    }
+    s->n = n_before;
+    s->finalized = false;
+  }
+};
+
 gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points* pts, int64_t n,
                              const uint64_t* probe_words, int probes) {
   return guard(ctx, [&] {
@@ -778,43 +820,10 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
     if (n == 0) return;
     const bool dev = is_device_ptr(pts->x);
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
-    const std::vector<std::mt19937_64> gens_backup = s->gens;  // restored if a batch fails
     const bool pw_dev = nw ? is_device_ptr(probe_words) : true;
     const int64_t CH = dev ? (int64_t{1} << 27) : (int64_t{1} << 24);
     const int64_t nchunks = ceil_div(n, CH);
-    // A batch larger than one chunk commits chunk by chunk; snapshot the accumulator so a
-    // failing later chunk still leaves it unchanged (the reference's single pass throws
-    // before returning any statistics).
-    const int64_t n_before = s->n;
-    if (nchunks > 1) {
-      DBuf& bm = ctx->buf("bk_mom");
-      bm.ensure(sizeof(double) * s->g.cells * s->Q + 8);
-      GSGPC_CUDA(cudaMemcpyAsync(bm.p, s->mom.p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice,
-                                 ctx->stream));
-      DBuf& by = ctx->buf("bk_yty");
-      by.ensure(sizeof(double));
-      GSGPC_CUDA(cudaMemcpyAsync(by.p, s->yty.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-      if (s->probes) {
-        DBuf& bp = ctx->buf("bk_pmom");
-        bp.ensure(sizeof(double) * s->g.cells * s->probes * s->QY);
-        GSGPC_CUDA(cudaMemcpyAsync(bp.p, s->pmom.p, sizeof(double) * s->g.cells * s->probes * s->QY,
-                                   cudaMemcpyDeviceToDevice, ctx->stream));
-      }
-    }
-    auto rollback = [&] {
-      s->gens = gens_backup;
-      if (nchunks > 1) {
-        cudaStreamSynchronize(ctx->stream);
-        cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
-        cudaMemcpy(s->yty.p, ctx->buf("bk_yty").p, sizeof(double), cudaMemcpyDeviceToDevice);
-        if (s->probes) {
-          cudaMemcpy(s->pmom.p, ctx->buf("bk_pmom").p, sizeof(double) * s->g.cells * s->probes * s->QY,
-                     cudaMemcpyDeviceToDevice);
-        }
-        s->n = n_before;
-        s->finalized = false;
-      }
-    };
+    StatsSnapshot snap(ctx, s, nchunks > 1);
     // host rows: double-buffered staging, the copy of chunk k+1 overlaps the compute of chunk k
     static const char* kSlot[2] = {"stage0", "stage1"};
     PointsDev staged[2];
@@ -863,9 +872,118 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
       if (!dev) GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
     } catch (...) {
       if (ctx->copy) cudaStreamSynchronize(ctx->copy);
-      rollback();
+      snap.restore();
       throw;
     }
+  });
+}
+
+// GSGPDAT1 ingest (BinaryRowStream, io.hpp:31-45 / io.cpp:103-122, driven like
+// sufficient_stats, interp.cpp:244-263).  A reader thread fills one pinned buffer while the
+// other is copied to the device (copy stream) and binned / accumulated (compute stream).
+// Errors keep the reference's texts and order: rows before a truncation point are processed
+// first (an out-of-grid row there wins), then "truncated file while reading coordinate /
+// response".  Transactional: on any error the accumulator is left unchanged.
+gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* s, const char* path, int64_t* rows_added) {
+  return guard(ctx, [&] {
+    if (!s) invalid("stats is NULL");
+    if (!path) invalid("path is NULL");
+    if (s->reduced) invalid("SufficientStatsAccumulator::add: statistics were all-reduced; create a new accumulator");
+    if (s->probes > 0 && !s->probe_seeded) {
+      invalid("this accumulator carries caller-supplied probe images: add rows with gsgpc_stats_add");
+    }
+    std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path, "rb"), std::fclose);
+    if (!f) invalid(std::string("cannot open binary dataset: ") + path);
+    char magic[8];
+    if (std::fread(magic, 1, 8, f.get()) != 8 || std::memcmp(magic, "GSGPDAT1", 8) != 0) {
+      invalid(std::string("bad magic in binary dataset: ") + path);
+    }
+    uint64_t hdr[2];
+    if (std::fread(&hdr[0], 8, 1, f.get()) != 1) invalid("truncated file while reading row count");
+    if (std::fread(&hdr[1], 8, 1, f.get()) != 1) invalid("truncated file while reading dimension");
+    const int64_t n = static_cast<int64_t>(hdr[0]);
+    const int64_t d = static_cast<int64_t>(hdr[1]);
+    if (d < 1 || d > 64) invalid("binary dataset: bad dimension");
+    if (d != s->g.d) invalid("sufficient_stats: stream/grid dimension mismatch");
+    if (n < 0) invalid("binary dataset: bad row count");
+    if (std::fseek(f.get(), 0, SEEK_END) != 0) invalid(std::string("cannot seek binary dataset: ") + path);
+    const int64_t size = static_cast<int64_t>(ftello(f.get()));
+    std::fseek(f.get(), 24, SEEK_SET);
+    const int64_t rowb = (d + 1) * 8;
+    const int64_t avail = std::min<int64_t>(n, std::max<int64_t>(0, size - 24) / rowb);
+    const bool truncated = avail < n;
+    const int64_t tail_fields = truncated ? (std::max<int64_t>(0, size - 24) - avail * rowb) / 8 : 0;
+    const int64_t CH = int64_t{1} << 22;  // rows per chunk (128 MiB of f64 rows at d = 3)
+    const int64_t nchunks = ceil_div(avail, CH);
+    StatsSnapshot snap(ctx, s, nchunks > 1 || (truncated && avail > 0));
+    ctx->ensure_copy_stream();
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));  // staging slots may still be in use
+    for (int b = 0; b < 2; ++b) ctx->file_pin[b].ensure(static_cast<size_t>(std::min(CH, std::max<int64_t>(avail, 1)) * rowb));
+    cudaEvent_t h2d[2];
+    for (int b = 0; b < 2; ++b) GSGPC_CUDA(cudaEventCreateWithFlags(&h2d[b], cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int b = 0; b < 2; ++b) cudaEventDestroy(e[b]);
+      }
+    } evg{h2d};
+    auto read_chunk = [&](int64_t k) -> bool {
+      const int64_t rows = std::min(CH, avail - k * CH);
+      return std::fread(ctx->file_pin[k & 1].p, static_cast<size_t>(rowb), static_cast<size_t>(rows), f.get()) ==
+             static_cast<size_t>(rows);
+    };
+    static const char* kSlot[2] = {"stage0", "stage1"};
+    int64_t done = 0;
+    try {
+      bool ok_next = nchunks > 0 ? read_chunk(0) : true;
+      for (int64_t k = 0; k < nchunks; ++k) {
+        if (!ok_next) invalid("truncated file while reading coordinate");
+        const int64_t rows = std::min(CH, avail - k * CH);
+        const int sl = static_cast<int>(k & 1);
+        gsgpc_points hp{};
+        hp.dtype = GSGPC_F64;
+        hp.x = ctx->file_pin[sl].p;
+        hp.x_row_stride = d + 1;
+        for (int j = 0; j < d; ++j) hp.x_col_offset[j] = j;
+        hp.y = static_cast<const double*>(ctx->file_pin[sl].p) + d;
+        hp.y_stride = d + 1;
+        if (k >= 2) GSGPC_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_free[sl], 0));
+        const PointsDev P = stage_points(ctx, &hp, static_cast<int>(d), 0, rows, true, kSlot[sl], ctx->copy);
+        GSGPC_CUDA(cudaEventRecord(h2d[sl], ctx->copy));
+        // read the next chunk into the other buffer while this one is copied and binned
+        std::thread reader;
+        bool ok = true;
+        if (k + 1 < nchunks) {
+          GSGPC_CUDA(cudaEventSynchronize(h2d[sl ^ 1]));  // its previous copy has finished
+          reader = std::thread([&] { ok = read_chunk(k + 1); });
+        }
+        try {
+          GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, h2d[sl], 0));
+          const uint64_t* pw = nullptr;
+          if (s->probe_seeded) {
+            gen_probe_words(ctx, s, rows);
+            pw = ctx->buf("probe_stage").as<uint64_t>();
+          }
+          add_chunk(ctx, s, GSGPC_F64, P, rows, done, pw, s->probes);
+          GSGPC_CUDA(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
+        } catch (...) {
+          if (reader.joinable()) reader.join();
+          throw;
+        }
+        if (reader.joinable()) reader.join();
+        ok_next = ok;
+        done += rows;
+      }
+      if (truncated) {
+        invalid(std::string("truncated file while reading ") + (tail_fields < d ? "coordinate" : "response"));
+      }
+      GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
+    } catch (...) {
+      cudaStreamSynchronize(ctx->copy);
+      snap.restore();
+      throw;
+    }
+    if (rows_added) *rows_added = done;
   });
 }
 

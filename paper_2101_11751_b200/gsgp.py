@@ -23,6 +23,7 @@ to the library as device pointers (zero copy).  All compute runs in libgsgpc.so 
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -579,6 +580,15 @@ class SufficientStatsAccumulator:
                                                   pw.vp if pw else None, int(probes)))
         self._rows += n
 
+    def add_file(self, path) -> int:
+        """Add every row of a GSGPDAT1 file (BinaryRowStream, io.cpp:103-122); returns the
+        rows added.  Reading, host-to-device copies and the precompute overlap."""
+        rows = C.c_int64(0)
+        self._ctx.check(_L.load().gsgpc_stats_add_file(self._ctx.handle, self._h, os.fsencode(path),
+                                                       C.byref(rows)))
+        self._rows += rows.value
+        return rows.value
+
     def enable_probes(self, probes: int = 30, seed: int = 0):
         """Accumulate W^T v_p for the reference's Rademacher probes p < probes (gp.cpp:16-25),
         generated in stream order by the library; call before adding rows."""
@@ -613,9 +623,69 @@ class _OwnedStats(SufficientStats):
     pass
 
 
+class BinaryRowStream:
+    """GSGPDAT1 dataset (io.hpp:31-45): 8-byte magic, u64 n, u64 d, n rows of (d+1) f64.
+    The constructor validates the header like io.cpp:103-113; the rows are read by the
+    library (gsgpc_stats_add_file) when the stream is handed to sufficient_stats."""
+
+    def __init__(self, path):
+        self.path = os.fspath(path)
+        try:
+            f = open(self.path, "rb")
+        except OSError:
+            raise InvalidArgument("cannot open binary dataset: " + self.path) from None
+        with f:
+            magic = f.read(8)
+            if magic != DATA_MAGIC:
+                raise InvalidArgument("bad magic in binary dataset: " + self.path)
+            hdr = f.read(8)
+            if len(hdr) < 8:
+                raise InvalidArgument("truncated file while reading row count")
+            self._n = int(np.frombuffer(hdr, "<u8")[0])
+            hdr = f.read(8)
+            if len(hdr) < 8:
+                raise InvalidArgument("truncated file while reading dimension")
+            self._d = int(np.frombuffer(hdr, "<u8")[0])
+        if self._d < 1 or self._d > 64:
+            raise InvalidArgument("binary dataset: bad dimension")
+
+    def dim(self) -> int:
+        return self._d
+
+    def rows(self) -> int:
+        return self._n
+
+
+DATA_MAGIC = b"GSGPDAT1"
+
+
+def write_dataset_binary(path, x, y):
+    """write_dataset_binary / BinaryDatasetWriter (io.cpp:139-186): GSGPDAT1, f64 AoS rows."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    y = np.asarray(y, dtype=np.float64).reshape(-1)
+    if x.shape[0] != y.size:
+        raise InvalidArgument("write_dataset_binary: size mismatch")
+    rows = np.empty((x.shape[0], x.shape[1] + 1), dtype="<f8")
+    rows[:, :-1] = x
+    rows[:, -1] = y
+    with open(path, "wb") as f:
+        f.write(DATA_MAGIC)
+        f.write(np.array([x.shape[0], x.shape[1]], dtype="<u8").tobytes())
+        f.write(rows.tobytes())
+
+
 def sufficient_stats(grid: Grid, scheme, x, y=None, ctx: Optional[Context] = None) -> SufficientStats:
-    """interp.cpp:244-263: single pass over the rows (in-memory stream)."""
+    """interp.cpp:244-263: single pass over the rows — an in-memory stream (x, y arrays or
+    packed rows) or a BinaryRowStream (GSGPDAT1 file, streamed by the library)."""
     ctx = ctx or default_context()
+    if isinstance(x, BinaryRowStream):
+        if x.dim() != grid.dim():
+            raise InvalidArgument("sufficient_stats: stream/grid dimension mismatch")
+        acc = SufficientStatsAccumulator(grid, scheme, ctx=ctx)
+        acc.add_file(x.path)
+        return acc.finalize()
     p, n, keep = _points(x, y, grid.dim())
     h = C.c_void_p()
     g = grid._c()
