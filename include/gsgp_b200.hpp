@@ -569,11 +569,15 @@ struct SlqOptions {
   double quad_tol = 0.01;
 };
 
+enum class LogdetRoute { Auto = 0, SymmetricGrid = 1, SkiOperator = 2, Dense = 3 };  // gp.hpp:55-60
+
 struct LoglikOptions {
   double solve_tol = 0.01;
   int probes = 30;
   SlqOptions slq;
   uint64_t seed = 0;
+  LogdetRoute route = LogdetRoute::Auto;
+  int64_t dense_cap = 2048;
   int maxiter = kDefaultMaxIter;
 };
 
@@ -584,8 +588,9 @@ struct LoglikResult {
   std::string logdet_route = "ski-operator-slq";
 };
 
-// SkiOperator route with probe images accumulated in the precompute
-// (SufficientStatsAccumulator::enable_probes(opts.probes, opts.seed) before adding rows).
+// gp.cpp:158-240.  The SkiOperator route reads probe images accumulated in the precompute
+// (SufficientStatsAccumulator::enable_probes(opts.probes, opts.seed) before adding rows);
+// SymmetricGrid / Dense need only the statistics; Auto chooses as the reference does.
 inline LoglikResult log_likelihood_gsgp(const SufficientStats& stats, const ToeplitzOperator& kg, double sigma,
                                         const LoglikOptions& opts) {
   gsgpc_loglik_options o{};
@@ -595,6 +600,8 @@ inline LoglikResult log_likelihood_gsgp(const SufficientStats& stats, const Toep
   o.quad_tol = opts.slq.quad_tol;
   o.seed = opts.seed;
   o.maxiter = opts.maxiter;
+  o.route = static_cast<int32_t>(opts.route);
+  o.dense_cap = opts.dense_cap;
   gsgpc_loglik_result r{};
   stats.context().check(gsgpc_log_likelihood_gsgp(stats.context().get(), stats.handle(), kg.handle(), sigma, &o, &r));
   LoglikResult out;
@@ -604,6 +611,7 @@ inline LoglikResult log_likelihood_gsgp(const SufficientStats& stats, const Toep
   out.const_term = r.const_term;
   out.probes_used = r.probes_used;
   out.solver_iterations = r.solver_iterations;
+  out.logdet_route = r.logdet_route == 1 ? "symmetric-grid-slq" : r.logdet_route == 3 ? "dense" : "ski-operator-slq";
   return out;
 }
 

@@ -236,19 +236,35 @@ typedef struct {
   double quad_tol;    /* SlqOptions::quad_tol */
   uint64_t seed;      /* LoglikOptions::seed */
   int32_t maxiter;    /* LoglikOptions::maxiter */
+  int32_t route;      /* LoglikOptions::route (gp.hpp:55-60): GSGPC_ROUTE_* */
+  int64_t dense_cap;  /* LoglikOptions::dense_cap (default 2048) */
 } gsgpc_loglik_options;
+
+/* LogdetRoute (gp.hpp:55-60) */
+enum {
+  GSGPC_ROUTE_AUTO = 0,           /* SkiOperator when probe images exist, else by conditioning */
+  GSGPC_ROUTE_SYMMETRIC_GRID = 1, /* SLQ(K WᵀW K + σ²K) − SLQ(K), m-dimensional probes */
+  GSGPC_ROUTE_SKI_OPERATOR = 2,   /* factorized SLQ over the precompute's probe images */
+  GSGPC_ROUTE_DENSE = 3           /* LU of K WᵀW + σ²I, m ≤ dense_cap */
+};
 
 typedef struct {
   double loglik, logdet_term, quad_term, const_term; /* LoglikResult (gp.hpp:62-72) */
   int32_t probes_used;
   int32_t solver_iterations;
   int32_t max_depth_used;
+  int32_t logdet_route;  /* the route taken (GSGPC_ROUTE_*, never AUTO) */
 } gsgpc_loglik_result;
 
-/* log_likelihood_gsgp (gp.hpp:86-90, gp.cpp:158-240) on the SkiOperator route
- * (slq_logdet_ski_factorized, gp.cpp:85-111) with the probe images W^T v_p accumulated
- * during the precompute (gsgpc_stats_add with probe words of the reference's
- * rademacher_probe streams, gp.cpp:16-25). */
+/* log_likelihood_gsgp (gp.hpp:86-90, gp.cpp:158-240).  Routes as the reference:
+ * SkiOperator = slq_logdet_ski_factorized (gp.cpp:85-111) over the probe images W^T v_p
+ * accumulated during the precompute (gsgpc_stats_enable_probes: the reference's
+ * rademacher_probe streams, gp.cpp:16-25) — the analogue of passing W; SymmetricGrid =
+ * slq_logdet (gp.cpp:67-83) of K WᵀW K + σ²K minus that of K with m-dimensional probes and
+ * quad_tol 0; Dense = dense_logdet_grid_system (gp.cpp:116-140); Auto picks SkiOperator
+ * when the statistics carry probe images, else Dense if
+ * estimate_grid_kernel_condition (gp.cpp:142-154) > 1e8 and m ≤ dense_cap, else
+ * SymmetricGrid. */
 gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc_kg* kg,
                                        double sigma, const gsgpc_loglik_options* opts,
                                        gsgpc_loglik_result* out);

@@ -1773,14 +1773,8 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
     const int64_t m = s->g.m;
     if (kg->m != m) invalid("log_likelihood_gsgp: kernel/grid size mismatch");
     const int P = opts->probes;
-    if (P < 1) invalid("slq_logdet_ski_factorized: need at least one probe");
-    if (s->probes < P) {
-      invalid("log_likelihood_gsgp: the SkiOperator logdet route needs probe images W^T v_p accumulated in the "
-              "precompute (gsgpc_stats_enable_probes)");
-    }
-    if (s->probe_seeded && s->probe_seed != opts->seed) {
-      invalid("log_likelihood_gsgp: probe images were accumulated with seed " + std::to_string(s->probe_seed));
-    }
+    const int64_t dense_cap = opts->dense_cap > 0 ? opts->dense_cap : 2048;
+    if (opts->route < GSGPC_ROUTE_AUTO || opts->route > GSGPC_ROUTE_DENSE) invalid("log_likelihood_gsgp: bad route");
     const Launch L = ctx->L();
     const double n = static_cast<double>(s->reduced ? static_cast<int64_t>(read_scalar(ctx, s->tail() + 1)) : s->n);
     const double sigma_sq = sigma * sigma;
@@ -1806,44 +1800,89 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
     double wz = 0.0;
     for (int64_t i = 0; i < m; ++i) wz += hw[i] * hz[i];
     const double quad = (yty - wz) / sigma_sq;
-    // SLQ over the probe images (gp.cpp:85-111)
-    const int depth = static_cast<int>(std::min<double>(opts->max_depth, n));
-    if (depth < 1) invalid("slq: need at least one Lanczos step");
-    DBuf& kwt = ctx->buf("ll_kwt");
-    DBuf& kt0 = ctx->buf("ll_kt0");
-    DBuf& kt1 = ctx->buf("ll_kt1");
-    kwt.ensure(sizeof(double) * P * m);
-    kt0.ensure(sizeof(double) * P * m);
-    kt1.ensure(sizeof(double) * P * m);
-    run_kg_batched(L, kg->dev, P, s->pimg(), kwt.as<double>(), kt0.as<double>(), kt1.as<double>());
-    DBuf& zd = ctx->buf("ll_z0");
-    zd.ensure(sizeof(double) * P);
-    std::vector<double> zs(P, n);  // v·v = n for ±1 probes
-    GSGPC_CUDA(cudaMemcpyAsync(zd.p, zs.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
-    const StencilDesc sd = stencil_desc(s);
-    double total = 0.0;
-    int max_used = 0;
-    for (int p0 = 0; p0 < P; p0 += 32) {
-      const int Pb = std::min(32, P - p0);
-      const EflaOut o = efla_run(L, sd, s->stencil(), kg->dev, Pb, kwt.as<double>() + static_cast<int64_t>(p0) * m,
-                                 s->pimg() + static_cast<int64_t>(p0) * m, zd.as<double>() + p0, sigma_sq, depth);
-      for (int p = 0; p < Pb; ++p) {
-        const auto q = quadrature_logdet_host(o.alpha.data() + static_cast<size_t>(p) * depth,
-                                              o.beta.data() + static_cast<size_t>(p) * depth, o.order[p], n,
-                                              opts->quad_tol);
-        total += q.first;
-        max_used = std::max(max_used, q.second);
+    // route (gp.cpp:181-232)
+    int route = opts->route;
+    if (route == GSGPC_ROUTE_AUTO) {
+      if (s->probes > 0) {
+        route = GSGPC_ROUTE_SKI_OPERATOR;
+      } else if (kg_condition_estimate(L, kg->dev) > 1e8 && m <= dense_cap) {
+        route = GSGPC_ROUTE_DENSE;
+      } else {
+        route = GSGPC_ROUTE_SYMMETRIC_GRID;
       }
     }
-    const double slq = total / P;
+    const StencilDesc sd = stencil_desc(s);
+    double logdet = 0.0;
+    int probes_used = 0, max_used = 0;
+    if (route == GSGPC_ROUTE_SKI_OPERATOR) {
+      // SLQ over the probe images (gp.cpp:85-111)
+      if (P < 1) invalid("slq_logdet_ski_factorized: need at least one probe");
+      if (s->probes < P) {
+        invalid("log_likelihood_gsgp: the SkiOperator logdet route needs probe images W^T v_p accumulated in the "
+                "precompute (gsgpc_stats_enable_probes)");
+      }
+      if (s->probe_seeded && s->probe_seed != opts->seed) {
+        invalid("log_likelihood_gsgp: probe images were accumulated with seed " + std::to_string(s->probe_seed));
+      }
+      const int depth = static_cast<int>(std::min<double>(opts->max_depth, n));
+      if (depth < 1) invalid("slq: need at least one Lanczos step");
+      DBuf& kwt = ctx->buf("ll_kwt");
+      DBuf& kt0 = ctx->buf("ll_kt0");
+      DBuf& kt1 = ctx->buf("ll_kt1");
+      kwt.ensure(sizeof(double) * P * m);
+      kt0.ensure(sizeof(double) * P * m);
+      kt1.ensure(sizeof(double) * P * m);
+      run_kg_batched(L, kg->dev, P, s->pimg(), kwt.as<double>(), kt0.as<double>(), kt1.as<double>());
+      DBuf& zd = ctx->buf("ll_z0");
+      zd.ensure(sizeof(double) * P);
+      std::vector<double> zs(P, n);  // v·v = n for ±1 probes
+      GSGPC_CUDA(cudaMemcpyAsync(zd.p, zs.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
+      double total = 0.0;
+      for (int p0 = 0; p0 < P; p0 += 32) {
+        const int Pb = std::min(32, P - p0);
+        const EflaOut o = efla_run(L, sd, s->stencil(), kg->dev, Pb, kwt.as<double>() + static_cast<int64_t>(p0) * m,
+                                   s->pimg() + static_cast<int64_t>(p0) * m, zd.as<double>() + p0, sigma_sq, depth);
+        for (int p = 0; p < Pb; ++p) {
+          const auto q = quadrature_logdet_host(o.alpha.data() + static_cast<size_t>(p) * depth,
+                                                o.beta.data() + static_cast<size_t>(p) * depth, o.order[p], n,
+                                                opts->quad_tol);
+          total += q.first;
+          max_used = std::max(max_used, q.second);
+        }
+      }
+      logdet = total / P - (n - static_cast<double>(m)) * std::log(sigma_sq);
+      probes_used = P;
+    } else if (route == GSGPC_ROUTE_SYMMETRIC_GRID) {
+      // slq_logdet(K WᵀW K + σ²K) − slq_logdet(K), shared probes, quad_tol 0 (gp.cpp:206-219)
+      const int Pb = std::min(P, 32);
+      DBuf& ku = ctx->buf("ll_sym_ku");
+      DBuf& wku = ctx->buf("ll_sym_wku");
+      DBuf& kt0 = ctx->buf("ll_kt0");
+      DBuf& kt1 = ctx->buf("ll_kt1");
+      for (DBuf* b : {&ku, &wku, &kt0, &kt1}) b->ensure(sizeof(double) * Pb * m);
+      const double s1 = slq_logdet_batched(L, m, P, opts->max_depth, 0.0, opts->seed, [&](int pb) {
+        return sym_op(L, sd, s->stencil(), kg->dev, pb, sigma_sq, ku.as<double>(), wku.as<double>(), kt0.as<double>(),
+                      kt1.as<double>());
+      });
+      const double s2 = slq_logdet_batched(L, m, P, opts->max_depth, 0.0, opts->seed, [&](int pb) {
+        return kg_op(L, kg->dev, pb, kt0.as<double>(), kt1.as<double>());
+      });
+      logdet = s1 - s2;
+      probes_used = 2 * P;
+      max_used = static_cast<int>(std::min<int64_t>(opts->max_depth, m));
+    } else {
+      if (m > dense_cap) invalid("log_likelihood_gsgp: grid too large for the dense logdet route");
+      logdet = dense_logdet_grid_system(L, sd, s->stencil(), kg->dev, sigma_sq);
+    }
     const double kLog2Pi = 1.8378770664093453;
-    out->logdet_term = slq - (n - static_cast<double>(m)) * std::log(sigma_sq);
+    out->logdet_term = logdet;
     out->quad_term = quad;
     out->const_term = n * kLog2Pi + (n - static_cast<double>(m)) * std::log(sigma_sq);
     out->loglik = -0.5 * (out->logdet_term + out->quad_term + out->const_term);
-    out->probes_used = P;
+    out->probes_used = probes_used;
     out->solver_iterations = cg.iterations;
     out->max_depth_used = max_used;
+    out->logdet_route = route;
   });
 }
 

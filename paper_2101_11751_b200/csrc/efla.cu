@@ -7,9 +7,12 @@
 // reorthogonalisation is a pair of batched GEMVs against the stored Q̂ / P̂ columns.
 // Per-probe scalars (c_q, e, β_prev, scale, breakdown) stay on the device; vectors are
 // probe-major [P][m].  Dots reduce through fixed per-block partials (deterministic).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <random>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -21,6 +24,7 @@
 #include "precompute.cuh"
 
 namespace gsgpc {
+namespace cg = cooperative_groups;
 
 constexpr int EF_NT = 256;
 constexpr int EF_MAXP = 32;
@@ -494,6 +498,435 @@ std::pair<double, int> quadrature_logdet_host(const double* alpha, const double*
     prev = est;
   }
   return {value, depth};
+}
+
+
+// =============================================================== plain Lanczos, batched
+// lanczos (solvers.cpp:351-389) for P start vectors at once on an m-dimensional operator:
+// classical Gram–Schmidt full reorthogonalisation exactly as the reference orders it
+// (w -= β q_{i-1}; α = q·w; w -= α q; c = Qᵀw; w -= Q c; β = ‖w‖; breakdown when
+// β ≤ 1e-12·scale).  Used by slq_logdet (gp.cpp:67-83) on the SymmetricGrid route and by
+// estimate_grid_kernel_condition (gp.cpp:142-154).
+struct LzScal {
+  double bprev, scale;
+  int done, order;
+};
+
+// w -= bprev·q_prev (i > 0); partial q_i·w
+__global__ void __launch_bounds__(EF_NT) k_lz_s1(int64_t m, int i, int k, const LzScal* sc, double* w, const double* Q,
+                                                 double* part, int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  const bool live = !sc[p].done && a < m;
+  double v = 0.0;
+  if (live) {
+    const int64_t o = static_cast<int64_t>(p) * m + a;
+    const double* Qp = Q + static_cast<int64_t>(p) * k * m;
+    double x = w[o];
+    if (i > 0) x -= sc[p].bprev * Qp[static_cast<int64_t>(i - 1) * m + a];
+    w[o] = x;
+    v = Qp[static_cast<int64_t>(i) * m + a] * x;
+  }
+  block_partial_store(v, part + static_cast<int64_t>(p) * nblk + blockIdx.x, sh);
+}
+
+__global__ void k_lz_c1(int P, int i, int k, LzScal* sc, const double* dots, double* alpha) {
+  const int p = threadIdx.x;
+  if (p >= P || sc[p].done) return;
+  const double a = dots[p];
+  alpha[p * k + i] = a;
+  sc[p].scale = fmax(sc[p].scale, fabs(a));
+  if (i == k - 1) {
+    sc[p].done = 1;
+    sc[p].order = k;
+  }
+}
+
+// w -= α q_i; partials q_j·w (j ≤ i)
+__global__ void __launch_bounds__(EF_NT) k_lz_s2(int64_t m, int i, int k, const LzScal* sc, const double* alpha,
+                                                 double* w, const double* Q, double* part, int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  const bool live = !sc[p].done && a < m;
+  const double* Qp = Q + static_cast<int64_t>(p) * k * m;
+  double x = 0.0;
+  if (live) {
+    const int64_t o = static_cast<int64_t>(p) * m + a;
+    x = w[o] - alpha[p * k + i] * Qp[static_cast<int64_t>(i) * m + a];
+    w[o] = x;
+  }
+  for (int j = 0; j <= i; ++j) {
+    const double v = live ? Qp[static_cast<int64_t>(j) * m + a] * x : 0.0;
+    block_partial_store(v, part + (static_cast<int64_t>(p) * (i + 1) + j) * nblk + blockIdx.x, sh);
+  }
+}
+
+// w -= Σ_j q_j c_j; partial w·w
+__global__ void __launch_bounds__(EF_NT) k_lz_g2(int64_t m, int i, int k, const LzScal* sc, const double* c, double* w,
+                                                 const double* Q, double* part, int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  const bool live = !sc[p].done && a < m;
+  double v = 0.0;
+  if (live) {
+    const double* Qp = Q + static_cast<int64_t>(p) * k * m;
+    const int64_t o = static_cast<int64_t>(p) * m + a;
+    double x = w[o];
+    for (int j = 0; j <= i; ++j) x -= Qp[static_cast<int64_t>(j) * m + a] * c[p * (i + 1) + j];
+    w[o] = x;
+    v = x * x;
+  }
+  block_partial_store(v, part + static_cast<int64_t>(p) * nblk + blockIdx.x, sh);
+}
+
+__global__ void k_lz_c3(int P, int i, int k, LzScal* sc, const double* dots, double* beta) {
+  const int p = threadIdx.x;
+  if (p >= P || sc[p].done) return;
+  const double b = sqrt(dots[p]);
+  if (b <= 1e-12 * fmax(sc[p].scale, 1e-300)) {
+    sc[p].done = 1;
+    sc[p].order = i + 1;
+    return;
+  }
+  beta[p * k + i] = b;
+  sc[p].scale = fmax(sc[p].scale, b);
+  sc[p].bprev = b;
+}
+
+// q_{i+1} = w / β (into Q and the contiguous operator input)
+__global__ void __launch_bounds__(EF_NT) k_lz_s4(int64_t m, int i, int k, const LzScal* sc, const double* w, double* Q,
+                                                 double* cur) {
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  if (sc[p].done || a >= m) return;
+  const int64_t o = static_cast<int64_t>(p) * m + a;
+  const double q = w[o] / sc[p].bprev;
+  Q[(static_cast<int64_t>(p) * k + i + 1) * m + a] = q;
+  cur[o] = q;
+}
+
+// q_0 = b / ‖b‖ (‖b‖ from a device reduction)
+__global__ void __launch_bounds__(EF_NT) k_lz_init(int64_t m, int k, const double* b, const double* bb, double* Q,
+                                                   double* cur) {
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  if (a >= m) return;
+  const int64_t o = static_cast<int64_t>(p) * m + a;
+  const double q = b[o] / sqrt(bb[p]);
+  Q[static_cast<int64_t>(p) * k * m + a] = q;
+  cur[o] = q;
+}
+
+__global__ void __launch_bounds__(EF_NT) k_lz_sq(int64_t m, const double* b, double* part, int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  const double v = a < m ? b[static_cast<int64_t>(p) * m + a] : 0.0;
+  block_partial_store(v * v, part + static_cast<int64_t>(p) * nblk + blockIdx.x, sh);
+}
+
+__global__ void k_lz_scal_init(int P, LzScal* sc) {
+  const int p = threadIdx.x;
+  if (p < P) sc[p] = LzScal{0.0, 0.0, 0, 0};
+}
+
+// out = op(in) for P probe-major vectors
+using BatchedOp = std::function<void(const double* in, double* out)>;
+
+LanczosOut lanczos_batched(const Launch& L, int64_t m, int P, int k, const double* start, const BatchedOp& op) {
+  if (k < 1 || k > m) invalid("lanczos: need 1 <= k <= dim");
+  const int nblk = static_cast<int>(ceil_div(m, EF_NT));
+  const size_t V = sizeof(double) * static_cast<size_t>(P) * m;
+  DevMem Q(V * k), cur(V), w(V);
+  DevMem part(sizeof(double) * static_cast<size_t>(P) * (k + 1) * nblk), dots(sizeof(double) * P * (k + 1));
+  DevMem al(sizeof(double) * P * k), be(sizeof(double) * P * k), scm(sizeof(LzScal) * P);
+  LzScal* sc = static_cast<LzScal*>(scm.p);
+  GSGPC_CUDA(cudaMemsetAsync(al.p, 0, sizeof(double) * P * k, L.s));
+  GSGPC_CUDA(cudaMemsetAsync(be.p, 0, sizeof(double) * P * k, L.s));
+  const dim3 gv(static_cast<unsigned>(nblk), static_cast<unsigned>(P));
+  k_lz_sq<<<gv, EF_NT, 0, L.s>>>(m, start, part.d(), nblk);
+  k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+  std::vector<double> bb(P);
+  GSGPC_CUDA(cudaMemcpyAsync(bb.data(), dots.p, sizeof(double) * P, cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaStreamSynchronize(L.s));
+  for (double v : bb)
+    if (v == 0.0) invalid("lanczos: start vector is zero");
+  k_lz_init<<<gv, EF_NT, 0, L.s>>>(m, k, start, dots.d(), Q.d(), cur.d());
+  k_lz_scal_init<<<1, 64, 0, L.s>>>(P, sc);
+  L.count(4);
+  for (int i = 0; i < k; ++i) {
+    op(cur.d(), w.d());
+    k_lz_s1<<<gv, EF_NT, 0, L.s>>>(m, i, k, sc, w.d(), Q.d(), part.d(), nblk);
+    k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+    k_lz_c1<<<1, 64, 0, L.s>>>(P, i, k, sc, dots.d(), al.d());
+    L.count(3);
+    if (i == k - 1) break;
+    k_lz_s2<<<gv, EF_NT, 0, L.s>>>(m, i, k, sc, al.d(), w.d(), Q.d(), part.d(), nblk);
+    k_ef_reduce<<<P * (i + 1), EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+    k_lz_g2<<<gv, EF_NT, 0, L.s>>>(m, i, k, sc, dots.d(), w.d(), Q.d(), part.d(), nblk);
+    k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+    k_lz_c3<<<1, 64, 0, L.s>>>(P, i, k, sc, dots.d(), be.d());
+    k_lz_s4<<<gv, EF_NT, 0, L.s>>>(m, i, k, sc, w.d(), Q.d(), cur.d());
+    L.count(6);
+  }
+  GSGPC_CUDA(cudaGetLastError());
+  LanczosOut o;
+  o.alpha.resize(static_cast<size_t>(P) * k);
+  o.beta.resize(static_cast<size_t>(P) * k);
+  std::vector<LzScal> hs(P);
+  GSGPC_CUDA(cudaMemcpyAsync(o.alpha.data(), al.p, sizeof(double) * P * k, cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaMemcpyAsync(o.beta.data(), be.p, sizeof(double) * P * k, cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaMemcpyAsync(hs.data(), scm.p, sizeof(LzScal) * P, cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaStreamSynchronize(L.s));
+  o.order.resize(P);
+  for (int p = 0; p < P; ++p) o.order[p] = hs[p].order > 0 ? hs[p].order : k;
+  return o;
+}
+
+// rademacher_probe (gp.cpp:16-25) for p0 .. p0+P-1, dimension m, probe-major ±1 doubles
+static std::vector<double> rademacher_block(int64_t m, uint64_t seed, int p0, int P) {
+  std::vector<double> v(static_cast<size_t>(P) * m);
+  for (int p = 0; p < P; ++p) {
+    const uint64_t pi = static_cast<uint64_t>(p0 + p);
+    std::seed_seq seq{static_cast<std::uint32_t>(seed), static_cast<std::uint32_t>(seed >> 32),
+                      static_cast<std::uint32_t>(pi), static_cast<std::uint32_t>(pi >> 32)};
+    std::mt19937_64 rng(seq);
+    double* o = v.data() + static_cast<size_t>(p) * m;
+    for (int64_t i = 0; i < m; ++i) o[i] = (rng() & 1ull) ? 1.0 : -1.0;
+  }
+  return v;
+}
+
+// slq_logdet (gp.cpp:67-83) with the probes batched EF_MAXP at a time
+double slq_logdet_batched(const Launch& L, int64_t m, int num_probes, int max_depth, double quad_tol, uint64_t seed,
+                          const std::function<BatchedOp(int)>& make_op) {
+  if (num_probes < 1) invalid("slq_logdet: need at least one probe");
+  const int depth = static_cast<int>(std::min<int64_t>(max_depth, m));
+  double total = 0.0;
+  for (int p0 = 0; p0 < num_probes; p0 += EF_MAXP) {
+    const int P = std::min(EF_MAXP, num_probes - p0);
+    const std::vector<double> hv = rademacher_block(m, seed, p0, P);
+    DevMem dv(sizeof(double) * hv.size());
+    GSGPC_CUDA(cudaMemcpyAsync(dv.p, hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, L.s));
+    const LanczosOut o = lanczos_batched(L, m, P, depth, dv.d(), make_op(P));
+    for (int p = 0; p < P; ++p) {
+      total += quadrature_logdet_host(o.alpha.data() + static_cast<size_t>(p) * depth,
+                                      o.beta.data() + static_cast<size_t>(p) * depth, o.order[p],
+                                      static_cast<double>(m), quad_tol)
+                   .first;
+    }
+  }
+  return total / num_probes;
+}
+
+// Batched operators of the SymmetricGrid route
+BatchedOp kg_op(const Launch& L, const KgDev& kg, int P, double* t0, double* t1) {
+  return [=](const double* in, double* out) { run_kg_batched(L, kg, P, in, out, t0, t1); };
+}
+
+// out = K WᵀW K u + σ² K u
+BatchedOp sym_op(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, double sigma_sq,
+                 double* ku, double* wku, double* t0, double* t1) {
+  return [=](const double* in, double* out) {
+    run_kg_batched(L, kg, P, in, ku, t0, t1);
+    ef_upload_offsets(sd, L.s);
+    launch_spmm(L, sd, A, ku, wku, P, nullptr);
+    run_kg_batched(L, kg, P, wku, out, t0, t1);
+    const int64_t n = static_cast<int64_t>(P) * sd.m;
+    k_add_scaled<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, L.s>>>(n, sigma_sq, ku, out);
+    L.count(2);
+  };
+}
+
+// estimate_grid_kernel_condition (gp.cpp:142-154): Lanczos on K_G from probe 0 of seed
+// 0x5eedf00d, depth min(30, m); hi / max(lo, 1e-18·hi) of the Ritz values.
+double kg_condition_estimate(const Launch& L, const KgDev& kg) {
+  const int64_t m = kg.m;
+  const int depth = static_cast<int>(std::min<int64_t>(30, m));
+  const std::vector<double> hv = rademacher_block(m, 0x5eedf00dull, 0, 1);
+  DevMem dv(sizeof(double) * m), t0(sizeof(double) * m), t1(sizeof(double) * m);
+  GSGPC_CUDA(cudaMemcpyAsync(dv.p, hv.data(), sizeof(double) * m, cudaMemcpyHostToDevice, L.s));
+  const LanczosOut o = lanczos_batched(L, m, 1, depth, dv.d(), kg_op(L, kg, 1, t0.d(), t1.d()));
+  std::vector<double> lam, z;
+  tridiag_eig_host(o.order[0], o.alpha.data(), o.beta.data(), lam, z);
+  const double hi = lam.back(), lo = lam.front();
+  if (!(hi > 0.0)) return INFINITY;
+  return hi / std::max(lo, hi * 1e-18);
+}
+
+// ------------------------------------------------------------ Dense route (gp.cpp:116-140)
+// log|det(K_G WᵀW + σ² I)| for m ≤ dense_cap: dense K_G (Kronecker of the generators) and
+// dense WᵀW (from the half stencil), one DGEMM, then LU with partial pivoting in a single
+// cooperative kernel (same pivot rule as the reference: first row of maximal |a|).
+__global__ void k_dense_kg(int64_t m, KgDev kg, double* K) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= m * m) return;
+  int64_t i = idx / m, j = idx % m;
+  double v = 1.0;
+  for (int k = kg.d - 1; k >= 0; --k) {
+    const int64_t ik = i % kg.sz[k], jk = j % kg.sz[k];
+    i /= kg.sz[k];
+    j /= kg.sz[k];
+    v *= kg.gen[k][ik > jk ? ik - jk : jk - ik];
+  }
+  K[idx] = v;
+}
+
+// dense WᵀW from the half stencil: row a, offset s ≥ 0: (a, a+o_s) and (a+o_s, a)
+__global__ void k_dense_wtw(int64_t m, int S_min, const double* A, double* D) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  for (int s2 = 0; s2 < S_min; ++s2) {
+    const int64_t b = a + c_off_flat[s2];
+    if (b < 0 || b >= m) continue;
+    const double v = A[static_cast<int64_t>(s2) * m + a];
+    if (v == 0.0) continue;
+    D[a * m + b] = v;
+    D[b * m + a] = v;
+  }
+}
+
+// C = A·B + σ² I (row-major m×m), 32×32 tiles
+__global__ void __launch_bounds__(256) k_dgemm_shift(int m, const double* __restrict__ A, const double* __restrict__ B,
+                                                     double sigma_sq, double* __restrict__ C) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 × 8
+  const int row0 = blockIdx.y * 32, col = blockIdx.x * 32 + tx;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < m; k0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const int gr = row0 + r, gk = k0 + tx;
+      As[r][tx] = (gr < m && gk < m) ? A[static_cast<int64_t>(gr) * m + gk] : 0.0;
+      const int bk = k0 + r;
+      Bs[r][tx] = (bk < m && col < m) ? B[static_cast<int64_t>(bk) * m + col] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double b = Bs[kk][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][kk], b, acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = row0 + ty + 8 * q;
+    if (r < m && col < m) C[static_cast<int64_t>(r) * m + col] = acc[q] + (r == col ? sigma_sq : 0.0);
+  }
+}
+
+// Right-looking LU with partial pivoting, one cooperative grid; logdet = Σ log|u_cc|.
+// Element updates are a[r][j] − f·a[c][j] with f = a[r][c] / a[c][c], rounded as the
+// reference's (no contraction).
+__global__ void __launch_bounds__(256) k_dense_lu_logdet(int m, double* a, double* red_v, int* red_i, double* out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[256];
+  __shared__ int si[256];
+  const int nthreads = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  double logdet = 0.0;
+  for (int c = 0; c < m; ++c) {
+    // pivot: first row r ≥ c with maximal |a[r][c]|
+    double bv = -1.0;
+    int bi = m;
+    for (int r = c + tid; r < m; r += nthreads) {
+      const double v = fabs(a[static_cast<int64_t>(r) * m + c]);
+      if (v > bv || (v == bv && r < bi)) {
+        bv = v;
+        bi = r;
+      }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (threadIdx.x < o) {
+        const double v2 = sv[threadIdx.x + o];
+        const int i2 = si[threadIdx.x + o];
+        if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+          sv[threadIdx.x] = v2;
+          si[threadIdx.x] = i2;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      red_v[blockIdx.x] = sv[0];
+      red_i[blockIdx.x] = si[0];
+    }
+    grid.sync();
+    // every thread reduces the block winners identically
+    double pv = -1.0;
+    int piv = m;
+    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) {
+      const double v2 = red_v[b];
+      const int i2 = red_i[b];
+      if (v2 > pv || (v2 == pv && i2 < piv)) {
+        pv = v2;
+        piv = i2;
+      }
+    }
+    if (piv != c) {
+      for (int j = c + tid; j < m; j += nthreads) {
+        const double t = a[static_cast<int64_t>(c) * m + j];
+        a[static_cast<int64_t>(c) * m + j] = a[static_cast<int64_t>(piv) * m + j];
+        a[static_cast<int64_t>(piv) * m + j] = t;
+      }
+    }
+    grid.sync();
+    const double dg = a[static_cast<int64_t>(c) * m + c];
+    logdet += log(fabs(dg));
+    if (dg != 0.0) {
+      const int64_t rows = m - c - 1, cols = m - c - 1;
+      for (int64_t e = tid; e < rows * cols; e += nthreads) {
+        const int r = c + 1 + static_cast<int>(e / cols);
+        const int j = c + 1 + static_cast<int>(e % cols);
+        const double f = __ddiv_rn(a[static_cast<int64_t>(r) * m + c], dg);
+        if (f == 0.0) continue;
+        a[static_cast<int64_t>(r) * m + j] =
+            __dsub_rn(a[static_cast<int64_t>(r) * m + j], __dmul_rn(f, a[static_cast<int64_t>(c) * m + j]));
+      }
+    }
+    grid.sync();
+  }
+  if (tid == 0) *out = logdet;
+}
+
+double dense_logdet_grid_system(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg,
+                                double sigma_sq) {
+  const int64_t m = sd.m;
+  const size_t MM = sizeof(double) * static_cast<size_t>(m) * m;
+  DevMem K(MM), D(MM), S(MM);
+  GSGPC_CUDA(cudaMemsetAsync(D.p, 0, MM, L.s));
+  k_dense_kg<<<static_cast<unsigned>(ceil_div(m * m, 256)), 256, 0, L.s>>>(m, kg, K.d());
+  ef_upload_offsets(sd, L.s);
+  k_dense_wtw<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(m, sd.S_min, A, D.d());
+  const dim3 gg(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(m, 32)));
+  k_dgemm_shift<<<gg, 256, 0, L.s>>>(static_cast<int>(m), K.d(), D.d(), sigma_sq, S.d());
+  L.count(3);
+  int dev = 0, sms = 0, per_sm = 0;
+  GSGPC_CUDA(cudaGetDevice(&dev));
+  GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lu_logdet, 256, 0));
+  const int blocks = std::max(1, sms * std::min(per_sm, 2));
+  DevMem rv(sizeof(double) * blocks), ri(sizeof(int) * blocks), out(sizeof(double));
+  int mi = static_cast<int>(m);
+  double* ap = S.d();
+  double* rvp = rv.d();
+  int* rip = static_cast<int*>(ri.p);
+  double* op = out.d();
+  void* args[] = {&mi, &ap, &rvp, &rip, &op};
+  GSGPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_dense_lu_logdet), dim3(blocks), dim3(256), args, 0,
+                                         L.s));
+  L.count();
+  double h = 0.0;
+  GSGPC_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaStreamSynchronize(L.s));
+  return h;
 }
 
 }  // namespace gsgpc

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <utility>
 #include <vector>
 
@@ -113,5 +114,20 @@ EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const 
 std::pair<double, int> quadrature_logdet_host(const double* alpha, const double* beta, int k, double probe_sq,
                                               double quad_tol);
 void run_kg_batched(const Launch& L, const KgDev& kg, int P, const double* v, double* out, double* t0, double* t1);
+// plain batched Lanczos (solvers.cpp:351-389) and the SymmetricGrid / Dense log-det routes
+struct LanczosOut {
+  std::vector<double> alpha, beta;  // P × k
+  std::vector<int> order;
+};
+using BatchedOp = std::function<void(const double* in, double* out)>;
+LanczosOut lanczos_batched(const Launch& L, int64_t m, int P, int k, const double* start, const BatchedOp& op);
+double slq_logdet_batched(const Launch& L, int64_t m, int num_probes, int max_depth, double quad_tol, uint64_t seed,
+                          const std::function<BatchedOp(int)>& make_op);
+BatchedOp kg_op(const Launch& L, const KgDev& kg, int P, double* t0, double* t1);
+BatchedOp sym_op(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, double sigma_sq,
+                 double* ku, double* wku, double* t0, double* t1);
+double kg_condition_estimate(const Launch& L, const KgDev& kg);
+double dense_logdet_grid_system(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg,
+                                double sigma_sq);
 
 }  // namespace gsgpc

@@ -876,6 +876,17 @@ class SlqOptions:
     quad_tol: float = 0.01
 
 
+class LogdetRoute(enum.IntEnum):
+    """gp.hpp:55-60."""
+    Auto = 0
+    SymmetricGrid = 1
+    SkiOperator = 2
+    Dense = 3
+
+
+ROUTE_NAMES = {1: "symmetric-grid-slq", 2: "ski-operator-slq", 3: "dense"}
+
+
 @dataclass
 class LoglikOptions:
     solve_tol: float = 0.01
@@ -883,6 +894,8 @@ class LoglikOptions:
     slq: SlqOptions = field(default_factory=SlqOptions)
     seed: int = 0
     maxiter: int = kDefaultMaxIter
+    route: LogdetRoute = LogdetRoute.Auto
+    dense_cap: int = 2048
 
 
 @dataclass
@@ -917,7 +930,8 @@ def factorized_lanczos_fused(kg: ToeplitzOperator, stats: SufficientStats, kgwt_
 
 def log_likelihood_gsgp(stats: SufficientStats, kg: ToeplitzOperator, sigma: float,
                         opts: LoglikOptions = None) -> LoglikResult:
-    """gp.cpp:158-240, SkiOperator route with the probe images accumulated in the precompute."""
+    """gp.cpp:158-240.  Routes (opts.route): SkiOperator over the probe images accumulated in the
+    precompute (enable_probes), SymmetricGrid, Dense, or Auto (as the reference chooses)."""
     opts = opts or LoglikOptions()
     ctx = stats.context
     o = _L.LoglikOptions_t()
@@ -927,8 +941,10 @@ def log_likelihood_gsgp(stats: SufficientStats, kg: ToeplitzOperator, sigma: flo
     o.quad_tol = opts.slq.quad_tol
     o.seed = opts.seed
     o.maxiter = opts.maxiter
+    o.route = int(opts.route)
+    o.dense_cap = int(opts.dense_cap)
     r = _L.LoglikResult_t()
     ctx.check(_L.load().gsgpc_log_likelihood_gsgp(ctx.handle, stats.handle, kg.handle, float(sigma), C.byref(o),
                                                   C.byref(r)))
     return LoglikResult(r.loglik, r.logdet_term, r.quad_term, r.const_term, r.probes_used, r.solver_iterations,
-                        "ski-operator-slq", r.max_depth_used)
+                        ROUTE_NAMES.get(r.logdet_route, "?"), r.max_depth_used)

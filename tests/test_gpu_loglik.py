@@ -1,5 +1,6 @@
-"""GPU parity of the probe images, probe-batched EFLA and the SLQ log-likelihood
-(SkiOperator route) against the oracle on identical probes (same reference generator)."""
+"""GPU parity of the probe images, probe-batched EFLA and the log-likelihood on every
+LogdetRoute (SkiOperator, SymmetricGrid, Dense, Auto) against the oracle on identical probes
+(same reference generator)."""
 import numpy as np
 import pytest
 
@@ -101,9 +102,75 @@ def test_loglik_matches_oracle():
     assert abs(r2.loglik - ref2["loglik"]) <= 1e-5 * abs(ref2["loglik"])
 
 
-def test_loglik_requires_probe_images():
+def test_ski_route_requires_probe_images():
     g, x, y = make_case(n=2000)
     st = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
     spec = G.KernelSpec(G.Hyperparams(0.1, [0.2, 0.25, 0.3], 1.0))
-    with pytest.raises(G.InvalidArgument):
-        G.log_likelihood_gsgp(st, G.ToeplitzOperator(g, spec), 0.1)
+    with pytest.raises(G.InvalidArgument, match="probe images"):
+        G.log_likelihood_gsgp(st, G.ToeplitzOperator(g, spec), 0.1,
+                              G.LoglikOptions(route=G.LogdetRoute.SkiOperator))
+
+
+def _grid_case(d, sizes, ls, n=6000, sigma=0.1):
+    g, x, y = make_case(d, sizes, n=n)
+    st = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    kg = G.ToeplitzOperator(g, G.KernelSpec(G.Hyperparams(sigma, ls, 1.0)))
+    og = ogrid(g)
+    ost = O.sufficient_stats(og, x, y)
+    okg = O.ToeplitzOperator(og, ls, 1.0, sigma)
+    return st, kg, ost, okg
+
+
+@pytest.mark.parametrize("d,sizes,ls", [(1, (60,), [0.03]), (2, (16, 14), [0.2, 0.25]), (3, (8, 7, 6), [0.3, 0.3, 0.4])])
+def test_symmetric_grid_route_matches_oracle(d, sizes, ls):
+    """slq_logdet(K WᵀW K + σ²K) − slq_logdet(K) (gp.cpp:206-219) on identical m-dimensional
+    probes: batched GPU Lanczos vs the oracle's sequential one.  Lengthscales keep K_G
+    invertible in fp64 (cond ≤ 1e8); on a numerically singular K_G (e.g. ℓ = 0.1 on the 60-node
+    1-D grid, cond ~1e301) SLQ(K) is rounding noise on either side — Auto routes those to
+    Dense."""
+    sigma = 0.1
+    st, kg, ost, okg = _grid_case(d, sizes, ls, sigma=sigma)
+    opts = G.LoglikOptions(solve_tol=1e-9, probes=6, slq=G.SlqOptions(max_depth=25, quad_tol=0.01), seed=3,
+                           maxiter=5000, route=G.LogdetRoute.SymmetricGrid)
+    r = G.log_likelihood_gsgp(st, kg, sigma, opts)
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, solve_tol=1e-9, probes=6, max_depth=25, quad_tol=0.01, seed=3,
+                                route="symmetric-grid", maxiter=5000)
+    assert r.logdet_route == ref["logdet_route"] == "symmetric-grid-slq"
+    assert r.probes_used == ref["probes_used"] == 12
+    assert abs(r.logdet_term - ref["logdet_term"]) <= 1e-6 * abs(ref["logdet_term"])
+    assert abs(r.loglik - ref["loglik"]) <= 1e-6 * abs(ref["loglik"])
+
+
+@pytest.mark.parametrize("d,sizes,ls", [(1, (80,), [0.1]), (2, (20, 18), [0.2, 0.25])])
+def test_dense_route_matches_oracle(d, sizes, ls):
+    """dense_logdet_grid_system (gp.cpp:116-140): LU with partial pivoting of K WᵀW + σ²I."""
+    sigma = 0.1
+    st, kg, ost, okg = _grid_case(d, sizes, ls, sigma=sigma)
+    opts = G.LoglikOptions(solve_tol=1e-9, maxiter=5000, route=G.LogdetRoute.Dense)
+    r = G.log_likelihood_gsgp(st, kg, sigma, opts)
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, solve_tol=1e-9, route="dense", maxiter=5000)
+    assert r.logdet_route == "dense"
+    assert abs(r.logdet_term - ref["logdet_term"]) <= 1e-9 * abs(ref["logdet_term"])
+    # the quadratic term (yᵀy − wᵀz̄)/σ² cancels: its agreement is set by the 1e-9 data-fit solve
+    assert abs(r.quad_term - ref["quad_term"]) <= 1e-5 * abs(ref["quad_term"])
+    assert abs(r.loglik - ref["loglik"]) <= 1e-6 * abs(ref["loglik"])
+    with pytest.raises(G.InvalidArgument, match="too large for the dense"):
+        G.log_likelihood_gsgp(st, kg, sigma, G.LoglikOptions(solve_tol=1e-9, maxiter=5000, route=G.LogdetRoute.Dense,
+                                                             dense_cap=10))
+
+
+def test_auto_route_selection_matches_oracle():
+    """Auto (gp.cpp:181-205): Dense when cond(K_G) > 1e8 and m ≤ dense_cap, else SymmetricGrid;
+    SkiOperator whenever the statistics carry probe images."""
+    sigma = 0.1
+    # long lengthscale on a fine 1-D grid: K_G is numerically singular → dense
+    st, kg, ost, okg = _grid_case(1, (120,), [0.5], sigma=sigma)
+    r = G.log_likelihood_gsgp(st, kg, sigma, G.LoglikOptions(solve_tol=1e-9, maxiter=20000))
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, solve_tol=1e-9, maxiter=20000)
+    assert r.logdet_route == ref["logdet_route"] == "dense"
+    assert abs(r.loglik - ref["loglik"]) <= 1e-6 * abs(ref["loglik"])
+    # short lengthscale: well conditioned → symmetric grid
+    st, kg, ost, okg = _grid_case(2, (12, 11), [0.1, 0.1], sigma=sigma)
+    r = G.log_likelihood_gsgp(st, kg, sigma, G.LoglikOptions(solve_tol=1e-9, probes=4, maxiter=5000))
+    ref = O.log_likelihood_gsgp(ost, okg, sigma, solve_tol=1e-9, probes=4, maxiter=5000)
+    assert r.logdet_route == ref["logdet_route"] == "symmetric-grid-slq"
