@@ -563,6 +563,82 @@ inline PosteriorModel posterior_mean_gsgp(std::shared_ptr<const SufficientStats>
   return model;
 }
 
+// ---------------------------------------------------------------- gp.hpp:132-169 covariance
+struct CovResult {
+  std::vector<double> cov;  // ns × ns row-major
+  double max_asymmetry = 0.0;
+  int total_iterations = 0;
+};
+
+namespace detail {
+inline gsgpc_points coords(const std::vector<double>& points, int d) {
+  gsgpc_points p{};
+  p.dtype = GSGPC_F64;
+  p.x = points.data();
+  p.x_row_stride = d;
+  for (int k = 0; k < d; ++k) p.x_col_offset[k] = k;
+  p.y = points.data();
+  return p;
+}
+}  // namespace detail
+
+// gp.cpp:381-427 (points row-major ns × d)
+inline CovResult posterior_cov_exact(const PosteriorModel& model, const std::vector<double>& points, double tol,
+                                     int maxiter = kDefaultMaxIter) {
+  if (!model.stats) throw std::invalid_argument("posterior_cov_exact: the model carries no sufficient statistics");
+  const int d = model.grid().dim();
+  const int64_t ns = static_cast<int64_t>(points.size()) / d;
+  const gsgpc_points p = detail::coords(points, d);
+  CovResult r;
+  r.cov.assign(static_cast<size_t>(ns * ns), 0.0);
+  int32_t it = 0;
+  const Context& ctx = model.stats->context();
+  ctx.check(gsgpc_posterior_cov_exact(ctx.get(), model.stats->handle(), model.kg->handle(), model.sigma, &p, ns, tol,
+                                      maxiter, r.cov.data(), &r.max_asymmetry, &it));
+  r.total_iterations = it;
+  return r;
+}
+
+class LowRankCov {
+ public:
+  int64_t rank() const {
+    int64_t r = 0;
+    if (h_) gsgpc_lowrank_rank(h_.get(), &r);
+    return r;
+  }
+  double query(const std::vector<double>& x, const std::vector<double>& x2) const {
+    double out = 0.0;
+    ctx_.check(gsgpc_lowrank_query(ctx_.get(), h_.get(), x.data(), x2.data(), &out));
+    return out;
+  }
+  std::vector<double> cov_matrix(const std::vector<double>& points) const {
+    const int64_t ns = static_cast<int64_t>(points.size()) / d_;
+    const gsgpc_points p = detail::coords(points, d_);
+    std::vector<double> cov(static_cast<size_t>(ns * ns));
+    ctx_.check(gsgpc_lowrank_cov_matrix(ctx_.get(), h_.get(), &p, ns, cov.data()));
+    return cov;
+  }
+
+ private:
+  friend LowRankCov posterior_cov_lowrank(const PosteriorModel&, int64_t);
+  std::shared_ptr<gsgpc_lowrank> h_;
+  Context ctx_{Context::default_context()};
+  int d_ = 1;
+};
+
+// gp.cpp:429-475
+inline LowRankCov posterior_cov_lowrank(const PosteriorModel& model, int64_t rank) {
+  if (!model.stats) throw std::invalid_argument("posterior_cov_lowrank: the model carries no sufficient statistics");
+  LowRankCov out;
+  out.ctx_ = model.stats->context();
+  out.d_ = model.grid().dim();
+  gsgpc_lowrank* h = nullptr;
+  out.ctx_.check(gsgpc_posterior_cov_lowrank(out.ctx_.get(), model.stats->handle(), model.kg->handle(), model.sigma,
+                                             rank, &h));
+  out.h_.reset(h, gsgpc_lowrank_destroy);
+  return out;
+}
+
 // ---------------------------------------------------------------- gp.hpp:25-90
 struct SlqOptions {
   int max_depth = 100;

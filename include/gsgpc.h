@@ -269,6 +269,31 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc
                                        double sigma, const gsgpc_loglik_options* opts,
                                        gsgpc_loglik_result* out);
 
+/* ---- posterior covariance (gp.cpp:381-528) */
+/* posterior_cov_exact (gp.cpp:381-427) for the model (stats, kg, sigma): one grid-rhs EFCG per
+ * test point (rel_tol = tol; the right-hand sides run batched, 32 per pass, one stencil read
+ * per iteration for all of them), cov(i,j) = w_iᵀK_G w_j − (K_G w_i)·x̂_j, symmetrised
+ * (cov, ns × ns row-major).  max_asymmetry / total_iterations may be NULL.  Errors:
+ * OUT_OF_GRID "interp_weights: ..." (row = test point), BREAKDOWN, NONCONVERGENCE
+ * "posterior_cov_exact: solver hit maxiter". */
+gsgpc_status gsgpc_posterior_cov_exact(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc_kg* kg, double sigma,
+                                       const gsgpc_points* pts, int64_t ns, double tol, int maxiter, double* cov,
+                                       double* max_asymmetry, int32_t* total_iterations);
+/* posterior_cov_lowrank (gp.cpp:429-475): EFLA of depth `rank` from ĝ = WᵀW1/‖WᵀW1‖ with
+ * the basis kept; the handle holds R = K_G(WᵀW Q̂ + d·WᵀWĝ/√(ĝᵀWᵀWĝ)) (device, rank × m),
+ * the tridiagonal T and its own copy of the K_G generators (LowRankCov, gp.hpp:148-167). */
+typedef struct gsgpc_lowrank gsgpc_lowrank;
+gsgpc_status gsgpc_posterior_cov_lowrank(gsgpc_ctx* ctx, gsgpc_stats* stats, gsgpc_kg* kg, double sigma,
+                                         int64_t rank, gsgpc_lowrank** out);
+void gsgpc_lowrank_destroy(gsgpc_lowrank* lr);
+/* LowRankCov::rank() — the Lanczos order reached (≤ rank). */
+gsgpc_status gsgpc_lowrank_rank(const gsgpc_lowrank* lr, int64_t* rank);
+/* LowRankCov::cov_matrix (gp.cpp:500-525), ns × ns row-major, symmetrised. */
+gsgpc_status gsgpc_lowrank_cov_matrix(gsgpc_ctx* ctx, gsgpc_lowrank* lr, const gsgpc_points* pts, int64_t ns,
+                                      double* cov);
+/* LowRankCov::query (gp.cpp:486-498): cov between two points (d doubles each). */
+gsgpc_status gsgpc_lowrank_query(gsgpc_ctx* ctx, gsgpc_lowrank* lr, const double* x, const double* x2, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,8 @@ def lib():
         "orc_quadrature_logdet": (C.c_int, [_vp, _vp, C.c_int, _d, _d, _pd, _pi]),
         "orc_tridiag_eig": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp]),
         "orc_slq_logdet_ski_factorized": (C.c_int, [_vp, _vp, C.c_int, _pd, _pd, _pi64, C.c_int, _vp, _i64, _d, C.c_int, C.c_int, _d, C.c_uint64, _pd, _pi]),
+        "orc_posterior_cov_exact": (C.c_int, [_vp, _vp, C.c_int, _d, _vp, _i64, _d, C.c_int, _vp, _pd, _pi]),
+        "orc_posterior_cov_lowrank": (C.c_int, [_vp, _vp, C.c_int, _d, _i64, _vp, _i64, _vp, _vp, _vp, _pd, _pi]),
         "orc_log_likelihood_gsgp": (C.c_int, [_vp, _vp, _d, _d, C.c_int, C.c_int, _d, C.c_uint64, C.c_int, _i64, C.c_int, C.c_int, _pd, _pd, _pi64, C.c_int, _vp, _i64, _vp, _vp]),
     }
     for name, (res, args) in sig.items():
@@ -409,3 +411,31 @@ def log_likelihood_gsgp(stats, kg, sigma, grid=None, x=None, scheme=CUBIC, solve
                                          _ptr(out), _ptr(iout)))
     return dict(loglik=out[0], logdet_term=out[1], quad_term=out[2], const_term=out[3],
                 probes_used=int(iout[0]), solver_iterations=int(iout[1]), logdet_route=ROUTE_NAMES[int(iout[2])])
+
+
+# ---------------------------------------------------------------- covariance (gp.cpp:381-528)
+def posterior_cov_exact(kg, stats, sigma, points, tol=1e-8, maxiter=1000, scheme=CUBIC):
+    pts = _f64(points).reshape(-1, kg.grid.dim)
+    ns = pts.shape[0]
+    cov = np.zeros((ns, ns))
+    asym, iters = _d(), C.c_int()
+    _check(lib().orc_posterior_cov_exact(kg._h, stats._h, scheme, sigma, _ptr(pts), ns, tol, maxiter, _ptr(cov),
+                                         C.byref(asym), C.byref(iters)))
+    return dict(cov=cov, max_asymmetry=asym.value, total_iterations=iters.value)
+
+
+def posterior_cov_lowrank(kg, stats, sigma, rank, points=None, query=None, scheme=CUBIC):
+    """Returns dict(rank, cov (at points), query (cov between the two query points))."""
+    d = kg.grid.dim
+    pts = _f64(points).reshape(-1, d) if points is not None else np.zeros((0, d))
+    ns = pts.shape[0]
+    cov = np.zeros((max(ns, 1), max(ns, 1)))
+    rk = C.c_int()
+    qo = _d()
+    qx = _f64(query[0]) if query is not None else None
+    qx2 = _f64(query[1]) if query is not None else None
+    _check(lib().orc_posterior_cov_lowrank(kg._h, stats._h, scheme, sigma, int(rank), _ptr(pts) if ns else None, ns,
+                                           _ptr(cov), _ptr(qx) if qx is not None else None,
+                                           _ptr(qx2) if qx2 is not None else None,
+                                           C.byref(qo) if query is not None else None, C.byref(rk)))
+    return dict(rank=rk.value, cov=cov[:ns, :ns], query=qo.value if query is not None else None)

@@ -964,6 +964,167 @@ Stats run_stats(const Grid& grid, int scheme, const T* x, const T* y, int64_t n,
   return s;
 }
 
+// ---------------------------------------------------------------- gp.cpp:381-427
+// posterior_cov_exact: one grid-rhs EFCG per test point (rel_tol = tol), then
+// cov(i, j) = w_iᵀ h_j − h_i · x̂_j with h_j = K_G w_j; returns the symmetrised matrix.
+struct CovOut {
+  Vec cov;
+  double max_asymmetry = 0.0;
+  int total_iterations = 0;
+};
+
+CovOut posterior_cov_exact(const Toeplitz& kg, const Stats& stats, int scheme, double sigma, const double* pts,
+                           int64_t ns, double tol, int maxiter) {
+  const int64_t m = kg.grid.m;
+  const int d = kg.grid.d;
+  std::vector<WeightVector> wx(ns);
+  std::vector<Vec> h(ns);
+  for (int64_t j = 0; j < ns; ++j) {
+    wx[j] = interp_weights(kg.grid, pts + j * d, scheme);
+    Vec dense(m, 0.0);
+    for (std::size_t a = 0; a < wx[j].indices.size(); ++a) dense[wx[j].indices[a]] = wx[j].values[a];
+    h[j] = kg.apply(dense);
+  }
+  CovOut res;
+  std::vector<Vec> solved(ns);
+  for (int64_t j = 0; j < ns; ++j) {
+    const GridSolveResult s = factorized_cg_grid_rhs(kg, stats, h[j], sigma, -1.0, tol, maxiter);
+    if (!s.converged) {
+      throw SolverNonConvergence("posterior_cov_exact: solver hit maxiter", s.residual_sq, s.iterations);
+    }
+    res.total_iterations += s.iterations;
+    solved[j] = s.xhat_d;
+  }
+  Vec cov(ns * ns);
+  for (int64_t i = 0; i < ns; ++i) {
+    for (int64_t j = 0; j < ns; ++j) {
+      double prior = 0.0;
+      for (std::size_t a = 0; a < wx[i].indices.size(); ++a) prior += wx[i].values[a] * h[j][wx[i].indices[a]];
+      cov[i * ns + j] = prior - dot(h[i], solved[j]);
+    }
+  }
+  res.cov.assign(ns * ns, 0.0);
+  for (int64_t i = 0; i < ns; ++i) {
+    for (int64_t j = 0; j < ns; ++j) {
+      res.max_asymmetry = std::max(res.max_asymmetry, std::abs(cov[i * ns + j] - cov[j * ns + i]));
+      res.cov[i * ns + j] = 0.5 * (cov[i * ns + j] + cov[j * ns + i]);
+    }
+  }
+  return res;
+}
+
+// ---------------------------------------------------------------- gp.cpp:429-528
+// posterior_cov_lowrank: EFLA from ĝ = WᵀW 1 / ‖·‖ with the basis kept;
+// R[:, j] = K_G (WᵀW q̂_j + d_j WᵀW ĝ / √(ĝᵀWᵀWĝ)), T = tridiag(α, β).
+struct LowRank {
+  int64_t m = 0;
+  int k = 0;
+  std::vector<Vec> r;  // columns
+  Vec alpha, beta;
+};
+
+LowRank posterior_cov_lowrank(const Toeplitz& kg, const Stats& stats, double sigma, int64_t rank) {
+  const int64_t m = kg.grid.m;
+  if (rank < 0 || rank > m) throw std::invalid_argument("posterior_cov_lowrank: need 0 <= rank <= grid size");
+  LowRank out;
+  out.m = m;
+  if (rank == 0 || stats.n == 0) return out;
+  const Vec g_raw = stats.apply_wtw(Vec(m, 1.0));
+  const double g_norm = std::sqrt(dot(g_raw, g_raw));
+  if (g_norm == 0.0) return out;
+  Vec ghat(m);
+  for (int64_t i = 0; i < m; ++i) ghat[i] = g_raw[i] / g_norm;
+  const Vec wt_z0 = stats.apply_wtw(ghat);
+  const Vec kgwt_z0 = kg.apply(wt_z0);
+  const double z0_sq = dot(ghat, wt_z0);
+  if (z0_sq <= 0.0) return out;
+  const Tridiag f = factorized_lanczos_fused(kg, stats, kgwt_z0, wt_z0, z0_sq, sigma * sigma,
+                                             static_cast<int>(rank), true);
+  const int k = static_cast<int>(f.alpha.size());
+  const double bn = std::sqrt(z0_sq);
+  out.k = k;
+  out.alpha = f.alpha;
+  out.beta = f.beta;
+  for (int j = 0; j < k; ++j) {
+    Vec u = stats.apply_wtw(f.basis[j]);
+    for (int64_t i = 0; i < m; ++i) u[i] += f.d[j] * (wt_z0[i] / bn);
+    out.r.push_back(kg.apply(u));
+  }
+  return out;
+}
+
+// T x = b for the symmetric tridiagonal T (LDLᵀ without pivoting; T is positive definite
+// for a positive definite operator — Eigen's LDLT agrees to rounding).
+Vec tridiag_solve(const Vec& a, const Vec& b_off, const Vec& rhs) {
+  const int k = static_cast<int>(a.size());
+  Vec dd(k), l(k > 1 ? k - 1 : 0), z(rhs);
+  dd[0] = a[0];
+  for (int i = 1; i < k; ++i) {
+    l[i - 1] = b_off[i - 1] / dd[i - 1];
+    dd[i] = a[i] - l[i - 1] * b_off[i - 1];
+  }
+  for (int i = 1; i < k; ++i) z[i] -= l[i - 1] * z[i - 1];
+  for (int i = 0; i < k; ++i) z[i] /= dd[i];
+  for (int i = k - 2; i >= 0; --i) z[i] -= l[i] * z[i + 1];
+  return z;
+}
+
+Vec lowrank_phi(const LowRank& lr, const WeightVector& w) {
+  Vec phi(lr.k, 0.0);
+  for (std::size_t a = 0; a < w.indices.size(); ++a)
+    for (int j = 0; j < lr.k; ++j) phi[j] += w.values[a] * lr.r[j][w.indices[a]];
+  return phi;
+}
+
+// LowRankCov::cov_matrix (gp.cpp:500-525)
+Vec lowrank_cov_matrix(const Toeplitz& kg, const LowRank& lr, int scheme, const double* pts, int64_t ns) {
+  const int64_t m = kg.grid.m;
+  const int d = kg.grid.d;
+  std::vector<WeightVector> wx(ns);
+  std::vector<Vec> h(ns);
+  for (int64_t j = 0; j < ns; ++j) {
+    wx[j] = interp_weights(kg.grid, pts + j * d, scheme);
+    Vec dense(m, 0.0);
+    for (std::size_t a = 0; a < wx[j].indices.size(); ++a) dense[wx[j].indices[a]] = wx[j].values[a];
+    h[j] = kg.apply(dense);
+  }
+  Vec cov(ns * ns);
+  for (int64_t i = 0; i < ns; ++i)
+    for (int64_t j = 0; j < ns; ++j) {
+      double prior = 0.0;
+      for (std::size_t a = 0; a < wx[i].indices.size(); ++a) prior += wx[i].values[a] * h[j][wx[i].indices[a]];
+      cov[i * ns + j] = prior;
+    }
+  if (lr.k > 0) {
+    std::vector<Vec> phi(ns), tphi(ns);
+    for (int64_t j = 0; j < ns; ++j) {
+      phi[j] = lowrank_phi(lr, wx[j]);
+      tphi[j] = tridiag_solve(lr.alpha, lr.beta, phi[j]);
+    }
+    for (int64_t i = 0; i < ns; ++i)
+      for (int64_t j = 0; j < ns; ++j) cov[i * ns + j] -= dot(phi[i], tphi[j]);
+  }
+  Vec out(ns * ns);
+  for (int64_t i = 0; i < ns; ++i)
+    for (int64_t j = 0; j < ns; ++j) out[i * ns + j] = 0.5 * (cov[i * ns + j] + cov[j * ns + i]);
+  return out;
+}
+
+// LowRankCov::query (gp.cpp:486-498)
+double lowrank_query(const Toeplitz& kg, const LowRank& lr, int scheme, const double* x, const double* x2) {
+  const int64_t m = kg.grid.m;
+  const WeightVector wa = interp_weights(kg.grid, x, scheme);
+  const WeightVector wb = interp_weights(kg.grid, x2, scheme);
+  Vec dense(m, 0.0);
+  for (std::size_t a = 0; a < wb.indices.size(); ++a) dense[wb.indices[a]] = wb.values[a];
+  const Vec hb = kg.apply(dense);
+  double prior = 0.0;
+  for (std::size_t a = 0; a < wa.indices.size(); ++a) prior += wa.values[a] * hb[wa.indices[a]];
+  if (lr.k == 0) return prior;
+  const Vec pa = lowrank_phi(lr, wa), pb = lowrank_phi(lr, wb);
+  return prior - dot(pa, tridiag_solve(lr.alpha, lr.beta, pb));
+}
+
 }  // namespace
 
 struct orc_stats {
@@ -1359,6 +1520,32 @@ int orc_log_likelihood_gsgp(const orc_stats* st, const orc_kg* kgh, double sigma
     iout[0] = probes_used;
     iout[1] = solve.iterations;
     iout[2] = r;
+  });
+}
+
+
+int orc_posterior_cov_exact(const orc_kg* kg, const orc_stats* st, int scheme, double sigma, const double* pts,
+                            int64_t ns, double tol, int maxiter, double* cov, double* max_asym, int* total_iters) {
+  return guard([&] {
+    const CovOut c = posterior_cov_exact(*kg->t, st->s, scheme, sigma, pts, ns, tol, maxiter);
+    std::memcpy(cov, c.cov.data(), sizeof(double) * ns * ns);
+    *max_asym = c.max_asymmetry;
+    *total_iters = c.total_iterations;
+  });
+}
+
+// low-rank covariance: rank used, then the cov matrix at ns points and (optionally) one query
+int orc_posterior_cov_lowrank(const orc_kg* kg, const orc_stats* st, int scheme, double sigma, int64_t rank,
+                              const double* pts, int64_t ns, double* cov, const double* qx, const double* qx2,
+                              double* qout, int* rank_used) {
+  return guard([&] {
+    const LowRank lr = posterior_cov_lowrank(*kg->t, st->s, sigma, rank);
+    *rank_used = lr.k;
+    if (ns > 0) {
+      const Vec c = lowrank_cov_matrix(*kg->t, lr, scheme, pts, ns);
+      std::memcpy(cov, c.data(), sizeof(double) * ns * ns);
+    }
+    if (qx && qx2 && qout) *qout = lowrank_query(*kg->t, lr, scheme, qx, qx2);
   });
 }
 

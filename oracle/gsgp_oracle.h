@@ -145,6 +145,14 @@ int orc_log_likelihood_gsgp(const orc_stats* st, const orc_kg* kg, double sigma,
                             const double* gmin, const double* gmax, const int64_t* gsize,
                             int scheme, const double* x, int64_t n, double* out, int* iout);
 
+/* posterior_cov_exact (gp.cpp:381-427): cov ns×ns symmetrised, max asymmetry, Σ iterations. */
+int orc_posterior_cov_exact(const orc_kg* kg, const orc_stats* st, int scheme, double sigma, const double* pts,
+                            int64_t ns, double tol, int maxiter, double* cov, double* max_asym, int* total_iters);
+/* posterior_cov_lowrank (gp.cpp:429-475) + LowRankCov::cov_matrix / query (gp.cpp:486-525). */
+int orc_posterior_cov_lowrank(const orc_kg* kg, const orc_stats* st, int scheme, double sigma, int64_t rank,
+                              const double* pts, int64_t ns, double* cov, const double* qx, const double* qx2,
+                              double* qout, int* rank_used);
+
 #ifdef __cplusplus
 }
 #endif

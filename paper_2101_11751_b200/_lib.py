@@ -95,6 +95,12 @@ SIGNATURES = {
     "gsgpc_posterior_mean_gsgp": (_i, [_vp, _vp, _vp, _d, _d, _i, _vp, _P(SolveInfo_t)]),
     "gsgpc_predict_mean": (_i, [_vp, _P(Grid_t), _i, _vp, _P(Points_t), _i64, _vp]),
     "gsgpc_factorized_lanczos_fused": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp]),
+    "gsgpc_posterior_cov_exact": (_i, [_vp, _vp, _vp, _d, _P(Points_t), _i64, _d, _i, _vp, _P(_d), _P(C.c_int32)]),
+    "gsgpc_posterior_cov_lowrank": (_i, [_vp, _vp, _vp, _d, _i64, _P(_vp)]),
+    "gsgpc_lowrank_destroy": (None, [_vp]),
+    "gsgpc_lowrank_rank": (_i, [_vp, _P(_i64)]),
+    "gsgpc_lowrank_cov_matrix": (_i, [_vp, _vp, _P(Points_t), _i64, _vp]),
+    "gsgpc_lowrank_query": (_i, [_vp, _vp, _vp, _vp, _P(_d)]),
     "gsgpc_log_likelihood_gsgp": (_i, [_vp, _vp, _vp, _d, _P(LoglikOptions_t), _P(LoglikResult_t)]),
 }
 

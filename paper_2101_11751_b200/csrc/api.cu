@@ -154,6 +154,21 @@ struct gsgpc_kg {
   KgDev dev{};
 };
 
+// LowRankCov (gp.hpp:148-167): R (k × m, row j = column j of the reference's r_), the
+// tridiagonal T, and its own copy of the K_G generators (the reference holds a shared_ptr
+// to the operator).
+struct gsgpc_lowrank {
+  int device = 0;
+  GridDev g{};
+  int scheme = 1;
+  int64_t m = 0;
+  int k = 0;
+  DBuf R;
+  std::vector<double> alpha, beta;
+  DBuf gen[GSGPC_MAX_DIM];
+  KgDev kg{};
+};
+
 struct CgCache {
   // buffers + a captured graph of B iterations for one (stats, kg) pairing
   const gsgpc_stats* stats = nullptr;
@@ -1883,6 +1898,270 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
     out->solver_iterations = cg.iterations;
     out->max_depth_used = max_used;
     out->logdet_route = route;
+  });
+}
+
+
+// ---------------------------------------------------------------- covariance (gp.cpp:381-528)
+namespace {
+
+struct TestWeights {
+  int cap = 0;
+  DBuf *idx = nullptr, *w = nullptr, *nnz = nullptr;
+};
+
+// interp_weights of the test points on the device (errors as the reference's interp_weights)
+TestWeights test_weights(gsgpc_ctx* ctx, const GridDev& g, const gsgpc_points* pts, int64_t ns, const char* tag) {
+  TestWeights t;
+  t.cap = 1;
+  for (int k = 0; k < g.d; ++k) t.cap *= g.W;
+  const std::string p(tag);
+  const bool dev = is_device_ptr(pts->x);
+  const PointsDev P = dev ? points_dev(pts, g.d, 0) : stage_points(ctx, pts, g.d, 0, ns, false, (p + "_stage").c_str());
+  t.idx = &ctx->buf(p + "_idx");
+  t.w = &ctx->buf(p + "_w");
+  t.nnz = &ctx->buf(p + "_nnz");
+  DBuf& st = ctx->buf(p + "_status");
+  t.idx->ensure(sizeof(int64_t) * ns * t.cap);
+  t.w->ensure(sizeof(double) * ns * t.cap);
+  t.nnz->ensure(sizeof(int) * ns);
+  st.ensure(sizeof(int) * ns);
+  run_interp_weights(ctx->L(), pts->dtype, P, ns, g, t.idx->as<int64_t>(), t.w->as<double>(), t.nnz->as<int>(),
+                     st.as<int>());
+  std::vector<int> hs(ns);
+  copy_out(ctx, hs.data(), st.p, sizeof(int) * ns);
+  for (int64_t i = 0; i < ns; ++i) {
+    if (hs[i] == PT_OUTSIDE) throw Error(GSGPC_OUT_OF_GRID, "interp_weights: point outside grid", i + 1);
+    if (hs[i] == PT_LEAVES) {
+      throw Error(GSGPC_OUT_OF_GRID,
+                  "interp_weights: stencil leaves the grid (point too close to the boundary for the requested scheme)",
+                  i + 1);
+    }
+  }
+  return t;
+}
+
+// H = K_G W_xᵀ rows (ns × m) and prior(i, j) = w_iᵀ h_j (ns × ns), both on the device
+void prior_and_h(gsgpc_ctx* ctx, const KgDev& kg, int64_t m, const TestWeights& t, int64_t ns, DBuf& H,
+                 DBuf& prior) {
+  const Launch L = ctx->L();
+  DBuf& wx = ctx->buf("cov_wx");
+  DBuf& t0 = ctx->buf("cov_t0");
+  DBuf& t1 = ctx->buf("cov_t1");
+  for (DBuf* b : {&wx, &H, &t0, &t1}) b->ensure(sizeof(double) * ns * m);
+  prior.ensure(sizeof(double) * ns * ns);
+  cov_scatter_w(L, ns, m, t.cap, t.idx->as<int64_t>(), t.w->as<double>(), t.nnz->as<int>(), wx.as<double>());
+  run_kg_apply_batched(L, kg, ns, wx.as<double>(), H.as<double>(), t0.as<double>(), t1.as<double>());
+  cov_gather(L, ns, ns, m, t.cap, t.idx->as<int64_t>(), t.w->as<double>(), t.nnz->as<int>(), H.as<double>(),
+             prior.as<double>());
+}
+
+// T y = b for the symmetric positive definite tridiagonal T (LDLᵀ, k small, on the host)
+void tridiag_solve_host(const std::vector<double>& a, const std::vector<double>& b, double* z) {
+  const int k = static_cast<int>(a.size());
+  std::vector<double> dd(k), l(k > 1 ? k - 1 : 0);
+  dd[0] = a[0];
+  for (int i = 1; i < k; ++i) {
+    l[i - 1] = b[i - 1] / dd[i - 1];
+    dd[i] = a[i] - l[i - 1] * b[i - 1];
+  }
+  for (int i = 1; i < k; ++i) z[i] -= l[i - 1] * z[i - 1];
+  for (int i = 0; i < k; ++i) z[i] /= dd[i];
+  for (int i = k - 2; i >= 0; --i) z[i] -= l[i] * z[i + 1];
+}
+
+// unsymmetrised low-rank covariance prior − φᵀ T⁻¹ φ at ns points (host out, ns × ns)
+std::vector<double> lowrank_cov_raw(gsgpc_ctx* ctx, gsgpc_lowrank* lr, const gsgpc_points* pts, int64_t ns) {
+  const Launch L = ctx->L();
+  const TestWeights t = test_weights(ctx, lr->g, pts, ns, "lr");
+  DBuf& H = ctx->buf("cov_h");
+  DBuf& prior = ctx->buf("cov_prior");
+  prior_and_h(ctx, lr->kg, lr->m, t, ns, H, prior);
+  if (lr->k > 0) {
+    DBuf& phi = ctx->buf("lr_phi");
+    DBuf& y = ctx->buf("lr_y");
+    phi.ensure(sizeof(double) * ns * lr->k);
+    y.ensure(sizeof(double) * ns * lr->k);
+    cov_gather(L, ns, lr->k, lr->m, t.cap, t.idx->as<int64_t>(), t.w->as<double>(), t.nnz->as<int>(),
+               lr->R.as<double>(), phi.as<double>());
+    std::vector<double> hp(static_cast<size_t>(ns) * lr->k);
+    copy_out(ctx, hp.data(), phi.p, sizeof(double) * hp.size());
+    for (int64_t i = 0; i < ns; ++i) tridiag_solve_host(lr->alpha, lr->beta, hp.data() + i * lr->k);
+    GSGPC_CUDA(cudaMemcpyAsync(y.p, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, ctx->stream));
+    cov_sub_abt(L, static_cast<int>(ns), lr->k, phi.as<double>(), y.as<double>(), prior.as<double>());
+  }
+  std::vector<double> c(static_cast<size_t>(ns) * ns);
+  copy_out(ctx, c.data(), prior.p, sizeof(double) * c.size());
+  return c;
+}
+
+}  // namespace
+
+gsgpc_status gsgpc_posterior_cov_exact(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, double sigma,
+                                       const gsgpc_points* pts, int64_t ns, double tol, int maxiter, double* cov,
+                                       double* max_asymmetry, int32_t* total_iterations) {
+  return guard(ctx, [&] {
+    if (!s || !kg || !cov) invalid("NULL argument");
+    check_points(pts, ns, false);
+    finalize_stats(ctx, s);
+    const int64_t m = s->g.m;
+    if (kg->m != m) invalid("posterior_cov_exact: kernel/grid size mismatch");
+    if (ns == 0) return;
+    const Launch L = ctx->L();
+    const TestWeights t = test_weights(ctx, s->g, pts, ns, "cov");
+    DBuf& H = ctx->buf("cov_h");
+    DBuf& C = ctx->buf("cov_prior");
+    prior_and_h(ctx, kg->dev, m, t, ns, H, C);
+    DBuf& X = ctx->buf("cov_x");
+    X.ensure(sizeof(double) * ns * m);
+    const StencilDesc sd = stencil_desc(s);
+    int64_t total = 0;
+    for (int64_t j0 = 0; j0 < ns; j0 += 32) {
+      const int P = static_cast<int>(std::min<int64_t>(32, ns - j0));
+      const BcgOut o = bcg_run(L, sd, s->stencil(), kg->dev, P, H.as<double>() + j0 * m, sigma, -1.0, tol, maxiter,
+                               X.as<double>() + j0 * m);
+      if (o.breakdown) {
+        throw Error(GSGPC_BREAKDOWN, "factorized_cg_grid_rhs: p^T A p <= 0, operator is not positive definite");
+      }
+      for (int p = 0; p < P; ++p) {
+        if (!o.converged[p]) {
+          ctx->err_row = o.iterations[p];
+          throw Error(GSGPC_NONCONVERGENCE, "posterior_cov_exact: solver hit maxiter");
+        }
+        total += o.iterations[p];
+      }
+    }
+    cov_sub_abt(L, static_cast<int>(ns), m, H.as<double>(), X.as<double>(), C.as<double>());
+    std::vector<double> c(static_cast<size_t>(ns) * ns);
+    copy_out(ctx, c.data(), C.p, sizeof(double) * c.size());
+    double asym = 0.0;
+    for (int64_t i = 0; i < ns; ++i)
+      for (int64_t j = 0; j < ns; ++j) {
+        asym = std::max(asym, std::fabs(c[i * ns + j] - c[j * ns + i]));
+        cov[i * ns + j] = 0.5 * (c[i * ns + j] + c[j * ns + i]);
+      }
+    if (max_asymmetry) *max_asymmetry = asym;
+    if (total_iterations) *total_iterations = static_cast<int32_t>(total);
+  });
+}
+
+gsgpc_status gsgpc_posterior_cov_lowrank(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, double sigma, int64_t rank,
+                                         gsgpc_lowrank** out) {
+  return guard(ctx, [&] {
+    if (!s || !kg || !out) invalid("NULL argument");
+    finalize_stats(ctx, s);
+    const int64_t m = s->g.m;
+    if (kg->m != m) invalid("posterior_cov_lowrank: kernel/grid size mismatch");
+    if (rank < 0 || rank > m) invalid("posterior_cov_lowrank: need 0 <= rank <= grid size");
+    std::unique_ptr<gsgpc_lowrank> lr(new gsgpc_lowrank());
+    lr->device = ctx->device;
+    lr->g = s->g;
+    lr->scheme = s->scheme;
+    lr->m = m;
+    lr->kg = kg->dev;
+    for (int k = 0; k < kg->dev.d; ++k) {
+      const size_t b = sizeof(double) * kg->dev.sz[k];
+      lr->gen[k].ensure(b);
+      GSGPC_CUDA(cudaMemcpyAsync(lr->gen[k].p, kg->dev.gen[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+      lr->kg.gen[k] = lr->gen[k].as<double>();
+    }
+    const double n = static_cast<double>(s->reduced ? static_cast<int64_t>(read_scalar(ctx, s->tail() + 1)) : s->n);
+    const Launch L = ctx->L();
+    if (rank > 0 && n > 0) {
+      // start direction ĝ = WᵀW 1 / ‖WᵀW 1‖ (gp.cpp:446-452)
+      const StencilDesc sd = stencil_desc(s);
+      upload_stencil_offsets(sd, ctx->stream);
+      DBuf& a = ctx->buf("lr_a");
+      DBuf& b = ctx->buf("lr_b");
+      DBuf& c = ctx->buf("lr_c");
+      DBuf& t0 = ctx->buf("lr_t0");
+      DBuf& t1 = ctx->buf("lr_t1");
+      for (DBuf* q : {&a, &b, &c, &t0, &t1}) q->ensure(sizeof(double) * m);
+      std::vector<double> h(m, 1.0);
+      GSGPC_CUDA(cudaMemcpyAsync(a.p, h.data(), sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+      run_spmv(L, sd, s->stencil(), a.as<double>(), b.as<double>());
+      copy_out(ctx, h.data(), b.p, sizeof(double) * m);
+      double gn = 0.0;
+      for (double v : h) gn += v * v;
+      gn = std::sqrt(gn);
+      if (gn != 0.0) {
+        for (double& v : h) v /= gn;
+        GSGPC_CUDA(cudaMemcpyAsync(a.p, h.data(), sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+        run_spmv(L, sd, s->stencil(), a.as<double>(), b.as<double>());        // wt_z0 = WᵀW ĝ
+        run_kg_apply(L, kg->dev, b.as<double>(), c.as<double>(), t0.as<double>(), t1.as<double>());  // K wt_z0
+        std::vector<double> wt(m);
+        copy_out(ctx, wt.data(), b.p, sizeof(double) * m);
+        double z0 = 0.0;
+        for (int64_t i = 0; i < m; ++i) z0 += h[i] * wt[i];
+        if (z0 > 0.0) {
+          DBuf& zd = ctx->buf("lr_z0");
+          zd.ensure(sizeof(double));
+          GSGPC_CUDA(cudaMemcpyAsync(zd.p, &z0, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+          DBuf& Q = ctx->buf("lr_basis");
+          Q.ensure(sizeof(double) * rank * m);
+          const EflaOut o = efla_run(L, sd, s->stencil(), kg->dev, 1, c.as<double>(), b.as<double>(), zd.as<double>(),
+                                     sigma * sigma, static_cast<int>(rank), Q.as<double>());
+          const int k = o.order[0];
+          lr->k = k;
+          lr->alpha.assign(o.alpha.begin(), o.alpha.begin() + k);
+          lr->beta.assign(o.beta.begin(), o.beta.begin() + (k > 1 ? k - 1 : 0));
+          // R[j] = K_G (WᵀW q̂_j + d_j · wt_z0 / √z0)   (gp.cpp:466-470)
+          DBuf& U = ctx->buf("lr_u");
+          DBuf& T0 = ctx->buf("lr_bt0");
+          DBuf& T1 = ctx->buf("lr_bt1");
+          for (DBuf* q : {&U, &T0, &T1}) q->ensure(sizeof(double) * k * m);
+          lr->R.ensure(sizeof(double) * k * m);
+          spmm_batched(L, sd, s->stencil(), Q.as<double>(), U.as<double>(), k);
+          const double bn = std::sqrt(z0);
+          for (int j = 0; j < k; ++j) {
+            run_axpby(L, m, 1.0, U.as<double>() + static_cast<int64_t>(j) * m, o.d[j] / bn, b.as<double>(),
+                      U.as<double>() + static_cast<int64_t>(j) * m);
+          }
+          run_kg_apply_batched(L, lr->kg, k, U.as<double>(), lr->R.as<double>(), T0.as<double>(), T1.as<double>());
+        }
+      }
+    }
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = lr.release();
+  });
+}
+
+void gsgpc_lowrank_destroy(gsgpc_lowrank* lr) { delete lr; }
+
+gsgpc_status gsgpc_lowrank_rank(const gsgpc_lowrank* lr, int64_t* rank) {
+  if (!lr || !rank) return GSGPC_INVALID_ARGUMENT;
+  *rank = lr->k;
+  return GSGPC_OK;
+}
+
+gsgpc_status gsgpc_lowrank_cov_matrix(gsgpc_ctx* ctx, gsgpc_lowrank* lr, const gsgpc_points* pts, int64_t ns,
+                                      double* cov) {
+  return guard(ctx, [&] {
+    if (!lr || !cov) invalid("NULL argument");
+    check_points(pts, ns, false);
+    if (ns == 0) return;
+    const std::vector<double> c = lowrank_cov_raw(ctx, lr, pts, ns);
+    for (int64_t i = 0; i < ns; ++i)
+      for (int64_t j = 0; j < ns; ++j) cov[i * ns + j] = 0.5 * (c[i * ns + j] + c[j * ns + i]);
+  });
+}
+
+gsgpc_status gsgpc_lowrank_query(gsgpc_ctx* ctx, gsgpc_lowrank* lr, const double* x, const double* x2, double* out) {
+  return guard(ctx, [&] {
+    if (!lr || !x || !x2 || !out) invalid("NULL argument");
+    const int d = lr->g.d;
+    std::vector<double> two(2 * d);
+    for (int k = 0; k < d; ++k) {
+      two[k] = x[k];
+      two[d + k] = x2[k];
+    }
+    gsgpc_points p{};
+    p.dtype = GSGPC_F64;
+    p.x = two.data();
+    p.x_row_stride = d;
+    for (int k = 0; k < d; ++k) p.x_col_offset[k] = k;
+    const std::vector<double> c = lowrank_cov_raw(ctx, lr, &p, 2);
+    *out = c[1];  // prior(x, x2) − φ(x)ᵀ T⁻¹ φ(x2)
   });
 }
 

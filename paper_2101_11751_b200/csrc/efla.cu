@@ -338,19 +338,12 @@ struct DevMem {
 };
 
 void run_kg_batched(const Launch& L, const KgDev& kg, int P, const double* v, double* out, double* t0, double* t1) {
-  // probes as an extra leading dimension with an identity factor
-  KgDev b = kg;
-  // fold P into dim 0's outer count by treating the batch as P independent vectors
-  for (int p = 0; p < P; ++p) {
-    run_kg_apply(L, kg, v + static_cast<int64_t>(p) * kg.m, out + static_cast<int64_t>(p) * kg.m,
-                 t0 + static_cast<int64_t>(p) * kg.m, t1 + static_cast<int64_t>(p) * kg.m);
-  }
-  (void)b;
+  run_kg_apply_batched(L, kg, P, v, out, t0, t1);
 }
 
 // Runs EFLA for P ≤ 32 probes; inputs are device arrays (P × m).
 EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, const double* kwt_in,
-                 const double* wt_in, const double* z0sq_dev, double s2, int k) {
+                 const double* wt_in, const double* z0sq_dev, double s2, int k, double* basis_out) {
   if (P < 1 || P > EF_MAXP) throw Error(GSGPC_UNSUPPORTED, "factorized_lanczos_fused: 1..32 start vectors per batch");
   if (k < 1) invalid("factorized_lanczos_fused: bad k");
   const int64_t m = sd.m;
@@ -404,6 +397,9 @@ EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const 
   GSGPC_CUDA(cudaMemcpyAsync(o.alpha.data(), al.p, sizeof(double) * P * k, cudaMemcpyDeviceToHost, L.s));
   GSGPC_CUDA(cudaMemcpyAsync(o.beta.data(), be.p, sizeof(double) * P * k, cudaMemcpyDeviceToHost, L.s));
   GSGPC_CUDA(cudaMemcpyAsync(hs.data(), scm.p, sizeof(EfScal) * P, cudaMemcpyDeviceToHost, L.s));
+  o.d.resize(static_cast<size_t>(P) * k);
+  GSGPC_CUDA(cudaMemcpyAsync(o.d.data(), dv.p, sizeof(double) * P * k, cudaMemcpyDeviceToHost, L.s));
+  if (basis_out) GSGPC_CUDA(cudaMemcpyAsync(basis_out, Qh.p, V * k, cudaMemcpyDeviceToDevice, L.s));
   GSGPC_CUDA(cudaStreamSynchronize(L.s));
   o.order.resize(P);
   for (int p = 0; p < P; ++p) o.order[p] = hs[p].order > 0 ? hs[p].order : k;
@@ -927,6 +923,263 @@ double dense_logdet_grid_system(const Launch& L, const StencilDesc& sd, const do
   GSGPC_CUDA(cudaMemcpyAsync(&h, out.p, sizeof(double), cudaMemcpyDeviceToHost, L.s));
   GSGPC_CUDA(cudaStreamSynchronize(L.s));
   return h;
+}
+
+
+// =============================================================== multi-RHS EFCG
+// factorized_cg_grid_rhs (solvers.cpp:271-336) for P right-hand sides at once: one stencil
+// read per iteration serves every RHS (k_spmm), K_G runs batched, per-RHS scalars (ρ, eps,
+// α, β, iterations, done/converged/breakdown) live on the device; each RHS follows exactly
+// its single-RHS recurrence and freezes when it converges.
+struct BcgScal {
+  double rho, eps, alpha, beta;
+  int iters, done, converged, breakdown;
+};
+
+// partial dots x_p · y_p
+__global__ void __launch_bounds__(EF_NT) k_bcg_dot(int64_t m, const double* x, const double* y, double* part,
+                                                   int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  const double v = a < m ? x[static_cast<int64_t>(p) * m + a] * y[static_cast<int64_t>(p) * m + a] : 0.0;
+  block_partial_store(v, part + static_cast<int64_t>(p) * nblk + blockIdx.x, sh);
+}
+
+// v += σ² r; s = u; z = v (init)
+__global__ void __launch_bounds__(EF_NT) k_bcg_init_dir(int64_t n, double s2, const double* r, const double* u, double* v,
+                                                        double* sdir, double* z) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  if (i >= n) return;
+  const double vv = v[i] + s2 * r[i];
+  v[i] = vv;
+  sdir[i] = u[i];
+  z[i] = vv;
+}
+
+__global__ void k_bcg_c0(int P, double eps_abs, double rel_tol, BcgScal* sc, const double* dots) {
+  const int p = threadIdx.x;
+  if (p >= P) return;
+  BcgScal s{};
+  s.rho = dots[p];
+  s.eps = eps_abs >= 0.0 ? eps_abs : rel_tol * rel_tol * s.rho;
+  if (s.rho <= s.eps) {
+    s.done = 1;
+    s.converged = 1;
+  }
+  sc[p] = s;
+}
+
+// pap → α (breakdown when pap ≤ 0)
+__global__ void k_bcg_c1(int P, int maxiter, BcgScal* sc, const double* dots) {
+  const int p = threadIdx.x;
+  if (p >= P) return;
+  BcgScal s = sc[p];
+  if (s.done) return;
+  if (s.iters >= maxiter) {
+    s.done = 1;
+  } else if (!(dots[p] > 0.0)) {
+    s.breakdown = 1;
+    s.done = 1;
+  } else {
+    s.alpha = s.rho / dots[p];
+  }
+  sc[p] = s;
+}
+
+// x += α s; r −= α z
+__global__ void __launch_bounds__(EF_NT) k_bcg_upd(int64_t m, const BcgScal* sc, double* x, double* r, const double* sdir,
+                                                   const double* z) {
+  const int p = blockIdx.y;
+  if (sc[p].done) return;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  if (a >= m) return;
+  const int64_t o = static_cast<int64_t>(p) * m + a;
+  const double al = sc[p].alpha;
+  x[o] += al * sdir[o];
+  r[o] -= al * z[o];
+}
+
+// v += σ² r (live RHS); partial u·r
+__global__ void __launch_bounds__(EF_NT) k_bcg_v(int64_t m, double s2, const BcgScal* sc, const double* r,
+                                                 const double* u, double* v, double* part, int nblk) {
+  __shared__ double sh[8];
+  const int p = blockIdx.y;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  double d = 0.0;
+  if (!sc[p].done && a < m) {
+    const int64_t o = static_cast<int64_t>(p) * m + a;
+    v[o] += s2 * r[o];
+    d = u[o] * r[o];
+  }
+  block_partial_store(d, part + static_cast<int64_t>(p) * nblk + blockIdx.x, sh);
+}
+
+// ρ' → converged / β
+__global__ void k_bcg_c2(int P, BcgScal* sc, const double* dots) {
+  const int p = threadIdx.x;
+  if (p >= P) return;
+  BcgScal s = sc[p];
+  if (s.done) return;
+  const double rn = dots[p];
+  s.iters += 1;
+  if (rn <= s.eps) {
+    s.converged = 1;
+    s.done = 1;
+    s.rho = rn;
+    s.beta = 0.0;
+  } else {
+    s.beta = rn / s.rho;
+    s.rho = rn;
+  }
+  sc[p] = s;
+}
+
+// s = u + β s; z = v + β z (RHS still iterating)
+__global__ void __launch_bounds__(EF_NT) k_bcg_dir(int64_t m, const BcgScal* sc, const double* u, const double* v,
+                                                   double* sdir, double* z) {
+  const int p = blockIdx.y;
+  if (sc[p].done) return;
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * EF_NT + threadIdx.x;
+  if (a >= m) return;
+  const int64_t o = static_cast<int64_t>(p) * m + a;
+  const double b = sc[p].beta;
+  sdir[o] = u[o] + b * sdir[o];
+  z[o] = v[o] + b * z[o];
+}
+
+BcgOut bcg_run(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, const double* rhat0,
+               double sigma, double eps_abs, double rel_tol, int maxiter, double* x) {
+  if (P < 1 || P > EF_MAXP) throw Error(GSGPC_UNSUPPORTED, "multi-RHS EFCG: 1..32 right-hand sides per batch");
+  const int64_t m = sd.m;
+  const int64_t pm = static_cast<int64_t>(P) * m;
+  const int nblk = static_cast<int>(ceil_div(m, EF_NT));
+  const size_t V = sizeof(double) * pm;
+  const double s2 = sigma * sigma;
+  DevMem r(V), u(V), v(V), sdir(V), z(V), t0(V), t1(V);
+  DevMem part(sizeof(double) * P * nblk), dots(sizeof(double) * P), scm(sizeof(BcgScal) * P);
+  BcgScal* sc = static_cast<BcgScal*>(scm.p);
+  const dim3 gv(static_cast<unsigned>(nblk), static_cast<unsigned>(P));
+  const unsigned gl = static_cast<unsigned>(ceil_div(pm, EF_NT));
+  GSGPC_CUDA(cudaMemcpyAsync(r.p, rhat0, V, cudaMemcpyDeviceToDevice, L.s));
+  GSGPC_CUDA(cudaMemsetAsync(x, 0, V, L.s));
+  ef_upload_offsets(sd, L.s);
+  launch_spmm(L, sd, A, r.d(), u.d(), P, nullptr);
+  run_kg_batched(L, kg, P, u.d(), v.d(), t0.d(), t1.d());
+  k_bcg_init_dir<<<gl, EF_NT, 0, L.s>>>(pm, s2, r.d(), u.d(), v.d(), sdir.d(), z.d());
+  k_bcg_dot<<<gv, EF_NT, 0, L.s>>>(m, u.d(), r.d(), part.d(), nblk);
+  k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+  k_bcg_c0<<<1, 64, 0, L.s>>>(P, eps_abs, rel_tol, sc, dots.d());
+  L.count(6);
+  std::vector<BcgScal> hs(P);
+  for (int it = 0; it < maxiter; ++it) {
+    k_bcg_dot<<<gv, EF_NT, 0, L.s>>>(m, sdir.d(), z.d(), part.d(), nblk);
+    k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+    k_bcg_c1<<<1, 64, 0, L.s>>>(P, maxiter, sc, dots.d());
+    k_bcg_upd<<<gv, EF_NT, 0, L.s>>>(m, sc, x, r.d(), sdir.d(), z.d());
+    launch_spmm(L, sd, A, r.d(), u.d(), P, nullptr);
+    run_kg_batched(L, kg, P, u.d(), v.d(), t0.d(), t1.d());
+    k_bcg_v<<<gv, EF_NT, 0, L.s>>>(m, s2, sc, r.d(), u.d(), v.d(), part.d(), nblk);
+    k_ef_reduce<<<P, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
+    k_bcg_c2<<<1, 64, 0, L.s>>>(P, sc, dots.d());
+    k_bcg_dir<<<gv, EF_NT, 0, L.s>>>(m, sc, u.d(), v.d(), sdir.d(), z.d());
+    L.count(9);
+    if ((it & 7) == 7 || it + 1 == maxiter) {
+      GSGPC_CUDA(cudaMemcpyAsync(hs.data(), scm.p, sizeof(BcgScal) * P, cudaMemcpyDeviceToHost, L.s));
+      GSGPC_CUDA(cudaStreamSynchronize(L.s));
+      bool all = true;
+      for (const auto& q : hs) all = all && q.done;
+      if (all) break;
+    }
+  }
+  GSGPC_CUDA(cudaMemcpyAsync(hs.data(), scm.p, sizeof(BcgScal) * P, cudaMemcpyDeviceToHost, L.s));
+  GSGPC_CUDA(cudaStreamSynchronize(L.s));
+  BcgOut o;
+  for (const auto& q : hs) {
+    o.iterations.push_back(q.iters);
+    o.converged.push_back(q.converged);
+    o.breakdown = o.breakdown || q.breakdown;
+    o.residual_sq.push_back(q.rho);
+  }
+  return o;
+}
+
+// =============================================================== covariance helpers
+// dense W_x rows [ns][m] from compact interp weights (idx/w [ns][cap], nnz)
+__global__ void k_cov_scatter_w(int64_t ns, int64_t m, int cap, const int64_t* idx, const double* w, const int* nnz,
+                                double* out) {
+  const int64_t i = blockIdx.x;
+  for (int a = threadIdx.x; a < nnz[i]; a += blockDim.x) out[i * m + idx[i * cap + a]] = w[i * cap + a];
+}
+
+// out[i][j] = Σ_a w_i[a] · H[j][idx_i[a]]   (rows of H: nh)
+__global__ void k_cov_gather(int64_t ni, int64_t nh, int64_t m, int cap, const int64_t* idx, const double* w,
+                             const int* nnz, const double* H, double* out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ni * nh) return;
+  const int64_t i = e / nh, j = e % nh;
+  double acc = 0.0;
+  for (int a = 0; a < nnz[i]; ++a) acc += w[i * cap + a] * H[j * m + idx[i * cap + a]];
+  out[e] = acc;
+}
+
+// C[i][j] −= Σ_r A[i][r] B[j][r]   (row-major, 32×32 tiles)
+__global__ void __launch_bounds__(256) k_cov_sub_abt(int n, int64_t m, const double* __restrict__ A,
+                                                     const double* __restrict__ B, double* __restrict__ C) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t r0 = 0; r0 < m; r0 += 32) {
+    for (int q = ty; q < 32; q += 8) {
+      const int64_t rr = r0 + tx;
+      As[q][tx] = (i0 + q < n && rr < m) ? A[static_cast<int64_t>(i0 + q) * m + rr] : 0.0;
+      Bs[q][tx] = (j0 + q < n && rr < m) ? B[static_cast<int64_t>(j0 + q) * m + rr] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double b = Bs[tx][kk];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][kk], b, acc[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ty + 8 * q, j = j0 + tx;
+    if (i < n && j < n) C[static_cast<int64_t>(i) * n + j] -= acc[q];
+  }
+}
+
+void cov_scatter_w(const Launch& L, int64_t ns, int64_t m, int cap, const int64_t* idx, const double* w,
+                   const int* nnz, double* out) {
+  GSGPC_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * ns * m, L.s));
+  if (ns > 0) k_cov_scatter_w<<<static_cast<unsigned>(ns), 64, 0, L.s>>>(ns, m, cap, idx, w, nnz, out);
+  L.count();
+}
+
+void cov_gather(const Launch& L, int64_t ni, int64_t nh, int64_t m, int cap, const int64_t* idx, const double* w,
+                const int* nnz, const double* H, double* out) {
+  if (ni * nh == 0) return;
+  k_cov_gather<<<static_cast<unsigned>(ceil_div(ni * nh, 256)), 256, 0, L.s>>>(ni, nh, m, cap, idx, w, nnz, H, out);
+  L.count();
+}
+
+void cov_sub_abt(const Launch& L, int n, int64_t m, const double* A, const double* B, double* C) {
+  if (n == 0) return;
+  const dim3 g(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(n, 32)));
+  k_cov_sub_abt<<<g, 256, 0, L.s>>>(n, m, A, B, C);
+  L.count();
+}
+
+void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P) {
+  ef_upload_offsets(sd, L.s);
+  for (int p0 = 0; p0 < P; p0 += EF_MAXP) {
+    const int pb = std::min(EF_MAXP, P - p0);
+    launch_spmm(L, sd, A, x + static_cast<int64_t>(p0) * sd.m, out + static_cast<int64_t>(p0) * sd.m, pb, nullptr);
+  }
+  L.count();
 }
 
 }  // namespace gsgpc

@@ -267,11 +267,12 @@ static void launch_toep(const Launch& L, int mode, ToepArgs t, dim3 grid, size_t
 }
 
 // Applies T_{d-1}, ..., T_1 (plain) and T_0 (MODE, possibly with the CG epilogue).
+// batch > 1: `batch` contiguous m-vectors, the batch index an extra outermost dimension.
 static void kg_chain(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1,
-                     int last_mode, CgEpi e) {
+                     int last_mode, CgEpi e, int64_t batch = 1) {
   const double* cur = v;
   for (int k = kg.d - 1; k >= 0; --k) {
-    int64_t inner = 1, outer = 1;
+    int64_t inner = 1, outer = batch;
     for (int j = k + 1; j < kg.d; ++j) inner *= kg.sz[j];
     for (int j = 0; j < k; ++j) outer *= kg.sz[j];
     ToepArgs t{};
@@ -290,6 +291,12 @@ static void kg_chain(const Launch& L, const KgDev& kg, const double* v, double* 
 void run_kg_apply(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1) {
   CgEpi e{};
   kg_chain(L, kg, v, out, tmp0, tmp1, 0, e);
+}
+
+void run_kg_apply_batched(const Launch& L, const KgDev& kg, int64_t batch, const double* v, double* out,
+                          double* tmp0, double* tmp1) {
+  CgEpi e{};
+  kg_chain(L, kg, v, out, tmp0, tmp1, 0, e, batch);
 }
 
 int cg_partials_needed(int64_t m) {

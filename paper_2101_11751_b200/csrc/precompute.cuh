@@ -71,6 +71,9 @@ struct KgDev {
   const double* gen[GSGPC_MAX_DIM];  // per-dim generator columns (outputscale folded into dim 0)
 };
 void run_kg_apply(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1);
+// `batch` contiguous m-vectors at once (tmp0 / tmp1 hold batch·m doubles)
+void run_kg_apply_batched(const Launch& L, const KgDev& kg, int64_t batch, const double* v, double* out,
+                          double* tmp0, double* tmp1);
 
 // EFCG (see operators.cu)
 struct CgState {
@@ -106,11 +109,12 @@ void run_predict(const Launch& L, int dtype, const PointsDev& p, int64_t n, cons
 
 // ---- efla.cu: probe-batched EFLA (P <= 32 per call; inputs device arrays P × m)
 struct EflaOut {
-  std::vector<double> alpha, beta;  // P × k
+  std::vector<double> alpha, beta, d;  // P × k
   std::vector<int> order;
 };
+// basis_out (optional, device P × k × m): the Q̂ columns (TridiagonalFactor::basis)
 EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, const double* kwt_in,
-                 const double* wt_in, const double* z0sq_dev, double s2, int k);
+                 const double* wt_in, const double* z0sq_dev, double s2, int k, double* basis_out = nullptr);
 std::pair<double, int> quadrature_logdet_host(const double* alpha, const double* beta, int k, double probe_sq,
                                               double quad_tol);
 void run_kg_batched(const Launch& L, const KgDev& kg, int P, const double* v, double* out, double* t0, double* t1);
@@ -129,5 +133,20 @@ BatchedOp sym_op(const Launch& L, const StencilDesc& sd, const double* A, const 
 double kg_condition_estimate(const Launch& L, const KgDev& kg);
 double dense_logdet_grid_system(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg,
                                 double sigma_sq);
+// multi-RHS EFCG (P ≤ 32 per call): x (P × m, device) ← x̂_d of each RHS
+struct BcgOut {
+  std::vector<int> iterations, converged;
+  std::vector<double> residual_sq;
+  bool breakdown = false;
+};
+BcgOut bcg_run(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, const double* rhat0,
+               double sigma, double eps_abs, double rel_tol, int maxiter, double* x);
+// covariance helpers (device, row-major)
+void cov_scatter_w(const Launch& L, int64_t ns, int64_t m, int cap, const int64_t* idx, const double* w,
+                   const int* nnz, double* out);
+void cov_gather(const Launch& L, int64_t ni, int64_t nh, int64_t m, int cap, const int64_t* idx, const double* w,
+                const int* nnz, const double* H, double* out);
+void cov_sub_abt(const Launch& L, int n, int64_t m, const double* A, const double* B, double* C);
+void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P);
 
 }  // namespace gsgpc

@@ -856,6 +856,81 @@ class PosteriorModel:
         return float(out[0]) if single else out
 
 
+@dataclass
+class CovResult:
+    """gp.hpp:132-136."""
+    cov: np.ndarray
+    max_asymmetry: float = 0.0
+    total_iterations: int = 0
+
+
+def _test_points(model, points):
+    pts = np.asarray(points, dtype=np.float64) if not (torch is not None and isinstance(points, torch.Tensor)) \
+        else points
+    if getattr(pts, "ndim", 2) == 1:
+        pts = pts.reshape(1, -1)
+    return _coords(pts, model.grid().dim())
+
+
+def posterior_cov_exact(model: "PosteriorModel", points, tol: float, maxiter: int = kDefaultMaxIter) -> CovResult:
+    """gp.cpp:381-427: exact posterior covariance between test points (one grid-rhs solve per
+    point; the solves run batched on the device)."""
+    ctx = model.stats.context
+    p, n, keep = _test_points(model, points)
+    cov = np.zeros((n, n))
+    asym = C.c_double(0.0)
+    iters = C.c_int32(0)
+    ctx.check(_L.load().gsgpc_posterior_cov_exact(ctx.handle, model.stats.handle, model.kg.handle, float(model.sigma),
+                                                  C.byref(p), n, float(tol), int(maxiter), cov.ctypes.data,
+                                                  C.byref(asym), C.byref(iters)))
+    return CovResult(cov, asym.value, iters.value)
+
+
+class LowRankCov:
+    """gp.hpp:148-167: rank-k posterior covariance from one factorized Lanczos run."""
+
+    def __init__(self, h, model, ctx):
+        self._h = h
+        self._model = model
+        self._ctx = ctx
+
+    def __del__(self):
+        try:
+            if self._h:
+                _L.load().gsgpc_lowrank_destroy(self._h)
+        except Exception:
+            pass
+
+    def rank(self) -> int:
+        r = C.c_int64(0)
+        _L.load().gsgpc_lowrank_rank(self._h, C.byref(r))
+        return r.value
+
+    def query(self, x, x2) -> float:
+        a = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        b = np.ascontiguousarray(x2, dtype=np.float64).reshape(-1)
+        out = C.c_double(0.0)
+        self._ctx.check(_L.load().gsgpc_lowrank_query(self._ctx.handle, self._h, a.ctypes.data, b.ctypes.data,
+                                                      C.byref(out)))
+        return out.value
+
+    def cov_matrix(self, points) -> np.ndarray:
+        p, n, keep = _test_points(self._model, points)
+        cov = np.zeros((n, n))
+        self._ctx.check(_L.load().gsgpc_lowrank_cov_matrix(self._ctx.handle, self._h, C.byref(p), n,
+                                                           cov.ctypes.data))
+        return cov
+
+
+def posterior_cov_lowrank(model: "PosteriorModel", rank: int) -> LowRankCov:
+    """gp.cpp:429-475."""
+    ctx = model.stats.context
+    h = C.c_void_p()
+    ctx.check(_L.load().gsgpc_posterior_cov_lowrank(ctx.handle, model.stats.handle, model.kg.handle,
+                                                    float(model.sigma), int(rank), C.byref(h)))
+    return LowRankCov(h, model, ctx)
+
+
 def posterior_mean_gsgp(stats: SufficientStats, kg: ToeplitzOperator, spec: KernelSpec, scheme, sigma: float,
                         tol: float, maxiter: int = kDefaultMaxIter) -> PosteriorModel:
     """gp.cpp:326-352."""
