@@ -1245,7 +1245,10 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
   if (nvalid <= 0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   if (g.d == 3 && g.W == 4) {
-    const int64_t range = 1024;
+    static const int64_t range = [] {  // rows per warp (GSGPC_K1_RANGE: diagnostics)
+      const char* e = getenv("GSGPC_K1_RANGE");
+      return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
+    }();
     const int64_t warps = ceil_div(nvalid, range);
     static const bool use_dfma = [] {
       const char* e = getenv("GSGPC_K1_DFMA");
