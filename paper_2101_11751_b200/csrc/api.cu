@@ -104,6 +104,13 @@ struct gsgpc_ctx {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   PinnedBuf file_pin[2];         // GSGPDAT1 ingest: host read buffers (reader thread fills one while
                                  // the other is copied to the device)
+  cudaStream_t sort = nullptr;   // slice sort of bucket group j+1 overlaps K1 of group j
+  void ensure_sort_stream() {
+    if (sort) return;
+    int lo = 0, hi = 0;
+    GSGPC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GSGPC_CUDA(cudaStreamCreateWithPriority(&sort, cudaStreamNonBlocking, hi));  // memory-bound: dispatch first
+  }
   Launch L() { return Launch{stream, &launches}; }
   void ensure_copy_stream() {
     if (copy) return;
@@ -471,6 +478,21 @@ gsgpc_stats* new_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme) {
 }
 
 // The precompute pipeline on one device-resident chunk.
+// Bucket groups for overlapping the slice sort (HBM-bound, high-priority sort stream) with
+// K1 (FP64-bound, compute stream).  Buckets are whole cells, so splitting K1 by bucket
+// ranges adds no moment flushes (splitting by row ranges re-flushed every cell per part).
+// Measured: no gain — K1 needs all its resident warps to hide DMMA latency, and sort blocks
+// co-scheduled on its SMs cost more than the overlap saves — so the default is sequential;
+// GSGPC_BUCKET_GROUPS = G > 1 enables the overlap.  Phase timing always runs sequentially.
+static int bucket_groups(gsgpc_ctx* ctx, int64_t nvalid, int nb) {
+  static const int env = [] {
+    const char* e = getenv("GSGPC_BUCKET_GROUPS");
+    return e ? std::max(1, atoi(e)) : 1;  // B200, config 3: 1 → 9.22, 2 → 9.29, 4 → 9.92, 8 → 10.8 ms
+  }();
+  if (ctx->timing || nvalid < (int64_t{1} << 22)) return 1;
+  return std::min(env, nb);
+}
+
 void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, int64_t n, int64_t row0,
                const uint64_t* pw_dev, int probes) {
   const Launch L = ctx->L();
@@ -509,32 +531,28 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   h = pt.begin(1);
   run_bucket_totals(L, bd, n, tcnt.as<int>(), gsum.as<int>(), bbase.as<int64_t>(), sbase.as<int64_t>());
   pt.end(h);
-  // one sync: error row + number of valid rows
-  struct {
-    unsigned long long err;
-    int64_t nvalid, nslices;
-  } hs{};
-  ctx->pin.ensure(64);
-  char* pin = static_cast<char*>(ctx->pin.p);
+  // one sync: error row + bucket row / slice offsets
+  const int64_t NB1 = bd.nb + 1;
+  ctx->pin.ensure(sizeof(int64_t) * (1 + 2 * NB1));
+  int64_t* pin = static_cast<int64_t*>(ctx->pin.p);
   GSGPC_CUDA(cudaMemcpyAsync(pin, err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaMemcpyAsync(pin + 8, bbase.as<int64_t>() + bd.nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaMemcpyAsync(pin + 16, sbase.as<int64_t>() + bd.nb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(pin + 1, bbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaMemcpyAsync(pin + 1 + NB1, sbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
   GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
-  std::memcpy(&hs.err, pin, 8);
-  std::memcpy(&hs.nvalid, pin + 8, 8);
-  std::memcpy(&hs.nslices, pin + 16, 8);
-  if (hs.err != ~0ull) {
-    const int64_t row = static_cast<int64_t>(hs.err >> 2);
-    const int kind = static_cast<int>(hs.err & 3);
+  const unsigned long long herr = static_cast<unsigned long long>(pin[0]);
+  const std::vector<int64_t> hb(pin + 1, pin + 1 + NB1), hsl(pin + 1 + NB1, pin + 1 + 2 * NB1);
+  if (herr != ~0ull) {
+    const int64_t row = static_cast<int64_t>(herr >> 2);
+    const int kind = static_cast<int>(herr & 3);
     const std::string what =
         kind == PT_OUTSIDE ? "interp_weights: point outside grid"
                            : "interp_weights: stencil leaves the grid (point too close to the boundary for the "
                              "requested scheme)";
     throw Error(GSGPC_OUT_OF_GRID, "sufficient_stats: stream row " + std::to_string(row) + ": " + what, row);
   }
-  // commit: yty, scatter, moments
+  // commit: yty, partition, then per bucket group: slice sort (sort stream) → K1 (compute stream)
   run_axpby(L, 1, 1.0, s->yty.as<double>(), 1.0, ychunk.as<double>(), s->yty.as<double>());
-  const int64_t nvalid = hs.nvalid;
+  const int64_t nvalid = hb[bd.nb], nslices = hsl[bd.nb];
   if (nvalid > 0) {
     const size_t es = dtype_size(dtype);
     DBuf& pay = ctx->buf("payload");
@@ -551,22 +569,59 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     DBuf& gcur = ctx->buf("bin_cursor");
     gcur.ensure(sizeof(int) * bd.nb);
     DBuf& scnt = ctx->buf("bin_scnt");
-    scnt.ensure(sizeof(int) * std::max<int64_t>(1, hs.nslices) * (int64_t{1} << bd.bsh));
+    scnt.ensure(sizeof(int) * std::max<int64_t>(1, nslices) * (int64_t{1} << bd.bsh));
     h = pt.begin(2);
     GSGPC_CUDA(cudaMemsetAsync(gcur.p, 0, sizeof(int) * bd.nb, ctx->stream));
     run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), bbase.as<int64_t>(), gcur.as<int>(), rows1.p,
                   cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr);
-    run_slice_sort(L, dtype, bd, g.cells, hs.nslices, rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
-                   sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p, nw ? pw1.as<uint64_t>() : nullptr,
-                   nw, nw ? pws.as<uint64_t>() : nullptr);
-    pt.end(h);
-    h = pt.begin(3);
-    run_moments(L, dtype, pay.p, off.as<int64_t>(), nvalid, g, s->mom.as<double>());
-    if (probes > 0) {
-      run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), nvalid, g, probes,
-                        s->pmom.as<double>());
+    // bucket groups of ~equal rows; group j's K1 overlaps group j+1's slice sort
+    const int G = bucket_groups(ctx, nvalid, bd.nb);
+    std::vector<int> gb(G + 1, bd.nb);
+    gb[0] = 0;
+    for (int j = 1; j < G; ++j) {
+      const int64_t target = nvalid * j / G;
+      gb[j] = static_cast<int>(std::upper_bound(hb.begin(), hb.end(), target) - hb.begin()) - 1;
+      gb[j] = std::max(gb[j], gb[j - 1]);
     }
-    pt.end(h);
+    cudaStream_t ss = ctx->stream;
+    std::vector<cudaEvent_t> evs;
+    struct EvFree {
+      std::vector<cudaEvent_t>* v;
+      ~EvFree() {
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
+      }
+    } evf{&evs};
+    auto record = [&](cudaStream_t st) {
+      cudaEvent_t e;
+      GSGPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      GSGPC_CUDA(cudaEventRecord(e, st));
+      return e;
+    };
+    if (G > 1) {
+      ctx->ensure_sort_stream();
+      ss = ctx->sort;
+      GSGPC_CUDA(cudaStreamWaitEvent(ss, record(ctx->stream), 0));
+    }
+    const Launch LS{ss, &ctx->launches};
+    for (int j = 0; j < G; ++j) {
+      const int b0 = gb[j], b1 = gb[j + 1];
+      if (b1 <= b0) continue;
+      run_slice_sort(LS, dtype, bd, g.cells, b0, b1, hsl[b0], hsl[b1], rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
+                     sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p,
+                     nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr);
+      if (j == 0) pt.end(h);  // (sequential when timing: G = 1)
+      if (G > 1) GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, record(ss), 0));
+      const int hk = pt.begin(3);
+      const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
+      const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
+      run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>());
+      if (probes > 0) {
+        run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
+                          probes, s->pmom.as<double>());
+      }
+      pt.end(hk);
+    }
   }
   s->n += n;
   s->finalized = false;
@@ -634,6 +689,10 @@ void gsgpc_ctx_destroy(gsgpc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->sort) {
+    cudaStreamSynchronize(ctx->sort);
+    cudaStreamDestroy(ctx->sort);
+  }
   ctx->cg.reset();
   ctx->bufs.clear();
   if (ctx->copy) {

@@ -429,9 +429,9 @@ __device__ __forceinline__ int slice_bucket(const int64_t* __restrict__ sbase, i
 
 __global__ void __launch_bounds__(256) k_slice_count(const int* __restrict__ cid1, const int64_t* __restrict__ bbase,
                                                      const int64_t* __restrict__ sbase, int bsh, int nb,
-                                                     int* __restrict__ scnt) {
+                                                     int* __restrict__ scnt, int64_t s0) {
   extern __shared__ int cnt[];
-  const int64_t sl = blockIdx.x;
+  const int64_t sl = s0 + blockIdx.x;
   const int b = slice_bucket(sbase, nb, sl);
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
@@ -457,9 +457,9 @@ __global__ void __launch_bounds__(256) k_slice_count(const int* __restrict__ cid
 // One block per bucket (1024 threads; 2^bsh ≤ 16384 cells → ≤ 16 per thread).
 __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, const int64_t* __restrict__ bbase,
                                                      const int64_t* __restrict__ sbase, int bsh, int nb,
-                                                     int64_t cells, int64_t* __restrict__ off) {
+                                                     int64_t cells, int64_t* __restrict__ off, int b0) {
   __shared__ int64_t wsum[32];
-  const int b = blockIdx.x;
+  const int b = b0 + blockIdx.x;
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
   const int ncell = static_cast<int>(imin64(nbin, cells - c0));
@@ -496,7 +496,9 @@ __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, con
       run += tot[q];
     }
   }
-  if (b == nb - 1 && threadIdx.x == 0) off[cells] = bbase[nb];
+  // boundary entry = the next bucket's first offset (same value): a K1 pass over this bucket
+  // group reads off[c + 1] of its last cell before the next group's scan has run
+  if (threadIdx.x == 0) off[c0 + ncell] = bbase[b + 1];
 }
 
 template <typename T>
@@ -506,10 +508,10 @@ __global__ void __launch_bounds__(256) k_slice_scatter(const Row4<T>* __restrict
                                                        int64_t cells, const int* __restrict__ scnt,
                                                        const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
                                                        const uint64_t* __restrict__ pw1, int nw,
-                                                       uint64_t* __restrict__ pws) {
+                                                       uint64_t* __restrict__ pws, int64_t s0) {
   constexpr int UNR = sizeof(T) == 4 ? 8 : 4;
   extern __shared__ int cur[];
-  const int64_t sl = blockIdx.x;
+  const int64_t sl = s0 + blockIdx.x;
   const int b = slice_bucket(sbase, nb, sl);
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
@@ -603,12 +605,12 @@ constexpr int D3C_STRIDE = 26;
 template <typename T>
 __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restrict__ pay,
                                                         const int64_t* __restrict__ off, int64_t cells,
-                                                        int64_t nvalid, GridDev g,
+                                                        int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
                                                         double* __restrict__ mom, int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
-  const int64_t r0 = warp * range;
+  const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
   double* S = sm[wib];
@@ -625,10 +627,10 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
 #pragma unroll
   for (int a = 0; a < 4; ++a) yacc[a][0] = yacc[a][1] = 0.0;
 
-  int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
+  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = upper_bound_i64(off, cells + 1, p) - 1;
+    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -749,12 +751,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
-                                                            int64_t nvalid, GridDev g, double* __restrict__ mom,
+                                                            int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g, double* __restrict__ mom,
                                                             int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
-  const int64_t r0 = warp * range;
+  const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
   double* S = sm[wib];
@@ -771,10 +773,10 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   for (int t = 0; t < 7; ++t) dx[t][0] = dx[t][1] = 0.0;
   dy[0] = dy[1] = 0.0;
 
-  int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
+  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = upper_bound_i64(off, cells + 1, p) - 1;
+    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -852,7 +854,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 template <int D, int W, typename T>
 __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict__ pay,
                                                      const int64_t* __restrict__ off, int64_t cells,
-                                                     int64_t nvalid, GridDev g,
+                                                     int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
                                                      double* __restrict__ mom, int64_t range) {
   constexpr int E = 2 * W - 1;
   constexpr int QX = D == 1 ? E : (D == 2 ? E * E : E * E * E);
@@ -860,16 +862,16 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   constexpr int Q = QX + QY;
   const int lane = threadIdx.x & 31;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t r0 = warp * range;
+  const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
   double acc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-  int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
+  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = upper_bound_i64(off, cells + 1, p) - 1;
+    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -942,14 +944,14 @@ template <int D, int W, typename T>
 __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict__ pay,
                                                       const uint64_t* __restrict__ pw,
                                                       const int64_t* __restrict__ off, int64_t cells,
-                                                      int64_t nvalid, GridDev g, int probes,
+                                                      int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g, int probes,
                                                       double* __restrict__ pmom /*cells × P × QY*/,
                                                       int64_t range, int pbase) {
   constexpr int QY = D == 1 ? W : (D == 2 ? W * W : W * W * W);
   __shared__ __align__(16) double sm[2][32 * (QY + 1)];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 2 + wib;
-  const int64_t r0 = warp * range;
+  const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
   const int nw = (probes + 63) >> 6;
@@ -960,10 +962,10 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
   double acc[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q) acc[q] = 0.0;
-  int64_t c = upper_bound_i64(off, cells + 1, r0) - 1;
+  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = upper_bound_i64(off, cells + 1, p) - 1;
+    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -1208,22 +1210,24 @@ void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, co
   GSGPC_CUDA(cudaGetLastError());
 }
 
-void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int64_t nslices, const void* rows1,
-                    const int* cid1, const int64_t* bbase, const int64_t* sbase, int* scnt, int64_t* off, void* out,
-                    const uint64_t* pw1, int nw, uint64_t* pws) {
+void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0,
+                    int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
+                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws) {
   const size_t sm = sizeof(int) * (size_t{1} << bd.bsh);
-  if (nslices > 0)
-    k_slice_count<<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt);
-  k_slice_scan<<<static_cast<unsigned>(bd.nb), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off);
-  if (nslices > 0) {
+  const int64_t ns = s1 - s0;
+  if (ns > 0)
+    k_slice_count<<<static_cast<unsigned>(ns), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt, s0);
+  if (b1 > b0)
+    k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0);
+  if (ns > 0) {
     if (dtype == GSGPC_F32)
-      k_slice_scatter<float><<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(
+      k_slice_scatter<float><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
           static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<float>*>(out), pw1, nw, pws);
+          static_cast<Row4<float>*>(out), pw1, nw, pws, s0);
     else
-      k_slice_scatter<double><<<static_cast<unsigned>(nslices), 256, sm, L.s>>>(
+      k_slice_scatter<double><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
           static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<double>*>(out), pw1, nw, pws);
+          static_cast<Row4<double>*>(out), pw1, nw, pws, s0);
   }
   L.count(3);
   GSGPC_CUDA(cudaGetLastError());
@@ -1240,16 +1244,16 @@ int moments_per_cell(int d, int W) {
 }
 
 template <typename T>
-static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t nvalid,
-                           const GridDev& g, double* mom) {
-  if (nvalid <= 0) return;
+static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
+                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom) {
+  if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   if (g.d == 3 && g.W == 4) {
     static const int64_t range = [] {  // rows per warp (GSGPC_K1_RANGE: diagnostics)
       const char* e = getenv("GSGPC_K1_RANGE");
       return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
     }();
-    const int64_t warps = ceil_div(nvalid, range);
+    const int64_t warps = ceil_div(nvalid - row0, range);
     static const bool use_dfma = [] {
       const char* e = getenv("GSGPC_K1_DFMA");
       return e && e[0] == '1';
@@ -1260,50 +1264,51 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
     if (use_dfma) {
-      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     } else if (minb == 8) {
-      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     } else if (minb == 7) {
-      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     } else if (minb == 6) {
-      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     } else if (minb == 5) {
-      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     } else {
-      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);
+      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     }
   } else {
     const int64_t range = 1024;
-    const int64_t warps = ceil_div(nvalid, range);
+    const int64_t warps = ceil_div(nvalid - row0, range);
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
 #define GSGPC_LM(DD, WW)                                                                          \
   if (g.d == DD && g.W == WW) {                                                                 \
-    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, g.cells, nvalid, g, mom, range);   \
+    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);   \
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
   }
 }
 
-void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t nvalid,
-                 const GridDev& g, double* mom) {
-  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, nvalid, g, mom);
-  else launch_moments<double>(L, pay, off, nvalid, g, mom);
-  if (nvalid > 0) L.count();
+void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom) {
+  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom);
+  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom);
+  if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
 
 template <typename T>
 static void launch_probe_moments(const Launch& L, const void* pay, const uint64_t* pw, const int64_t* off,
-                                 int64_t nvalid, const GridDev& g, int probes, double* pmom) {
-  if (nvalid <= 0) return;
+                                 int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
+                                 int probes, double* pmom) {
+  if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   const int64_t range = 1024;
-  const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid, range), 2));
+  const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 2));
   for (int pb = 0; pb < probes; pb += 32) {
 #define GSGPC_PM(DD, WW)                                                                                  \
   if (g.d == DD && g.W == WW) {                                                                         \
-    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, g.cells, nvalid, g, probes, pmom, range, pb); \
+    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, g, probes, pmom, range, pb); \
   }
     GSGPC_PM(1, 2) GSGPC_PM(1, 4) GSGPC_PM(2, 2) GSGPC_PM(2, 4) GSGPC_PM(3, 2) GSGPC_PM(3, 4)
 #undef GSGPC_PM
@@ -1312,9 +1317,10 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
 }
 
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
-                       int64_t nvalid, const GridDev& g, int probes, double* pmom) {
-  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, nvalid, g, probes, pmom);
-  else launch_probe_moments<double>(L, pay, pw, off, nvalid, g, probes, pmom);
+                       int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
+                       double* pmom) {
+  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom);
+  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom);
   GSGPC_CUDA(cudaGetLastError());
 }
 
