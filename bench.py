@@ -7,7 +7,8 @@ One JSON line on rank 0 (contract in the task prompt):
   value   — whole-job precompute throughput, inputs resident in HBM (CUDA events, max over ranks)
   e2e     — same metric through the public API with HOST (pinned) rows: H2D of the rows and
             D2H of W^T y, y^T y, n inside the timed region
-  roofline— K1 (per-cell moments kernel) vs measured HBM and measured FP64 peaks
+  roofline— K1 (per-cell moments kernel) vs its binding peak: the FP64 tensor pipe at d = 3
+            (DMMA peak measured live), HBM otherwise; the HBM view is kept as a sub-object
   cpu_baseline — the oracle restatement of the reference (hash-map accumulation, all
             host threads) on a bounded prefix sample of the same workload
 `--impl reference` times only the reference CPU path (the oracle port: the reference
@@ -281,18 +282,35 @@ def run_ours(args):
         except Exception:  # noqa: BLE001
             traffic = None
     achieved = b_pre / (k1_ms / 1e3) / 1e9
-    roofline = {
-        "bound": "hbm", "kernel": "k_moments_d3c (K1: per-cell polynomial moments)",
-        "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-        "traffic": traffic, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
-        "algorithmic_bytes_per_launch": b_pre,
-        "k1_ms": k1_ms, "phase_ms": ph_ms,
-        "step_achieved_gbs": b_pre / (ms / 1e3) / 1e9 / 1.0,
-        "fp64": {"achieved": flops_pt * n / (k1_ms / 1e3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
-                 "frac": flops_pt * n / (k1_ms / 1e3) / 1e12 / fp64_peak, "flops_per_point": flops_pt,
-                 "peak_source": "measured (gsgpc_diag_fp64_peak DFMA loop, this run)",
-                 "note": "K1 is FP64-bound at d=3: 407 moment FMAs per 16-byte point"},
-    }
+    flops_ach = flops_pt * n / (k1_ms / 1e3) / 1e12
+    hbm = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+           "traffic": traffic, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
+           "algorithmic_bytes_per_launch": b_pre}
+    if cfg.d == 3:
+        # K1 at d = 3 runs its 407 moment MACs per row on the FP64 tensor pipe (DMMA): that pipe,
+        # not HBM, binds it (814 flop per 16-byte row).  MEASURED_PEAKS.json has no FP64 figure
+        # and B200_PROFILING.md none either, so the peak is measured in this run by the
+        # library's DMMA loop (gsgpc_diag_fp64_tensor).
+        dmma_peak = ctx.fp64_tensor_tflops()[0]
+        roofline = {
+            "bound": "tensor", "kernel": "k_moments_d3c_mma (K1: per-cell polynomial moments, FP64 DMMA)",
+            "achieved": flops_ach, "peak": dmma_peak, "unit": "TFLOP/s", "frac": flops_ach / dmma_peak,
+            "traffic": traffic,
+            "peak_source": "measured in this run: gsgpc_diag_fp64_tensor (mma.sync.m8n8k4.f64 loop); "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "flops_per_point": flops_pt, "algorithmic_flops_per_launch": flops_pt * n,
+            "k1_ms": k1_ms, "phase_ms": ph_ms,
+            "hbm": hbm,
+            "fp64_dfma_peak": fp64_peak,
+            "note": "algorithmic flops = one FMA per needed moment (343 + 64 per row); the DMMA tiles execute "
+                    "512 FMAs per row (8 m8n8k4 per 4 rows)",
+        }
+    else:
+        roofline = dict(hbm, kernel="k_moments_lane (K1: per-cell polynomial moments)", k1_ms=k1_ms, phase_ms=ph_ms,
+                        fp64={"achieved": flops_ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                              "frac": flops_ach / fp64_peak, "flops_per_point": flops_pt,
+                              "peak_source": "measured (gsgpc_diag_fp64_peak DFMA loop, this run)"})
+    roofline["step_achieved_gbs"] = b_pre / (ms / 1e3) / 1e9
 
     # factorized CG on the merged statistics: the posterior-mean solve (r̂0 = -K_G W^T y/σ²,
     # eps = tol²·yᵀy, gp.cpp:326-352) timed over its iteration loop (loop_seconds, as the

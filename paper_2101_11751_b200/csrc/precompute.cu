@@ -575,7 +575,9 @@ __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double
       double uu = __dsub_rn(x, g.mn[k]) * g.isp[k];
       const double rr = rint(uu);
       const double dd = fabs(uu - rr);
-      const double e = 1e-12 + fabs(uu) * 3.552713678800501e-15;
+      // sorted rows are in-grid (0 ≤ u ≤ size − 1): the per-row rounding bound
+      // 1e-12 + |u|·2^-48 is at most its value at u = size, a loop invariant
+      const double e = 1e-12 + static_cast<double>(g.sz[k]) * 3.552713678800501e-15;
       if (dd >= 1e-9 - e && dd <= 1e-9 + e) {
         int64_t i0;
         stencil_dim(x, g.mn[k], g.sp[k], g.sz[k], i0, t[k]);
@@ -629,6 +631,9 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
 
   int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
+  // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
+  // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
+  Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
     if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
@@ -636,10 +641,11 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
     const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
+      const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
       {
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
-        if (v) row_t<T>(g, pay[b + lane], t, y);
+        if (v) row_t<T>(g, cur_row, t, y);
         double* P = S + lane * D3C_STRIDE;
         double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
 #pragma unroll
@@ -775,6 +781,9 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 
   int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
+  // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
+  // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
+  Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
     if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
     const int64_t cs = off[c], ce = off[c + 1];
@@ -782,10 +791,11 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
     const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
+      const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
       {
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
-        if (v) row_t<T>(g, pay[b + lane], t, y);
+        if (v) row_t<T>(g, cur_row, t, y);
         double* P = S + lane * D3C_STRIDE;
         double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
 #pragma unroll
@@ -812,13 +822,16 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
         const double2 p23 = *reinterpret_cast<const double2*>(P + 10);
         const double2 p45 = *reinterpret_cast<const double2*>(P + 12);
         const double p6 = P[14];
-        const double bt[7] = {t2n * p01.x, t2n * p01.y, t2n * p23.x, t2n * p23.y,
+        // t1^0 = 1 (0 on an empty lane, where t2n = 0 too): no multiply for tile 0
+        const double bt[7] = {t2n, t2n * p01.y, t2n * p23.x, t2n * p23.y,
                               t2n * p45.x, t2n * p45.y, t2n * p6};
+        (void)p01.x;
 #pragma unroll
         for (int tt = 0; tt < 7; ++tt) dmma(dx[tt][0], dx[tt][1], ax, bt[tt]);
         dmma(dy[0], dy[1], ay, by);
       }
       __syncwarp();
+      cur_row = next_row;
     }
     // flush this lane's fragment entries
     double* M = mom + c * D3C_Q;
@@ -1260,7 +1273,7 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     }();
     static const int minb = [] {
       const char* e = getenv("GSGPC_K1_MINB");
-      return e ? atoi(e) : 6;  // resident blocks/SM; B200: 4 → 6.39 ms, 5 → 5.76, 6 → 5.52 (config 3)
+      return e ? atoi(e) : 5;  // resident blocks/SM (B200, config 3, row prefetch): 5 → 5.36, 6 → 5.39, 7 → 5.45 ms
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
     if (use_dfma) {
