@@ -167,7 +167,18 @@ struct alignas(sizeof(T) * 4) Row4 {
 };
 
 constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threads × SORT_UNR × 16
-constexpr int PART_NT = 1024;     // partition: one 1024-thread block per SM
+// Build-time knobs (B200, config 3, partition + slice sort = 2.20 ms with the defaults):
+// 512-thread partition blocks ×2 per SM 2.32 ms, slice scatter at 4 blocks/SM 2.31 ms.
+#ifndef PART_NT_DEF
+#define PART_NT_DEF 1024
+#endif
+#ifndef PART_MINB
+#define PART_MINB 1
+#endif
+#ifndef SS_MINB
+#define SS_MINB 3
+#endif
+constexpr int PART_NT = PART_NT_DEF;  // partition: PART_MINB blocks of PART_NT threads per SM
 constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints
 
 template <typename T, bool PACKED, int D>
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ 
 // ran at ~1.1 TB/s whatever the DRAM traffic: the stores' address spread, not the bytes,
 // was the limit.
 template <typename T, bool PACKED, int RPT>
-__global__ void __launch_bounds__(PART_NT, 1) k_partition(PointsDev pts, int64_t n, int d,
+__global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts, int64_t n, int d,
                                                           const int* __restrict__ cellid, int bsh, int nb,
                                                           const int64_t* __restrict__ bbase, int* __restrict__ gcur,
                                                           Row4<T>* __restrict__ rows1, int* __restrict__ cid1,
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(PART_NT, 1) k_partition(PointsDev pts, int64_t
     if (lane == 31) wsum[w] = incl;
     __syncthreads();
     if (w == 0) {
-      int x = wsum[lane];
+      int x = lane < PART_NT / 32 ? wsum[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -502,7 +513,7 @@ __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, con
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
+__global__ void __launch_bounds__(256, SS_MINB) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
                                                        const int64_t* __restrict__ bbase,
                                                        const int64_t* __restrict__ sbase, int bsh, int nb,
                                                        int64_t cells, const int* __restrict__ scnt,
@@ -1198,7 +1209,7 @@ template <typename T>
 static void launch_partition(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
                              const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
                              const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk) {
-  const size_t budget = 200 * 1024 - 2 * sizeof(int) * bd.nb;
+  const size_t budget = 200 * 1024 / PART_MINB - 2 * sizeof(int) * bd.nb;
   const size_t per_rpt = PART_NT * (sizeof(Row4<T>) + sizeof(int));
   if (budget >= 8 * per_rpt)
     launch_partition_r<T, 8>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
@@ -1216,7 +1227,7 @@ void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, co
   int dev = 0, sms = 148;
   GSGPC_CUDA(cudaGetDevice(&dev));
   GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, PART_NT), sms)));
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, PART_NT), sms * PART_MINB)));
   if (dtype == GSGPC_F32) launch_partition<float>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
   else launch_partition<double>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
   L.count();
