@@ -144,7 +144,7 @@ struct gsgpc_stats {
   // seeded Rademacher probes (gsgpc_stats_enable_probes): one generator per probe
   bool probe_seeded = false;
   uint64_t probe_seed = 0;
-  std::vector<std::mt19937_64> gens;
+  DBuf rng;  // probe_seeded: per probe the MT19937-64 state (312 words) + index, on the device
   int64_t fin_count() const { return static_cast<int64_t>(S_min) * g.m + g.m + static_cast<int64_t>(probes) * g.m + 2; }
   double* stencil() const { return fin.as<double>(); }
   double* wty() const { return fin.as<double>() + static_cast<int64_t>(S_min) * g.m; }
@@ -627,31 +627,22 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   s->finalized = false;
 }
 
-// Draw the next `rows` values of every probe stream and pack them (bit p of word i = probe p
-// is +1 at row i), then upload to the "probe_stage" device buffer.
+// Draw the next `rows` values of every probe stream on the device (probe_rng.cu) and pack
+// them into the "probe_stage" buffer (bit p of word i = probe p is +1 at row i).
 void gen_probe_words(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t rows) {
-  const int P = s->probes;
-  std::vector<uint64_t> words(rows, 0ull);
-  std::vector<std::vector<uint8_t>> bits(P);
-  auto work = [&](int p) {
-    bits[p].assign(rows, 0);
-    std::mt19937_64& g = s->gens[p];
-    for (int64_t i = 0; i < rows; ++i) bits[p][i] = static_cast<uint8_t>(g() & 1ull);
-  };
-  const int nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), static_cast<unsigned>(P)));
-  for (int p0 = 0; p0 < P; p0 += nt) {
-    std::vector<std::thread> th;
-    for (int p = p0; p < std::min(P, p0 + nt); ++p) th.emplace_back(work, p);
-    for (auto& t : th) t.join();
-  }
-  for (int p = 0; p < P; ++p) {
-    const uint64_t bit = 1ull << p;
-    const uint8_t* b = bits[p].data();
-    for (int64_t i = 0; i < rows; ++i) words[i] |= b[i] ? bit : 0ull;
-  }
   DBuf& st = ctx->buf("probe_stage");
   st.ensure(sizeof(uint64_t) * rows);
-  GSGPC_CUDA(cudaMemcpyAsync(st.p, words.data(), sizeof(uint64_t) * rows, cudaMemcpyHostToDevice, ctx->stream));
+  DBuf& planes = ctx->buf("probe_planes");
+  planes.ensure(static_cast<size_t>(s->probes) * std::min(rows, probe_rng_slab()));
+  run_probe_rng(ctx->L(), s->rng.as<uint64_t>(), s->probes, rows, planes.as<uint8_t>(), st.as<uint64_t>());
+}
+
+// initial generator states of rademacher_probe(·, seed, p), p < probes
+void seed_probe_streams(gsgpc_ctx* ctx, gsgpc_stats* s) {
+  std::vector<uint64_t> h(static_cast<size_t>(s->probes) * 313);
+  for (int p = 0; p < s->probes; ++p) mt_seed_state(s->probe_seed, static_cast<uint64_t>(p), h.data() + p * 313);
+  s->rng.ensure(sizeof(uint64_t) * h.size());
+  GSGPC_CUDA(cudaMemcpyAsync(s->rng.p, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
   GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -835,8 +826,13 @@ struct StatsSnapshot {
   gsgpc_stats* s;
   bool active = false;
   int64_t n_before = 0;
-  std::vector<std::mt19937_64> gens;
-  StatsSnapshot(gsgpc_ctx* c, gsgpc_stats* st, bool take) : ctx(c), s(st), active(take), n_before(st->n), gens(st->gens) {
+  StatsSnapshot(gsgpc_ctx* c, gsgpc_stats* st, bool take) : ctx(c), s(st), active(take), n_before(st->n) {
+    if (s->probe_seeded) {  // probe stream positions (restored on any failure)
+      DBuf& br = ctx->buf("bk_rng");
+      br.ensure(sizeof(uint64_t) * s->probes * 313);
+      GSGPC_CUDA(cudaMemcpyAsync(br.p, s->rng.p, sizeof(uint64_t) * s->probes * 313, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+    }
     if (!active) return;
     DBuf& bm = ctx->buf("bk_mom");
     bm.ensure(sizeof(double) * s->g.cells * s->Q + 8);
@@ -853,7 +849,10 @@ struct StatsSnapshot {
     }
   }
   void restore() {
-    s->gens = gens;
+    if (s->probe_seeded) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaMemcpy(s->rng.p, ctx->buf("bk_rng").p, sizeof(uint64_t) * s->probes * 313, cudaMemcpyDeviceToDevice);
+    }
     if (!active) return;
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
@@ -1069,14 +1068,7 @@ gsgpc_status gsgpc_stats_enable_probes(gsgpc_ctx* ctx, gsgpc_stats* s, int probe
     s->probes = probes;
     s->probe_seeded = true;
     s->probe_seed = seed;
-    s->gens.clear();
-    for (int p = 0; p < probes; ++p) {
-      // rademacher_probe (gp.cpp:16-25)
-      std::seed_seq seq{static_cast<std::uint32_t>(seed), static_cast<std::uint32_t>(seed >> 32),
-                        static_cast<std::uint32_t>(static_cast<uint64_t>(p)),
-                        static_cast<std::uint32_t>(static_cast<uint64_t>(p) >> 32)};
-      s->gens.emplace_back(seq);
-    }
+    seed_probe_streams(ctx, s);  // rademacher_probe (gp.cpp:16-25) streams, generated on the device
     s->pmom.ensure(sizeof(double) * s->g.cells * probes * s->QY);
     GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * probes * s->QY, ctx->stream));
   });
@@ -1093,6 +1085,7 @@ gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* s) {
     s->n = 0;
     s->finalized = false;
     s->reduced = false;
+    if (s->probe_seeded) seed_probe_streams(ctx, s);  // a fresh pass restarts the probe streams
   });
 }
 

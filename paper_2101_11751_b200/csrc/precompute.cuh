@@ -152,4 +152,11 @@ void cov_gather(const Launch& L, int64_t ni, int64_t nh, int64_t m, int cap, con
 void cov_sub_abt(const Launch& L, int n, int64_t m, const double* A, const double* B, double* C);
 void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P);
 
+// ---- probe_rng.cu: rademacher_probe streams (std::mt19937_64 per probe) on the device
+void mt_seed_state(uint64_t seed, uint64_t p, uint64_t* st /*313*/);
+int64_t probe_rng_slab();
+// next `rows` draws of every probe: states P × 313 (device), planes ≥ P × slab bytes scratch,
+// words[rows] (bit p = probe p is +1)
+void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words);
+
 }  // namespace gsgpc

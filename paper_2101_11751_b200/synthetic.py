@@ -43,7 +43,8 @@ CONFIGS = {
     # — at 1e-6 the factorized CG needs > 5000 iterations on this system.
     3: Config("3d-radar-like", 3, 120_000_000, (80, 80, 20), (0.03, 0.03, 0.1), 0.01, 1.0, "f32", tol=0.01),
     4: Config("2d-sweep", 2, 1_000_000, (1024, 1024), (0.05, 0.05), 1.0, 1.0, "f32"),
-    5: Config("3d-loglik", 3, 50_000_000, (64, 64, 64), (0.1, 0.1, 0.1), 0.01, 1.0, "f64"),
+    # config 5: same tolerance choice (at 1e-6 the data-fit solve needs > 5000 iterations)
+    5: Config("3d-loglik", 3, 50_000_000, (64, 64, 64), (0.1, 0.1, 0.1), 0.01, 1.0, "f64", tol=0.01),
 }
 
 
