@@ -46,59 +46,79 @@ __device__ __forceinline__ uint64_t mt_mix(uint64_t hi_word, uint64_t lo_word, u
   return far ^ (x >> 1) ^ ((x & 1ull) ? MT_A : 0ull);
 }
 
-// One twist of the warp-resident state (shared memory), lanes 0..31.
-__device__ __forceinline__ void mt_twist(uint64_t* mt, int lane) {
-  for (int base = 0; base < MT_N - MT_M; base += 32) {  // i < 156: old words only
-    const int i = base + lane;
-    uint64_t v = 0;
-    if (i < MT_N - MT_M) v = mt_mix(mt[i], mt[i + 1], mt[i + MT_M]);
-    __syncwarp();
-    if (i < MT_N - MT_M) mt[i] = v;
-    __syncwarp();
-  }
-  for (int base = MT_N - MT_M; base < MT_N - 1; base += 32) {  // 156 ≤ i < 311: new word i − 156
-    const int i = base + lane;
-    uint64_t v = 0;
-    if (i < MT_N - 1) v = mt_mix(mt[i], mt[i + 1], mt[i - (MT_N - MT_M)]);
-    __syncwarp();
-    if (i < MT_N - 1) mt[i] = v;
-    __syncwarp();
-  }
-  if (lane == 0) mt[MT_N - 1] = mt_mix(mt[MT_N - 1], mt[0], mt[MT_M - 1]);
-  __syncwarp();
+// Bit 0 of the tempered output (the only bit rademacher_probe reads).  Expanding the four
+// tempering steps (y ^= (y>>29)&0x55…; y ^= (y<<17)&0x71D6…; y ^= (y<<37)&0xFFF7…; y ^= y>>43):
+// bit 0 = y0 ^ y29 ^ (bit 43 of step 3) = y0 ^ y29 ^ y43 ^ y26 ^ y55 ^ y6 ^ y35 — the parity
+// of y & 0x0080080824000041 (checked against the full tempering on random words).
+__device__ __forceinline__ unsigned mt_temper_bit0(uint64_t y) {
+  return static_cast<unsigned>(__popcll(y & 0x0080080824000041ull)) & 1u;
 }
 
-__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
-  y ^= (y >> 29) & 0x5555555555555555ull;
-  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
-  y ^= (y << 37) & 0xFFF7EEE000000000ull;
-  y ^= y >> 43;
-  return y;
+constexpr int MT_R = (MT_N + 31) / 32;  // 10 registers per lane: word 32 r + lane
+
+// One twist of the register-resident state R[r] = mt[32 r + lane].  Words are produced in
+// increasing index order, so each step still reads the old words above it (i + 1, i + m)
+// and, for i ≥ n − m, the new words i − (n − m) below it — the sequential recurrence.
+// Shuffles run on all lanes; the lane's own word is selected afterwards.
+__device__ __forceinline__ void mt_twist_reg(uint64_t (&R)[MT_R], int lane) {
+  const unsigned FULL = 0xffffffffu;
+#pragma unroll
+  for (int r = 0; r < MT_R; ++r) {
+    // mt[i + 1]: lane + 1 of register r, or lane 0 of register r + 1 for the last lane
+    const uint64_t up = __shfl_down_sync(FULL, R[r], 1);
+    const uint64_t nx = r + 1 < MT_R ? __shfl_sync(FULL, R[r + 1 < MT_R ? r + 1 : r], 0) : 0ull;
+    const uint64_t next = lane == 31 ? nx : up;
+    const int i = 32 * r + lane;
+    uint64_t v = R[r];
+    if (r <= 4) {
+      // i < 156: mt[i + 156] (old) = register r + 4 of lane + 28, or register r + 5 of lane − 4
+      const uint64_t f4 = __shfl_sync(FULL, R[r + 4], (lane + 28) & 31);
+      const uint64_t f5 = __shfl_sync(FULL, R[r + 5 < MT_R ? r + 5 : r], (lane + 28) & 31);
+      if (i < MT_N - MT_M) v = mt_mix(R[r], next, lane < 4 ? f4 : f5);
+    }
+    if (r >= 4) {
+      // 156 ≤ i < 311: mt[i − 156] (new) = register r − 5 of lane + 4, or register r − 4 of lane − 28
+      const uint64_t b5 = __shfl_sync(FULL, R[r >= 5 ? r - 5 : r], (lane + 4) & 31);
+      const uint64_t b4 = __shfl_sync(FULL, R[r - 4], (lane + 4) & 31);
+      if (i >= MT_N - MT_M && i < MT_N - 1) v = mt_mix(R[r], next, lane < 28 ? b5 : b4);
+    }
+    R[r] = v;
+  }
+  // i = 311 (register 9, lane 23): mix(old mt[311], new mt[0], new mt[155])
+  const uint64_t m0 = __shfl_sync(FULL, R[0], 0);
+  const uint64_t m155 = __shfl_sync(FULL, R[4], 27);
+  if (lane == (MT_N - 1) % 32) R[MT_R - 1] = mt_mix(R[MT_R - 1], m0, m155);
 }
 
 // One warp per probe: `rows` draws → bit 0 into planes[p][0, rows).
 __global__ void __launch_bounds__(32) k_probe_rng(uint64_t* __restrict__ states, int64_t rows,
                                                   uint8_t* __restrict__ planes) {
-  __shared__ uint64_t mt[MT_N];
   const int p = blockIdx.x, lane = threadIdx.x;
   uint64_t* st = states + static_cast<int64_t>(p) * (MT_N + 1);
-  for (int i = lane; i < MT_N; i += 32) mt[i] = st[i];
+  uint64_t R[MT_R];
+#pragma unroll
+  for (int r = 0; r < MT_R; ++r) R[r] = 32 * r + lane < MT_N ? st[32 * r + lane] : 0ull;
   int idx = static_cast<int>(st[MT_N]);
-  __syncwarp();
   uint8_t* out = planes + static_cast<int64_t>(p) * rows;
   int64_t done = 0;
   while (done < rows) {
     if (idx == MT_N) {
-      mt_twist(mt, lane);
+      mt_twist_reg(R, lane);
       idx = 0;
     }
     const int k = static_cast<int>(imin64(MT_N - idx, rows - done));
-    for (int j = lane; j < k; j += 32) out[done + j] = static_cast<uint8_t>(mt_temper(mt[idx + j]) & 1ull);
+    // draws idx .. idx + k − 1 of this block → rows done .. done + k − 1
+#pragma unroll
+    for (int r = 0; r < MT_R; ++r) {
+      const int j = 32 * r + lane - idx;
+      if (j >= 0 && j < k) out[done + j] = static_cast<uint8_t>(mt_temper_bit0(R[r]));
+    }
     idx += k;
     done += k;
   }
-  __syncwarp();
-  for (int i = lane; i < MT_N; i += 32) st[i] = mt[i];
+#pragma unroll
+  for (int r = 0; r < MT_R; ++r)
+    if (32 * r + lane < MT_N) st[32 * r + lane] = R[r];
   if (lane == 0) st[MT_N] = static_cast<uint64_t>(idx);
 }
 
