@@ -74,18 +74,18 @@ void upload_poly_tables(int W, cudaStream_t s) {
 // exactly (i0 == 0 || i0 + 2 >= size) && t ∉ {0, 1} for cubic and never for linear.
 // Rows whose |u - round(u)| lies within a few ulp of the 1e-9 snap tolerance take the
 // exact-division path.
+// Exact (division) path for the rare rows near the snap tolerance; coordinates by value and
+// (status, cell) packed in the return value so the never-taken call forces nothing to the stack.
 template <int D>
-__device__ __noinline__ int classify_exact(const GridDev& g, const double* x, int& cell) {
+__device__ __noinline__ long long classify_exact(const GridDev& g, double x0, double x1, double x2) {
   int64_t i0[GSGPC_MAX_DIM];
   double t[GSGPC_MAX_DIM];
-  double xx[GSGPC_MAX_DIM] = {0.0, 0.0, 0.0};
-  for (int k = 0; k < D; ++k) xx[k] = x[k];
+  double xx[GSGPC_MAX_DIM] = {x0, x1, x2};
   int64_t c = 0;
   GridDev gd = g;
   gd.d = D;
   const int st = classify(gd, xx, i0, t, c);
-  cell = static_cast<int>(c);
-  return st;
+  return (static_cast<long long>(st) << 32) | static_cast<unsigned>(c);
 }
 
 template <int D>
@@ -98,10 +98,14 @@ __device__ __forceinline__ int classify_d(const GridDev& g, const double* x, int
     const double r = rint(uu);
     const double dd = fabs(uu - r);
     const double e = 1e-12 + fabs(uu) * 3.552713678800501e-15;
-    band = band || (dd >= 1e-9 - e && dd <= 1e-9 + e);
+    band = band || fabs(dd - 1e-9) <= e;  // dd within e of the snap tolerance
     u[k] = dd < 1e-9 ? r : uu;
   }
-  if (band) return classify_exact<D>(g, x, cell);
+  if (band) {
+    const long long pk = classify_exact<D>(g, x[0], D > 1 ? x[1] : 0.0, D > 2 ? x[2] : 0.0);
+    cell = static_cast<int>(static_cast<unsigned>(pk));
+    return static_cast<int>(pk >> 32);
+  }
   bool outside = false;
 #pragma unroll
   for (int k = 0; k < D; ++k) outside = outside || u[k] < 0.0 || u[k] > static_cast<double>(g.sz[k] - 1);
@@ -111,7 +115,7 @@ __device__ __forceinline__ int classify_d(const GridDev& g, const double* x, int
   for (int k = 0; k < D; ++k) {
     const bool isnan_k = u[k] != u[k];
     const int sz = static_cast<int>(g.sz[k]);
-    int i0 = isnan_k ? 0 : static_cast<int>(floor(u[k]));
+    int i0 = isnan_k ? 0 : __double2int_rd(u[k]);
     i0 = min(i0, sz - 2);
     const double t = u[k] - static_cast<double>(i0);
     const bool leaves = g.W == 4 && (i0 == 0 || i0 + 2 >= sz) && t != 0.0 && t != 1.0;
