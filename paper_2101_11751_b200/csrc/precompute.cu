@@ -579,6 +579,17 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t* __restrict__ a
   return lo;
 }
 
+// Cell of row p for a warp walking sorted rows forward from cell c: step over a few
+// (empty) cells linearly — consecutive offsets share cache lines — and binary-search only
+// after a long gap.  A binary search per cell boundary cost ~20 dependent loads per cell,
+// which dominated sparse grids (1–100 rows per cell).
+__device__ __forceinline__ int64_t next_cell(const int64_t* __restrict__ off, int64_t c, int64_t p, int64_t c_lo,
+                                             int64_t cells) {
+  for (int k = 0; k < 8 && off[c + 1] <= p; ++k) ++c;
+  if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
+  return c;
+}
+
 // Recompute (t_0..t_{d-1}) of a sorted (valid) row: same snap decision as classify_d, t to
 // within a few ulp of the reference's (exact division in the rare snap band).
 template <typename T>
@@ -650,7 +661,7 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
-    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
+    c = next_cell(off, c, p, c_lo, cells);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -800,7 +811,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
-    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
+    c = next_cell(off, c, p, c_lo, cells);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -875,6 +886,103 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   }
 }
 
+// ------------------------------------------------------------------ K1, d = 2 cubic, FP64 MMA
+// M[a][b] = Σ t0^a t1^b (a, b ≤ 6), Y[a][b] = Σ y t0^a t1^b (a, b ≤ 3), 2 mma.sync.m8n8k4.f64
+// per 4 rows:
+//   X tile: A rows a = 0..6 → t0^a, row 7 → y;  B[k][n] = t1^n (n < 7) → M and Y[0][n];
+//   Y tile: A rows r < 3 → y t0^(r+1);          B[k][n] = t1^n (n < 4) → Y[1..3][n].
+// Rows are staged 32 at a time regardless of cell boundaries, and each cell segment inside the
+// batch runs masked steps, so sparse cells (1–100 rows, config 4) cost one step and one flush of
+// the lane's fragment entries — no cross-lane reduction (the lane kernel's 65 warp sums per
+// cell and 248 registers made it latency-bound).
+constexpr int D2C_STRIDE = 16;  // t0^0..6, y, t1^0..6, pad
+constexpr int D2C_QX = 49, D2C_Q = 49 + 16;
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay,
+                                                         const int64_t* __restrict__ off, int64_t cells,
+                                                         int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
+                                                         double* __restrict__ mom, int64_t range) {
+  __shared__ __align__(16) double sm[4][32 * D2C_STRIDE];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
+  const int64_t r0 = row0 + warp * range;
+  if (r0 >= nvalid) return;
+  const int64_t rend = min(r0 + range, nvalid);
+  double* S = sm[wib];
+  const int r = lane >> 2, kq = lane & 3, cb = 2 * (lane & 3);
+  double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
+  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
+  bool started_here = off[c] >= r0;  // the current cell's first row lies in this warp's range
+  for (int64_t b = r0; b < rend; b += 32) {
+    const int64_t bend = min(b + 32, rend);
+    {
+      double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
+      const bool v = b + lane < bend;
+      if (v) row_t<T>(g, pay[b + lane], t, y);
+      double* P = S + lane * D2C_STRIDE;
+      double q0 = v ? 1.0 : 0.0, q1 = q0;
+#pragma unroll
+      for (int e = 0; e < 7; ++e) {
+        P[e] = q0;
+        P[8 + e] = q1;
+        q0 *= t[0];
+        q1 *= t[1];
+      }
+      P[7] = v ? y : 0.0;
+    }
+    __syncwarp();
+    int64_t s0 = b;
+    while (s0 < bend) {
+      c = next_cell(off, c, s0, c_lo, cells);
+      if (off[c] == s0) started_here = true;
+      const int64_t ce = off[c + 1];
+      const int64_t s1 = min(ce, bend);
+      const int steps = static_cast<int>((s1 - s0 + 3) >> 2);
+      for (int st = 0; st < steps; ++st) {
+        const int64_t row = s0 + 4 * st + kq;
+        const bool v = row < s1;
+        const double* P = S + (row - b) * D2C_STRIDE;
+        const double ax = v ? (r < 7 ? P[r] : P[7]) : 0.0;
+        const double bx = v && r < 7 ? P[8 + r] : 0.0;
+        const double ay = v && r < 3 ? P[7] * P[r + 1] : 0.0;
+        const double by = v && r < 4 ? P[8 + r] : 0.0;
+        dmma(dx0, dx1, ax, bx);
+        dmma(dy0, dy1, ay, by);
+      }
+      if (ce <= bend) {  // the cell ends in this batch: flush this lane's fragment entries
+        const bool owned = started_here && ce <= rend;
+        double* M = mom + c * D2C_Q;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int col = cb + i;
+          const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
+          if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx, owned);
+          else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx, owned);  // Y[0][col]
+          if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy, owned);
+        }
+        dx0 = dx1 = dy0 = dy1 = 0.0;
+        started_here = false;
+      }
+      s0 = s1;
+    }
+    __syncwarp();
+  }
+  // a cell still open at the end of the range continues in the next warp's range: add this
+  // range's part atomically
+  if (off[c + 1] > rend) {
+    double* M = mom + c * D2C_Q;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int col = cb + i;
+      const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
+      if (col < 7 && r < 7) atomicAdd(M + r * 7 + col, vx);
+      else if (r == 7 && col < 4) atomicAdd(M + D2C_QX + col, vx);
+      if (r < 3 && col < 4) atomicAdd(M + D2C_QX + (r + 1) * 4 + col, vy);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K1, generic (lane per point)
 // d ≤ 2 (any scheme) and d = 3 linear: every lane accumulates all QX + QY moments of its
 // own points in registers; a segment flush warp-reduces them (butterfly) and the lanes
@@ -899,7 +1007,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
+    c = next_cell(off, c, p, c_lo, cells);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -993,7 +1101,7 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
   int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
   int64_t p = r0;
   while (p < rend) {
-    if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
+    c = next_cell(off, c, p, c_lo, cells);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     const bool owned = cs >= r0 && ce <= rend;
@@ -1304,6 +1412,10 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     } else {
       k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
     }
+  } else if (g.d == 2 && g.W == 4) {
+    const int64_t range = 512;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
+    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid - row0, range);
