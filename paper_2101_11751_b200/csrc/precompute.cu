@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 // batch runs masked steps, so sparse cells (1–100 rows, config 4) cost one step and one flush of
 // the lane's fragment entries — no cross-lane reduction (the lane kernel's 65 warp sums per
 // cell and 248 registers made it latency-bound).
-constexpr int D2C_STRIDE = 16;  // t0^0..6, y, t1^0..6, pad
+constexpr int D2C_STRIDE = 17;  // t0^0..6, y, t1^0..6, pad (odd: lanes spread over the banks)
 constexpr int D2C_QX = 49, D2C_Q = 49 + 16;
 
 template <typename T>
