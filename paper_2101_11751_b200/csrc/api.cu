@@ -521,8 +521,9 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   DBuf& ychunk = ctx->buf("yty_chunk");
   ychunk.ensure(sizeof(double));
 
+  // err: reset once per public call (stats_add / add_file), checked by the caller after the
+  // whole batch — see BinGate (precompute.cu)
   int h = pt.begin(0);
-  GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
   GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
   run_classify(L, dtype, P, n, row0, g, bd, tcnt.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
                cellid.as<int>());
@@ -531,29 +532,22 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   h = pt.begin(1);
   run_bucket_totals(L, bd, n, tcnt.as<int>(), gsum.as<int>(), bbase.as<int64_t>(), sbase.as<int64_t>());
   pt.end(h);
-  // one sync: error row + bucket row / slice offsets
-  const int64_t NB1 = bd.nb + 1;
-  ctx->pin.ensure(sizeof(int64_t) * (1 + 2 * NB1));
-  int64_t* pin = static_cast<int64_t*>(ctx->pin.p);
-  GSGPC_CUDA(cudaMemcpyAsync(pin, err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaMemcpyAsync(pin + 1, bbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaMemcpyAsync(pin + 1 + NB1, sbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
-  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
-  const unsigned long long herr = static_cast<unsigned long long>(pin[0]);
-  const std::vector<int64_t> hb(pin + 1, pin + 1 + NB1), hsl(pin + 1 + NB1, pin + 1 + 2 * NB1);
-  if (herr != ~0ull) {
-    const int64_t row = static_cast<int64_t>(herr >> 2);
-    const int kind = static_cast<int>(herr & 3);
-    const std::string what =
-        kind == PT_OUTSIDE ? "interp_weights: point outside grid"
-                           : "interp_weights: stencil leaves the grid (point too close to the boundary for the "
-                             "requested scheme)";
-    throw Error(GSGPC_OUT_OF_GRID, "sufficient_stats: stream row " + std::to_string(row) + ": " + what, row);
+  const unsigned long long* errp = err.as<unsigned long long>();
+  run_commit_add(L, errp, ychunk.as<double>(), s->yty.as<double>());
+  // binning → moments without a host round trip: sizes are upper bounds (every row valid),
+  // the kernels read the true counts from bbase / sbase
+  const int64_t nvalid = n, nslices = bin_slices_max(n, bd);
+  const int G = bucket_groups(ctx, nvalid, bd.nb);
+  std::vector<int64_t> hb, hsl;
+  if (G > 1) {  // the optional overlap needs the bucket offsets on the host
+    const int64_t NB1 = bd.nb + 1;
+    hb.resize(NB1);
+    hsl.resize(NB1);
+    GSGPC_CUDA(cudaMemcpyAsync(hb.data(), bbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
+    GSGPC_CUDA(cudaMemcpyAsync(hsl.data(), sbase.p, sizeof(int64_t) * NB1, cudaMemcpyDeviceToHost, ctx->stream));
+    GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
   }
-  // commit: yty, partition, then per bucket group: slice sort (sort stream) → K1 (compute stream)
-  run_axpby(L, 1, 1.0, s->yty.as<double>(), 1.0, ychunk.as<double>(), s->yty.as<double>());
-  const int64_t nvalid = hb[bd.nb], nslices = hsl[bd.nb];
-  if (nvalid > 0) {
+  {
     const size_t es = dtype_size(dtype);
     DBuf& pay = ctx->buf("payload");
     pay.ensure(es * 4 * nvalid);
@@ -573,58 +567,92 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     h = pt.begin(2);
     GSGPC_CUDA(cudaMemsetAsync(gcur.p, 0, sizeof(int) * bd.nb, ctx->stream));
     run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), bbase.as<int64_t>(), gcur.as<int>(), rows1.p,
-                  cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr);
-    // bucket groups of ~equal rows; group j's K1 overlaps group j+1's slice sort
-    const int G = bucket_groups(ctx, nvalid, bd.nb);
-    std::vector<int> gb(G + 1, bd.nb);
-    gb[0] = 0;
-    for (int j = 1; j < G; ++j) {
-      const int64_t target = nvalid * j / G;
-      gb[j] = static_cast<int>(std::upper_bound(hb.begin(), hb.end(), target) - hb.begin()) - 1;
-      gb[j] = std::max(gb[j], gb[j - 1]);
-    }
-    cudaStream_t ss = ctx->stream;
-    std::vector<cudaEvent_t> evs;
-    struct EvFree {
-      std::vector<cudaEvent_t>* v;
-      ~EvFree() {
-        for (cudaEvent_t e : *v) cudaEventDestroy(e);
-      }
-    } evf{&evs};
-    auto record = [&](cudaStream_t st) {
-      cudaEvent_t e;
-      GSGPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      evs.push_back(e);
-      GSGPC_CUDA(cudaEventRecord(e, st));
-      return e;
-    };
-    if (G > 1) {
-      ctx->ensure_sort_stream();
-      ss = ctx->sort;
-      GSGPC_CUDA(cudaStreamWaitEvent(ss, record(ctx->stream), 0));
-    }
-    const Launch LS{ss, &ctx->launches};
-    for (int j = 0; j < G; ++j) {
-      const int b0 = gb[j], b1 = gb[j + 1];
-      if (b1 <= b0) continue;
-      run_slice_sort(LS, dtype, bd, g.cells, b0, b1, hsl[b0], hsl[b1], rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
+                  cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr, errp);
+    const int64_t* rows_end = bbase.as<int64_t>() + bd.nb;
+    if (G == 1) {
+      run_slice_sort(L, dtype, bd, g.cells, 0, bd.nb, 0, nslices, rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
                      sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p,
-                     nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr);
-      if (j == 0) pt.end(h);  // (sequential when timing: G = 1)
-      if (G > 1) GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, record(ss), 0));
+                     nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr, errp);
+      pt.end(h);
       const int hk = pt.begin(3);
-      const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
-      const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
-      run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>());
+      run_moments(L, dtype, pay.p, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(), errp, rows_end);
       if (probes > 0) {
-        run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
-                          probes, s->pmom.as<double>());
+        run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
+                          s->pmom.as<double>(), errp, rows_end);
       }
       pt.end(hk);
+    } else {
+      // bucket groups of ~equal rows; group j's K1 overlaps group j+1's slice sort
+      const int64_t nv = hb[bd.nb];
+      std::vector<int> gb(G + 1, bd.nb);
+      gb[0] = 0;
+      for (int j = 1; j < G; ++j) {
+        const int64_t target = nv * j / G;
+        gb[j] = static_cast<int>(std::upper_bound(hb.begin(), hb.end(), target) - hb.begin()) - 1;
+        gb[j] = std::max(gb[j], gb[j - 1]);
+      }
+      std::vector<cudaEvent_t> evs;
+      struct EvFree {
+        std::vector<cudaEvent_t>* v;
+        ~EvFree() {
+          for (cudaEvent_t e : *v) cudaEventDestroy(e);
+        }
+      } evf{&evs};
+      auto record = [&](cudaStream_t st) {
+        cudaEvent_t e;
+        GSGPC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+        GSGPC_CUDA(cudaEventRecord(e, st));
+        return e;
+      };
+      ctx->ensure_sort_stream();
+      const cudaStream_t ss = ctx->sort;
+      GSGPC_CUDA(cudaStreamWaitEvent(ss, record(ctx->stream), 0));
+      const Launch LS{ss, &ctx->launches};
+      for (int j = 0; j < G; ++j) {
+        const int b0 = gb[j], b1 = gb[j + 1];
+        if (b1 <= b0) continue;
+        run_slice_sort(LS, dtype, bd, g.cells, b0, b1, hsl[b0], hsl[b1], rows1.p, cid1.as<int>(),
+                       bbase.as<int64_t>(), sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p,
+                       nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr, errp);
+        GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, record(ss), 0));
+        const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
+        const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
+        run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>(), errp);
+        if (probes > 0) {
+          run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
+                            probes, s->pmom.as<double>(), errp);
+        }
+      }
+      pt.end(h);
     }
   }
   s->n += n;
   s->finalized = false;
+}
+
+// Out-of-grid check of a whole add call: the classify pass records the first bad row
+// (atomicMin of (row+1) << 2 | status) and every committing kernel after it is a no-op.
+void bin_error_reset(gsgpc_ctx* ctx) {
+  DBuf& err = ctx->buf("err");
+  err.ensure(sizeof(unsigned long long) * 2);
+  GSGPC_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
+}
+
+void bin_error_check(gsgpc_ctx* ctx) {
+  ctx->pin.ensure(64);
+  GSGPC_CUDA(cudaMemcpyAsync(ctx->pin.p, ctx->buf("err").p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long e = 0;
+  std::memcpy(&e, ctx->pin.p, 8);
+  if (e == ~0ull) return;
+  const int64_t row = static_cast<int64_t>(e >> 2);
+  const int kind = static_cast<int>(e & 3);
+  const std::string what =
+      kind == PT_OUTSIDE ? "interp_weights: point outside grid"
+                         : "interp_weights: stencil leaves the grid (point too close to the boundary for the "
+                           "requested scheme)";
+  throw Error(GSGPC_OUT_OF_GRID, "sufficient_stats: stream row " + std::to_string(row) + ": " + what, row);
 }
 
 // Draw the next `rows` values of every probe stream on the device (probe_rng.cu) and pack
@@ -853,6 +881,8 @@ struct StatsSnapshot {
       cudaStreamSynchronize(ctx->stream);
       cudaMemcpy(s->rng.p, ctx->buf("bk_rng").p, sizeof(uint64_t) * s->probes * 313, cudaMemcpyDeviceToDevice);
     }
+    s->n = n_before;  // the failing batch's add_chunk counted its rows before the check
+    s->finalized = false;
     if (!active) return;
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
@@ -908,6 +938,7 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
       GSGPC_CUDA(cudaEventRecord(ctx->ev_copied[sl], ctx->copy));
     };
     try {
+      bin_error_reset(ctx);
       if (!dev) {
         ctx->ensure_copy_stream();
         // the staging buffers may still be read by earlier work on the compute stream
@@ -943,6 +974,7 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
         if (!dev) GSGPC_CUDA(cudaEventRecord(ctx->ev_free[k & 1], ctx->stream));
       }
       if (!dev) GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
+      bin_error_check(ctx);
     } catch (...) {
       if (ctx->copy) cudaStreamSynchronize(ctx->copy);
       snap.restore();
@@ -1008,6 +1040,7 @@ gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* s, const char* pa
     static const char* kSlot[2] = {"stage0", "stage1"};
     int64_t done = 0;
     try {
+      bin_error_reset(ctx);
       bool ok_next = nchunks > 0 ? read_chunk(0) : true;
       for (int64_t k = 0; k < nchunks; ++k) {
         if (!ok_next) invalid("truncated file while reading coordinate");
@@ -1047,10 +1080,11 @@ gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* s, const char* pa
         ok_next = ok;
         done += rows;
       }
+      GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
+      bin_error_check(ctx);  // a bad row before the truncation point is reported first
       if (truncated) {
         invalid(std::string("truncated file while reading ") + (tail_fields < d ? "coordinate" : "response"));
       }
-      GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
     } catch (...) {
       cudaStreamSynchronize(ctx->copy);
       snap.restore();

@@ -151,6 +151,21 @@ __device__ __forceinline__ void load_row(const PointsDev& p, int d, int64_t i, T
   }
 }
 
+// ------------------------------------------------------------------ device gate
+// The binning → moments chain of a batch runs without a host round trip: kernels are sized
+// by host upper bounds (rows of the batch) and read the true counts (rows binned, slices)
+// from the device; every kernel that commits to the accumulator returns at once when the
+// classify pass recorded an out-of-grid row (the host checks that word once per call, after
+// the work, and throws — nothing was committed).
+struct BinGate {
+  const unsigned long long* err;  // ~0: no error
+  const int64_t* rows_end;        // rows binned (bbase[nb]); nullptr → the host value
+  __device__ __forceinline__ bool closed() const { return err != nullptr && *err != ~0ull; }
+  __device__ __forceinline__ int64_t rows(int64_t host_value) const {
+    return rows_end != nullptr ? min(host_value, *rows_end) : host_value;
+  }
+};
+
 // ------------------------------------------------------------------ K2 binning
 // Two-level counting sort, no per-row global atomics.  Rows are cut into tiles of
 // TILE_ROWS; cells into buckets of 2^bsh consecutive (row-major) cells, nb ≤ ~1024 buckets.
@@ -336,8 +351,9 @@ __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts,
                                                           const int64_t* __restrict__ bbase, int* __restrict__ gcur,
                                                           Row4<T>* __restrict__ rows1, int* __restrict__ cid1,
                                                           const uint64_t* __restrict__ pw_in, int nw,
-                                                          uint64_t* __restrict__ pw1) {
+                                                          uint64_t* __restrict__ pw1, BinGate gate) {
   constexpr int R = RPT * PART_NT;
+  if (gate.closed()) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
   int* stage_c = reinterpret_cast<int*>(stage + R);
@@ -444,9 +460,10 @@ __device__ __forceinline__ int slice_bucket(const int64_t* __restrict__ sbase, i
 
 __global__ void __launch_bounds__(256) k_slice_count(const int* __restrict__ cid1, const int64_t* __restrict__ bbase,
                                                      const int64_t* __restrict__ sbase, int bsh, int nb,
-                                                     int* __restrict__ scnt, int64_t s0) {
+                                                     int* __restrict__ scnt, int64_t s0, BinGate gate) {
   extern __shared__ int cnt[];
   const int64_t sl = s0 + blockIdx.x;
+  if (gate.closed() || sl >= sbase[nb]) return;  // grids are sized by an upper bound
   const int b = slice_bucket(sbase, nb, sl);
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
@@ -472,9 +489,11 @@ __global__ void __launch_bounds__(256) k_slice_count(const int* __restrict__ cid
 // One block per bucket (1024 threads; 2^bsh ≤ 16384 cells → ≤ 16 per thread).
 __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, const int64_t* __restrict__ bbase,
                                                      const int64_t* __restrict__ sbase, int bsh, int nb,
-                                                     int64_t cells, int64_t* __restrict__ off, int b0) {
+                                                     int64_t cells, int64_t* __restrict__ off, int b0,
+                                                     BinGate gate) {
   __shared__ int64_t wsum[32];
   const int b = b0 + blockIdx.x;
+  if (gate.closed()) return;
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
   const int ncell = static_cast<int>(imin64(nbin, cells - c0));
@@ -523,10 +542,11 @@ __global__ void __launch_bounds__(256, SS_MINB) k_slice_scatter(const Row4<T>* _
                                                        int64_t cells, const int* __restrict__ scnt,
                                                        const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
                                                        const uint64_t* __restrict__ pw1, int nw,
-                                                       uint64_t* __restrict__ pws, int64_t s0) {
+                                                       uint64_t* __restrict__ pws, int64_t s0, BinGate gate) {
   constexpr int UNR = sizeof(T) == 4 ? 8 : 4;
   extern __shared__ int cur[];
   const int64_t sl = s0 + blockIdx.x;
+  if (gate.closed() || sl >= sbase[nb]) return;
   const int b = slice_bucket(sbase, nb, sl);
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
@@ -633,11 +653,13 @@ constexpr int D3C_STRIDE = 26;
 template <typename T>
 __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restrict__ pay,
                                                         const int64_t* __restrict__ off, int64_t cells,
-                                                        int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
+                                                        int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
                                                         double* __restrict__ mom, int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
@@ -783,11 +805,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
-                                                            int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g, double* __restrict__ mom,
+                                                            int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, double* __restrict__ mom,
                                                             int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
@@ -901,11 +925,13 @@ constexpr int D2C_QX = 49, D2C_Q = 49 + 16;
 template <typename T>
 __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay,
                                                          const int64_t* __restrict__ off, int64_t cells,
-                                                         int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
+                                                         int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
                                                          double* __restrict__ mom, int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D2C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
@@ -990,7 +1016,7 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
 template <int D, int W, typename T>
 __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict__ pay,
                                                      const int64_t* __restrict__ off, int64_t cells,
-                                                     int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g,
+                                                     int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
                                                      double* __restrict__ mom, int64_t range) {
   constexpr int E = 2 * W - 1;
   constexpr int QX = D == 1 ? E : (D == 2 ? E * E : E * E * E);
@@ -998,6 +1024,8 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   constexpr int Q = QX + QY;
   const int lane = threadIdx.x & 31;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
@@ -1080,13 +1108,15 @@ template <int D, int W, typename T>
 __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict__ pay,
                                                       const uint64_t* __restrict__ pw,
                                                       const int64_t* __restrict__ off, int64_t cells,
-                                                      int64_t nvalid, int64_t row0, int64_t c_lo, GridDev g, int probes,
+                                                      int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, int probes,
                                                       double* __restrict__ pmom /*cells × P × QY*/,
                                                       int64_t range, int pbase) {
   constexpr int QY = D == 1 ? W : (D == 2 ? W * W : W * W * W);
   __shared__ __align__(16) double sm[2][32 * (QY + 1)];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 2 + wib;
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
@@ -1288,6 +1318,16 @@ void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int
   GSGPC_CUDA(cudaGetLastError());
 }
 
+__global__ void k_commit_add(const unsigned long long* err, const double* src, double* dst) {
+  if (*err == ~0ull) *dst += *src;
+}
+
+void run_commit_add(const Launch& L, const unsigned long long* err, const double* src, double* dst) {
+  k_commit_add<<<1, 1, 0, L.s>>>(err, src, dst);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
 void run_sum_partials(const Launch& L, const double* part, int np, double* acc) {
   k_sum_partials<<<1, 256, 0, L.s>>>(part, np, acc);
   L.count();
@@ -1308,62 +1348,65 @@ int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd) { return ceil_div(nval
 template <typename T, int RPT>
 static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
                                const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                               const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk) {
+                               const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk, BinGate gate) {
   Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
   const size_t sm = static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 2 * sizeof(int) * bd.nb;
   auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT> : k_partition<T, false, RPT>;
   GSGPC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, bbase, gcur, r1, cid1, pw_in, nw, pw1);
+  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, bbase, gcur, r1, cid1, pw_in, nw, pw1, gate);
 }
 
 // rows per thread so that the staged sub-tile + 2 nb counters fit the shared memory
 template <typename T>
 static void launch_partition(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
                              const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                             const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk) {
+                             const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk, BinGate gate) {
   const size_t budget = 200 * 1024 / PART_MINB - 2 * sizeof(int) * bd.nb;
   const size_t per_rpt = PART_NT * (sizeof(Row4<T>) + sizeof(int));
   if (budget >= 8 * per_rpt)
-    launch_partition_r<T, 8>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+    launch_partition_r<T, 8>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
   else if (budget >= 4 * per_rpt)
-    launch_partition_r<T, 4>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+    launch_partition_r<T, 4>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
   else if (budget >= 2 * per_rpt)
-    launch_partition_r<T, 2>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+    launch_partition_r<T, 2>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
   else
-    launch_partition_r<T, 1>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+    launch_partition_r<T, 1>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
 }
 
 void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
                    const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                   const uint64_t* pw_in, int nw, uint64_t* pw1) {
+                   const uint64_t* pw_in, int nw, uint64_t* pw1, const unsigned long long* err) {
+  const BinGate gate{err, nullptr};
   int dev = 0, sms = 148;
   GSGPC_CUDA(cudaGetDevice(&dev));
   GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, PART_NT), sms * PART_MINB)));
-  if (dtype == GSGPC_F32) launch_partition<float>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
-  else launch_partition<double>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk);
+  if (dtype == GSGPC_F32) launch_partition<float>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  else launch_partition<double>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
 
 void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0,
                     int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
-                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws) {
+                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws,
+                    const unsigned long long* err) {
+  const BinGate gate{err, nullptr};
   const size_t sm = sizeof(int) * (size_t{1} << bd.bsh);
   const int64_t ns = s1 - s0;
   if (ns > 0)
-    k_slice_count<<<static_cast<unsigned>(ns), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt, s0);
+    k_slice_count<<<static_cast<unsigned>(ns), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt, s0, gate);
   if (b1 > b0)
-    k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0);
+    k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0, gate);
   if (ns > 0) {
     if (dtype == GSGPC_F32)
       k_slice_scatter<float><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
           static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<float>*>(out), pw1, nw, pws, s0);
+          static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
     else
       k_slice_scatter<double><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
           static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<double>*>(out), pw1, nw, pws, s0);
+          static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
   }
   L.count(3);
   GSGPC_CUDA(cudaGetLastError());
@@ -1381,7 +1424,7 @@ int moments_per_cell(int d, int W) {
 
 template <typename T>
 static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom) {
+                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, BinGate gate) {
   if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   if (g.d == 3 && g.W == 4) {
@@ -1400,29 +1443,29 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
     if (use_dfma) {
-      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     } else if (minb == 8) {
-      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     } else if (minb == 7) {
-      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     } else if (minb == 6) {
-      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     } else if (minb == 5) {
-      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     } else {
-      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
     }
   } else if (g.d == 2 && g.W == 4) {
     const int64_t range = 512;
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
-    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);
+    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid - row0, range);
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
 #define GSGPC_LM(DD, WW)                                                                          \
   if (g.d == DD && g.W == WW) {                                                                 \
-    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, g, mom, range);   \
+    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);   \
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
@@ -1430,9 +1473,11 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
 }
 
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom) {
-  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom);
-  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom);
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, const unsigned long long* err,
+                 const int64_t* rows_end) {
+  const BinGate gate{err, rows_end};
+  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, gate);
+  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, gate);
   if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1440,7 +1485,7 @@ void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off
 template <typename T>
 static void launch_probe_moments(const Launch& L, const void* pay, const uint64_t* pw, const int64_t* off,
                                  int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
-                                 int probes, double* pmom) {
+                                 int probes, double* pmom, BinGate gate) {
   if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   const int64_t range = 1024;
@@ -1448,7 +1493,7 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
   for (int pb = 0; pb < probes; pb += 32) {
 #define GSGPC_PM(DD, WW)                                                                                  \
   if (g.d == DD && g.W == WW) {                                                                         \
-    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, g, probes, pmom, range, pb); \
+    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, range, pb); \
   }
     GSGPC_PM(1, 2) GSGPC_PM(1, 4) GSGPC_PM(2, 2) GSGPC_PM(2, 4) GSGPC_PM(3, 2) GSGPC_PM(3, 4)
 #undef GSGPC_PM
@@ -1458,9 +1503,10 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
 
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
                        int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom) {
-  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom);
-  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom);
+                       double* pmom, const unsigned long long* err, const int64_t* rows_end) {
+  const BinGate gate{err, rows_end};
+  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate);
+  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate);
   GSGPC_CUDA(cudaGetLastError());
 }
 

@@ -37,20 +37,26 @@ void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, const int*
                        int64_t* sbase);
 int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd);
 // rows → bucket-contiguous rows1 / cid1 / pw1 (gcur: nb zeroed cursors)
+// Kernels that commit take the device error word of the classify pass (err) and return at
+// once when it records an out-of-grid row; rows_end (device) bounds the rows binned.
 void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
                    const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                   const uint64_t* pw_in, int nw, uint64_t* pw1);
+                   const uint64_t* pw_in, int nw, uint64_t* pw1, const unsigned long long* err);
+// dst += src unless err records an error
+void run_commit_add(const Launch& L, const unsigned long long* err, const double* src, double* dst);
 // bucket-contiguous → cell-sorted rows (out, pws) and off[] for buckets [b0, b1) = slices [s0, s1)
 // (off[cells] written by the last bucket); scnt: slices × 2^bsh
 void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0,
                     int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
-                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws);
+                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws,
+                    const unsigned long long* err);
 // K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there)
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom);
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, const unsigned long long* err = nullptr,
+                 const int64_t* rows_end = nullptr);
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
                        int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom);
+                       double* pmom, const unsigned long long* err = nullptr, const int64_t* rows_end = nullptr);
 void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
                   double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems);
 
