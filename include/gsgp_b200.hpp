@@ -655,6 +655,7 @@ struct LoglikOptions {
   LogdetRoute route = LogdetRoute::Auto;
   int64_t dense_cap = 2048;
   int maxiter = kDefaultMaxIter;
+  int probe_begin = 0, probe_end = 0;  // SLQ probe shard; (0, 0) = all probes
 };
 
 struct LoglikResult {
@@ -662,6 +663,9 @@ struct LoglikResult {
   int probes_used = 0;
   int solver_iterations = 0;
   std::string logdet_route = "ski-operator-slq";
+  double slq_sum = 0.0;  // probe-shard combine: logdet = Σ slq_sum / Σ slq_count + logdet_shift
+  int slq_count = 0;
+  double logdet_shift = 0.0;
 };
 
 // gp.cpp:158-240.  The SkiOperator route reads probe images accumulated in the precompute
@@ -678,6 +682,8 @@ inline LoglikResult log_likelihood_gsgp(const SufficientStats& stats, const Toep
   o.maxiter = opts.maxiter;
   o.route = static_cast<int32_t>(opts.route);
   o.dense_cap = opts.dense_cap;
+  o.probe_begin = opts.probe_begin;
+  o.probe_end = opts.probe_end;
   gsgpc_loglik_result r{};
   stats.context().check(gsgpc_log_likelihood_gsgp(stats.context().get(), stats.handle(), kg.handle(), sigma, &o, &r));
   LoglikResult out;
@@ -688,6 +694,9 @@ inline LoglikResult log_likelihood_gsgp(const SufficientStats& stats, const Toep
   out.probes_used = r.probes_used;
   out.solver_iterations = r.solver_iterations;
   out.logdet_route = r.logdet_route == 1 ? "symmetric-grid-slq" : r.logdet_route == 3 ? "dense" : "ski-operator-slq";
+  out.slq_sum = r.slq_sum;
+  out.slq_count = r.slq_count;
+  out.logdet_shift = r.logdet_shift;
   return out;
 }
 

@@ -238,6 +238,9 @@ typedef struct {
   int32_t maxiter;    /* LoglikOptions::maxiter */
   int32_t route;      /* LoglikOptions::route (gp.hpp:55-60): GSGPC_ROUTE_* */
   int64_t dense_cap;  /* LoglikOptions::dense_cap (default 2048) */
+  /* SLQ probe shard [probe_begin, probe_end) of the `probes` probes (0, 0: all).  Ranks that
+   * split the probes add their slq_sum / slq_count (gsgpc_loglik_result) to combine. */
+  int32_t probe_begin, probe_end;
 } gsgpc_loglik_options;
 
 /* LogdetRoute (gp.hpp:55-60) */
@@ -254,6 +257,12 @@ typedef struct {
   int32_t solver_iterations;
   int32_t max_depth_used;
   int32_t logdet_route;  /* the route taken (GSGPC_ROUTE_*, never AUTO) */
+  /* probe-shard combine: logdet_term = slq_sum / slq_count + logdet_shift over the whole probe
+   * set (SkiOperator: shift −(n − m) log σ²; SymmetricGrid: sum of SLQ(sym) − SLQ(K) per probe;
+   * Dense: slq_count = 0, logdet_term exact) */
+  double slq_sum;
+  int32_t slq_count;
+  double logdet_shift;
 } gsgpc_loglik_result;
 
 /* log_likelihood_gsgp (gp.hpp:86-90, gp.cpp:158-240).  Routes as the reference:

@@ -37,13 +37,14 @@ class SolveInfo_t(C.Structure):
 class LoglikOptions_t(C.Structure):
     _fields_ = [("solve_tol", C.c_double), ("probes", C.c_int32), ("max_depth", C.c_int32),
                 ("quad_tol", C.c_double), ("seed", C.c_uint64), ("maxiter", C.c_int32), ("route", C.c_int32),
-                ("dense_cap", C.c_int64)]
+                ("dense_cap", C.c_int64), ("probe_begin", C.c_int32), ("probe_end", C.c_int32)]
 
 
 class LoglikResult_t(C.Structure):
     _fields_ = [("loglik", C.c_double), ("logdet_term", C.c_double), ("quad_term", C.c_double),
                 ("const_term", C.c_double), ("probes_used", C.c_int32), ("solver_iterations", C.c_int32),
-                ("max_depth_used", C.c_int32), ("logdet_route", C.c_int32)]
+                ("max_depth_used", C.c_int32), ("logdet_route", C.c_int32), ("slq_sum", C.c_double),
+                ("slq_count", C.c_int32), ("logdet_shift", C.c_double)]
 
 
 _vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double

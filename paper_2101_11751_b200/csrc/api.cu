@@ -1875,6 +1875,9 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
     if (kg->m != m) invalid("log_likelihood_gsgp: kernel/grid size mismatch");
     const int P = opts->probes;
     const int64_t dense_cap = opts->dense_cap > 0 ? opts->dense_cap : 2048;
+    const bool all_probes = opts->probe_begin == 0 && opts->probe_end == 0;
+    const int pb = all_probes ? 0 : opts->probe_begin, pe = all_probes ? P : opts->probe_end;
+    if (pb < 0 || pe < pb || pe > P) invalid("log_likelihood_gsgp: bad probe range");
     if (opts->route < GSGPC_ROUTE_AUTO || opts->route > GSGPC_ROUTE_DENSE) invalid("log_likelihood_gsgp: bad route");
     const Launch L = ctx->L();
     const double n = static_cast<double>(s->reduced ? static_cast<int64_t>(read_scalar(ctx, s->tail() + 1)) : s->n);
@@ -1913,8 +1916,8 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
       }
     }
     const StencilDesc sd = stencil_desc(s);
-    double logdet = 0.0;
-    int probes_used = 0, max_used = 0;
+    double logdet = 0.0, slq_sum = 0.0, logdet_shift = 0.0;
+    int probes_used = 0, max_used = 0, slq_count = 0;
     if (route == GSGPC_ROUTE_SKI_OPERATOR) {
       // SLQ over the probe images (gp.cpp:85-111)
       if (P < 1) invalid("slq_logdet_ski_factorized: need at least one probe");
@@ -1939,8 +1942,8 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
       std::vector<double> zs(P, n);  // v·v = n for ±1 probes
       GSGPC_CUDA(cudaMemcpyAsync(zd.p, zs.data(), sizeof(double) * P, cudaMemcpyHostToDevice, ctx->stream));
       double total = 0.0;
-      for (int p0 = 0; p0 < P; p0 += 32) {
-        const int Pb = std::min(32, P - p0);
+      for (int p0 = pb; p0 < pe; p0 += 32) {
+        const int Pb = std::min(32, pe - p0);
         const EflaOut o = efla_run(L, sd, s->stencil(), kg->dev, Pb, kwt.as<double>() + static_cast<int64_t>(p0) * m,
                                    s->pimg() + static_cast<int64_t>(p0) * m, zd.as<double>() + p0, sigma_sq, depth);
         for (int p = 0; p < Pb; ++p) {
@@ -1951,29 +1954,36 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
           max_used = std::max(max_used, q.second);
         }
       }
-      logdet = total / P - (n - static_cast<double>(m)) * std::log(sigma_sq);
-      probes_used = P;
+      slq_sum = total;
+      slq_count = pe - pb;
+      logdet_shift = -(n - static_cast<double>(m)) * std::log(sigma_sq);
+      logdet = (slq_count > 0 ? total / slq_count : 0.0) + logdet_shift;
+      probes_used = slq_count;
     } else if (route == GSGPC_ROUTE_SYMMETRIC_GRID) {
       // slq_logdet(K WᵀW K + σ²K) − slq_logdet(K), shared probes, quad_tol 0 (gp.cpp:206-219)
+      if (P < 1) invalid("slq_logdet: need at least one probe");
       const int Pb = std::min(P, 32);
       DBuf& ku = ctx->buf("ll_sym_ku");
       DBuf& wku = ctx->buf("ll_sym_wku");
       DBuf& kt0 = ctx->buf("ll_kt0");
       DBuf& kt1 = ctx->buf("ll_kt1");
       for (DBuf* b : {&ku, &wku, &kt0, &kt1}) b->ensure(sizeof(double) * Pb * m);
-      const double s1 = slq_logdet_batched(L, m, P, opts->max_depth, 0.0, opts->seed, [&](int pb) {
-        return sym_op(L, sd, s->stencil(), kg->dev, pb, sigma_sq, ku.as<double>(), wku.as<double>(), kt0.as<double>(),
-                      kt1.as<double>());
+      const double s1 = slq_logdet_sum(L, m, pb, pe, opts->max_depth, 0.0, opts->seed, [&](int np) {
+        return sym_op(L, sd, s->stencil(), kg->dev, np, sigma_sq, ku.as<double>(), wku.as<double>(),
+                      kt0.as<double>(), kt1.as<double>());
       });
-      const double s2 = slq_logdet_batched(L, m, P, opts->max_depth, 0.0, opts->seed, [&](int pb) {
-        return kg_op(L, kg->dev, pb, kt0.as<double>(), kt1.as<double>());
+      const double s2 = slq_logdet_sum(L, m, pb, pe, opts->max_depth, 0.0, opts->seed, [&](int np) {
+        return kg_op(L, kg->dev, np, kt0.as<double>(), kt1.as<double>());
       });
-      logdet = s1 - s2;
-      probes_used = 2 * P;
+      slq_sum = s1 - s2;
+      slq_count = pe - pb;
+      logdet = slq_count > 0 ? slq_sum / slq_count : 0.0;
+      probes_used = 2 * slq_count;
       max_used = static_cast<int>(std::min<int64_t>(opts->max_depth, m));
     } else {
       if (m > dense_cap) invalid("log_likelihood_gsgp: grid too large for the dense logdet route");
       logdet = dense_logdet_grid_system(L, sd, s->stencil(), kg->dev, sigma_sq);
+      slq_sum = logdet;
     }
     const double kLog2Pi = 1.8378770664093453;
     out->logdet_term = logdet;
@@ -1984,6 +1994,9 @@ gsgpc_status gsgpc_log_likelihood_gsgp(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg*
     out->solver_iterations = cg.iterations;
     out->max_depth_used = max_used;
     out->logdet_route = route;
+    out->slq_sum = slq_sum;
+    out->slq_count = slq_count;
+    out->logdet_shift = logdet_shift;
   });
 }
 

@@ -697,13 +697,14 @@ static std::vector<double> rademacher_block(int64_t m, uint64_t seed, int p0, in
 }
 
 // slq_logdet (gp.cpp:67-83) with the probes batched EF_MAXP at a time
-double slq_logdet_batched(const Launch& L, int64_t m, int num_probes, int max_depth, double quad_tol, uint64_t seed,
-                          const std::function<BatchedOp(int)>& make_op) {
-  if (num_probes < 1) invalid("slq_logdet: need at least one probe");
+// Σ of the per-probe quadrature estimates over probes [p_begin, p_end) (the caller divides by
+// the total probe count: shards of the probe set add up across ranks)
+double slq_logdet_sum(const Launch& L, int64_t m, int p_begin, int p_end, int max_depth, double quad_tol,
+                      uint64_t seed, const std::function<BatchedOp(int)>& make_op) {
   const int depth = static_cast<int>(std::min<int64_t>(max_depth, m));
   double total = 0.0;
-  for (int p0 = 0; p0 < num_probes; p0 += EF_MAXP) {
-    const int P = std::min(EF_MAXP, num_probes - p0);
+  for (int p0 = p_begin; p0 < p_end; p0 += EF_MAXP) {
+    const int P = std::min(EF_MAXP, p_end - p0);
     const std::vector<double> hv = rademacher_block(m, seed, p0, P);
     DevMem dv(sizeof(double) * hv.size());
     GSGPC_CUDA(cudaMemcpyAsync(dv.p, hv.data(), sizeof(double) * hv.size(), cudaMemcpyHostToDevice, L.s));
@@ -715,7 +716,7 @@ double slq_logdet_batched(const Launch& L, int64_t m, int num_probes, int max_de
                    .first;
     }
   }
-  return total / num_probes;
+  return total;
 }
 
 // Batched operators of the SymmetricGrid route

@@ -134,8 +134,8 @@ struct LanczosOut {
 };
 using BatchedOp = std::function<void(const double* in, double* out)>;
 LanczosOut lanczos_batched(const Launch& L, int64_t m, int P, int k, const double* start, const BatchedOp& op);
-double slq_logdet_batched(const Launch& L, int64_t m, int num_probes, int max_depth, double quad_tol, uint64_t seed,
-                          const std::function<BatchedOp(int)>& make_op);
+double slq_logdet_sum(const Launch& L, int64_t m, int p_begin, int p_end, int max_depth, double quad_tol,
+                      uint64_t seed, const std::function<BatchedOp(int)>& make_op);
 BatchedOp kg_op(const Launch& L, const KgDev& kg, int P, double* t0, double* t1);
 BatchedOp sym_op(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, int P, double sigma_sq,
                  double* ku, double* wku, double* t0, double* t1);

@@ -37,6 +37,57 @@ def allreduce_stats(stats, group=None):
     return stats
 
 
+def probe_shard(probes: int, world: int, rank: int):
+    """Contiguous ⌈P/G⌉ probe shard of rank `rank` (SLQ probes split over GPUs)."""
+    per = -(-probes // world)
+    b = min(probes, rank * per)
+    return b, min(probes, b + per)
+
+
+def combine_loglik(results, quad_term, const_term):
+    """Combine per-shard LoglikResults (same statistics, disjoint probe shards): the log
+    determinant is the mean of the per-probe estimates over all shards, plus the route's
+    shift; the quadratic and constant terms are the same on every shard."""
+    from .gsgp import LoglikResult
+
+    total = sum(r.slq_sum for r in results)
+    count = sum(r.slq_count for r in results)
+    r0 = results[0]
+    logdet = total / count + r0.logdet_shift if count > 0 else r0.logdet_term
+    return LoglikResult(-0.5 * (logdet + quad_term + const_term), logdet, quad_term, const_term,
+                        sum(r.probes_used for r in results), r0.solver_iterations, r0.logdet_route,
+                        max(r.max_depth_used for r in results), total, count, r0.logdet_shift)
+
+
+def log_likelihood_gsgp_sharded(stats, kg, sigma, opts=None, group=None):
+    """log_likelihood_gsgp with the SLQ probes split over the ranks of `group` (every rank holds
+    the all-reduced statistics, including every probe image): rank r runs its ⌈P/G⌉ probes,
+    the per-probe sums are all-reduced, and every rank returns the same result."""
+    import dataclasses
+
+    from .gsgp import LoglikOptions, log_likelihood_gsgp
+
+    opts = opts or LoglikOptions()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    b, e = probe_shard(opts.probes, world, rank)
+    if e == b:  # more ranks than probes: an empty shard still takes part in the reduction
+        b, e = 0, 0
+        mine = dataclasses.replace(opts, probe_begin=0, probe_end=min(1, opts.probes))
+        r = log_likelihood_gsgp(stats, kg, sigma, mine)
+        r.slq_sum, r.slq_count, r.probes_used = 0.0, 0, 0
+    else:
+        r = log_likelihood_gsgp(stats, kg, sigma, dataclasses.replace(opts, probe_begin=b, probe_end=e))
+    t = torch.tensor([r.slq_sum, float(r.slq_count), float(r.probes_used)], dtype=torch.float64,
+                     device=torch.device("cuda", stats.context.device))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    total, count, used = float(t[0]), int(t[1]), int(t[2])
+    r.slq_sum, r.slq_count = total, count
+    out = combine_loglik([r], r.quad_term, r.const_term)
+    out.probes_used = used
+    return out
+
+
 def merge_buffers_host(buffers):
     """Host restatement of the combine step (used by the gloo CPU tests)."""
     out = buffers[0].clone()

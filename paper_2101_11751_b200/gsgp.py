@@ -971,6 +971,8 @@ class LoglikOptions:
     maxiter: int = kDefaultMaxIter
     route: LogdetRoute = LogdetRoute.Auto
     dense_cap: int = 2048
+    probe_begin: int = 0   # SLQ probe shard [probe_begin, probe_end); (0, 0) = all probes
+    probe_end: int = 0
 
 
 @dataclass
@@ -983,6 +985,9 @@ class LoglikResult:
     solver_iterations: int = 0
     logdet_route: str = "ski-operator-slq"
     max_depth_used: int = 0
+    slq_sum: float = 0.0      # probe-shard combine: logdet = Σ slq_sum / Σ slq_count + logdet_shift
+    slq_count: int = 0
+    logdet_shift: float = 0.0
 
 
 def factorized_lanczos_fused(kg: ToeplitzOperator, stats: SufficientStats, kgwt_z0, wt_z0, z0_sq, sigma_sq: float,
@@ -1018,8 +1023,11 @@ def log_likelihood_gsgp(stats: SufficientStats, kg: ToeplitzOperator, sigma: flo
     o.maxiter = opts.maxiter
     o.route = int(opts.route)
     o.dense_cap = int(opts.dense_cap)
+    o.probe_begin = int(opts.probe_begin)
+    o.probe_end = int(opts.probe_end)
     r = _L.LoglikResult_t()
     ctx.check(_L.load().gsgpc_log_likelihood_gsgp(ctx.handle, stats.handle, kg.handle, float(sigma), C.byref(o),
                                                   C.byref(r)))
     return LoglikResult(r.loglik, r.logdet_term, r.quad_term, r.const_term, r.probes_used, r.solver_iterations,
-                        ROUTE_NAMES.get(r.logdet_route, "?"), r.max_depth_used)
+                        ROUTE_NAMES.get(r.logdet_route, "?"), r.max_depth_used, r.slq_sum, r.slq_count,
+                        r.logdet_shift)

@@ -75,3 +75,27 @@ def test_host_merge_helper():
     a = torch.arange(5, dtype=torch.float64)
     b = torch.ones(5, dtype=torch.float64)
     assert torch.equal(merge_buffers_host([a, b]), a + b)
+
+
+def test_probe_shards_cover_the_probe_set():
+    from paper_2101_11751_b200.distributed import probe_shard
+
+    for P in (1, 7, 30, 64):
+        for world in (1, 2, 3, 8):
+            shards = [probe_shard(P, world, r) for r in range(world)]
+            covered = [p for b, e in shards for p in range(b, e)]
+            assert covered == list(range(P))
+            assert max(e - b for b, e in shards) == -(-P // world)
+
+
+def test_combine_loglik_arithmetic():
+    from paper_2101_11751_b200.distributed import combine_loglik
+    from paper_2101_11751_b200.gsgp import LoglikResult
+
+    parts = [LoglikResult(slq_sum=10.0, slq_count=4, logdet_shift=-2.0, probes_used=4, max_depth_used=5),
+             LoglikResult(slq_sum=8.0, slq_count=4, logdet_shift=-2.0, probes_used=4, max_depth_used=7),
+             LoglikResult(slq_sum=3.0, slq_count=2, logdet_shift=-2.0, probes_used=2, max_depth_used=6)]
+    r = combine_loglik(parts, quad_term=5.0, const_term=1.0)
+    assert r.logdet_term == 21.0 / 10 - 2.0
+    assert r.loglik == -0.5 * (r.logdet_term + 5.0 + 1.0)
+    assert r.probes_used == 10 and r.max_depth_used == 7
