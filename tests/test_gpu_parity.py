@@ -341,3 +341,57 @@ def test_full_size_config3_properties():
     assert rel_err(st2.stencil()[0], vals) <= 1e-10
     del rows
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_point_layouts_columns_and_strided_records(where):
+    """gsgpc_points layouts beyond the Python helpers' (x, y) and packed rows: columnar SoA
+    (x_row_stride = 1, column offsets k·n) and AoS records with extra fields (row stride 6,
+    coordinates at offsets 1, 3, 4, y at offset 5) give the same statistics as plain rows."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2101_11751_b200 import _lib as L
+
+    d, n, sizes = 3, 20000, (11, 9, 8)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    x, y = points(d, n, 31)
+    ref = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    ref_v, _ = ref.stencil()
+    cols = np.ascontiguousarray(x.T).reshape(-1)           # [x0 … | x1 … | x2 …]
+    rec = np.zeros((n, 6))
+    rec[:, 1], rec[:, 3], rec[:, 4], rec[:, 5] = x[:, 0], x[:, 1], x[:, 2], y
+    ctx = G.default_context()
+    lib = L.load()
+
+    def stats_of(p, keep):
+        acc = G.SufficientStatsAccumulator(g, ctx=ctx)
+        ctx.check(lib.gsgpc_stats_add(ctx.handle, acc._h, C.byref(p), n, None, 0))
+        acc._rows += n
+        return acc.finalize()
+
+    def ptr(a):
+        if where == "host":
+            return a.ctypes.data, a
+        t = torch.as_tensor(a).cuda()
+        return t.data_ptr(), t
+
+    xc, kx = ptr(cols)
+    yc, ky = ptr(np.ascontiguousarray(y))
+    p = L.Points_t()
+    p.dtype, p.x, p.x_row_stride, p.y, p.y_stride = L.F64, xc, 1, yc, 1
+    for k in range(d):
+        p.x_col_offset[k] = k * n
+    st = stats_of(p, (kx, ky))
+    v, _ = st.stencil()
+    assert rel_err(v, ref_v) <= 1e-12 and rel_err(st.wty(), ref.wty()) <= 1e-12 and st.n() == n
+
+    rp, kr = ptr(np.ascontiguousarray(rec).reshape(-1))
+    p = L.Points_t()
+    p.dtype, p.x, p.x_row_stride, p.y, p.y_stride = L.F64, rp, 6, rp + 5 * 8, 6
+    p.x_col_offset[0], p.x_col_offset[1], p.x_col_offset[2] = 1, 3, 4
+    st = stats_of(p, (kr,))
+    v, _ = st.stencil()
+    assert rel_err(v, ref_v) <= 1e-12 and rel_err(st.wty(), ref.wty()) <= 1e-12
+    assert abs(st.yty() - ref.yty()) <= 1e-12 * ref.yty()
