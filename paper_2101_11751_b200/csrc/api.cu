@@ -924,17 +924,39 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
     const bool dev = is_device_ptr(pts->x);
     const int nw = probes > 0 ? (probes + 63) / 64 : 0;
     const bool pw_dev = nw ? is_device_ptr(probe_words) : true;
-    const int64_t CH = dev ? (int64_t{1} << 27) : (int64_t{1} << 24);
+    static const int host_chunk_log2 = [] {
+      const char* e = getenv("GSGPC_HOST_CHUNK_LOG2");  // diagnostics: host staging chunk (rows)
+      return e ? std::max(16, std::min(28, atoi(e))) : 23;  // B200 config 3 e2e: 2^22 37.5, 2^23 36.9, 2^24 37.3 ms
+    }();
+    // host rows: equal chunks of at most 2^host_chunk_log2 rows (no short last chunk)
+    const int64_t CH0 = dev ? (int64_t{1} << 27) : (int64_t{1} << host_chunk_log2);
+    const int64_t CH = ceil_div(n, ceil_div(n, CH0));
     const int64_t nchunks = ceil_div(n, CH);
     StatsSnapshot snap(ctx, s, nchunks > 1);
     // host rows: double-buffered staging, the copy of chunk k+1 overlaps the compute of chunk k
     static const char* kSlot[2] = {"stage0", "stage1"};
     PointsDev staged[2];
+    static const bool trace = [] {
+      const char* e = getenv("GSGPC_E2E_TRACE");  // diagnostics: per-chunk copy / compute timeline
+      return e && e[0] == '1';
+    }();
+    std::vector<cudaEvent_t> tev;  // trace: per chunk copy begin/end, compute begin/end
+    auto tmark = [&](cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      GSGPC_CUDA(cudaEventCreate(&e));
+      GSGPC_CUDA(cudaEventRecord(e, st));
+      tev.push_back(e);
+    };
+    std::vector<int> tkind;
     auto stage = [&](int64_t k) {
       const int sl = static_cast<int>(k & 1);
       const int64_t a0 = k * CH, a1 = std::min(n, a0 + CH);
       if (k >= 2) GSGPC_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev_free[sl], 0));
+      tmark(ctx->copy);
       staged[sl] = stage_points(ctx, pts, s->g.d, a0, a1, true, kSlot[sl], ctx->copy);
+      tmark(ctx->copy);
+      if (trace) tkind.push_back(0);
       GSGPC_CUDA(cudaEventRecord(ctx->ev_copied[sl], ctx->copy));
     };
     try {
@@ -970,10 +992,23 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
             pw = b.as<uint64_t>();
           }
         }
+        tmark(ctx->stream);
         add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
+        tmark(ctx->stream);
+        if (trace) tkind.push_back(1);
         if (!dev) GSGPC_CUDA(cudaEventRecord(ctx->ev_free[k & 1], ctx->stream));
       }
       if (!dev) GSGPC_CUDA(cudaStreamSynchronize(ctx->copy));
+      if (trace && !tev.empty()) {
+        GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (size_t i = 0; i < tkind.size(); ++i) {
+          float a = 0.0f, b = 0.0f;
+          GSGPC_CUDA(cudaEventElapsedTime(&a, tev[0], tev[2 * i]));
+          GSGPC_CUDA(cudaEventElapsedTime(&b, tev[0], tev[2 * i + 1]));
+          std::fprintf(stderr, "[gsgpc e2e trace] %s %8.3f .. %8.3f ms\n", tkind[i] ? "compute" : "copy   ", a, b);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+      }
       bin_error_check(ctx);
     } catch (...) {
       if (ctx->copy) cudaStreamSynchronize(ctx->copy);

@@ -590,24 +590,39 @@ __global__ void k_sum_partials(const double* __restrict__ part, int np, double* 
 }
 
 // ------------------------------------------------------------------ K1 helpers
-__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* __restrict__ a, int64_t n, int64_t key) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (a[mid] <= key) lo = mid + 1; else hi = mid;
+// Largest c in [lo, hi) with off[c] <= p, given off[lo] <= p < off[hi] (hi may be the end
+// sentinel).  Warp-cooperative: the 32 lanes probe 32 evenly spaced offsets per round, so a
+// search over 1e5+ cells costs 4 dependent loads instead of ~17 (warp-uniform call).
+__device__ __forceinline__ int64_t warp_find_cell(const int64_t* __restrict__ off, int64_t lo, int64_t hi, int64_t p,
+                                                  int lane) {
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) >> 5;
+    const int64_t j = lo + step * (lane + 1);  // lane 31 probes ≥ hi
+    const unsigned gt = __ballot_sync(0xffffffffu, j >= hi || off[j] > p);
+    const int f = __ffs(gt) - 1;  // first probe past p; probe f − 1 (or lo) is ≤ p
+    const int64_t nhi = min(hi, lo + step * (f + 1));
+    lo += step * f;
+    hi = nhi;
   }
   return lo;
 }
 
-// Cell of row p for a warp walking sorted rows forward from cell c: step over a few
-// (empty) cells linearly — consecutive offsets share cache lines — and binary-search only
-// after a long gap.  A binary search per cell boundary cost ~20 dependent loads per cell,
-// which dominated sparse grids (1–100 rows per cell).
-__device__ __forceinline__ int64_t next_cell(const int64_t* __restrict__ off, int64_t c, int64_t p, int64_t c_lo,
-                                             int64_t cells) {
-  for (int k = 0; k < 8 && off[c + 1] <= p; ++k) ++c;
-  if (off[c + 1] <= p) c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, p) - 1;
-  return c;
+// Cell of row p for a warp walking sorted rows forward from cell c (off[c] <= p): one
+// coalesced probe of the next 32 offsets (consecutive cells, usually the answer), then
+// the cooperative search over the rest.  A per-lane binary search per cell boundary cost
+// ~20 dependent loads, which dominated sparse grids and small batches.
+__device__ __forceinline__ int64_t next_cell(const int64_t* __restrict__ off, int64_t c, int64_t p, int64_t cells,
+                                             int lane) {
+  const int64_t j = c + 1 + lane;
+  const unsigned gt = __ballot_sync(0xffffffffu, j >= cells || off[j] > p);
+  if (gt) return c + __ffs(gt) - 1;
+  return warp_find_cell(off, c + 32, cells, p, lane);
+}
+
+// Cell of row r0 in [c_lo, cells) (off[c_lo] <= r0 < off[cells]).
+__device__ __forceinline__ int64_t first_cell(const int64_t* __restrict__ off, int64_t c_lo, int64_t cells, int64_t r0,
+                                              int lane) {
+  return warp_find_cell(off, c_lo, cells, r0, lane);
 }
 
 // Recompute (t_0..t_{d-1}) of a sorted (valid) row: same snap decision as classify_d, t to
@@ -637,9 +652,10 @@ __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double
   y = static_cast<double>(r.v[3]);
 }
 
-__device__ __forceinline__ void flush_val(double* p, double v, bool owned) {
-  if (owned) *p += v; else atomicAdd(p, v);
-}
+// Moment flushes are fire-and-forget reductions (RED.ADD.F64): a load-add-store of a cell
+// the warp owns stalled the warp on a DRAM read per boundary, which dominated sparse cells
+// (config 3, 2.56e6 rows: K1 1.65 → 0.49 ms; the 1.2e8-row step is unchanged).
+__device__ __forceinline__ void flush_val(double* p, double v) { atomicAdd(p, v); }
 
 // ------------------------------------------------------------------ K1, d = 3 cubic
 // One warp = 4 groups of 8 lanes; group g takes every 4th point of a 32-point batch.
@@ -677,16 +693,15 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
 #pragma unroll
   for (int a = 0; a < 4; ++a) yacc[a][0] = yacc[a][1] = 0.0;
 
-  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
   // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
-    c = next_cell(off, c, p, c_lo, cells);
+    c = next_cell(off, c, p, cells, lane);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
-    const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
       const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
@@ -767,12 +782,12 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
 #pragma unroll
         for (int i = 0; i < 7; ++i)
 #pragma unroll
-          for (int j = 0; j < 7; ++j) flush_val(M + i * 49 + gl * 7 + j, acc[i][j], owned);
+          for (int j = 0; j < 7; ++j) flush_val(M + i * 49 + gl * 7 + j, acc[i][j]);
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0, yacc[a][0], owned);
-        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0 + 1, yacc[a][1], owned);
+        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0, yacc[a][0]);
+        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0 + 1, yacc[a][1]);
       }
     }
 #pragma unroll
@@ -829,16 +844,15 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   for (int t = 0; t < 7; ++t) dx[t][0] = dx[t][1] = 0.0;
   dy[0] = dy[1] = 0.0;
 
-  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
   // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
-    c = next_cell(off, c, p, c_lo, cells);
+    c = next_cell(off, c, p, cells, lane);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
-    const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
       const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
@@ -892,9 +906,9 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
         const int col = cb + i;
         if (col < 7) {
           if (r < 7) {
-            flush_val(M + r * 49 + tt * 7 + col, dx[tt][i], owned);
+            flush_val(M + r * 49 + tt * 7 + col, dx[tt][i]);
           } else if (tt < 4 && col < 4) {
-            flush_val(M + D3C_QX + tt * 4 + col, dx[tt][i], owned);  // Y[a=0][b=tt][c=col]
+            flush_val(M + D3C_QX + tt * 4 + col, dx[tt][i]);  // Y[a=0][b=tt][c=col]
           }
         }
         dx[tt][i] = 0.0;
@@ -903,7 +917,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int col = cb + i;
-      if (yrow) flush_val(M + D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i], owned);
+      if (yrow) flush_val(M + D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i]);
       dy[i] = 0.0;
     }
     p = seg_end;
@@ -938,8 +952,7 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
   double* S = sm[wib];
   const int r = lane >> 2, kq = lane & 3, cb = 2 * (lane & 3);
   double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
-  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
-  bool started_here = off[c] >= r0;  // the current cell's first row lies in this warp's range
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
   for (int64_t b = r0; b < rend; b += 32) {
     const int64_t bend = min(b + 32, rend);
     {
@@ -960,8 +973,7 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
     __syncwarp();
     int64_t s0 = b;
     while (s0 < bend) {
-      c = next_cell(off, c, s0, c_lo, cells);
-      if (off[c] == s0) started_here = true;
+      c = next_cell(off, c, s0, cells, lane);
       const int64_t ce = off[c + 1];
       const int64_t s1 = min(ce, bend);
       const int steps = static_cast<int>((s1 - s0 + 3) >> 2);
@@ -977,18 +989,16 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
         dmma(dy0, dy1, ay, by);
       }
       if (ce <= bend) {  // the cell ends in this batch: flush this lane's fragment entries
-        const bool owned = started_here && ce <= rend;
         double* M = mom + c * D2C_Q;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int col = cb + i;
           const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
-          if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx, owned);
-          else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx, owned);  // Y[0][col]
-          if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy, owned);
+          if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx);
+          else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx);  // Y[0][col]
+          if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy);
         }
         dx0 = dx1 = dy0 = dy1 = 0.0;
-        started_here = false;
       }
       s0 = s1;
     }
@@ -1032,13 +1042,12 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   double acc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
   while (p < rend) {
-    c = next_cell(off, c, p, c_lo, cells);
+    c = next_cell(off, c, p, cells, lane);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
-    const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p + lane; b < seg_end; b += 32) {
       double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
       row_t<T>(g, pay[b], t, y);
@@ -1094,7 +1103,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
     double* M = mom + c * Q;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      if ((q & 31) == lane) flush_val(M + q, acc[q], owned);
+      if ((q & 31) == lane) flush_val(M + q, acc[q]);
       acc[q] = 0.0;
     }
     p = seg_end;
@@ -1128,13 +1137,12 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
   double acc[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q) acc[q] = 0.0;
-  int64_t c = c_lo + upper_bound_i64(off + c_lo, cells - c_lo + 1, r0) - 1;
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
   while (p < rend) {
-    c = next_cell(off, c, p, c_lo, cells);
+    c = next_cell(off, c, p, cells, lane);
     const int64_t cs = off[c], ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
-    const bool owned = cs >= r0 && ce <= rend;
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
       {
@@ -1178,7 +1186,7 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
     if (plive) {
       double* M = pmom + (c * probes + pj) * QY;
 #pragma unroll
-      for (int q = 0; q < QY; ++q) flush_val(M + q, acc[q], owned);
+      for (int q = 0; q < QY; ++q) flush_val(M + q, acc[q]);
     }
 #pragma unroll
     for (int q = 0; q < QY; ++q) acc[q] = 0.0;
