@@ -664,6 +664,7 @@ __device__ __forceinline__ void flush_val(double* p, double v) { atomicAdd(p, v)
 // batch's powers t^0..t^6 per dimension are computed once per point by a loader lane and
 // staged in shared memory (stride 26 doubles: the four groups' rows fall in distinct banks).
 constexpr int D3C_QX = 343, D3C_QY = 64, D3C_Q = 407;
+static_assert(D3C_Q == D3C_QX + D3C_QY, "moment record = x-moments + y-moments");
 constexpr int D3C_STRIDE = 26;
 
 template <typename T>
@@ -700,7 +701,7 @@ __global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restric
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
-    const int64_t cs = off[c], ce = off[c + 1];
+    const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
-    const int64_t cs = off[c], ce = off[c + 1];
+    const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
@@ -1046,7 +1047,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   int64_t p = r0;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
-    const int64_t cs = off[c], ce = off[c + 1];
+    const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     for (int64_t b = p + lane; b < seg_end; b += 32) {
       double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
@@ -1141,7 +1142,7 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
   int64_t p = r0;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
-    const int64_t cs = off[c], ce = off[c + 1];
+    const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
@@ -1243,7 +1244,7 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
       v[i][e] = ok ? __ldg(in + addr) : 0.0;
     }
   }
-  if (YM) {
+  if constexpr (YM) {
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < W; ++i)
@@ -1251,23 +1252,113 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
       for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_P[i * 4 + e], acc);
     const int qo = q_hi * x.inner_q + q_lo;  // digit k collapsed to extent 1
     out[static_cast<int64_t>(qo) * x.sp_out + sp] = acc;
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int dq = 0; dq < E; ++dq) {
-    const int delta = dq - (W - 1);
-    const int64_t qo = static_cast<int64_t>(q_hi * E + dq) * x.inner_q + q_lo;
-    if (x.half && qo < x.c0) continue;
+    for (int dq = 0; dq < E; ++dq) {
+      const int delta = dq - (W - 1);
+      const int64_t qo = static_cast<int64_t>(q_hi * E + dq) * x.inner_q + q_lo;
+      if (x.half && qo < x.c0) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        const int j = i + delta;
+        if (j >= 0 && j < W) {
+#pragma unroll
+          for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_C[(i * 4 + j) * 7 + e], acc);
+        }
+      }
+      out[(x.half ? qo - x.c0 : qo) * x.sp_out + sp] = acc;
+    }
+  }
+}
+
+// First transform (innermost dimension k = d−1) of both chains straight from the
+// cell-major moments.  Cells along the last dimension are consecutive records, so a block
+// stages the records of one tile of a grid line ([cell][Q] fp64, contiguous) in shared
+// memory with coalesced loads and produces every x output (node a, exponent digits before
+// k, offset δ) and y output (node a, digits before k) of the tile from it — the per-thread
+// k_xform read of 4 × 7 values at a 407-double stride between lanes was L1-wavefront bound.
+struct XformFirst {
+  int Q, QX;                 // record stride, x-moments per record (y-moments follow)
+  int ext_in, ext_out;       // cells / nodes along k
+  int lines;                 // Π cells of the other dimensions
+  int tiles, TA;             // node tiles per line, nodes per tile
+  int qx_rest, qy_rest;      // E^{d−1}, W^{d−1}
+  int sp_out;                // lines × ext_out
+  int shift;                 // cubic 1, linear 0
+};
+
+template <int W>
+__global__ void __launch_bounds__(256, 2) k_xform_first(const double* __restrict__ mom, double* __restrict__ outx,
+                                                     double* __restrict__ outy, XformFirst x) {
+  constexpr int E = 2 * W - 1;
+  extern __shared__ double rec[];
+  const int line = blockIdx.x / x.tiles, tile = blockIdx.x - line * x.tiles;
+  const int a0 = tile * x.TA;
+  const int na = min(x.TA, x.ext_out - a0);
+  const int c_lo = max(0, a0 + x.shift - (W - 1));
+  const int c_hi = min(x.ext_in - 1, a0 + na - 1 + x.shift);
+  {
+    // 8 independent loads in flight per thread (a plain strided loop serialises on latency)
+    const double* src = mom + (static_cast<int64_t>(line) * x.ext_in + c_lo) * x.Q;
+    const int cnt = (c_hi - c_lo + 1) * x.Q;
+    constexpr int U = 8;
+    for (int i0 = threadIdx.x; i0 < cnt; i0 += U * 256) {
+      double t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) t[u] = i0 + u * 256 < cnt ? __ldcs(src + i0 + u * 256) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * 256 < cnt) rec[i0 + u * 256] = t[u];
+    }
+  }
+  __syncthreads();
+  const int sp0 = line * x.ext_out + a0;
+  const int nx = na * x.qx_rest;
+  for (int it = threadIdx.x; it < nx; it += blockDim.x) {
+    const int q_hi = it / na, ai = it - q_hi * na;
+    const int a = a0 + ai;
+    // per cell slot i: 7 exponents in registers, added into every offset that pairs with i
+    // (same summation order as k_xform: i ascending, then e)
+    double acc[E];
+#pragma unroll
+    for (int dq = 0; dq < E; ++dq) acc[dq] = 0.0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const int c = a + x.shift - i;
+      if (c >= 0 && c < x.ext_in) {
+        const double* r = rec + (c - c_lo) * x.Q + q_hi * E;
+        double v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = r[e];
+#pragma unroll
+        for (int dq = 0; dq < E; ++dq) {
+          const int j = i + dq - (W - 1);
+          if (j >= 0 && j < W) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[dq] = fma(v[e], c_C[(i * 4 + j) * 7 + e], acc[dq]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int dq = 0; dq < E; ++dq) outx[static_cast<int64_t>(q_hi * E + dq) * x.sp_out + sp0 + ai] = acc[dq];
+  }
+  const int ny = na * x.qy_rest;
+  for (int it = threadIdx.x; it < ny; it += blockDim.x) {
+    const int q_hi = it / na, ai = it - q_hi * na;
+    const int a = a0 + ai;
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-      const int j = i + delta;
-      if (j >= 0 && j < W) {
+      const int c = a + x.shift - i;
+      if (c >= 0 && c < x.ext_in) {
+        const double* r = rec + (c - c_lo) * x.Q + x.QX + q_hi * W;
 #pragma unroll
-        for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_C[(i * 4 + j) * 7 + e], acc);
+        for (int e = 0; e < W; ++e) acc = fma(r[e], c_P[i * 4 + e], acc);
       }
     }
-    out[(x.half ? qo - x.c0 : qo) * x.sp_out + sp] = acc;
+    outy[static_cast<int64_t>(q_hi) * x.sp_out + sp0 + ai] = acc;
   }
 }
 
@@ -1522,7 +1613,7 @@ void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64
 // moments (cell-major [cell][P][QY]) → probe images [P][m].
 void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
                   double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems) {
-  const int d = g.d, W = g.W, E = 2 * W - 1;
+  const int d = std::max(1, std::min(g.d, GSGPC_MAX_DIM)), W = g.W, E = 2 * W - 1;
   const int Q = moments_per_cell(d, W);
   int QX = 1, QY = 1;
   for (int k = 0; k < d; ++k) {
@@ -1530,21 +1621,25 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
     QY *= W;
   }
   upload_poly_tables(W, L.s);
+  const int64_t half = ws_elems / 2;
   double* bufA = ws;
-  double* bufB = ws + ws_elems / 2;
-  // chain over k = d-1 .. 0; the first pass reads the cell-major moments directly
-  auto chain = [&](bool ymode, const double* src, int64_t cstride, int64_t qoff, int qk0, double* final_out,
-                   int64_t c0) {
-    int64_t ext[3], qext[3];
+  double* bufB = ws + half;
+  // chain over k = k_start .. 0.  Pass k_start reads `src`: cell-major records (stride
+  // cstride, offset qoff) when cell_major, else the moment-major output of a pass over
+  // k_start + 1 (ext / qext describe its extents).  Intermediates ping-pong between p0, p1.
+  auto chain = [&](bool ymode, const double* src, bool cell_major, int k_start, int64_t cstride, int64_t qoff,
+                   int qk0, double* final_out, int64_t c0, double* p0, double* p1) {
+    int64_t ext[3] = {1, 1, 1}, qext[3] = {1, 1, 1};
     for (int k = 0; k < d; ++k) {
-      ext[k] = g.nc[k];
-      qext[k] = qk0;
+      ext[k] = k > k_start ? g.sz[k] : g.nc[k];
+      qext[k] = k > k_start ? (ymode ? 1 : E) : qk0;
     }
     const double* cur = src;
-    bool first = true;
-    for (int k = d - 1; k >= 0; --k) {
+    bool first = cell_major;
+    for (int k = k_start; k >= 0; --k) {
       XformDims x{};
-      int64_t ext_out[3], qext_out[3], sp_in = 1, sp_out = 1, inner_sp = 1, inner_q = 1, qrest = 1;
+      int64_t ext_out[3] = {1, 1, 1}, qext_out[3] = {1, 1, 1}, sp_in = 1, sp_out = 1, inner_sp = 1, inner_q = 1,
+              qrest = 1;
       for (int j = 0; j < d; ++j) {
         ext_out[j] = j == k ? g.sz[k] : ext[j];
         qext_out[j] = j == k ? (ymode ? 1 : E) : qext[j];
@@ -1569,7 +1664,7 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
       const bool last = k == 0;
       x.half = (last && !ymode) ? 1 : 0;
       x.c0 = c0;
-      double* dst = last ? final_out : (cur == bufA ? bufB : bufA);
+      double* dst = last ? final_out : (cur == p0 ? p1 : p0);
       const dim3 grid(static_cast<unsigned>(ceil_div(sp_out, 256)), static_cast<unsigned>(qrest));
       if (W == 4) {
         if (ymode) k_xform<4, true><<<grid, 256, 0, L.s>>>(cur, dst, x);
@@ -1581,17 +1676,66 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
       L.count();
       cur = dst;
       first = false;
-      for (int j = 0; j < d; ++j) {
+      for (int j = 0; j < 3; ++j) {
         ext[j] = ext_out[j];
         qext[j] = qext_out[j];
       }
     }
   };
-  chain(true, mom, Q, QX, W, wty, 0);
-  chain(false, mom, Q, 0, E, stencil, (static_cast<int64_t>(QX) - 1) / 2);
+  const int64_t c0 = (static_cast<int64_t>(QX) - 1) / 2;
+  // shared first pass (d ≥ 2): one tile of a last-dimension line staged in shared memory
+  constexpr int64_t kFirstSmem = 96 * 1024;
+  const int64_t rec_bytes = sizeof(double) * static_cast<int64_t>(Q);
+  const int64_t max_cells = kFirstSmem / rec_bytes;
+  const int ext_out = static_cast<int>(g.sz[d - 1]);
+  const int TA = static_cast<int>(std::min<int64_t>(ext_out, max_cells - (W - 1)));
+  if (d >= 2 && TA >= 8) {
+    XformFirst f{};
+    f.Q = Q;
+    f.QX = QX;
+    f.ext_in = static_cast<int>(g.nc[d - 1]);
+    f.ext_out = ext_out;
+    int64_t lines = 1;
+    for (int k = 0; k < d - 1; ++k) lines *= g.nc[k];
+    f.lines = static_cast<int>(lines);
+    f.TA = TA;
+    f.tiles = static_cast<int>(ceil_div(ext_out, TA));
+    f.qx_rest = QX / E;
+    f.qy_rest = QY / W;
+    f.sp_out = static_cast<int>(lines * ext_out);
+    f.shift = W == 4 ? 1 : 0;
+    const size_t smem = static_cast<size_t>(std::min<int64_t>(f.ext_in, TA + W - 1) * rec_bytes);
+    // y intermediates live in bufB (QY·big ≤ half/2 for every (d, W) with d ≥ 2)
+    double* yA = bufB;
+    double* yB = bufB + half / 2;
+    const unsigned blocks = static_cast<unsigned>(lines * f.tiles);
+    if (W == 4) {
+      static bool attr = false;
+      if (!attr) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_xform_first<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kFirstSmem)));
+        attr = true;
+      }
+      k_xform_first<4><<<blocks, 256, smem, L.s>>>(mom, bufA, yA, f);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_xform_first<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kFirstSmem)));
+        attr = true;
+      }
+      k_xform_first<2><<<blocks, 256, smem, L.s>>>(mom, bufA, yA, f);
+    }
+    L.count();
+    chain(true, yA, false, d - 2, 0, 0, W, wty, 0, yB, yA);
+    chain(false, bufA, false, d - 2, 0, 0, E, stencil, c0, bufB, bufA);
+  } else {
+    chain(true, mom, true, d - 1, Q, QX, W, wty, 0, bufA, bufB);
+    chain(false, mom, true, d - 1, Q, 0, E, stencil, c0, bufA, bufB);
+  }
   for (int pj = 0; pj < probes && pmom != nullptr; ++pj) {
-    chain(true, pmom, static_cast<int64_t>(probes) * QY, static_cast<int64_t>(pj) * QY, W,
-          pimg + static_cast<int64_t>(pj) * g.m, 0);
+    chain(true, pmom, true, d - 1, static_cast<int64_t>(probes) * QY, static_cast<int64_t>(pj) * QY, W,
+          pimg + static_cast<int64_t>(pj) * g.m, 0, bufA, bufB);
   }
   GSGPC_CUDA(cudaGetLastError());
 }
