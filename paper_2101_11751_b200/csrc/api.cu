@@ -470,8 +470,9 @@ gsgpc_stats* new_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme) {
   }
   s->QY = qy;
   s->S_min = (S + 1) / 2;
-  s->mom.ensure(sizeof(double) * s->g.cells * s->Q);
-  GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * s->g.cells * s->Q, ctx->stream));
+  // + 2 doubles: finalize's bulk copies of record tiles round their size up to 16 bytes
+  s->mom.ensure(sizeof(double) * (s->g.cells * s->Q + 2));
+  GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * (s->g.cells * s->Q + 2), ctx->stream));
   s->yty.ensure(sizeof(double));
   GSGPC_CUDA(cudaMemsetAsync(s->yty.p, 0, sizeof(double), ctx->stream));
   return s.release();

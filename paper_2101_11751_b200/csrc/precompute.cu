@@ -1292,27 +1292,36 @@ template <int W>
 __global__ void __launch_bounds__(256, 2) k_xform_first(const double* __restrict__ mom, double* __restrict__ outx,
                                                      double* __restrict__ outy, XformFirst x) {
   constexpr int E = 2 * W - 1;
-  extern __shared__ double rec[];
+  extern __shared__ __align__(16) double stage[];
   const int line = blockIdx.x / x.tiles, tile = blockIdx.x - line * x.tiles;
   const int a0 = tile * x.TA;
   const int na = min(x.TA, x.ext_out - a0);
   const int c_lo = max(0, a0 + x.shift - (W - 1));
   const int c_hi = min(x.ext_in - 1, a0 + na - 1 + x.shift);
-  {
-    // 8 independent loads in flight per thread (a plain strided loop serialises on latency)
-    const double* src = mom + (static_cast<int64_t>(line) * x.ext_in + c_lo) * x.Q;
-    const int cnt = (c_hi - c_lo + 1) * x.Q;
-    constexpr int U = 8;
-    for (int i0 = threadIdx.x; i0 < cnt; i0 += U * 256) {
-      double t[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) t[u] = i0 + u * 256 < cnt ? __ldcs(src + i0 + u * 256) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i0 + u * 256 < cnt) rec[i0 + u * 256] = t[u];
-    }
+  // the tile's records in one bulk copy (TMA engine, no registers or warps tied up):
+  // start rounded down to 16 bytes, size up to 16 bytes (the moment buffer has 2 spare doubles)
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t first = (static_cast<int64_t>(line) * x.ext_in + c_lo) * x.Q;
+  const int pre = static_cast<int>(first & 1);
+  const int cnt = (c_hi - c_lo + 1) * x.Q;
+  const unsigned bytes = static_cast<unsigned>(((pre + cnt + 1) & ~1) * sizeof(double));
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(stage))),
+                 "l"(mom + (first - pre)), "r"(bytes), "r"(bar_s)
+                 : "memory");
+  }
+  asm volatile(
+      "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W%=;\n}\n" ::"r"(bar_s)
+      : "memory");
+  const double* rec = stage + pre;
   const int sp0 = line * x.ext_out + a0;
   const int nx = na * x.qx_rest;
   for (int it = threadIdx.x; it < nx; it += blockDim.x) {
@@ -1686,7 +1695,7 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
   // shared first pass (d ≥ 2): one tile of a last-dimension line staged in shared memory
   constexpr int64_t kFirstSmem = 96 * 1024;
   const int64_t rec_bytes = sizeof(double) * static_cast<int64_t>(Q);
-  const int64_t max_cells = kFirstSmem / rec_bytes;
+  const int64_t max_cells = (kFirstSmem - 16) / rec_bytes;
   const int ext_out = static_cast<int>(g.sz[d - 1]);
   const int TA = static_cast<int>(std::min<int64_t>(ext_out, max_cells - (W - 1)));
   if (d >= 2 && TA >= 8) {
@@ -1704,7 +1713,7 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
     f.qy_rest = QY / W;
     f.sp_out = static_cast<int>(lines * ext_out);
     f.shift = W == 4 ? 1 : 0;
-    const size_t smem = static_cast<size_t>(std::min<int64_t>(f.ext_in, TA + W - 1) * rec_bytes);
+    const size_t smem = static_cast<size_t>(std::min<int64_t>(f.ext_in, TA + W - 1) * rec_bytes) + 16;
     // y intermediates live in bufB (QY·big ≤ half/2 for every (d, W) with d ≥ 2)
     double* yA = bufB;
     double* yB = bufB + half / 2;
