@@ -39,6 +39,7 @@ struct PcgArgs {
   CgState* st;
   PcgMode mode[3];
   int init;
+  int plane;  // d = 3: modes 2 and 1 fused per x0-plane (pcg_plane_modes)
   unsigned long long* tbuf;  // optional phase trace: tbuf[iter * 8 + phase] = %globaltimer (ns)
 };
 
@@ -94,9 +95,22 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
     for (int uu = threadIdx.x; uu < ngroups; uu += PCG_NT) {
       int tl, ar;
       toep_group(uu, nl, na, c.inner == 1, tl, ar);
+      const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
+      // epilogue operands issued before the dot so their latency hides under it
+      double er[TOEP_RB], eu[TOEP_RB], es[TOEP_RB], ez[TOEP_RB];
+      if (EPI) {
+#pragma unroll
+        for (int r = 0; r < TOEP_RB; ++r) {
+          const bool ok = ar + r < na;
+          const int64_t g = (o * n + a0 + ar + r) * c.inner + i;
+          er[r] = ok ? __ldcg(a.r + g) : 0.0;
+          eu[r] = ok ? __ldcg(a.u + g) : 0.0;
+          es[r] = ok ? __ldcg(a.s + g) : 0.0;
+          ez[r] = ok ? __ldcg(a.z + g) : 0.0;
+        }
+      }
       double acc[TOEP_RB];
       toep_dot4(Ts, Xs, n, c.TL, tl, a0 + ar, acc);
-      const int64_t l = l0 + tl, o = l / c.inner, i = l % c.inner;
 #pragma unroll
       for (int r = 0; r < TOEP_RB; ++r) {
         if (ar + r >= na) break;
@@ -104,14 +118,101 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
         if (!EPI) {
           Y[g] = acc[r];
         } else {
-          const double v = acc[r] + s2 * __ldcg(a.r + g);
-          const double sn = __ldcg(a.u + g) + beta * a.s[g];
-          const double zn = v + beta * a.z[g];
+          const double v = acc[r] + s2 * er[r];
+          const double sn = eu[r] + beta * es[r];
+          const double zn = v + beta * ez[r];
           a.s[g] = sn;
           a.z[g] = zn;
           dot = fma(sn, zn, dot);
         }
       }
+    }
+  }
+}
+
+// d = 3: the last two Toeplitz modes of K_G û in ONE grid phase.  Work item = (x0-plane p,
+// part q of the plane's x1 outputs): the block stages the plane (n1 × n2) in shared memory,
+// applies mode 2 to all of it, then mode 1 for its x1 outputs only — the plane's mode 2 is
+// recomputed by each of its parts, which is cheaper than a grid barrier and a second
+// phase (each part has ~n1·n2·n2 + n1·n2·n1/P FMAs).  Sums run in the order of toep_dot4
+// (j ascending), so results equal the two-phase path bit for bit.
+// Σ_j T[a + r − j] · x(j), r < 4, over j = 0..n−1 in order (toep_dot4's sliding window);
+// T = Ts + 1 + (n − 1) of a zero-padded mirrored generator (toep_ts_doubles(n) doubles).
+template <typename X>
+__device__ __forceinline__ void plane_dot4(const double* Ts, int n, int a, X x, double* acc) {
+  const double* tp = Ts + 1 + (n - 1) + a;
+  double w0 = tp[0], w1 = tp[1], w2 = tp[2], w3 = tp[3];
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < n; ++j) {
+    const double v = x(j);
+    c0 = fma(w0, v, c0);
+    c1 = fma(w1, v, c1);
+    c2 = fma(w2, v, c2);
+    c3 = fma(w3, v, c3);
+    w3 = w2;
+    w2 = w1;
+    w1 = w0;
+    w0 = tp[-(j + 1)];
+  }
+  acc[0] = c0;
+  acc[1] = c1;
+  acc[2] = c2;
+  acc[3] = c3;
+}
+
+__device__ __forceinline__ void plane_gen(double* Ts, const double* g, int n) {
+  if (threadIdx.x < 5) Ts[threadIdx.x == 0 ? 0 : 2 * n - 1 + threadIdx.x] = 0.0;
+  for (int q = threadIdx.x; q < 2 * n - 1; q += PCG_NT) Ts[1 + q] = g[abs(q - (n - 1))];
+}
+
+__device__ __forceinline__ void pcg_plane_modes(const PcgArgs& a, double* smem) {
+  const int n0 = static_cast<int>(a.mode[0].n), n1 = static_cast<int>(a.mode[1].n), n2 = static_cast<int>(a.mode[2].n);
+  const int pl = n1 * n2;
+  const int g2 = (n2 + 3) >> 2, g1 = (n1 + 3) >> 2;  // 4-output groups per line
+  const int P = max(1, min(g1, static_cast<int>(gridDim.x) / n0));  // parts per plane
+  double* T2 = smem;
+  double* T1 = T2 + toep_ts_doubles(n2);
+  double* X = T1 + toep_ts_doubles(n1);
+  double* Y = X + pl;
+  __syncthreads();
+  plane_gen(T2, a.mode[2].gen, n2);
+  plane_gen(T1, a.mode[1].gen, n1);
+  for (int w = blockIdx.x; w < n0 * P; w += gridDim.x) {
+    const int p = w / P, part = w - p * P;
+    const double* src = a.u + static_cast<int64_t>(p) * pl;
+    __syncthreads();
+    for (int i0 = threadIdx.x; i0 < pl; i0 += 8 * PCG_NT) {  // 8 loads in flight per thread
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = i0 + u * PCG_NT < pl ? __ldcg(src + i0 + u * PCG_NT) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u * PCG_NT < pl) X[i0 + u * PCG_NT] = t[u];
+    }
+    __syncthreads();
+    // mode 2 over the whole plane: Y[i1][a2]
+    for (int o = threadIdx.x; o < n1 * g2; o += PCG_NT) {
+      const int i1 = o / g2, ar = (o - i1 * g2) * 4;
+      const double* xr = X + i1 * n2;
+      double acc[4];
+      plane_dot4(T2, n2, ar, [&](int j) { return xr[j]; }, acc);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ar + r < n2) Y[i1 * n2 + ar + r] = acc[r];
+    }
+    __syncthreads();
+    // mode 1 for this part's x1 outputs (groups of 4 consecutive a1 per column i2)
+    const int q_lo = part * g1 / P, q_hi = (part + 1) * g1 / P;
+    double* dst = a.t0 + static_cast<int64_t>(p) * pl;
+    for (int o = threadIdx.x; o < (q_hi - q_lo) * n2; o += PCG_NT) {
+      const int gq = q_lo + o / n2, i2 = o - (o / n2) * n2;
+      const int ar = gq * 4;
+      double acc[4];
+      plane_dot4(T1, n1, ar, [&](int j) { return Y[j * n2 + i2]; }, acc);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ar + r < n1) dst[(ar + r) * n2 + i2] = acc[r];
     }
   }
 }
@@ -149,7 +250,15 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
   auto kg_phase = [&](double beta) {
     double dot = 0.0;
     const double* src = a.u;
-    for (int k = a.d - 1; k >= 1; --k) {
+    int k_top = a.d - 1;
+    if (a.plane) {
+      pcg_plane_modes(a, smem);
+      grid.sync();
+      stamp(3);
+      src = a.t0;
+      k_top = 0;
+    }
+    for (int k = k_top; k >= 1; --k) {
       double* dst = (src == a.t0) ? a.t1 : a.t0;
       pcg_mode<false>(a.mode[k], src, dst, smem, a, beta, s2, dot);
       grid.sync();
@@ -312,6 +421,14 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
   for (int k = 0; k < kg.d; ++k) {
     a.mode[k] = mode_cfg(kg, k);
     smem = std::max(smem, sizeof(double) * static_cast<size_t>(toep_smem_doubles(a.mode[k].n, a.mode[k].TL)));
+  }
+  if (kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {  // GSGPC_CG_NOPLANE=1: three mode phases (diagnostics)
+    const int64_t n1 = a.mode[1].n, n2 = a.mode[2].n;
+    const int64_t need = toep_ts_doubles(n1) + toep_ts_doubles(n2) + 2 * n1 * n2;
+    if (need <= 6144) {
+      a.plane = 1;
+      smem = std::max(smem, sizeof(double) * static_cast<size_t>(need));
+    }
   }
   switch (sd.S_min) {
     case 172: launch_pcg<172>(L, a, smem); break;

@@ -27,18 +27,40 @@ __device__ __forceinline__ void toep_load_tile(const double* __restrict__ X, con
     const int64_t dd = q - (n - 1);
     Ts[1 + q] = gen[dd < 0 ? -dd : dd];
   }
+  // U loads in flight per thread: the tile is ~TL·n doubles from L2 and a one-load-per-
+  // iteration loop serialised on its latency
+  constexpr int U = 8;
   if (inner == 1) {
-    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(nl) * n; q += nthreads) {
-      const int64_t tl = q / n, j = q % n;
-      Xs[j * TL + tl] = __ldcg(X + (l0 + tl) * n + j);
+    const int64_t cnt = static_cast<int64_t>(nl) * n;
+    for (int64_t q0 = threadIdx.x; q0 < cnt; q0 += static_cast<int64_t>(U) * nthreads) {
+      double t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + static_cast<int64_t>(u) * nthreads;
+        t[u] = q < cnt ? __ldcg(X + l0 * n + q) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + static_cast<int64_t>(u) * nthreads;
+        if (q < cnt) Xs[(q % n) * TL + q / n] = t[u];
+      }
     }
   } else {
-    for (int64_t q = threadIdx.x; q < static_cast<int64_t>(TL) * n; q += nthreads) {
-      const int tl = static_cast<int>(q % TL);
-      const int64_t j = q / TL;
-      if (tl < nl) {
+    const int64_t cnt = static_cast<int64_t>(TL) * n;
+    for (int64_t q0 = threadIdx.x; q0 < cnt; q0 += static_cast<int64_t>(U) * nthreads) {
+      double t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + static_cast<int64_t>(u) * nthreads;
+        const int tl = static_cast<int>(q % TL);
+        const int64_t j = q / TL;
         const int64_t l = l0 + tl, o = l / inner, i = l % inner;
-        Xs[j * TL + tl] = __ldcg(X + (o * n + j) * inner + i);
+        t[u] = (q < cnt && tl < nl) ? __ldcg(X + (o * n + j) * inner + i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = q0 + static_cast<int64_t>(u) * nthreads;
+        if (q < cnt && static_cast<int>(q % TL) < nl) Xs[(q / TL) * TL + q % TL] = t[u];
       }
     }
   }
