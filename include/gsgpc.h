@@ -179,6 +179,12 @@ gsgpc_status gsgpc_stats_apply_wtw(gsgpc_ctx* ctx, gsgpc_stats* stats, const dou
  * call gsgpc_stats_mark_reduced() afterwards (the object then accepts no more add()). */
 gsgpc_status gsgpc_stats_reduce_buffer(gsgpc_ctx* ctx, gsgpc_stats* stats, double** dev_ptr,
                                        int64_t* count);
+/* Device bytes (cells x 3^d, 0/1) recording which zero-weight patterns each cell's rows had:
+ * the structure of W^T W (the reference's hash keys, interp.cpp:188-200), kept apart from
+ * the values.  Ranks combine them with an in-place MAX all-reduce (= OR) before
+ * gsgpc_stats_mark_reduced(). */
+gsgpc_status gsgpc_stats_pattern_buffer(gsgpc_ctx* ctx, gsgpc_stats* stats, uint8_t** dev_ptr,
+                                        int64_t* count);
 gsgpc_status gsgpc_stats_mark_reduced(gsgpc_ctx* ctx, gsgpc_stats* stats);
 /* save_stats / load_stats (io.hpp:82-97, io.cpp:192-262), "GSGPSST1" layout. */
 gsgpc_status gsgpc_stats_save(gsgpc_ctx* ctx, gsgpc_stats* stats, const char* path);

@@ -85,6 +85,7 @@ SIGNATURES = {
     "gsgpc_stats_export_csr": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "gsgpc_stats_apply_wtw": (_i, [_vp, _vp, _vp, _vp]),
     "gsgpc_stats_reduce_buffer": (_i, [_vp, _vp, _P(_vp), _P(_i64)]),
+    "gsgpc_stats_pattern_buffer": (_i, [_vp, _vp, _P(_vp), _P(_i64)]),
     "gsgpc_stats_mark_reduced": (_i, [_vp, _vp]),
     "gsgpc_stats_save": (_i, [_vp, _vp, C.c_char_p]),
     "gsgpc_stats_load": (_i, [_vp, C.c_char_p, _P(_vp)]),

@@ -134,6 +134,9 @@ struct gsgpc_stats {
   GridDev g{};
   int Q = 0, QY = 0, S_min = 0;
   DBuf mom;      // cells × Q
+  int NP = 1;    // zero-weight patterns per cell (3^d)
+  DBuf pat;      // cells × NP bytes: W^T W structure (see run_touched)
+  std::vector<uint8_t> loaded_touched;  // GSGPSST1-loaded statistics: structure from the file
   DBuf pmom;     // cells × P × QY
   DBuf yty;      // device scalar Σ y²
   DBuf fin;      // [S_min·m | m | P·m | yty | n]
@@ -475,6 +478,9 @@ gsgpc_stats* new_stats(gsgpc_ctx* ctx, const gsgpc_grid* grid, int scheme) {
   GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * (s->g.cells * s->Q + 2), ctx->stream));
   s->yty.ensure(sizeof(double));
   GSGPC_CUDA(cudaMemsetAsync(s->yty.p, 0, sizeof(double), ctx->stream));
+  for (int k = 0; k < s->g.d; ++k) s->NP *= 3;
+  s->pat.ensure(static_cast<size_t>(s->g.cells) * s->NP);
+  GSGPC_CUDA(cudaMemsetAsync(s->pat.p, 0, static_cast<size_t>(s->g.cells) * s->NP, ctx->stream));
   return s.release();
 }
 
@@ -576,7 +582,8 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
                      nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr, errp);
       pt.end(h);
       const int hk = pt.begin(3);
-      run_moments(L, dtype, pay.p, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(), errp, rows_end);
+      run_moments(L, dtype, pay.p, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
+                  s->pat.as<uint8_t>(), errp, rows_end);
       if (probes > 0) {
         run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
                           s->pmom.as<double>(), errp, rows_end);
@@ -619,7 +626,8 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
         GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, record(ss), 0));
         const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
         const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
-        run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>(), errp);
+        run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>(),
+                    s->pat.as<uint8_t>(), errp);
         if (probes > 0) {
           run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
                             probes, s->pmom.as<double>(), errp);
@@ -867,6 +875,10 @@ struct StatsSnapshot {
     bm.ensure(sizeof(double) * s->g.cells * s->Q + 8);
     GSGPC_CUDA(cudaMemcpyAsync(bm.p, s->mom.p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice,
                                ctx->stream));
+    DBuf& bq = ctx->buf("bk_pat");
+    bq.ensure(static_cast<size_t>(s->g.cells) * s->NP);
+    GSGPC_CUDA(cudaMemcpyAsync(bq.p, s->pat.p, static_cast<size_t>(s->g.cells) * s->NP, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
     DBuf& by = ctx->buf("bk_yty");
     by.ensure(sizeof(double));
     GSGPC_CUDA(cudaMemcpyAsync(by.p, s->yty.p, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -888,6 +900,7 @@ struct StatsSnapshot {
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(s->mom.p, ctx->buf("bk_mom").p, sizeof(double) * s->g.cells * s->Q, cudaMemcpyDeviceToDevice);
     cudaMemcpy(s->yty.p, ctx->buf("bk_yty").p, sizeof(double), cudaMemcpyDeviceToDevice);
+    cudaMemcpy(s->pat.p, ctx->buf("bk_pat").p, static_cast<size_t>(s->g.cells) * s->NP, cudaMemcpyDeviceToDevice);
     if (s->probes) {
       cudaMemcpy(s->pmom.p, ctx->buf("bk_pmom").p, sizeof(double) * s->g.cells * s->probes * s->QY,
                  cudaMemcpyDeviceToDevice);
@@ -1148,6 +1161,8 @@ gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* s) {
   return guard(ctx, [&] {
     if (!s) invalid("stats is NULL");
     GSGPC_CUDA(cudaMemsetAsync(s->mom.p, 0, sizeof(double) * s->g.cells * s->Q, ctx->stream));
+    GSGPC_CUDA(cudaMemsetAsync(s->pat.p, 0, static_cast<size_t>(s->g.cells) * s->NP, ctx->stream));
+    s->loaded_touched.clear();
     if (s->probes) {
       GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * s->probes * s->QY, ctx->stream));
     }
@@ -1172,6 +1187,7 @@ gsgpc_status gsgpc_stats_merge(gsgpc_ctx* ctx, gsgpc_stats* dst, const gsgpc_sta
     const Launch L = ctx->L();
     const int64_t nm = dst->g.cells * dst->Q;
     run_axpby(L, nm, 1.0, dst->mom.as<double>(), 1.0, src->mom.as<double>(), dst->mom.as<double>());
+    run_or_bytes(L, dst->g.cells * dst->NP, dst->pat.as<uint8_t>(), src->pat.as<uint8_t>());
     if (dst->probes) {
       const int64_t np = dst->g.cells * dst->probes * dst->QY;
       run_axpby(L, np, 1.0, dst->pmom.as<double>(), 1.0, src->pmom.as<double>(), dst->pmom.as<double>());
@@ -1280,6 +1296,17 @@ HostCsr build_csr(gsgpc_ctx* ctx, gsgpc_stats* s) {
   const int d = s->g.d, W = s->g.W, E = 2 * W - 1;
   std::vector<double> st(static_cast<size_t>(s->S_min) * m);
   copy_out(ctx, st.data(), s->stencil(), sizeof(double) * st.size());
+  // structure: the pairs some row touched (the reference's hash keys), not the nonzero values
+  std::vector<uint8_t> tmask;
+  const std::vector<uint8_t>* touched = &s->loaded_touched;
+  if (s->loaded_touched.empty()) {
+    DBuf& tb = ctx->buf("touched");
+    tb.ensure(st.size());
+    run_touched(ctx->L(), s->g, s->S_min, s->pat.as<uint8_t>(), tb.as<uint8_t>());
+    tmask.resize(st.size());
+    copy_out(ctx, tmask.data(), tb.p, tmask.size());
+    touched = &tmask;
+  }
   int S = 1;
   for (int k = 0; k < d; ++k) S *= E;
   const int c0 = (S - 1) / 2;
@@ -1317,10 +1344,8 @@ HostCsr build_csr(gsgpc_ctx* ctx, gsgpc_stats* s) {
       }
       if (!ok) continue;
       const int64_t b = a + fl[q];
-      double v;
-      if (q >= c0) v = st[static_cast<size_t>(q - c0) * m + a];
-      else v = st[static_cast<size_t>((S - 1 - q) - c0) * m + b];
-      if (v != 0.0) row.emplace_back(b, v);
+      const size_t h = q >= c0 ? static_cast<size_t>(q - c0) * m + a : static_cast<size_t>((S - 1 - q) - c0) * m + b;
+      if ((*touched)[h]) row.emplace_back(b, st[h]);
     }
     std::sort(row.begin(), row.end());
     for (auto& e : row) {
@@ -1378,6 +1403,15 @@ gsgpc_status gsgpc_stats_reduce_buffer(gsgpc_ctx* ctx, gsgpc_stats* s, double** 
     finalize_stats(ctx, s);
     *dev_ptr = s->fin.as<double>();
     *count = s->fin_count();
+  });
+}
+
+gsgpc_status gsgpc_stats_pattern_buffer(gsgpc_ctx* ctx, gsgpc_stats* s, uint8_t** dev_ptr, int64_t* count) {
+  return guard(ctx, [&] {
+    if (!s || !dev_ptr || !count) invalid("NULL argument");
+    if (s->reduced) invalid("gsgpc_stats_pattern_buffer: statistics were already all-reduced");
+    *dev_ptr = s->pat.as<uint8_t>();
+    *count = s->g.cells * s->NP;
   });
 }
 
@@ -1476,6 +1510,7 @@ gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** ou
     for (int k = 0; k < d; ++k) S *= E;
     const int c0 = (S - 1) / 2;
     std::vector<double> st(static_cast<size_t>(s->S_min) * m, 0.0);
+    s->loaded_touched.assign(st.size(), 0);
     for (int64_t i = 0; i < nnz; ++i) {
       const int64_t r = static_cast<int64_t>(u64("triplet row"));
       const int64_t c = static_cast<int64_t>(u64("triplet col"));
@@ -1496,7 +1531,10 @@ gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** ou
       }
       if (!ok) throw Error(GSGPC_UNSUPPORTED, "stats file: W^T W entry outside the grid stencil");
       for (int k = 0; k < d; ++k) q = q * E + dig[k] + (W - 1);
-      if (q >= c0) st[static_cast<size_t>(q - c0) * m + r] = v;
+      if (q >= c0) {
+        st[static_cast<size_t>(q - c0) * m + r] = v;
+        s->loaded_touched[static_cast<size_t>(q - c0) * m + r] = 1;
+      }
     }
     s->fin.ensure(sizeof(double) * s->fin_count());
     GSGPC_CUDA(cudaMemcpyAsync(s->stencil(), st.data(), sizeof(double) * st.size(), cudaMemcpyHostToDevice, ctx->stream));

@@ -657,149 +657,37 @@ __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double
 // (config 3, 2.56e6 rows: K1 1.65 → 0.49 ms; the 1.2e8-row step is unchanged).
 __device__ __forceinline__ void flush_val(double* p, double v) { atomicAdd(p, v); }
 
+// ------------------------------------------------------------------ W^T W structure
+// The reference's W^T W holds an entry for every node pair to which some point gives two
+// nonzero weights (interp.cpp:188-200; zero weights are dropped, interp.cpp:94-99), however
+// small the sum.  The moment reconstruction can round such a sum (e.g. the corner pair of a
+// one-point cell with t ≈ 1: ~1e-17) to exactly 0, so the structure is tracked apart from
+// the values: per cell, which zero-weight patterns its rows had.  Per dimension a row is
+// interior (0 < t < 1: every stencil weight nonzero), on its cell's first node (t == 0:
+// only slot W/2 − 1 nonzero) or on its last (t == 1, u == size − 1: only slot W/2);
+// pattern p = Σ_k p_k 3^k, one byte per (cell, pattern), 0/1 — idempotent stores, merged by
+// OR (MAX over ranks).  K_TOUCHED turns the patterns into the stencil's structure.
+__device__ __forceinline__ int dim_pat(double t) { return t == 0.0 ? 1 : (t == 1.0 ? 2 : 0); }
+
+template <int D>
+__device__ __forceinline__ unsigned pat_bit(const double* t) {
+  int p = 0;
+#pragma unroll
+  for (int k = D - 1; k >= 0; --k) p = p * 3 + dim_pat(t[k]);
+  return 1u << p;
+}
+
+// lane p < P writes byte p of the cell's pattern record when bit p of mask is set
+__device__ __forceinline__ void flush_pat(uint8_t* __restrict__ pat, int64_t c, int P, unsigned mask, int lane) {
+  if (lane < P && ((mask >> lane) & 1u)) pat[c * P + lane] = 1;
+}
+
 // ------------------------------------------------------------------ K1, d = 3 cubic
-// One warp = 4 groups of 8 lanes; group g takes every 4th point of a 32-point batch.
-// Lane l of a group owns the x-moments with e_1 = l (7 lanes, lane 7 duplicates l = 6 and
-// discards) as a 7×7 register tile over (e_0, e_2), plus 8 of the 64 y-moments.  The
-// batch's powers t^0..t^6 per dimension are computed once per point by a loader lane and
-// staged in shared memory (stride 26 doubles: the four groups' rows fall in distinct banks).
+// Moment record per cell: 343 x-moments + 64 y-moments; the row's powers t^0..t^6 per
+// dimension are staged in shared memory (stride 26 doubles).
 constexpr int D3C_QX = 343, D3C_QY = 64, D3C_Q = 407;
 static_assert(D3C_Q == D3C_QX + D3C_QY, "moment record = x-moments + y-moments");
 constexpr int D3C_STRIDE = 26;
-
-template <typename T>
-__global__ void __launch_bounds__(128, 2) k_moments_d3c(const Row4<T>* __restrict__ pay,
-                                                        const int64_t* __restrict__ off, int64_t cells,
-                                                        int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
-                                                        double* __restrict__ mom, int64_t range) {
-  __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
-  if (gate.closed()) return;
-  nvalid = gate.rows(nvalid);
-  const int64_t r0 = row0 + warp * range;
-  if (r0 >= nvalid) return;
-  const int64_t rend = min(r0 + range, nvalid);
-  double* S = sm[wib];
-  const int grp = lane >> 3, gl = lane & 7;
-  const int e1 = gl < 7 ? gl : 6;
-  const int yb = gl >> 1, yc0 = (gl & 1) * 2;
-
-  double acc[7][7];
-  double yacc[4][2];
-#pragma unroll
-  for (int i = 0; i < 7; ++i)
-#pragma unroll
-    for (int j = 0; j < 7; ++j) acc[i][j] = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) yacc[a][0] = yacc[a][1] = 0.0;
-
-  int64_t c = first_cell(off, c_lo, cells, r0, lane);
-  int64_t p = r0;
-  // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
-  // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
-  Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
-  while (p < rend) {
-    c = next_cell(off, c, p, cells, lane);
-    const int64_t ce = off[c + 1];
-    const int64_t seg_end = min(ce, rend);
-    for (int64_t b = p; b < seg_end; b += 32) {
-      const int nb = static_cast<int>(imin64(32, seg_end - b));
-      const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
-      {
-        double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
-        const bool v = lane < nb;
-        if (v) row_t<T>(g, cur_row, t, y);
-        double* P = S + lane * D3C_STRIDE;
-        double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
-#pragma unroll
-        for (int e = 0; e < 7; ++e) {
-          P[e] = q0;
-          P[8 + e] = q1;
-          P[16 + e] = q2;
-          q0 *= t[0];
-          q1 *= t[1];
-          q2 *= t[2];
-        }
-        P[7] = v ? y : 0.0;
-      }
-      __syncwarp();
-      const int rounds = (nb + 3) >> 2;
-      for (int r = 0; r < rounds; ++r) {
-        const double* P = S + (4 * r + grp) * D3C_STRIDE;
-        double p0[7], B[7];
-        const double2 a01 = *reinterpret_cast<const double2*>(P);
-        const double2 a23 = *reinterpret_cast<const double2*>(P + 2);
-        const double2 a45 = *reinterpret_cast<const double2*>(P + 4);
-        const double2 a67 = *reinterpret_cast<const double2*>(P + 6);
-        p0[0] = a01.x; p0[1] = a01.y; p0[2] = a23.x; p0[3] = a23.y;
-        p0[4] = a45.x; p0[5] = a45.y; p0[6] = a67.x;
-        const double y = a67.y;
-        const double t1e = P[8 + e1];
-        const double t1b = P[8 + yb];
-        const double2 c01 = *reinterpret_cast<const double2*>(P + 16);
-        const double2 c23 = *reinterpret_cast<const double2*>(P + 18);
-        const double2 c45 = *reinterpret_cast<const double2*>(P + 20);
-        const double c6 = P[22];
-        B[0] = t1e * c01.x; B[1] = t1e * c01.y; B[2] = t1e * c23.x; B[3] = t1e * c23.y;
-        B[4] = t1e * c45.x; B[5] = t1e * c45.y; B[6] = t1e * c6;
-#pragma unroll
-        for (int i = 0; i < 7; ++i)
-#pragma unroll
-          for (int j = 0; j < 7; ++j) acc[i][j] = fma(p0[i], B[j], acc[i][j]);
-        const double yv = y * t1b;
-        const double y0 = yv * P[16 + yc0];
-        const double y1 = yv * P[17 + yc0];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          yacc[a][0] = fma(p0[a], y0, yacc[a][0]);
-          yacc[a][1] = fma(p0[a], y1, yacc[a][1]);
-        }
-      }
-      __syncwarp();
-    }
-    // flush: sum the four groups, group 0 writes
-#pragma unroll
-    for (int i = 0; i < 7; ++i)
-#pragma unroll
-      for (int j = 0; j < 7; ++j) {
-        double v = acc[i][j];
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        acc[i][j] = v;
-      }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        double v = yacc[a][k];
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        yacc[a][k] = v;
-      }
-    if (grp == 0) {
-      double* M = mom + c * D3C_Q;
-      if (gl < 7) {
-#pragma unroll
-        for (int i = 0; i < 7; ++i)
-#pragma unroll
-          for (int j = 0; j < 7; ++j) flush_val(M + i * 49 + gl * 7 + j, acc[i][j]);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0, yacc[a][0]);
-        flush_val(M + D3C_QX + a * 16 + yb * 4 + yc0 + 1, yacc[a][1]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 7; ++i)
-#pragma unroll
-      for (int j = 0; j < 7; ++j) acc[i][j] = 0.0;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) yacc[a][0] = yacc[a][1] = 0.0;
-    p = seg_end;
-  }
-}
 
 // ------------------------------------------------------------------ K1, d = 3 cubic, FP64 MMA
 // The per-cell moment sums are a GEMM over the cell's points:
@@ -822,7 +710,7 @@ template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
                                                             int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, double* __restrict__ mom,
-                                                            int64_t range) {
+                                                            uint8_t* __restrict__ pat, int64_t range) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
@@ -844,6 +732,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 #pragma unroll
   for (int t = 0; t < 7; ++t) dx[t][0] = dx[t][1] = 0.0;
   dy[0] = dy[1] = 0.0;
+  unsigned pm = 0;  // zero-weight patterns of the cell's rows (W^T W structure)
 
   int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
@@ -861,6 +750,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
         if (v) row_t<T>(g, cur_row, t, y);
+        pm |= __reduce_or_sync(0xffffffffu, v ? pat_bit<3>(t) : 0u);
         double* P = S + lane * D3C_STRIDE;
         double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
 #pragma unroll
@@ -921,6 +811,8 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
       if (yrow) flush_val(M + D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i]);
       dy[i] = 0.0;
     }
+    flush_pat(pat, c, 27, pm, lane);
+    pm = 0;
     p = seg_end;
   }
 }
@@ -929,20 +821,57 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 // M[a][b] = Σ t0^a t1^b (a, b ≤ 6), Y[a][b] = Σ y t0^a t1^b (a, b ≤ 3), 2 mma.sync.m8n8k4.f64
 // per 4 rows:
 //   X tile: A rows a = 0..6 → t0^a, row 7 → y;  B[k][n] = t1^n (n < 7) → M and Y[0][n];
-//   Y tile: A rows r < 3 → y t0^(r+1);          B[k][n] = t1^n (n < 4) → Y[1..3][n].
+//   Y tile: A row r → (y t0) · t0^r (rows r < 3 used); same B → Y[1..3][n] (n < 4).
 // Rows are staged 32 at a time regardless of cell boundaries, and each cell segment inside the
 // batch runs masked steps, so sparse cells (1–100 rows, config 4) cost one step and one flush of
 // the lane's fragment entries — no cross-lane reduction (the lane kernel's 65 warp sums per
 // cell and 248 registers made it latency-bound).
-constexpr int D2C_STRIDE = 17;  // t0^0..6, y, t1^0..6, pad (odd: lanes spread over the banks)
+// Cell segments come from the cells the lanes recompute for their own rows (row_tc: the same
+// exact classification as K2a), compared across neighbouring lanes — no off[] lookups on the
+// critical path.  Staged row R keeps element e at R·16 + (e ^ swz(R)): the staging stores (one
+// row per lane) and the fragment loads (4 rows × 8 elements per step) are both conflict-free
+// (2 wavefronts per 32 doubles; the odd stride-17 layout it replaces cost 3.7 per load and
+// bound the kernel on the shared-memory pipe at config 4).
 constexpr int D2C_QX = 49, D2C_Q = 49 + 16;
 
+__device__ __forceinline__ int d2c_swz(int R) { return ((R & 1) << 3) | ((R >> 1) & 7); }
+
+// row_t plus the flat cell of the row (classify's numbering: row-major over nc[k]).
 template <typename T>
-__global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay,
-                                                         const int64_t* __restrict__ off, int64_t cells,
-                                                         int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
-                                                         double* __restrict__ mom, int64_t range) {
-  __shared__ __align__(16) double sm[4][32 * D2C_STRIDE];
+__device__ __forceinline__ int row_tc(const GridDev& g, const Row4<T>& r, double* t, double& y) {
+  int cell = 0;
+#pragma unroll
+  for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
+    if (k < g.d) {
+      const double x = static_cast<double>(r.v[k]);
+      double uu = __dsub_rn(x, g.mn[k]) * g.isp[k];
+      const double rr = rint(uu);
+      const double dd = fabs(uu - rr);
+      const double e = 1e-12 + static_cast<double>(g.sz[k]) * 3.552713678800501e-15;
+      int i0;
+      if (dd >= 1e-9 - e && dd <= 1e-9 + e) {
+        int64_t j0;
+        stencil_dim(x, g.mn[k], g.sp[k], g.sz[k], j0, t[k]);
+        i0 = static_cast<int>(j0);
+      } else {
+        if (dd < 1e-9) uu = rr;
+        const double f = fmin(floor(uu), static_cast<double>(g.sz[k] - 2));
+        t[k] = uu - f;
+        i0 = static_cast<int>(f);
+      }
+      cell = cell * static_cast<int>(g.nc[k]) + i0;
+    }
+  }
+  y = static_cast<double>(r.v[3]);
+  return cell;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay, int64_t nvalid,
+                                                         int64_t row0, BinGate gate, GridDev g,
+                                                         double* __restrict__ mom, uint8_t* __restrict__ pat,
+                                                         int64_t range) {
+  __shared__ __align__(16) double sm[4][32 * 16];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
   if (gate.closed()) return;
@@ -951,73 +880,85 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
   if (r0 >= nvalid) return;
   const int64_t rend = min(r0 + range, nvalid);
   double* S = sm[wib];
-  const int r = lane >> 2, kq = lane & 3, cb = 2 * (lane & 3);
+  const int r = lane >> 2, cb = 2 * (lane & 3);
   double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
-  int64_t c = first_cell(off, c_lo, cells, r0, lane);
-  for (int64_t b = r0; b < rend; b += 32) {
-    const int64_t bend = min(b + 32, rend);
-    {
-      double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
-      const bool v = b + lane < bend;
-      if (v) row_t<T>(g, pay[b + lane], t, y);
-      double* P = S + lane * D2C_STRIDE;
-      double q0 = v ? 1.0 : 0.0, q1 = q0;
-#pragma unroll
-      for (int e = 0; e < 7; ++e) {
-        P[e] = q0;
-        P[8 + e] = q1;
-        q0 *= t[0];
-        q1 *= t[1];
-      }
-      P[7] = v ? y : 0.0;
-    }
-    __syncwarp();
-    int64_t s0 = b;
-    while (s0 < bend) {
-      c = next_cell(off, c, s0, cells, lane);
-      const int64_t ce = off[c + 1];
-      const int64_t s1 = min(ce, bend);
-      const int steps = static_cast<int>((s1 - s0 + 3) >> 2);
-      for (int st = 0; st < steps; ++st) {
-        const int64_t row = s0 + 4 * st + kq;
-        const bool v = row < s1;
-        const double* P = S + (row - b) * D2C_STRIDE;
-        const double ax = v ? (r < 7 ? P[r] : P[7]) : 0.0;
-        const double bx = v && r < 7 ? P[8 + r] : 0.0;
-        const double ay = v && r < 3 ? P[7] * P[r + 1] : 0.0;
-        const double by = v && r < 4 ? P[8 + r] : 0.0;
-        dmma(dx0, dx1, ax, bx);
-        dmma(dy0, dy1, ay, by);
-      }
-      if (ce <= bend) {  // the cell ends in this batch: flush this lane's fragment entries
-        double* M = mom + c * D2C_Q;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int col = cb + i;
-          const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
-          if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx);
-          else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx);  // Y[0][col]
-          if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy);
-        }
-        dx0 = dx1 = dy0 = dy1 = 0.0;
-      }
-      s0 = s1;
-    }
-    __syncwarp();
-  }
-  // a cell still open at the end of the range continues in the next warp's range: add this
-  // range's part atomically
-  if (off[c + 1] > rend) {
-    double* M = mom + c * D2C_Q;
+  int open = -1;   // cell held in the fragments
+  unsigned pm = 0;  // its rows' zero-weight patterns (W^T W structure)
+  auto flush = [&]() {
+    flush_pat(pat, open, 9, pm, lane);
+    pm = 0;
+    double* M = mom + static_cast<int64_t>(open) * D2C_Q;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int col = cb + i;
       const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
-      if (col < 7 && r < 7) atomicAdd(M + r * 7 + col, vx);
-      else if (r == 7 && col < 4) atomicAdd(M + D2C_QX + col, vx);
-      if (r < 3 && col < 4) atomicAdd(M + D2C_QX + (r + 1) * 4 + col, vy);
+      if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx);
+      else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx);  // Y[0][col]
+      if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy);
     }
+    dx0 = dx1 = dy0 = dy1 = 0.0;
+  };
+  // the next batch's row is loaded one batch ahead (its latency hides under this batch)
+  Row4<T> cur = pay[imin64(r0 + lane, rend - 1)];
+  for (int64_t b = r0; b < rend; b += 32) {
+    const int nb = static_cast<int>(imin64(32, rend - b));
+    const Row4<T> nxt = pay[imin64(b + 32 + lane, rend - 1)];
+    const bool v = lane < nb;
+    int cell = 0x7fffffff;
+    unsigned bit = 0;
+    {
+      double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
+      if (v) {
+        cell = row_tc<T>(g, cur, t, y);
+        bit = pat_bit<2>(t);
+      }
+      double* P = S + lane * 16;
+      const int sw = d2c_swz(lane);
+      double q0 = v ? 1.0 : 0.0, q1 = q0;
+#pragma unroll
+      for (int e = 0; e < 7; ++e) {
+        P[e ^ sw] = q0;
+        P[(8 + e) ^ sw] = q1;
+        q0 *= t[0];
+        q1 *= t[1];
+      }
+      P[7 ^ sw] = v ? y : 0.0;
+      P[15 ^ sw] = v ? y * t[0] : 0.0;
+    }
+    __syncwarp();
+    const int prev = __shfl_up_sync(0xffffffffu, cell, 1);
+    unsigned starts = __ballot_sync(0xffffffffu, v && (lane == 0 || cell != prev));
+    while (starts) {
+      const int s0 = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int s1 = starts ? __ffs(starts) - 1 : nb;
+      const int sc = __shfl_sync(0xffffffffu, cell, s0);
+      if (sc != open) {
+        if (open >= 0) flush();
+        open = sc;
+      }
+      pm |= __reduce_or_sync(0xffffffffu, lane >= s0 && lane < s1 ? bit : 0u);
+      const int steps = (s1 - s0 + 3) >> 2;
+      for (int st = 0; st < steps; ++st) {
+        const int R = s0 + 4 * st + (lane & 3);
+        const int Rc = R & 31;  // masked tail rows wrap onto staged (finite) rows
+        const double* P = S + Rc * 16;
+        const int sw = d2c_swz(Rc);
+        const double axr = P[r ^ sw];
+        const double bx = P[(8 + r) ^ sw];
+        const double yt = P[15 ^ sw];
+        const bool ok = R < s1;
+        const double ax = ok ? axr : 0.0;
+        const double ay = ok ? yt * axr : 0.0;
+        dmma(dx0, dx1, ax, bx);
+        dmma(dy0, dy1, ay, bx);
+      }
+    }
+    __syncwarp();
+    cur = nxt;
   }
+  // the open cell may continue in the next warp's range: its part is added atomically too
+  if (open >= 0) flush();
 }
 
 // ------------------------------------------------------------------ K1, generic (lane per point)
@@ -1028,8 +969,9 @@ template <int D, int W, typename T>
 __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict__ pay,
                                                      const int64_t* __restrict__ off, int64_t cells,
                                                      int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
-                                                     double* __restrict__ mom, int64_t range) {
+                                                     double* __restrict__ mom, uint8_t* __restrict__ pat, int64_t range) {
   constexpr int E = 2 * W - 1;
+  constexpr int NP = D == 1 ? 3 : (D == 2 ? 9 : 27);
   constexpr int QX = D == 1 ? E : (D == 2 ? E * E : E * E * E);
   constexpr int QY = D == 1 ? W : (D == 2 ? W * W : W * W * W);
   constexpr int Q = QX + QY;
@@ -1049,9 +991,11 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
+    unsigned pl = 0;
     for (int64_t b = p + lane; b < seg_end; b += 32) {
       double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
       row_t<T>(g, pay[b], t, y);
+      pl |= pat_bit<D>(t);
       double pw[D][E];
 #pragma unroll
       for (int k = 0; k < D; ++k) {
@@ -1107,6 +1051,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
       if ((q & 31) == lane) flush_val(M + q, acc[q]);
       acc[q] = 0.0;
     }
+    flush_pat(pat, c, NP, __reduce_or_sync(0xffffffffu, pl), lane);
     p = seg_end;
   }
 }
@@ -1532,7 +1477,7 @@ int moments_per_cell(int d, int W) {
 
 template <typename T>
 static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, BinGate gate) {
+                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, BinGate gate) {
   if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   if (g.d == 3 && g.W == 4) {
@@ -1541,39 +1486,29 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
       return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
     }();
     const int64_t warps = ceil_div(nvalid - row0, range);
-    static const bool use_dfma = [] {
-      const char* e = getenv("GSGPC_K1_DFMA");
-      return e && e[0] == '1';
-    }();
     static const int minb = [] {
       const char* e = getenv("GSGPC_K1_MINB");
       return e ? atoi(e) : 5;  // resident blocks/SM (B200, config 3, row prefetch): 5 → 5.36, 6 → 5.39, 7 → 5.45 ms
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
-    if (use_dfma) {
-      k_moments_d3c<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    } else if (minb == 8) {
-      k_moments_d3c_mma<T, 8><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    } else if (minb == 7) {
-      k_moments_d3c_mma<T, 7><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    } else if (minb == 6) {
-      k_moments_d3c_mma<T, 6><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    } else if (minb == 5) {
-      k_moments_d3c_mma<T, 5><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    } else {
-      k_moments_d3c_mma<T, 4><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
-    }
+#define GSGPC_D3(MB) k_moments_d3c_mma<T, MB><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range)
+    if (minb >= 8) GSGPC_D3(8);
+    else if (minb == 7) GSGPC_D3(7);
+    else if (minb == 6) GSGPC_D3(6);
+    else if (minb == 5) GSGPC_D3(5);
+    else GSGPC_D3(4);
+#undef GSGPC_D3
   } else if (g.d == 2 && g.W == 4) {
     const int64_t range = 512;
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
-    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);
+    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range);
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid - row0, range);
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
 #define GSGPC_LM(DD, WW)                                                                          \
   if (g.d == DD && g.W == WW) {                                                                 \
-    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, range);   \
+    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range); \
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
@@ -1581,11 +1516,11 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
 }
 
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, const unsigned long long* err,
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err,
                  const int64_t* rows_end) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, gate);
-  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, gate);
+  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate);
+  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate);
   if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1760,4 +1695,87 @@ int64_t finalize_ws_elems(const GridDev& g) {
   return 2 * std::max(QX, QY) * big;  // two ping-pong buffers of the largest intermediate
 }
 
+// ------------------------------------------------------------------ W^T W structure (export)
+// touched[s][a] = 1 iff some row gave nonzero weights to both node a and node a + o_s: a cell
+// whose stencil covers both and one of its zero-weight patterns (see pat_bit) keeps both
+// slots nonzero in every dimension.
+__global__ void k_touched(GridDev g, int64_t total, const uint8_t* __restrict__ pat, uint8_t* __restrict__ out) {
+  const int W = g.W, E = 2 * W - 1, o = W / 2 - 1;
+  int S = 1, P = 1;
+  for (int k = 0; k < g.d; ++k) {
+    S *= E;
+    P *= 3;
+  }
+  const int c0 = (S - 1) / 2;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(idx / g.m);
+    int64_t a = idx - static_cast<int64_t>(s) * g.m;
+    int q = c0 + s;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, ak[3] = {0, 0, 0}, dk[3] = {0, 0, 0};
+    bool ok = true;
+    for (int k = g.d - 1; k >= 0; --k) {
+      dk[k] = q % E - (W - 1);
+      q /= E;
+      ak[k] = static_cast<int>(a % g.sz[k]);
+      a /= g.sz[k];
+      const int b = ak[k] + dk[k];
+      if (b < 0 || b >= g.sz[k]) ok = false;
+      lo[k] = max(max(ak[k], b) - (W - 1 - o), 0);
+      hi[k] = min(min(ak[k], b) + o, static_cast<int>(g.nc[k]) - 1);
+      if (lo[k] > hi[k]) ok = false;
+    }
+    bool hit = false;
+    if (ok) {
+      for (int i0 = lo[0]; i0 <= hi[0] && !hit; ++i0)
+        for (int i1 = g.d > 1 ? lo[1] : 0; i1 <= (g.d > 1 ? hi[1] : 0) && !hit; ++i1)
+          for (int i2 = g.d > 2 ? lo[2] : 0; i2 <= (g.d > 2 ? hi[2] : 0) && !hit; ++i2) {
+            const int ic[3] = {i0, i1, i2};
+            int64_t cell = 0;
+            int allow[3] = {1, 1, 1};  // bit j: pattern j allowed in dimension k
+            for (int k = 0; k < g.d; ++k) {
+              cell = cell * g.nc[k] + ic[k];
+              const int sa = ak[k] - ic[k] + o;
+              if (dk[k] == 0 && sa == o) allow[k] |= 2;
+              if (dk[k] == 0 && sa == o + 1) allow[k] |= 4;
+            }
+            const uint8_t* pc = pat + cell * P;
+            for (int p = 0; p < P && !hit; ++p) {
+              int r = p;
+              bool al = true;
+              for (int k = 0; k < g.d; ++k) {
+                al = al && ((allow[k] >> (r % 3)) & 1);
+                r /= 3;
+              }
+              hit = al && pc[p] != 0;
+            }
+          }
+    }
+    out[idx] = hit ? 1 : 0;
+  }
+}
+
+void run_touched(const Launch& L, const GridDev& g, int S_min, const uint8_t* pat, uint8_t* out) {
+  const int64_t total = static_cast<int64_t>(S_min) * g.m;
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 16)));
+  k_touched<<<blocks, 256, 0, L.s>>>(g, total, pat, out);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+__global__ void k_or_bytes(int64_t n, uint8_t* __restrict__ dst, const uint8_t* __restrict__ src) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] |= src[i];
+}
+
+void run_or_bytes(const Launch& L, int64_t n, uint8_t* dst, const uint8_t* src) {
+  if (n <= 0) return;
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)));
+  k_or_bytes<<<blocks, 256, 0, L.s>>>(n, dst, src);
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
 }  // namespace gsgpc
+

@@ -52,11 +52,16 @@ void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells
                     const unsigned long long* err);
 // K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there)
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, const unsigned long long* err = nullptr,
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err = nullptr,
                  const int64_t* rows_end = nullptr);
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
                        int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
                        double* pmom, const unsigned long long* err = nullptr, const int64_t* rows_end = nullptr);
+// W^T W structure: touched[S_min][m] (0/1) from the per-cell zero-weight patterns
+// (cells × 3^d bytes written by K1); byte-wise OR for merges.
+void run_touched(const Launch& L, const GridDev& g, int S_min, const uint8_t* pat, uint8_t* out);
+void run_or_bytes(const Launch& L, int64_t n, uint8_t* dst, const uint8_t* src);
+
 void run_finalize(const Launch& L, const GridDev& g, const double* mom, int probes, const double* pmom,
                   double* stencil, double* wty, double* pimg, double* ws, int64_t ws_elems);
 

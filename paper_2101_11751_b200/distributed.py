@@ -14,8 +14,8 @@ import torch.distributed as dist
 
 
 class _DevView:
-    def __init__(self, ptr: int, count: int):
-        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+    def __init__(self, ptr: int, count: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None}
 
 
@@ -26,12 +26,22 @@ def stats_buffer_tensor(stats, device=None) -> torch.Tensor:
     return torch.as_tensor(_DevView(ptr, count), device=dev)
 
 
+def stats_pattern_tensor(stats, device=None) -> torch.Tensor:
+    """A torch view (no copy) of the stats' per-cell zero-weight pattern bytes (the W^T W
+    structure, kept apart from the values); ranks combine them by MAX (= OR)."""
+    ptr, count = stats.pattern_buffer()
+    dev = device if device is not None else torch.device("cuda", stats.context.device)
+    return torch.as_tensor(_DevView(ptr, count, "|u1"), device=dev)
+
+
 def allreduce_stats(stats, group=None):
     """Sum the finalized statistics of every rank in place (all ranks end with the merged
     statistics) and mark the object reduced."""
     buf = stats_buffer_tensor(stats)
+    pat = stats_pattern_tensor(stats)
     stats.context.synchronize()
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(pat, op=dist.ReduceOp.MAX, group=group)
     torch.cuda.current_stream(buf.device).synchronize()
     stats.mark_reduced()
     return stats

@@ -535,6 +535,12 @@ class SufficientStats:
         self._ctx.check(_L.load().gsgpc_stats_reduce_buffer(self._ctx.handle, self._h, C.byref(p), C.byref(c)))
         return int(p.value), int(c.value)
 
+    def pattern_buffer(self):
+        """(device pointer, count) of the per-cell zero-weight pattern bytes (W^T W structure)."""
+        p, c = C.c_void_p(), C.c_int64()
+        self._ctx.check(_L.load().gsgpc_stats_pattern_buffer(self._ctx.handle, self._h, C.byref(p), C.byref(c)))
+        return int(p.value), int(c.value)
+
     def mark_reduced(self):
         self._ctx.check(_L.load().gsgpc_stats_mark_reduced(self._ctx.handle, self._h))
 

@@ -41,6 +41,24 @@ def _pack(st, sizes):
     return np.concatenate([half.reshape(-1), wty, [st.yty, float(st.n)]])
 
 
+def _sparse():
+    # ~0.5 rows per cell: every shard touches a different set of W^T W pairs
+    rng = np.random.default_rng(12)
+    x = rng.random((1500, 2))
+    x[:300, 0] = np.round(x[:300, 0] * 40) / 40  # some rows on grid lines (t = 0 in dimension 0)
+    y = rng.standard_normal(1500)
+    g = O.fit_grid_to_data([0, 0], [1, 1], [60, 50])
+    return g, x, y
+
+
+def _structure(st, sizes):
+    """The touched-pair mask of W^T W in half-stencil layout, one byte per entry — what
+    gsgpc_stats_pattern_buffer's per-cell patterns encode and ranks combine by MAX (= OR)."""
+    rp, col, _, _ = st.csr()
+    mask = csr_to_half_stencil(rp, col, np.ones(len(col)), sizes, 4)
+    return mask.reshape(-1).astype(np.uint8)
+
+
 def _worker(rank, world, port, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -51,6 +69,11 @@ def _worker(rank, world, port, out_path):
     t = torch.from_numpy(_pack(st, [17, 15]))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     np.save(f"{out_path}.{rank}.npy", t.numpy())
+    gs, xs, ys = _sparse()
+    lo, hi = rank * xs.shape[0] // world, (rank + 1) * xs.shape[0] // world
+    mk = torch.from_numpy(_structure(O.sufficient_stats(gs, xs[lo:hi], ys[lo:hi]), [60, 50]))
+    dist.all_reduce(mk, op=dist.ReduceOp.MAX)
+    np.save(f"{out_path}.mask.{rank}.npy", mk.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -66,6 +89,11 @@ def test_gloo_allreduce_equals_merge(tmp_path):
         got = np.load(f"{out}.{r}.npy")
         assert got[-1] == full[-1]  # n exact
         np.testing.assert_allclose(got, full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+    gs, xs, ys = _sparse()
+    full_mask = _structure(O.sufficient_stats(gs, xs, ys), [60, 50])
+    for r in range(world):
+        got = np.load(f"{out}.mask.{r}.npy")
+        assert np.array_equal(got, full_mask)  # structure of the union = OR of the shards'
 
 
 def test_host_merge_helper():

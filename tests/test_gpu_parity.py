@@ -51,9 +51,12 @@ CASES = [
     (1, G.InterpScheme.Linear, np.float32, (37,), 5000),
     (2, G.InterpScheme.Cubic, np.float32, (23, 17), 20000),
     (2, G.InterpScheme.Linear, np.float64, (23, 17), 20000),
+    (2, G.InterpScheme.Cubic, np.float64, (200, 150), 20000),  # < 1 row per cell: one-row segments
+    (2, G.InterpScheme.Cubic, np.float32, (8, 7), 60000),      # cells spanning batches and warp ranges
     (3, G.InterpScheme.Cubic, np.float32, (11, 9, 8), 6000),
     (3, G.InterpScheme.Cubic, np.float64, (9, 10, 7), 6000),
     (3, G.InterpScheme.Linear, np.float32, (11, 9, 8), 6000),
+    (3, G.InterpScheme.Cubic, np.float64, (30, 25, 20), 4000),  # ~0.3 rows per cell
 ]
 
 
@@ -73,6 +76,38 @@ def test_precompute_matches_oracle(d, scheme, dtype, sizes, n):
     assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
     assert rel_err(val, oval) <= 1e-10
     assert gs.max_row_nnz() == os_.max_row_nnz() <= (7 if scheme == G.InterpScheme.Cubic else 3) ** d
+
+
+@pytest.mark.parametrize("d,scheme", [(1, G.InterpScheme.Cubic), (2, G.InterpScheme.Cubic),
+                                      (2, G.InterpScheme.Linear), (3, G.InterpScheme.Cubic),
+                                      (3, G.InterpScheme.Linear)])
+def test_structure_with_on_node_rows(d, scheme):
+    """W^T W structure = the reference's touched pairs (hash keys, interp.cpp:188-200) when rows
+    sit exactly on grid nodes in some dimensions (t = 0, and t = 1 on the last node: zero
+    weights dropped) and cells hold one or two rows (tiny sums the moment reconstruction can
+    round to zero)."""
+    sizes = {1: (40,), 2: (30, 24), 3: (12, 11, 10)}[d]
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes, scheme)
+    og = O.fit_grid_to_data(np.zeros(d), np.ones(d), sizes, int(scheme))
+    rng = np.random.default_rng(7 + d)
+    n = 3000
+    x = rng.random((n, d))
+    mins = np.array([g.min(k) for k in range(d)])
+    sp = np.array([(g.max(k) - g.min(k)) / (g.size(k) - 1) for k in range(d)])
+    for k in range(d):
+        on = rng.random(n) < 0.3  # 30 % of the rows on a node of dimension k
+        lo_node, hi_node = (2, sizes[k] - 3) if scheme == G.InterpScheme.Cubic else (0, sizes[k] - 1)
+        nodes = rng.integers(lo_node, hi_node + 1, size=n)
+        x[on, k] = mins[k] + nodes[on] * sp[k]
+    y = rng.standard_normal(n)
+    gs = G.sufficient_stats(g, scheme, x, y)
+    os_ = O.sufficient_stats(og, x, y, scheme=int(scheme), nthreads=4)
+    rp, col, val = gs.csr()
+    orp, ocol, oval, _ = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    diag = np.abs(oval).max()
+    assert np.abs(val - oval).max() <= 1e-10 * diag
+    assert gs.max_row_nnz() == os_.max_row_nnz()
 
 
 @pytest.mark.parametrize("d", [1, 2, 3])
