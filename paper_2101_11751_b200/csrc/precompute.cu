@@ -187,15 +187,12 @@ struct alignas(sizeof(T) * 4) Row4 {
 
 constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threads × SORT_UNR × 16
 // Build-time knobs (B200, config 3, partition + slice sort = 2.20 ms with the defaults):
-// 512-thread partition blocks ×2 per SM 2.32 ms, slice scatter at 4 blocks/SM 2.31 ms.
+// 512-thread partition blocks ×2 per SM 2.32 ms.
 #ifndef PART_NT_DEF
 #define PART_NT_DEF 1024
 #endif
 #ifndef PART_MINB
 #define PART_MINB 1
-#endif
-#ifndef SS_MINB
-#define SS_MINB 3
 #endif
 constexpr int PART_NT = PART_NT_DEF;  // partition: PART_MINB blocks of PART_NT threads per SM
 constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints
@@ -535,8 +532,13 @@ __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, con
   if (threadIdx.x == 0) off[c0 + ncell] = bbase[b + 1];
 }
 
+// Slice scatter, direct: every thread stores its rows at its cell's shared cursor.  Used when
+// a slice's runs per cell are long (≥ 32 rows on average), where the stores coalesce in L2
+// anyway and the staged kernel's extra block barriers cost more (B200: config 3 2.20 vs
+// 2.29 ms, config 5 1.55 vs 1.64 ms, config 2 0.27 vs 0.28 ms; config 4, 8-row runs: staged
+// 2.29 vs direct 3.03 ms).
 template <typename T>
-__global__ void __launch_bounds__(256, SS_MINB) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
+__global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
                                                        const int64_t* __restrict__ bbase,
                                                        const int64_t* __restrict__ sbase, int bsh, int nb,
                                                        int64_t cells, const int* __restrict__ scnt,
@@ -577,6 +579,125 @@ __global__ void __launch_bounds__(256, SS_MINB) k_slice_scatter(const Row4<T>* _
         for (int w2 = 0; w2 < nw; ++w2) pws[pos * nw + w2] = pw1[i * nw + w2];
       }
     }
+  }
+}
+
+// Slice scatter, staged: the slice is taken SS_SUB rows at a time; each sub-slice is
+// counting-sorted by cell in shared memory (shared-atomic ranks, block scan) and written out
+// linearly, so consecutive lanes store consecutive rows of one cell's run (rows stored
+// straight from registers sent every lane of a warp to a different cell: ~32 partial-line
+// writes per store instruction and DRAM read-modify-writes at config 4).
+constexpr int SS_NT = 512;
+template <typename T>
+__host__ __device__ constexpr int ss_sub() { return sizeof(T) == 4 ? 4096 : 2048; }
+
+template <typename T>
+size_t slice_scatter_smem(int nbin, int nw) {
+  const size_t R = ss_sub<T>();
+  return R * sizeof(Row4<T>) + R * sizeof(uint64_t) * (nw > 0 ? 1 : 0) + R * 2 * sizeof(uint16_t) +
+         2 * sizeof(int) * (static_cast<size_t>(nbin) + 1);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
+                                                            const int64_t* __restrict__ bbase,
+                                                            const int64_t* __restrict__ sbase, int bsh, int nb,
+                                                            int64_t cells, const int* __restrict__ scnt,
+                                                            const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
+                                                            const uint64_t* __restrict__ pw1, int nw,
+                                                            uint64_t* __restrict__ pws, int64_t s0, BinGate gate) {
+  constexpr int R = ss_sub<T>(), RPT = R / SS_NT;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int64_t sl = s0 + blockIdx.x;
+  if (gate.closed() || sl >= sbase[nb]) return;
+  const int b = slice_bucket(sbase, nb, sl);
+  const int nbin = 1 << bsh;
+  const int64_t c0 = static_cast<int64_t>(b) << bsh;
+  const int ncell = static_cast<int>(imin64(nbin, cells - c0));
+  Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
+  uint64_t* stage_w = reinterpret_cast<uint64_t*>(stage + R);
+  uint16_t* stage_c = reinterpret_cast<uint16_t*>(stage_w + (nw > 0 ? R : 0));
+  uint16_t* stage_i = stage_c + R;
+  int* cnt = reinterpret_cast<int*>(stage_i + R);  // per cell: count, then local start; [ncell] = total
+  int* gcur = cnt + nbin + 1;                      // per cell: next global slot
+  __shared__ int wsum[SS_NT / 32];
+  const int64_t r0s = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
+  const int64_t r1s = imin64(r0s + SLICE_ROWS, bbase[b + 1]);
+  for (int j = threadIdx.x; j < ncell; j += SS_NT)
+    gcur[j] = static_cast<int>(off[c0 + j]) + scnt[sl * nbin + j];  // rows per add < 2^31
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t r0 = r0s; r0 < r1s; r0 += R) {
+    const int nr = static_cast<int>(imin64(R, r1s - r0));
+    for (int j = threadIdx.x; j < ncell; j += SS_NT) cnt[j] = 0;
+    __syncthreads();
+    Row4<T> rr[RPT];
+    int lc[RPT], rank[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = u * SS_NT + threadIdx.x;
+      lc[u] = -1;
+      if (i < nr) {
+        lc[u] = static_cast<int>(__ldcs(cid1 + r0 + i) - c0);
+        rr[u] = rows1[r0 + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) rank[u] = lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0;
+    __syncthreads();
+    // exclusive scan of cnt[0..ncell) (each thread a contiguous segment)
+    const int per = (ncell + SS_NT - 1) / SS_NT;
+    const int j0 = threadIdx.x * per;
+    int local = 0;
+    for (int q = 0; q < per; ++q)
+      if (j0 + q < ncell) local += cnt[j0 + q];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int x = lane < SS_NT / 32 ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < SS_NT / 32) wsum[lane] = x;
+    }
+    __syncthreads();
+    int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+    for (int q = 0; q < per; ++q) {
+      const int j = j0 + q;
+      if (j < ncell) {
+        const int k = cnt[j];
+        cnt[j] = run;
+        run += k;
+      }
+    }
+    if (threadIdx.x == 0) cnt[ncell] = nr;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (lc[u] >= 0) {
+        const int lp = cnt[lc[u]] + rank[u];
+        stage[lp] = rr[u];
+        stage_c[lp] = static_cast<uint16_t>(lc[u]);
+        stage_i[lp] = static_cast<uint16_t>(u * SS_NT + threadIdx.x);
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nr; j += SS_NT) {
+      const int c = stage_c[j];
+      const int64_t pos = static_cast<int64_t>(gcur[c]) + (j - cnt[c]);
+      out[pos] = stage[j];
+      for (int q = 0; q < nw; ++q) pws[pos * nw + q] = pw1[(r0 + stage_i[j]) * nw + q];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < ncell; j += SS_NT) gcur[j] += cnt[j + 1] - cnt[j];
+    __syncthreads();  // cnt is reset by the next sub-slice
   }
 }
 
@@ -1452,14 +1573,39 @@ void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells
   if (b1 > b0)
     k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0, gate);
   if (ns > 0) {
-    if (dtype == GSGPC_F32)
-      k_slice_scatter<float><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+    const int nbin = 1 << bd.bsh;
+    if (SLICE_ROWS / nbin >= 32) {
+      if (dtype == GSGPC_F32)
+        k_slice_scatter_direct<float><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+            static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+            static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
+      else
+        k_slice_scatter_direct<double><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+            static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+            static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
+    } else if (dtype == GSGPC_F32) {
+      const size_t ssm = slice_scatter_smem<float>(nbin, nw);
+      static size_t set_f = 0;
+      if (ssm > set_f) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_slice_scatter<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssm)));
+        set_f = ssm;
+      }
+      k_slice_scatter<float><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
           static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
           static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
-    else
-      k_slice_scatter<double><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+    } else {
+      const size_t ssm = slice_scatter_smem<double>(nbin, nw);
+      static size_t set_d = 0;
+      if (ssm > set_d) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_slice_scatter<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssm)));
+        set_d = ssm;
+      }
+      k_slice_scatter<double><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
           static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
           static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
+    }
   }
   L.count(3);
   GSGPC_CUDA(cudaGetLastError());

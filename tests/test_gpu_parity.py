@@ -78,6 +78,26 @@ def test_precompute_matches_oracle(d, scheme, dtype, sizes, n):
     assert gs.max_row_nnz() == os_.max_row_nnz() <= (7 if scheme == G.InterpScheme.Cubic else 3) ** d
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_precompute_large_grid_sparse_cells(dtype):
+    """A 600 × 600 grid (359,001 cells → 512-cell buckets) with ~0.5 rows per cell: the
+    binning takes its staged slice scatter (short per-cell runs) and K1 its one-row segments."""
+    sizes = (600, 600)
+    g = G.fit_grid_to_data(np.zeros(2), np.ones(2), sizes, G.InterpScheme.Cubic)
+    og = O.fit_grid_to_data(np.zeros(2), np.ones(2), sizes, 1)
+    x, y = points(2, 200_000, 17)
+    x, y = x.astype(dtype), y.astype(dtype)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(og, x, y, scheme=1, nthreads=8)
+    rp, col, val = gs.csr()
+    orp, ocol, oval, owty = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert np.abs(val - oval).max() <= 1e-10 * np.abs(oval).max()
+    assert rel_err(gs.wty(), owty) <= 1e-10
+    assert abs(gs.yty() - os_.yty) <= 1e-12 * os_.yty
+    assert gs.n() == os_.n
+
+
 @pytest.mark.parametrize("d,scheme", [(1, G.InterpScheme.Cubic), (2, G.InterpScheme.Cubic),
                                       (2, G.InterpScheme.Linear), (3, G.InterpScheme.Cubic),
                                       (3, G.InterpScheme.Linear)])
