@@ -1392,7 +1392,23 @@ gsgpc_status gsgpc_stats_apply_wtw(gsgpc_ctx* ctx, gsgpc_stats* s, const double*
     upload_stencil_offsets(sd, ctx->stream);
     const double* dv = dev_in(ctx, v, sd.m, "wtw_in");
     DevOut o(ctx, out, sd.m, "wtw_out");
-    run_spmv(ctx->L(), sd, s->stencil(), dv, o.dev);
+    DBuf& fl = ctx->buf("wtw_flag");
+    fl.ensure(sizeof(int));
+    GSGPC_CUDA(cudaMemsetAsync(fl.p, 0, sizeof(int), ctx->stream));
+    run_spmv(ctx->L(), sd, s->stencil(), dv, o.dev, fl.as<int>());
+    int bad = 0;
+    copy_out(ctx, &bad, fl.p, sizeof(int));
+    if (bad) {  // non-finite input met: the rows at stake follow the reference's stored pairs
+      const size_t nt = static_cast<size_t>(s->S_min) * sd.m;
+      DBuf& tb = ctx->buf("touched");
+      tb.ensure(nt);
+      if (!s->loaded_touched.empty()) {
+        GSGPC_CUDA(cudaMemcpyAsync(tb.p, s->loaded_touched.data(), nt, cudaMemcpyHostToDevice, ctx->stream));
+      } else {
+        run_touched(ctx->L(), s->g, s->S_min, s->pat.as<uint8_t>(), tb.as<uint8_t>());
+      }
+      run_spmv_touched(ctx->L(), sd, s->stencil(), dv, tb.as<uint8_t>(), o.dev);
+    }
     o.finish();
   });
 }

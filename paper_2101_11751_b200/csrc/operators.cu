@@ -58,47 +58,6 @@ void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ K3 stencil SpMV
-__device__ __forceinline__ double spmv_node(const StencilDesc& sd, const double* __restrict__ A,
-                                            const double* __restrict__ v, int64_t a) {
-  int64_t co[3] = {0, 0, 0};
-  int64_t r = a;
-  bool interior = true;
-  const int R = sd.W - 1;
-#pragma unroll
-  for (int k = GSGPC_MAX_DIM - 1; k >= 0; --k) {
-    if (k < sd.d) {
-      co[k] = r % sd.sz[k];
-      r /= sd.sz[k];
-      interior = interior && co[k] >= R && co[k] < sd.sz[k] - R;
-    }
-  }
-  const int64_t m = sd.m;
-  double acc = A[a] * v[a];
-  if (interior) {
-    for (int s = 1; s < sd.S_min; ++s) {
-      const int64_t o = c_off_flat[s];
-      acc = fma(A[s * m + a], v[a + o], acc);
-      acc = fma(A[s * m + a - o], v[a - o], acc);
-    }
-  } else {
-    for (int s = 1; s < sd.S_min; ++s) {
-      const int64_t o = c_off_flat[s];
-      bool fwd = true, bwd = true;
-#pragma unroll
-      for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
-        if (k < sd.d) {
-          const int64_t dk = c_off_d[s][k];
-          fwd = fwd && co[k] + dk >= 0 && co[k] + dk < sd.sz[k];
-          bwd = bwd && co[k] - dk >= 0 && co[k] - dk < sd.sz[k];
-        }
-      }
-      if (fwd) acc = fma(A[s * m + a], v[a + o], acc);
-      if (bwd) acc = fma(A[s * m + a - o], v[a - o], acc);
-    }
-  }
-  return acc;
-}
-
 // Check-free variant for the solvers' internal (finite) vectors.  With row-major
 // flattening, a partner node outside the grid maps either outside [0, m) (masked) or to a
 // stored entry that is exactly zero: the pair (a, a+δ) with a+δ off-grid is never touched
@@ -129,15 +88,73 @@ __device__ __forceinline__ double spmv_node_any(const StencilDesc& sd, const dou
   }
 }
 
+// Public apply_wtw.  Every row runs the fast (batched-load, range-mask-only) dot; a row whose
+// sum is not finite sets *flag, and apply_wtw then recomputes those rows with
+// k_spmv_touched, which multiplies only the pairs the reference's CSR stores (its touched
+// pairs, see run_touched): an inf/NaN partner met through an untouched or edge-crossing
+// entry (0·inf = NaN here) is skipped there.  Finite rows are exact either way: the skipped
+// terms are 0·v with v finite.
+template <int SMIN>
 __global__ void __launch_bounds__(256) k_spmv(StencilDesc sd, const double* __restrict__ A,
-                                              const double* __restrict__ v, double* __restrict__ out) {
+                                              const double* __restrict__ v, double* __restrict__ out,
+                                              int* __restrict__ flag) {
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a >= sd.m) return;
-  out[a] = spmv_node(sd, A, v, a);
+  const double acc = spmv_node_fast<SMIN>(sd.m, A, v, a);
+  if (flag && !isfinite(acc)) *flag = 1;
+  out[a] = acc;
 }
 
-void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out) {
-  k_spmv<<<static_cast<unsigned>(ceil_div(sd.m, 256)), 256, 0, L.s>>>(sd, A, v, out);
+__global__ void __launch_bounds__(256) k_spmv_touched(StencilDesc sd, const double* __restrict__ A,
+                                                      const double* __restrict__ v, const uint8_t* __restrict__ touched,
+                                                      double* __restrict__ out) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= sd.m || isfinite(out[a])) return;
+  int64_t co[3] = {0, 0, 0};
+  int64_t r = a;
+#pragma unroll
+  for (int k = GSGPC_MAX_DIM - 1; k >= 0; --k) {
+    if (k < sd.d) {
+      co[k] = r % sd.sz[k];
+      r /= sd.sz[k];
+    }
+  }
+  const int64_t m = sd.m;
+  double acc = touched[a] ? A[a] * v[a] : 0.0;
+  for (int s = 1; s < sd.S_min; ++s) {
+    const int64_t o = c_off_flat[s];
+    bool fwd = true, bwd = true;
+#pragma unroll
+    for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
+      if (k < sd.d) {
+        const int64_t dk = c_off_d[s][k];
+        fwd = fwd && co[k] + dk >= 0 && co[k] + dk < sd.sz[k];
+        bwd = bwd && co[k] - dk >= 0 && co[k] - dk < sd.sz[k];
+      }
+    }
+    if (fwd && touched[s * m + a]) acc = fma(A[s * m + a], v[a + o], acc);
+    if (bwd && touched[s * m + a - o]) acc = fma(A[s * m + a - o], v[a - o], acc);
+  }
+  out[a] = acc;
+}
+
+void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out, int* flag) {
+  const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, 256));
+  switch (sd.S_min) {
+    case 172: k_spmv<172><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    case 25: k_spmv<25><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    case 4: k_spmv<4><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    case 14: k_spmv<14><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    case 5: k_spmv<5><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    default: k_spmv<2><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+  }
+  L.count();
+  GSGPC_CUDA(cudaGetLastError());
+}
+
+void run_spmv_touched(const Launch& L, const StencilDesc& sd, const double* A, const double* v,
+                      const uint8_t* touched, double* out) {
+  k_spmv_touched<<<static_cast<unsigned>(ceil_div(sd.m, 256)), 256, 0, L.s>>>(sd, A, v, touched, out);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }

@@ -75,7 +75,12 @@ struct StencilDesc {
 };
 void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s);
 // out = (W^T W) v ; if dot_out != nullptr also dot(out, dotv) via deterministic partials.
-void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out);
+// flag (optional, device int): set to 1 when some row's sum is not finite (see k_spmv)
+void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out,
+              int* flag = nullptr);
+// recompute the non-finite rows of out over the touched pairs only (touched: [S_min][m] bytes)
+void run_spmv_touched(const Launch& L, const StencilDesc& sd, const double* A, const double* v,
+                      const uint8_t* touched, double* out);
 
 // Kronecker K_G (Toeplitz mode products)
 struct KgDev {

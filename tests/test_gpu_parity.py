@@ -222,6 +222,17 @@ def test_operators_match_oracle(d):
     os_ = O.sufficient_stats(og, x, y, nthreads=4)
     v = np.random.default_rng(0).standard_normal(g.num_points())
     assert rel_err(gs.apply_wtw(v), os_.apply_wtw(v)) <= 1e-10
+    # non-finite entries on touched nodes at the last / first index of the fastest dimension:
+    # the reference's CSR SpMV touches only stored entries, so rows across the grid edge (flat
+    # neighbours, not stencil neighbours) stay finite
+    vb = v.copy()
+    mid = [n // 2 for n in sizes[:-1]]
+    vb[int(np.ravel_multi_index(tuple(mid) + (sizes[-1] - 2,), sizes))] = np.inf
+    vb[int(np.ravel_multi_index(tuple(mid) + (1,), sizes)) + (sizes[-1] if d > 1 else 0)] = np.nan
+    got, ref = gs.apply_wtw(vb), os_.apply_wtw(vb)
+    assert np.array_equal(np.isnan(got), np.isnan(ref)) and np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert fin.sum() > 0 and rel_err(got[fin], ref[fin]) <= 1e-10
     spec = G.KernelSpec(G.Hyperparams(0.1, [0.2, 0.15, 0.3][:d], 1.7))
     kg = G.ToeplitzOperator(g, spec)
     okg = O.ToeplitzOperator(og, [0.2, 0.15, 0.3][:d], 1.7, 0.1)
