@@ -27,6 +27,8 @@ struct PcgMode {
   int TL, TA;
   int64_t tiles, chunks;
   const double* gen;
+  int mm_stride, mm_cw, mm_ach;  // pcg_mode_mma: staged line stride, column tiles and row tiles per block task
+  int mm_tz;                     // offset (doubles) of this mode's mirrored generator in shared memory
 };
 
 struct PcgArgs {
@@ -40,6 +42,8 @@ struct PcgArgs {
   PcgMode mode[3];
   int init;
   int plane;  // d = 3: modes 2 and 1 fused per x0-plane (pcg_plane_modes)
+  int mma;    // Toeplitz modes on the FP64 tensor cores (pcg_mode_mma)
+  int mm_xs;  // shared-memory offset (doubles) of the staged lines; the generators sit below it
   unsigned long long* tbuf;  // optional phase trace: tbuf[iter * 8 + phase] = %globaltimer (ns)
 };
 
@@ -121,6 +125,127 @@ __device__ __forceinline__ void pcg_mode(const PcgMode& c, const double* X, doub
           const double v = acc[r] + s2 * er[r];
           const double sn = eu[r] + beta * es[r];
           const double zn = v + beta * ez[r];
+          a.s[g] = sn;
+          a.z[g] = zn;
+          dot = fma(sn, zn, dot);
+        }
+      }
+    }
+  }
+}
+
+// One Toeplitz mode on the FP64 tensor cores (mma.sync.m8n8k4.f64).  A block task = 8·CW
+// lines × ACH row tiles: the block stages the lines in shared memory with all its threads
+// (many loads in flight), then each warp item (8 lines × 8 outputs) accumulates
+// D[a][line] = Σ_j T[a − j] · X(line, j) over j in k-steps of 4 — A = an 8 × 4 tile of the
+// Toeplitz matrix from the mirrored generator Tz, B = 4 positions × 8 staged lines — in two
+// independent accumulator chains (even / odd k-steps).  The CUDA-core tile kernel ran one
+// 4-output dot of length n per thread on ~L·n/1024 blocks (config 2's 256-node modes: 72 busy
+// blocks, ~12–17 µs per mode).
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int64_t mm_gen_doubles(int64_t n) { return 2 * n + 12; }
+// staged line stride ≡ 4 (mod 16) doubles: the B-fragment loads (8 lines × 4 positions) hit
+// every bank pair twice — 2 wavefronts per 32 doubles
+__host__ __device__ inline int64_t mm_stride(int64_t n) {
+  const int64_t n4 = (n + 3) & ~int64_t{3};
+  return n4 + ((4 - n4 % 16) + 16) % 16;
+}
+
+template <bool EPI>
+__device__ __forceinline__ void pcg_mode_mma(const PcgMode& c, const double* X, double* Y, double* smem,
+                                             const PcgArgs& a, double beta, double s2, double& dot) {
+  const int n = static_cast<int>(c.n);
+  const int64_t inner = c.inner, L = c.L;
+  const int stride = c.mm_stride, CW = c.mm_cw, ACH = c.mm_ach;
+  const double* Tz = smem + c.mm_tz;  // written once at kernel start (pcg_mma_gens)
+  double* Xs = smem + a.mm_xs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r8 = lane >> 2, kq = lane & 3;
+  const int nat = (n + 7) >> 3, nk = (n + 3) >> 2, n4 = 4 * nk;
+  const int TLN = 8 * CW;
+  const int64_t nlb = (L + TLN - 1) / TLN;
+  const int nac = (nat + ACH - 1) / ACH;
+  const int64_t ntask = nlb * nac;
+  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int64_t lb = task / nac;
+    const int ac = static_cast<int>(task - lb * nac);
+    const int64_t l0 = lb * TLN;
+    const int nl = static_cast<int>(imin64(TLN, L - l0));
+    __syncthreads();  // previous task's Xs consumed
+    // stage lines [l0, l0 + nl) × positions [0, n4) (zeros past n and past the last line)
+    const int cnt = TLN * n4;
+    for (int q0 = threadIdx.x; q0 < cnt; q0 += 8 * PCG_NT) {
+      double t[8];
+      int dst[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u * PCG_NT;
+        int ln, j;
+        if (inner == 1) {  // lines contiguous: positions fastest
+          ln = q / n4;
+          j = q - ln * n4;
+        } else {           // positions strided by inner: lines fastest (coalesced)
+          j = q / TLN;
+          ln = q - j * TLN;
+        }
+        dst[u] = q < cnt ? ln * stride + j : -1;
+        const int64_t l = l0 + ln;
+        const bool ok = q < cnt && ln < nl && j < n;
+        const int64_t lo = l / inner, li = l - lo * inner;
+        t[u] = ok ? __ldcg(X + (lo * n + j) * inner + li) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (dst[u] >= 0) Xs[dst[u]] = t[u];
+    }
+    __syncthreads();
+    const int at0 = ac * ACH;
+    const int na = min(ACH, nat - at0);
+    for (int it = warp; it < CW * na; it += PCG_NT / 32) {
+      const int cw = it % CW, at = at0 + it / CW;
+      const double* xs = Xs + (cw * 8 + r8) * stride + kq;
+      const double* tz = Tz + (n + 3) + at * 8 + r8 - kq;
+      const int aa = at * 8 + r8;
+      // epilogue operands issued before the k-loop (their latency hides under the MMAs)
+      int64_t gi[2] = {-1, -1};
+      double er[2] = {0.0, 0.0}, eu[2] = {0.0, 0.0}, es[2] = {0.0, 0.0}, ez[2] = {0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int lc = cw * 8 + 2 * kq + e;
+        if (aa < n && lc < nl) {
+          const int64_t ll = l0 + lc;
+          const int64_t oo = ll / inner, ii = ll - oo * inner;
+          gi[e] = (oo * n + aa) * inner + ii;
+          if (EPI) {
+            er[e] = __ldcg(a.r + gi[e]);
+            eu[e] = __ldcg(a.u + gi[e]);
+            es[e] = __ldcg(a.s + gi[e]);
+            ez[e] = __ldcg(a.z + gi[e]);
+          }
+        }
+      }
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      int s = 0;
+      for (; s + 1 < nk; s += 2) {
+        dmma(d0, d1, tz[-4 * s], xs[4 * s]);
+        dmma(e0, e1, tz[-4 * (s + 1)], xs[4 * (s + 1)]);
+      }
+      if (s < nk) dmma(d0, d1, tz[-4 * s], xs[4 * s]);
+      const double acc[2] = {d0 + e0, d1 + e1};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t g = gi[e];
+        if (g < 0) continue;
+        if (!EPI) {
+          Y[g] = acc[e];
+        } else {
+          const double v = acc[e] + s2 * er[e];
+          const double sn = eu[e] + beta * es[e];
+          const double zn = v + beta * ez[e];
           a.s[g] = sn;
           a.z[g] = zn;
           dot = fma(sn, zn, dot);
@@ -218,7 +343,7 @@ __device__ __forceinline__ void pcg_plane_modes(const PcgArgs& a, double* smem) 
 }
 
 template <int SMIN>
-__global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
+__global__ void __launch_bounds__(PCG_NT, 2) k_efcg_persistent(PcgArgs a) {
   extern __shared__ double smem[];
   __shared__ double sh[8];
   __shared__ double sh1;
@@ -233,6 +358,18 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
   const int tid = blockIdx.x * PCG_NT + threadIdx.x;
   const int nthr = gridDim.x * PCG_NT;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  if (a.mma) {  // mirrored generators of every mode, resident for the whole solve
+    for (int k = 0; k < a.d; ++k) {
+      const int n = static_cast<int>(a.mode[k].n);
+      double* Tz = smem + a.mode[k].mm_tz;  // Tz[(n + 3) + q] = g[|q|] for |q| < n, else 0
+      for (int q = threadIdx.x; q < mm_gen_doubles(n); q += PCG_NT) {
+        const int dq = q - (n + 3);
+        const int ad = dq < 0 ? -dq : dq;
+        Tz[q] = ad < n ? a.mode[k].gen[ad] : 0.0;
+      }
+    }
+    __syncthreads();
+  }
 
   auto spmv_phase = [&]() {
     double dot = 0.0;
@@ -251,6 +388,19 @@ __global__ void __launch_bounds__(PCG_NT) k_efcg_persistent(PcgArgs a) {
     double dot = 0.0;
     const double* src = a.u;
     int k_top = a.d - 1;
+    if (a.mma) {
+      for (int k = k_top; k >= 1; --k) {
+        double* dst = (src == a.t0) ? a.t1 : a.t0;
+        pcg_mode_mma<false>(a.mode[k], src, dst, smem, a, beta, s2, dot);
+        grid.sync();
+        stamp(5 - k);
+        src = dst;
+      }
+      pcg_mode_mma<true>(a.mode[0], src, nullptr, smem, a, beta, s2, dot);
+      const double bs = block_sum<PCG_NT>(dot, sh);
+      if (threadIdx.x == 0) a.part_b[blockIdx.x] = bs;
+      return;
+    }
     if (a.plane) {
       pcg_plane_modes(a, smem);
       grid.sync();
@@ -422,7 +572,42 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     a.mode[k] = mode_cfg(kg, k);
     smem = std::max(smem, sizeof(double) * static_cast<size_t>(toep_smem_doubles(a.mode[k].n, a.mode[k].TL)));
   }
-  if (kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {  // GSGPC_CG_NOPLANE=1: three mode phases (diagnostics)
+  // FP64 tensor-core modes whenever every mode has enough lines to fill the grid (d ≥ 2 at
+  // the BASELINE sizes; d = 1 has a single line).  GSGPC_CG_TOEP_SIMT=1: the CUDA-core tiles.
+  static const bool simt = [] {
+    const char* e = getenv("GSGPC_CG_TOEP_SIMT");
+    return e && e[0] == '1';
+  }();
+  bool mma = !simt && kg.d >= 2;
+  int64_t gens = 0;
+  for (int k = 0; k < kg.d; ++k) gens += mm_gen_doubles(a.mode[k].n);
+  size_t mm_smem = 0;
+  for (int k = 0, tz = 0; k < kg.d && mma; ++k) {
+    PcgMode& c = a.mode[k];
+    const int64_t st = mm_stride(c.n);
+    const int64_t cwmax = std::min<int64_t>(8, (6144 - gens) / (8 * st));
+    if (c.L < 64 || cwmax < 1) {
+      mma = false;
+      break;
+    }
+    const int64_t target = 296;  // one block task per resident block (2 per SM), one wave
+    const int64_t nlt = ceil_div(c.L, 8);
+    const int64_t cw = std::max<int64_t>(1, std::min<int64_t>(cwmax, ceil_div(nlt, target)));
+    const int64_t nlb = ceil_div(nlt, cw);
+    const int64_t nat = ceil_div(c.n, 8);
+    const int64_t nac = std::max<int64_t>(1, std::min<int64_t>(nat, target / nlb));
+    c.mm_stride = static_cast<int>(st);
+    c.mm_cw = static_cast<int>(cw);
+    c.mm_ach = static_cast<int>(ceil_div(nat, nac));
+    c.mm_tz = tz;
+    tz += static_cast<int>(mm_gen_doubles(c.n));
+    mm_smem = std::max(mm_smem, sizeof(double) * static_cast<size_t>(gens + 8 * cw * st));
+  }
+  a.mm_xs = static_cast<int>(gens);
+  if (mma) smem = std::max(smem, mm_smem);
+  if (mma) {
+    a.mma = 1;
+  } else if (kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {  // GSGPC_CG_NOPLANE=1: three mode phases (diagnostics)
     const int64_t n1 = a.mode[1].n, n2 = a.mode[2].n;
     const int64_t need = toep_ts_doubles(n1) + toep_ts_doubles(n2) + 2 * n1 * n2;
     if (need <= 6144) {
