@@ -44,6 +44,8 @@ struct PcgArgs {
   int plane;  // d = 3: modes 2 and 1 fused per x0-plane (pcg_plane_modes)
   int mma;    // Toeplitz modes on the FP64 tensor cores (pcg_mode_mma)
   int mm_xs;  // shared-memory offset (doubles) of the staged lines; the generators sit below it
+  int mm_plane;              // d = 3: modes 2 and 1 fused per x0-plane on the tensor cores (pcg_plane_mma)
+  int mp_parts, mp_ys;       // pcg_plane_mma: parts per plane, row stride of the mode-2 image
   unsigned long long* tbuf;  // optional phase trace: tbuf[iter * 8 + phase] = %globaltimer (ns)
 };
 
@@ -255,6 +257,96 @@ __device__ __forceinline__ void pcg_mode_mma(const PcgMode& c, const double* X, 
   }
 }
 
+// One warp item of a tensor-core mode product from shared memory: D[a][col] for the 8 rows
+// a = at·8 + r8 and the 8 columns of the tile, D = Σ_j T[a − j] · B(j, col), with
+// B(j, col) = xs[j · js + col · cs] (j = 4 s + kq, col = r8 for the fragment load).
+__device__ __forceinline__ void mm_item(const double* Tz, int n, int at, const double* xs, int js, int cs, int r8,
+                                        int kq, double* acc) {
+  const double* tz = Tz + (n + 3) + at * 8 + r8 - kq;
+  const double* xb = xs + kq * js + r8 * cs;
+  const int nk = (n + 3) >> 2;
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  int s = 0;
+  for (; s + 1 < nk; s += 2) {
+    dmma(d0, d1, tz[-4 * s], xb[4 * s * js]);
+    dmma(e0, e1, tz[-4 * (s + 1)], xb[4 * (s + 1) * js]);
+  }
+  if (s < nk) dmma(d0, d1, tz[-4 * s], xb[4 * s * js]);
+  acc[0] = d0 + e0;
+  acc[1] = d1 + e1;
+}
+
+// d = 3, tensor cores: modes 2 and 1 of K_G û in ONE grid phase.  Task = (x0-plane p, part):
+// stage the plane X[i1][i2] (row stride mm_stride(n2), zero-padded), mode 2 over all of it
+// into Y[i1][a2] (row stride mp_ys ≡ 8 mod 16 so the mode-1 fragment loads are
+// conflict-free), then mode 1 for the part's a1 row tiles → t0.  Each part redoes the
+// plane's mode 2 (n1·n2² MACs, a few hundred MMAs) instead of paying a grid barrier and a
+// second phase.
+__device__ __forceinline__ void pcg_plane_mma(const PcgArgs& a, double* smem) {
+  const PcgMode &c1 = a.mode[1], &c2 = a.mode[2];
+  const int n0 = static_cast<int>(a.mode[0].n), n1 = static_cast<int>(c1.n), n2 = static_cast<int>(c2.n);
+  const int xs_st = c2.mm_stride, ys_st = a.mp_ys, P = a.mp_parts;
+  const int n1p = (n1 + 7) & ~7, n2p4 = (n2 + 3) & ~3, n1p4 = (n1 + 3) & ~3;
+  const double* T2 = smem + c2.mm_tz;
+  const double* T1 = smem + c1.mm_tz;
+  double* X = smem + a.mm_xs;
+  double* Y = X + static_cast<int64_t>(n1p) * xs_st;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r8 = lane >> 2, kq = lane & 3;
+  const int nat1 = (n1 + 7) >> 3, nat2 = (n2 + 7) >> 3, nlt2 = n1p >> 3, nlt1 = (n2 + 7) >> 3;
+  for (int task = blockIdx.x; task < n0 * P; task += gridDim.x) {
+    const int p = task / P, part = task - p * P;
+    const double* src = a.u + static_cast<int64_t>(p) * n1 * n2;
+    __syncthreads();
+    // stage rows i1 < n1p, positions < n2p4 (zeros outside the plane)
+    const int cnt = n1p * n2p4;
+    for (int q0 = threadIdx.x; q0 < cnt; q0 += 8 * PCG_NT) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u * PCG_NT;
+        const int i1 = q / n2p4, i2 = q - i1 * n2p4;
+        t[u] = (q < cnt && i1 < n1 && i2 < n2) ? __ldcg(src + i1 * n2 + i2) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u * PCG_NT;
+        const int i1 = q / n2p4, i2 = q - i1 * n2p4;
+        if (q < cnt) X[i1 * xs_st + i2] = t[u];
+      }
+    }
+    // Y rows past n1 (read as zero positions by mode 1)
+    for (int q = threadIdx.x; q < (n1p4 - n1) * ys_st; q += PCG_NT) Y[n1 * ys_st + q] = 0.0;
+    __syncthreads();
+    // mode 2: lines i1 (columns), positions i2 → Y[i1][a2]
+    for (int it = warp; it < nlt2 * nat2; it += PCG_NT / 32) {
+      const int lt = it / nat2, at = it - lt * nat2;
+      double acc[2];
+      mm_item(T2, n2, at, X + lt * 8 * xs_st, 1, xs_st, r8, kq, acc);
+      const int a2 = at * 8 + r8;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i1 = lt * 8 + 2 * kq + e;
+        if (a2 < n2) Y[i1 * ys_st + a2] = acc[e];  // rows ≥ n1 hold zeros' images (0)
+      }
+    }
+    __syncthreads();
+    // mode 1 for this part's a1 row tiles: lines i2 (columns), positions i1 → t0[p][a1][i2]
+    const int q_lo = part * nat1 / P, q_hi = (part + 1) * nat1 / P;
+    double* dst = a.t0 + static_cast<int64_t>(p) * n1 * n2;
+    for (int it = warp; it < nlt1 * (q_hi - q_lo); it += PCG_NT / 32) {
+      const int lt = it % nlt1, at = q_lo + it / nlt1;
+      double acc[2];
+      mm_item(T1, n1, at, Y + lt * 8, ys_st, 1, r8, kq, acc);
+      const int a1 = at * 8 + r8;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i2 = lt * 8 + 2 * kq + e;
+        if (a1 < n1 && i2 < n2) dst[a1 * n2 + i2] = acc[e];
+      }
+    }
+  }
+}
+
 // d = 3: the last two Toeplitz modes of K_G û in ONE grid phase.  Work item = (x0-plane p,
 // part q of the plane's x1 outputs): the block stages the plane (n1 × n2) in shared memory,
 // applies mode 2 to all of it, then mode 1 for its x1 outputs only — the plane's mode 2 is
@@ -389,6 +481,13 @@ __global__ void __launch_bounds__(PCG_NT, 2) k_efcg_persistent(PcgArgs a) {
     const double* src = a.u;
     int k_top = a.d - 1;
     if (a.mma) {
+      if (a.mm_plane) {
+        pcg_plane_mma(a, smem);
+        grid.sync();
+        stamp(3);
+        src = a.t0;
+        k_top = 0;
+      }
       for (int k = k_top; k >= 1; --k) {
         double* dst = (src == a.t0) ? a.t1 : a.t0;
         pcg_mode_mma<false>(a.mode[k], src, dst, smem, a, beta, s2, dot);
@@ -511,6 +610,8 @@ static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
   static size_t grid_smem = 0;
   if (grid == 0 || grid_smem != smem) {
     int dev = 0, sms = 0, per_sm = 0;
+    GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
     GSGPC_CUDA(cudaGetDevice(&dev));
     GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
@@ -604,6 +705,22 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     mm_smem = std::max(mm_smem, sizeof(double) * static_cast<size_t>(gens + 8 * cw * st));
   }
   a.mm_xs = static_cast<int>(gens);
+  if (mma && kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {
+    // plane fusion of modes 2 and 1 when the staged plane and its mode-2 image fit in 48 KB
+    // per block.  Measured (B200, per iteration): config 3 (80·20-node planes) modes
+    // 23.6 → 18.9 µs; config 5 (64·64-node planes, 75 KB) 25.3 → 26.2 µs — there every part
+    // re-stages and re-transforms a 4096-node plane, more than the saved barrier.
+    const int64_t n0 = a.mode[0].n, n1 = a.mode[1].n, n2 = a.mode[2].n;
+    const int64_t n1p = (n1 + 7) & ~int64_t{7}, n1p4 = (n1 + 3) & ~int64_t{3};
+    const int64_t ys = ((n2 + 7) & ~int64_t{7}) + ((((n2 + 7) & ~int64_t{7}) % 16) == 0 ? 8 : 0);
+    const int64_t need = gens + n1p * mm_stride(n2) + std::max(n1p, n1p4) * ys;
+    if (need * 8 <= 48 * 1024) {
+      a.mm_plane = 1;
+      a.mp_ys = static_cast<int>(ys);
+      a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 296 / n0)));
+      smem = std::max(smem, static_cast<size_t>(need * 8));
+    }
+  }
   if (mma) smem = std::max(smem, mm_smem);
   if (mma) {
     a.mma = 1;
