@@ -612,6 +612,9 @@ static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
     int dev = 0, sms = 0, per_sm = 0;
     GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+    // smallest shared-memory carveout that holds two blocks: the rest is L1
+    const int pct = static_cast<int>(std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+    GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     GSGPC_CUDA(cudaGetDevice(&dev));
     GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
@@ -705,6 +708,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     mm_smem = std::max(mm_smem, sizeof(double) * static_cast<size_t>(gens + 8 * cw * st));
   }
   a.mm_xs = static_cast<int>(gens);
+  size_t mp_smem = 0;
   if (mma && kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {
     // plane fusion of modes 2 and 1 when the staged plane and its mode-2 image fit in 48 KB
     // per block.  Measured (B200, per iteration): config 3 (80·20-node planes) modes
@@ -718,10 +722,13 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
       a.mm_plane = 1;
       a.mp_ys = static_cast<int>(ys);
       a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 296 / n0)));
-      smem = std::max(smem, static_cast<size_t>(need * 8));
+      mp_smem = static_cast<size_t>(need * 8);
     }
   }
-  if (mma) smem = std::max(smem, mm_smem);
+  // the tensor-core path needs only its own shared memory (generators + staged lines /
+  // plane): the rest of the SM's 256 KB stays L1, which serves the SpMV's vector and
+  // mirrored-stencil reads
+  if (mma) smem = std::max(mm_smem, a.mm_plane ? mp_smem : size_t{0});
   if (mma) {
     a.mma = 1;
   } else if (kg.d == 3 && !getenv("GSGPC_CG_NOPLANE")) {  // GSGPC_CG_NOPLANE=1: three mode phases (diagnostics)
