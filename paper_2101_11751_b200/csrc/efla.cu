@@ -32,6 +32,8 @@ constexpr int EF_MAXP = 32;
 // stencil offsets for this translation unit (no relocatable device code)
 __constant__ long long c_off_flat[172];
 __constant__ signed char c_off_d[172][4];
+__constant__ int c_pen_ob[49];
+__constant__ int c_pen_s[49][7];
 
 static void ef_upload_offsets(const StencilDesc& sd, cudaStream_t s) {
   const int E = 2 * sd.W - 1;
@@ -56,6 +58,31 @@ static void ef_upload_offsets(const StencilDesc& sd, cudaStream_t s) {
   }
   GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_flat, flat, sizeof(long long) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
   GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_d, dd, sizeof(dd[0]) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
+  // pencils of the full stencil along the last dimension (k_spmm_pencil): base flat offset of
+  // pencil q (last digit 0) and, per last-dimension shift, the stored half index (≥ 0: the
+  // entry sits at the node itself) or −(index + 1) (mirrored: at the partner node)
+  int npen = 1;
+  for (int k = 0; k + 1 < sd.d; ++k) npen *= E;
+  int pen_ob[49];
+  int pen_s[49][7];
+  for (int q = 0; q < npen; ++q) {
+    int dig[3] = {0, 0, 0};
+    int r = q;
+    for (int k = sd.d - 2; k >= 0; --k) {
+      dig[k] = r % E - (sd.W - 1);
+      r /= E;
+    }
+    long long f = 0;
+    for (int k = 0; k < sd.d; ++k) f = f * sd.sz[k] + (k + 1 < sd.d ? dig[k] : 0);
+    pen_ob[q] = static_cast<int>(f);
+    for (int t = 0; t < E; ++t) {
+      int full = 0;
+      for (int k = 0; k < sd.d; ++k) full = full * E + (k + 1 < sd.d ? dig[k] : t - (sd.W - 1)) + (sd.W - 1);
+      pen_s[q][t] = full >= c0 ? full - c0 : -((S - 1 - full) - c0) - 1;
+    }
+  }
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pen_ob, pen_ob, sizeof(int) * npen, 0, cudaMemcpyHostToDevice, s));
+  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pen_s, pen_s, sizeof(pen_s[0]) * npen, 0, cudaMemcpyHostToDevice, s));
 }
 
 struct EfScal {
@@ -213,8 +240,94 @@ __global__ void __launch_bounds__(128) k_spmm(int64_t m, const double* __restric
     if (p < P && !(sc && sc[p].done)) out[p * m + a] = acc[p];
 }
 
+// Batched SpMV over P right-hand sides, tiled along the last grid dimension.  The grid-stride
+// version (k_spmm) read x[p][a ± o_s] for 2·S_min offsets × P vectors per node straight from
+// L2 (P = 30 vectors of 2 MB do not stay in L1): ~21 GB of L2 traffic per call at config 5.
+// Here a block owns T = 128 consecutive nodes; for each pencil of the full stencil (the E
+// offsets that differ only in the last dimension, E^(d−1) pencils) it stages the P windows
+// x[p][a0 + o_pencil − (W−1) .. + T + (W−1)) in shared memory once and every node then
+// applies the pencil's E coefficients from it — x is read ~E× less from L2.  Coefficients
+// come from the stored half at the node (A[s][a]) or mirrored at the partner (A[s'][a + o]);
+// partners across the grid edge meet stored exact zeros (check-free, finite vectors).
+constexpr int PEN_T = 128;
+
+template <int PB, int W>
+__global__ void __launch_bounds__(PEN_T) k_spmm_pencil(int m, int npen, const double* __restrict__ A,
+                                                       const double* __restrict__ x, double* __restrict__ out, int P,
+                                                       const EfScal* sc) {
+  constexpr int E = 2 * W - 1, WL = PEN_T + 2 * (W - 1);
+  extern __shared__ double win[];  // [P][WL]
+  const int a0 = blockIdx.x * PEN_T;
+  const int a = a0 + threadIdx.x;
+  double acc[PB];
+#pragma unroll
+  for (int p = 0; p < PB; ++p) acc[p] = 0.0;
+  for (int q = 0; q < npen; ++q) {
+    const int ob = c_pen_ob[q];
+    __syncthreads();
+    for (int i = threadIdx.x; i < P * WL; i += PEN_T) {
+      const int p = i / WL, t = i - p * WL;
+      const int g = a0 + ob - (W - 1) + t;
+      win[i] = (g >= 0 && g < m) ? __ldcg(x + static_cast<int64_t>(p) * m + g) : 0.0;
+    }
+    __syncthreads();
+    if (a < m) {
+#pragma unroll
+      for (int t = 0; t < E; ++t) {
+        const int sidx = c_pen_s[q][t];
+        const int o = ob + t - (W - 1);
+        double c;
+        if (sidx >= 0) {
+          c = __ldg(A + static_cast<int64_t>(sidx) * m + a);
+        } else {
+          const int b = a + o;
+          c = (b >= 0 && b < m) ? __ldg(A + static_cast<int64_t>(-sidx - 1) * m + b) : 0.0;
+        }
+        const double* wp = win + threadIdx.x + t;
+#pragma unroll
+        for (int p = 0; p < PB; ++p)
+          if (p < P) acc[p] = fma(c, wp[p * WL], acc[p]);
+      }
+    }
+  }
+  if (a < m) {
+#pragma unroll
+    for (int p = 0; p < PB; ++p)
+      if (p < P && !(sc && sc[p].done)) out[static_cast<int64_t>(p) * m + a] = acc[p];
+  }
+}
+
 static void launch_spmm(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P,
                         const EfScal* sc) {
+  static const bool grid_stride = [] {
+    const char* e = getenv("GSGPC_SPMM_GRID");
+    return e && e[0] == '1';
+  }();
+  if (!grid_stride && sd.d >= 2 && sd.m < (int64_t{1} << 31)) {
+    int npen = 1;
+    for (int k = 0; k + 1 < sd.d; ++k) npen *= 2 * sd.W - 1;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, PEN_T));
+    const int WL = PEN_T + 2 * (sd.W - 1);
+    const size_t smem = sizeof(double) * static_cast<size_t>(P) * WL;
+    if (sd.W == 4) {
+      static bool attr = false;
+      if (!attr) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_spmm_pencil<EF_MAXP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 6))));
+        attr = true;
+      }
+      k_spmm_pencil<EF_MAXP, 4><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+    } else {
+      static bool attr = false;
+      if (!attr) {
+        GSGPC_CUDA(cudaFuncSetAttribute(k_spmm_pencil<EF_MAXP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 2))));
+        attr = true;
+      }
+      k_spmm_pencil<EF_MAXP, 2><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+    }
+    return;
+  }
   const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, 128));
   switch (sd.S_min) {
     case 172: k_spmm<EF_MAXP, 172><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
