@@ -19,6 +19,9 @@ namespace cg = cooperative_groups;
 namespace gsgpc {
 
 constexpr int PCG_NT = 256;
+#ifndef PCG_MINB
+#define PCG_MINB 2  // resident blocks per SM (register cap 65536 / (256 · MINB))
+#endif
 
 __constant__ int c_pcg_off[172];
 
@@ -435,7 +438,7 @@ __device__ __forceinline__ void pcg_plane_modes(const PcgArgs& a, double* smem) 
 }
 
 template <int SMIN>
-__global__ void __launch_bounds__(PCG_NT, 2) k_efcg_persistent(PcgArgs a) {
+__global__ void __launch_bounds__(PCG_NT, PCG_MINB) k_efcg_persistent(PcgArgs a) {
   extern __shared__ double smem[];
   __shared__ double sh[8];
   __shared__ double sh1;
