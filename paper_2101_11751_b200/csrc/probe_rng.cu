@@ -5,7 +5,9 @@
 // takes bit 0 (1 → +1, 0 → −1).  The streams are sequential, so each probe runs on one warp:
 // the 312-word MT19937-64 twist is split into its three dependency phases (i < n−m from the
 // old state; n−m ≤ i < n−1 from the new words i−(n−m); i = n−1 last), 32 words at a time, and
-// the tempered outputs of a block are written one byte per row (coalesced).  A second kernel
+// the tempered outputs of a block are written one byte per row (coalesced).  The default is
+// the block-per-probe variant below (k_probe_rng_blk: state in registers, one barrier per
+// twist; config 5's 30 × 5e7 draws 112 → 44 ms); GSGPC_PROBE_RNG_WARP=1 selects this one.  A second kernel
 // packs the bytes into one 64-bit word per row (bit p = probe p), the layout the binning
 // carries with the rows.  The initial state is built on the host exactly as
 // mersenne_twister_engine(seed_seq&) does ([rand.eng.mers]: generate 2n 32-bit words,
@@ -14,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <random>
 #include <vector>
 
@@ -122,6 +125,71 @@ __global__ void __launch_bounds__(32) k_probe_rng(uint64_t* __restrict__ states,
   if (lane == 0) st[MT_N] = static_cast<uint64_t>(idx);
 }
 
+// One block per probe (the warp version above spends most of its time on the serial shuffle
+// chain of the twist: ~0.45e9 draws/s per probe).  Thread j < 156 keeps words j and 156 + j
+// of the state in registers; a twist needs only thread j + 1's old words (exchanged through a
+// double-buffered shared array, one barrier per twist):
+//   new[j]       = mix(old[j], old[j + 1], old[j + 156])          (old[156] = thread 0's 2nd word)
+//   new[156 + j] = mix(old[156 + j], old[157 + j], new[j])        (j < 155)
+//   new[311]     = mix(old[311], new[0], new[155])                (thread 155 recomputes new[0])
+// then every thread tempers its two new words into the byte planes.
+constexpr int MT_BT = 160;  // 5 warps; threads ≥ 156 only help with the global state copy
+
+__global__ void __launch_bounds__(MT_BT) k_probe_rng_blk(uint64_t* __restrict__ states, int64_t rows,
+                                                         uint8_t* __restrict__ planes) {
+  __shared__ uint64_t xa[2][MT_M + 1], xb[2][MT_M + 1];
+  const int p = blockIdx.x, j = threadIdx.x;
+  const bool act = j < MT_M;
+  uint64_t* st = states + static_cast<int64_t>(p) * (MT_N + 1);
+  uint64_t wa = act ? st[j] : 0ull, wb = act ? st[MT_M + j] : 0ull;
+  int idx = static_cast<int>(st[MT_N]);
+  uint8_t* out = planes + static_cast<int64_t>(p) * rows;
+  int64_t done = 0;
+  if (idx < MT_N) {  // draws left in the current state
+    const int k = static_cast<int>(imin64(MT_N - idx, rows));
+    if (act) {
+      if (j >= idx && j - idx < k) out[j - idx] = static_cast<uint8_t>(mt_temper_bit0(wa));
+      const int w2 = MT_M + j;
+      if (w2 >= idx && w2 - idx < k) out[w2 - idx] = static_cast<uint8_t>(mt_temper_bit0(wb));
+    }
+    idx += k;
+    done += k;
+  }
+  int buf = 0;
+  while (done < rows) {
+    if (act) {
+      xa[buf][j] = wa;
+      xb[buf][j] = wb;
+    }
+    __syncthreads();
+    if (act) {
+      const uint64_t a1 = j + 1 < MT_M ? xa[buf][j + 1] : xb[buf][0];  // old[j + 1]
+      const uint64_t na = mt_mix(wa, a1, wb);
+      uint64_t nb;
+      if (j + 1 < MT_M) {
+        nb = mt_mix(wb, xb[buf][j + 1], na);
+      } else {  // word 311: new[0] recomputed from thread 0's and 1's old words
+        const uint64_t n0 = mt_mix(xa[buf][0], xa[buf][1], xb[buf][0]);
+        nb = mt_mix(wb, n0, na);
+      }
+      wa = na;
+      wb = nb;
+      const int k = static_cast<int>(imin64(MT_N, rows - done));
+      if (j < k) out[done + j] = static_cast<uint8_t>(mt_temper_bit0(wa));
+      if (MT_M + j < k) out[done + MT_M + j] = static_cast<uint8_t>(mt_temper_bit0(wb));
+    }
+    const int k = static_cast<int>(imin64(MT_N, rows - done));
+    done += k;
+    idx = k;
+    buf ^= 1;
+  }
+  if (act) {
+    st[j] = wa;
+    st[MT_M + j] = wb;
+  }
+  if (j == 0) st[MT_N] = static_cast<uint64_t>(idx);
+}
+
 // words[i] = Σ_p planes[p][i] << p
 __global__ void __launch_bounds__(256) k_probe_pack(const uint8_t* __restrict__ planes, int P, int64_t rows,
                                                     uint64_t* __restrict__ words) {
@@ -138,7 +206,12 @@ void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8
   const int64_t slab = probe_rng_slab();
   for (int64_t r0 = 0; r0 < rows; r0 += slab) {
     const int64_t nr = std::min(slab, rows - r0);
-    k_probe_rng<<<P, 32, 0, L.s>>>(states, nr, planes);
+    static const bool warp_rng = [] {
+      const char* e = getenv("GSGPC_PROBE_RNG_WARP");
+      return e && e[0] == '1';
+    }();
+    if (warp_rng) k_probe_rng<<<P, 32, 0, L.s>>>(states, nr, planes);
+    else k_probe_rng_blk<<<P, MT_BT, 0, L.s>>>(states, nr, planes);
     k_probe_pack<<<static_cast<unsigned>(ceil_div(nr, 256)), 256, 0, L.s>>>(planes, P, nr, words + r0);
     L.count(2);
   }
