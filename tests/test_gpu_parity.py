@@ -409,6 +409,67 @@ def test_full_size_config3_properties():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("cfg_id,n", [(1, None), (2, None), (4, 100_000_000), (5, None)])
+def test_full_size_properties_other_configs(cfg_id, n):
+    """BASELINE configs 1, 2, 4 (at 1e8 rows) and 5 at full size through size-independent
+    invariants: partition of unity Σ_ab (W^T W)_ab = n (every in-grid row's weights sum to 1 in
+    each dimension), Σ_a (W^T y)_a = Σ y, yᵀy, n, the symmetric structure bound (≤ 7^d per row)
+    and batch-split invariance (two add() calls = one)."""
+    import torch
+
+    from paper_2101_11751_b200 import synthetic as S
+
+    cfg = S.CONFIGS[cfg_id]
+    rows = S.generate_torch(cfg_id, n, device="cuda")
+    g = S.grid_for(cfg)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, rows)
+    nn = rows.shape[0]
+    assert gs.n() == nn
+    vals, _ = gs.stencil()
+    total = vals[0].sum() + 2.0 * vals[1:].sum()
+    assert abs(total - nn) <= 1e-9 * nn
+    yv = rows[:, cfg.d].double()
+    ysum = yv.sum().item()
+    assert abs(gs.wty().sum() - ysum) <= 1e-9 * max(abs(ysum), float(nn) ** 0.5) + 1e-6
+    yty = (yv ** 2).sum().item()
+    assert abs(gs.yty() - yty) <= 1e-10 * yty
+    assert gs.max_row_nnz() <= 7 ** cfg.d
+    acc = G.SufficientStatsAccumulator(g)
+    h = nn // 3
+    acc.add(rows[:h])
+    acc.add(rows[h:])
+    st2 = acc.finalize()
+    assert rel_err(st2.stencil()[0], vals) <= 1e-10
+    assert rel_err(st2.wty(), gs.wty()) <= 1e-10
+    del rows
+    torch.cuda.empty_cache()
+
+
+def test_full_size_config2_solve_reproducible():
+    """Config 2 at full n: two factorized-CG posterior-mean solves (gp.cpp:326-352) on the same
+    statistics are bitwise identical (the persistent kernel reduces every dot in a fixed
+    order), over a fixed window of 400 iterations (at tol 1e-6 this system needs more than
+    5000), with a decreasing residual trace."""
+    from paper_2101_11751_b200 import synthetic as S
+
+    cfg = S.CONFIGS[2]
+    rows = S.generate_torch(2, device="cuda")
+    g = S.grid_for(cfg)
+    st = G.sufficient_stats(g, G.InterpScheme.Cubic, rows)
+    del rows
+    kg = G.ToeplitzOperator(g, S.kernel_for(cfg))
+    s2 = cfg.noise_std ** 2
+    r0 = -kg.apply(st.wty()) / s2
+    tol = G.GridRhsTolerance(eps_abs=cfg.tol * cfg.tol * st.yty())
+    a = G.factorized_cg_grid_rhs(kg, st, r0, cfg.noise_std, tol, 400)
+    b = G.factorized_cg_grid_rhs(kg, st, r0, cfg.noise_std, tol, 400)
+    assert a.iterations == b.iterations == 400 and not a.converged
+    assert np.array_equal(np.asarray(a.xhat_d), np.asarray(b.xhat_d))
+    assert np.array_equal(np.asarray(a.residual_trace), np.asarray(b.residual_trace))
+    tr = np.asarray(a.residual_trace)
+    assert np.all(np.isfinite(tr)) and tr[-1] < 1e-2 * tr[0]
+
+
 @pytest.mark.parametrize("where", ["host", "device"])
 def test_point_layouts_columns_and_strided_records(where):
     """gsgpc_points layouts beyond the Python helpers' (x, y) and packed rows: columnar SoA
