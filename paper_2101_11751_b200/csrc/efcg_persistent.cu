@@ -19,6 +19,9 @@ namespace cg = cooperative_groups;
 namespace gsgpc {
 
 constexpr int PCG_NT = 256;
+#ifndef PCG_SPMV_U
+#define PCG_SPMV_U 8  // offsets per load batch in the SpMV phase
+#endif
 #ifndef PCG_MINB
 #define PCG_MINB 2  // resident blocks per SM (register cap 65536 / (256 · MINB))
 #endif
@@ -79,7 +82,7 @@ struct PcgOff {
 template <int SMIN>
 __device__ __forceinline__ double pcg_spmv_node(int m, const double* __restrict__ A, const double* __restrict__ v,
                                                 int a) {
-  return stencil_row_dot<SMIN>(m, A, v, a, PcgOff{});
+  return stencil_row_dot<SMIN, PcgOff, PCG_SPMV_U>(m, A, v, a, PcgOff{});
 }
 
 // One Toeplitz mode product (grid-stride over line tiles × output chunks).  EPI: fused

@@ -22,10 +22,9 @@ namespace gsgpc {
 // persistent EFCG kernel, which rewrites v between grid barriers: grid.sync() invalidates
 // L1 (CCTL.IVALL in the SASS).  Measured: config 3 SpMV phase 52 → 47.5 µs, config 5
 // 102 → 91 µs, versus L2-only (ld.global.cg) loads.
-template <int SMIN, typename OFF>
+template <int SMIN, typename OFF, int U = 8>
 __device__ __forceinline__ double stencil_row_dot(int m, const double* __restrict__ A, const double* __restrict__ v,
                                                   int a, OFF off) {
-  constexpr int U = 8;
   auto ldv = [&](int i) -> double { return __ldca(v + i); };
   double acc0 = __ldg(A + a) * ldv(a), acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
   int s = 1;
