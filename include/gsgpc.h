@@ -18,7 +18,10 @@
  * single pass would have thrown.  A failed call leaves its handles unchanged.
  *
  * Threading: one CUDA stream per context; calls on one context are serialised by the
- * caller (the C++/Python wrappers do this).  Contexts on different devices are
+ * caller (the C++/Python wrappers do this).  Device-resident inputs are read on the
+ * context's stream (gsgpc_ctx_stream / gsgpc_ctx_set_stream): the caller orders their
+ * producers before the call (the Python mirror waits for torch's current stream), and
+ * device-resident outputs are complete once the context's stream is.  Contexts on different devices are
  * independent; multi-GPU precompute combines per-device statistics with an all-reduce
  * over gsgpc_stats_reduce_buffer() (merge() semantics, interp.cpp:202-210).
  */

@@ -71,13 +71,23 @@ struct PinnedBuf {
   }
 };
 
+// cudaPointerGetAttributes may hand back an error an earlier call left pending (runtime calls
+// report the last recorded non-sticky error); that must not turn a device pointer into a
+// "host" one, so a failure clears the error and asks once more.
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a{};
-  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
   if (e != cudaSuccess) {
+    static const bool dbg = getenv("GSGPC_DEBUG_PTR") != nullptr;
+    if (dbg) fprintf(stderr, "[gsgpc] cudaPointerGetAttributes: %s (retrying)\n", cudaGetErrorString(e));
     cudaGetLastError();
-    return false;
+    a = cudaPointerAttributes{};
+    e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
   }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
@@ -439,6 +449,11 @@ void finalize_stats(gsgpc_ctx* ctx, gsgpc_stats* s) {
   const int64_t ws = finalize_ws_elems(s->g);
   DBuf& w = ctx->buf("finalize_ws");
   w.ensure(sizeof(double) * ws);
+  static const bool poison = [] {  // diagnostics: NaN-fill the workspace (reads of unwritten data show up)
+    const char* e = getenv("GSGPC_DEBUG_POISON_WS");
+    return e && e[0] == '1';
+  }();
+  if (poison) GSGPC_CUDA(cudaMemsetAsync(w.p, 0xFF, sizeof(double) * ws, ctx->stream));
   run_finalize(L, s->g, s->mom.as<double>(), s->probes, s->probes ? s->pmom.as<double>() : nullptr, s->stencil(),
                s->wty(), s->pimg(), w.as<double>(), ws);
   // tail: yty, n

@@ -177,6 +177,10 @@ class _Arr:
                 if writable:
                     raise InvalidArgument("output tensor must be contiguous")
                 t = t.contiguous()
+            if t.is_cuda:
+                # the library runs on its own stream: the work torch queued for this tensor
+                # (its producer, or the conversion above) must be complete before it reads it
+                torch.cuda.current_stream(t.device).synchronize()
             self.keep = t
             self.ptr = t.data_ptr()
             self.device = t.is_cuda
@@ -473,6 +477,8 @@ class SufficientStats:
         out = np.zeros(self.grid_size()) if out is None else out
         oa = _Arr(out, np.float64, writable=True)
         self._ctx.check(_L.load().gsgpc_stats_copy_wty(self._ctx.handle, self._h, oa.vp))
+        if oa.device:  # results on the library stream: complete before torch uses them
+            self._ctx.synchronize()
         return out
 
     def stencil(self):
@@ -524,6 +530,8 @@ class SufficientStats:
         oa = _Arr(out, np.float64, writable=True)
         self._ctx.check(_L.load().gsgpc_stats_apply_wtw(self._ctx.handle, self._h, va.vp, oa.vp))
         self._wtw_count += 1
+        if oa.device:  # results on the library stream: complete before torch uses them
+            self._ctx.synchronize()
         return out
 
     def matvec_count(self) -> int:
@@ -765,6 +773,8 @@ class ToeplitzOperator:
         oa = _Arr(out, np.float64, writable=True)
         self._ctx.check(_L.load().gsgpc_kg_apply(self._ctx.handle, self._h, va.vp, oa.vp))
         self._count += 1
+        if oa.device:  # results on the library stream: complete before torch uses them
+            self._ctx.synchronize()
         return out
 
     def matvec_count(self) -> int:
