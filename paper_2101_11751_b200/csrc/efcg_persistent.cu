@@ -628,9 +628,18 @@ static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
     grid = sms * std::min(per_sm, 4);
     grid_smem = smem;
   }
+  // small grids: about one node per thread, at least 32 blocks — every grid barrier costs
+  // more with more blocks (config 1, m = 1000: 296 blocks 0.064, 32 blocks 0.032 ms/iteration;
+  // 16 blocks 0.048)
+  int nblk = std::min<int>(grid, std::max<int>(32, static_cast<int>(ceil_div(a.m, PCG_NT))));
+  static const int force = [] {  // diagnostics: GSGPC_CG_BLOCKS = persistent grid size
+    const char* e = getenv("GSGPC_CG_BLOCKS");
+    return e ? atoi(e) : 0;
+  }();
+  if (force > 0) nblk = std::min(grid, force);
   PcgArgs aa = a;
   void* params[] = {&aa};
-  GSGPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_efcg_persistent<SMIN>), dim3(grid), dim3(PCG_NT),
+  GSGPC_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_efcg_persistent<SMIN>), dim3(nblk), dim3(PCG_NT),
                                          params, smem, L.s));
   L.count();
 }
