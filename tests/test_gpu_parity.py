@@ -409,6 +409,29 @@ def test_full_size_config3_properties():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("cfg_id,n", [(3, 100_000), (5, 60_000), (2, 400_000), (4, 300_000)])
+def test_baseline_config_prefix_matches_oracle(cfg_id, n):
+    """the BASELINE configurations' own grids and value distributions on a
+    deterministic prefix the oracle finishes in seconds — W^T W (CSR structure and values),
+    W^T y, yᵀy and n against the hash-map restatement of SufficientStatsAccumulator::add."""
+    from paper_2101_11751_b200 import synthetic as S
+
+    cfg = S.CONFIGS[cfg_id]
+    rows = S.generate_torch(cfg_id, n, device="cuda")
+    g = S.grid_for(cfg)
+    og = ogrid(g)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, rows)
+    host = rows.cpu().numpy().astype(np.float64)
+    os_ = O.sufficient_stats(og, host[:, : cfg.d], host[:, cfg.d], scheme=1, nthreads=8)
+    rp, col, val = gs.csr()
+    orp, ocol, oval, owty = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert np.abs(val - oval).max() <= 1e-10 * np.abs(oval).max()
+    assert rel_err(gs.wty(), owty) <= 1e-10
+    assert abs(gs.yty() - os_.yty) <= 1e-12 * os_.yty
+    assert gs.n() == os_.n == n
+
+
 @pytest.mark.parametrize("cfg_id,n", [(1, None), (2, None), (4, 100_000_000), (5, None)])
 def test_full_size_properties_other_configs(cfg_id, n):
     """BASELINE configs 1, 2, 4 (at 1e8 rows) and 5 at full size through size-independent
