@@ -355,10 +355,26 @@ def run_ours(args):
         barrier()
         el = (time.perf_counter() - t0) / args.steps
         el = max_over_ranks(el)
-        e2e = {"value": world * n / el, "unit": "points/s", "h2d_bytes_per_step": int(host_rows.numel() *
-                                                                                        host_rows.element_size()),
+        h2d = int(host_rows.numel() * host_rows.element_size())
+        # the link roofline of the end-to-end number: pinned host→device copy bandwidth, measured
+        # here with one 512 MiB copy (best of 3)
+        hb = torch.empty(1 << 27, dtype=torch.float32).pin_memory()
+        db = torch.empty(1 << 27, dtype=torch.float32, device=f"cuda:{local}")
+        best = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            db.copy_(hb, non_blocking=True)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t1)
+        link_gbs = hb.numel() * 4 / best / 1e9
+        del hb, db
+        e2e = {"value": world * n / el, "unit": "points/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(wty.nbytes + 16), "ms_per_step": el * 1e3,
-               "timing": "host perf_counter around synchronous API calls (H2D staging + compute + D2H)"}
+               "timing": "host perf_counter around synchronous API calls (H2D staging + compute + D2H)",
+               "roofline": {"bound": "h2d_link", "achieved": h2d / el / 1e9, "peak": link_gbs, "unit": "GB/s",
+                            "frac": h2d / el / 1e9 / link_gbs,
+                            "peak_source": "measured in this run: one 512 MiB pinned host→device copy, best of 3"}}
         assert nn == n * world and np.isfinite(yty)
         del host_rows
 
