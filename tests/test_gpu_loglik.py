@@ -25,13 +25,17 @@ def make_case(d=3, sizes=(10, 9, 8), n=6000, seed=5):
     return g, x, y
 
 
-@pytest.mark.parametrize("d,sizes", [(1, (40,)), (2, (16, 14)), (3, (10, 9, 8))])
-def test_probe_images_match_oracle(d, sizes):
-    g, x, y = make_case(d, sizes, n=5000)
+@pytest.mark.parametrize("d,sizes,n", [(1, (40,), 5000), (2, (16, 14), 5000), (3, (10, 9, 8), 5000),
+                                       (2, (600, 600), 150_000)])  # 512-cell buckets: staged slice scatter
+def test_probe_images_match_oracle(d, sizes, n):
+    g, x, y = make_case(d, sizes, n=n)
     acc = G.SufficientStatsAccumulator(g)
     acc.enable_probes(5, seed=7)
     acc.add(x[:2000], y[:2000])  # streams continue across batches
     acc.add(x[2000:], y[2000:])
+    ost = O.sufficient_stats(ogrid(g), x, y, nthreads=8) if n > 10000 else None
+    if ost is not None:  # the rows' statistics on the same (staged) path
+        assert rel_err(acc.finalize().wty(), ost.csr()[3]) <= 1e-10
     st = acc.finalize()
     img = st.probe_images()
     og = ogrid(g)
