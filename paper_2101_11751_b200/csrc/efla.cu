@@ -331,6 +331,87 @@ __global__ void __launch_bounds__(PEN_T) k_spmm_pencil(int m, int npen, const do
   }
 }
 
+// Two consecutive nodes per thread and half of the probes per block (grid.y = 2): one window
+// of E + 1 partners serves both nodes' E terms, read as 16-byte shared loads — 43 % fewer
+// shared-memory wavefronts per FMA than one node per thread.
+constexpr int PEN2_T = 128;  // threads per block (2 · 128 nodes)
+
+template <int PH, int W>
+__global__ void __launch_bounds__(PEN2_T) k_spmm_pencil2(int m, int npen, const double* __restrict__ A,
+                                                         const double* __restrict__ x, double* __restrict__ out,
+                                                         int P, const EfScal* sc) {
+  constexpr int E = 2 * W - 1, NT = 2 * PEN2_T, WL = NT + 2 * (W - 1) + 2;  // even row length
+  extern __shared__ __align__(16) double win2[];  // [PH][WL]
+  const int p0 = blockIdx.y * PH;
+  const int np = min(PH, P - p0);
+  if (np <= 0) return;
+  const int a0 = blockIdx.x * NT;
+  const int a = a0 + 2 * threadIdx.x;
+  const bool ok0 = a < m, ok1 = a + 1 < m;
+  const bool vec = (m & 1) == 0;
+  double acc0[PH], acc1[PH];
+#pragma unroll
+  for (int p = 0; p < PH; ++p) acc0[p] = acc1[p] = 0.0;
+  for (int q = 0; q < npen; ++q) {
+    const int ob = c_pen_ob[q];
+    __syncthreads();
+    for (int i = threadIdx.x; i < np * WL; i += PEN2_T) {
+      const int p = i / WL, t = i - p * WL;
+      const int g = a0 + ob - (W - 1) + t;
+      win2[i] = (g >= 0 && g < m) ? __ldcg(x + static_cast<int64_t>(p0 + p) * m + g) : 0.0;
+    }
+    __syncthreads();
+    double c0[E], c1[E];
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+      const int sidx = c_pen_s[q][t];
+      const int o = ob + t - (W - 1);
+      c0[t] = c1[t] = 0.0;
+      if (sidx >= 0) {
+        const double* As = A + static_cast<int64_t>(sidx) * m;
+        if (ok1 && vec) {
+          const double2 cc = __ldg(reinterpret_cast<const double2*>(As + a));
+          c0[t] = cc.x;
+          c1[t] = cc.y;
+        } else {
+          c0[t] = ok0 ? __ldg(As + a) : 0.0;
+          c1[t] = ok1 ? __ldg(As + a + 1) : 0.0;
+        }
+      } else {
+        const double* As = A + static_cast<int64_t>(-sidx - 1) * m;
+        const int b = a + o;
+        c0[t] = (ok0 && b >= 0 && b < m) ? __ldg(As + b) : 0.0;
+        c1[t] = (ok1 && b + 1 >= 0 && b + 1 < m) ? __ldg(As + b + 1) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PH; ++p) {
+      if (p < np) {
+        const double2* wp = reinterpret_cast<const double2*>(win2 + p * WL + 2 * threadIdx.x);
+        double w[E + 1];
+#pragma unroll
+        for (int k = 0; k < (E + 1) / 2; ++k) {
+          const double2 v = wp[k];
+          w[2 * k] = v.x;
+          w[2 * k + 1] = v.y;
+        }
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          acc0[p] = fma(c0[t], w[t], acc0[p]);
+          acc1[p] = fma(c1[t], w[t + 1], acc1[p]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < PH; ++p) {
+    if (p < np && !(sc && sc[p0 + p].done)) {
+      if (ok0) out[static_cast<int64_t>(p0 + p) * m + a] = acc0[p];
+      if (ok1) out[static_cast<int64_t>(p0 + p) * m + a + 1] = acc1[p];
+    }
+  }
+}
+
 static void launch_spmm(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P,
                         const EfScal* sc) {
   static const bool grid_stride = [] {
@@ -343,7 +424,16 @@ static void launch_spmm(const Launch& L, const StencilDesc& sd, const double* A,
     const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, PEN_T));
     const int WL = PEN_T + 2 * (sd.W - 1);
     const size_t smem = sizeof(double) * static_cast<size_t>(P) * WL;
-    if (sd.W == 4) {
+    static const bool one_node = [] {
+      const char* e = getenv("GSGPC_SPMM_ONE_NODE");  // diagnostics: one node per thread
+      return e && e[0] == '1';
+    }();
+    if (sd.W == 4 && !one_node) {
+      constexpr int PH = 16, WL2 = 2 * PEN2_T + 6 + 2;
+      const size_t sm2 = sizeof(double) * PH * WL2;
+      const dim3 g2(static_cast<unsigned>(ceil_div(sd.m, 2 * PEN2_T)), static_cast<unsigned>(ceil_div(P, PH)));
+      k_spmm_pencil2<PH, 4><<<g2, PEN2_T, sm2, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+    } else if (sd.W == 4) {
       static bool attr = false;
       if (!attr) {
         GSGPC_CUDA(cudaFuncSetAttribute(k_spmm_pencil<EF_MAXP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
