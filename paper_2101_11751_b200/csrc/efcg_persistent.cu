@@ -547,9 +547,26 @@ __global__ void __launch_bounds__(PCG_NT, PCG_MINB) k_efcg_persistent(PcgArgs a)
     }
     const double alpha = rho / pap;
     stamp(0);
-    for (int i = tid; i < m; i += nthr) {
-      a.x[i] += alpha * __ldcg(a.s + i);  // ŝ, z̄ were written by other blocks
-      a.r[i] -= alpha * __ldcg(a.z + i);
+    // ŝ, z̄ were written by other blocks (L2 loads); 4 elements per thread in flight
+    for (int i0 = tid; i0 < m; i0 += 4 * nthr) {
+      double sv[4], zv[4], xv[4], rv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthr;
+        const bool in = i < m;
+        sv[u] = in ? __ldcg(a.s + i) : 0.0;
+        zv[u] = in ? __ldcg(a.z + i) : 0.0;
+        xv[u] = in ? a.x[i] : 0.0;
+        rv[u] = in ? a.r[i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < m) {
+          a.x[i] = xv[u] + alpha * sv[u];
+          a.r[i] = rv[u] - alpha * zv[u];
+        }
+      }
     }
     if (leader) a.alphas[iter] = alpha;
     grid.sync();
