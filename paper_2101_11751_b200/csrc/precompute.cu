@@ -1671,6 +1671,115 @@ void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off
   GSGPC_CUDA(cudaGetLastError());
 }
 
+// K1p on the FP64 tensor cores (d = 3 cubic): per cell, Σ_rows s_p(row) · Π_k t_k^{e_k} is a
+// GEMM over the cell's rows — A = the 64 monomials of 4 rows (8 tiles of 8), B = the ±1 signs
+// of 16 probes for those rows (2 tiles of 8): 16 mma.sync.m8n8k4.f64 per 4 rows, 94 % of the
+// MAC slots needed (the lane-per-probe kernel ran 64 dependent FMAs per row per lane on 8
+// resident warps per SM).  Monomials are staged per row (lane) in shared memory with the
+// XOR swizzle of the d = 2 K1 (conflict-free stores and fragment loads).
+constexpr int PMM_PT = 2;  // probe tiles of 8 per pass
+
+template <typename T>
+__global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restrict__ pay,
+                                                          const uint64_t* __restrict__ pw,
+                                                          const int64_t* __restrict__ off, int64_t cells,
+                                                          int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate,
+                                                          GridDev g, int probes, double* __restrict__ pmom,
+                                                          int64_t range, int pbase) {
+  constexpr int QY = 64;
+  __shared__ __align__(16) double sm[2][32 * QY];
+  __shared__ uint64_t swd[2][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * 2 + wib;
+  if (gate.closed()) return;
+  nvalid = gate.rows(nvalid);
+  const int64_t r0 = row0 + warp * range;
+  if (r0 >= nvalid) return;
+  const int64_t rend = min(r0 + range, nvalid);
+  const int nw = (probes + 63) >> 6;
+  double* S = sm[wib];
+  uint64_t* SW = swd[wib];
+  const int r = lane >> 2, kq = lane & 3, cb = 2 * (lane & 3);
+  double d[8][PMM_PT][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < PMM_PT; ++b) d[a][b][0] = d[a][b][1] = 0.0;
+  int64_t c = first_cell(off, c_lo, cells, r0, lane);
+  int64_t p = r0;
+  while (p < rend) {
+    c = next_cell(off, c, p, cells, lane);
+    const int64_t ce = off[c + 1];
+    const int64_t seg_end = min(ce, rend);
+    for (int64_t b0 = p; b0 < seg_end; b0 += 32) {
+      const int nb = static_cast<int>(imin64(32, seg_end - b0));
+      {
+        double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
+        const bool v = lane < nb;
+        if (v) row_t<T>(g, pay[b0 + lane], t, y);
+        double pk[3][4];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double q = 1.0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pk[k][e] = q;
+            q *= t[k];
+          }
+        }
+        double* P = S + lane * QY;
+        const int sw = d2c_swz(lane);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const double ab = v ? pk[0][a] * pk[1][b] : 0.0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int q = (a * 4 + b) * 4 + e;
+              P[(q & ~15) | ((q & 15) ^ sw)] = ab * pk[2][e];
+            }
+          }
+        SW[lane] = v ? pw[(b0 + lane) * nw + (pbase >> 6)] : 0ull;
+      }
+      __syncwarp();
+      const int steps = (nb + 3) >> 2;
+      for (int st = 0; st < steps; ++st) {
+        const int R = 4 * st + kq;  // rows ≥ nb were staged as zeros
+        const double* P = S + R * QY;
+        const int sw = d2c_swz(R);
+        const uint64_t bits = SW[R];
+        double bv[PMM_PT];
+#pragma unroll
+        for (int tb = 0; tb < PMM_PT; ++tb) {
+          const int pj = (pbase & 63) + 8 * tb + r;
+          bv[tb] = ((bits >> (pj & 63)) & 1ull) ? 1.0 : -1.0;
+        }
+#pragma unroll
+        for (int ta = 0; ta < 8; ++ta) {
+          const int q = 8 * ta + r;
+          const double av = P[(q & ~15) | ((q & 15) ^ sw)];
+#pragma unroll
+          for (int tb = 0; tb < PMM_PT; ++tb) dmma(d[ta][tb][0], d[ta][tb][1], av, bv[tb]);
+        }
+      }
+      __syncwarp();
+    }
+    // flush: D[r][cb + i] = monomial 8 ta + r of probe pbase + 8 tb + cb + i
+#pragma unroll
+    for (int ta = 0; ta < 8; ++ta)
+#pragma unroll
+      for (int tb = 0; tb < PMM_PT; ++tb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int pj = pbase + 8 * tb + cb + i;
+          if (pj < probes) flush_val(pmom + (c * probes + pj) * QY + 8 * ta + r, d[ta][tb][i]);
+          d[ta][tb][i] = 0.0;
+        }
+    p = seg_end;
+  }
+}
+
 template <typename T>
 static void launch_probe_moments(const Launch& L, const void* pay, const uint64_t* pw, const int64_t* off,
                                  int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
@@ -1679,6 +1788,20 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   const int64_t range = 1024;
   const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 2));
+  static const bool lane_pm = [] {
+    const char* e = getenv("GSGPC_PROBE_MOM_LANE");  // diagnostics: lane-per-probe kernel
+    return e && e[0] == '1';
+  }();
+  if (g.d == 3 && g.W == 4 && !lane_pm) {
+    const int64_t rng = 512;
+    const unsigned blk = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, rng), 2));
+    for (int pb = 0; pb < probes; pb += 8 * PMM_PT) {
+      k_probe_moments_mma<T><<<blk, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, rng,
+                                                   pb);
+      L.count();
+    }
+    return;
+  }
   for (int pb = 0; pb < probes; pb += 32) {
 #define GSGPC_PM(DD, WW)                                                                                  \
   if (g.d == DD && g.W == WW) {                                                                         \
