@@ -750,10 +750,15 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     const int64_t n1p = (n1 + 7) & ~int64_t{7}, n1p4 = (n1 + 3) & ~int64_t{3};
     const int64_t ys = ((n2 + 7) & ~int64_t{7}) + ((((n2 + 7) & ~int64_t{7}) % 16) == 0 ? 8 : 0);
     const int64_t need = gens + n1p * mm_stride(n2) + std::max(n1p, n1p4) * ys;
-    if (need * 8 <= 48 * 1024) {
+    static const int64_t plane_kb = [] {  // diagnostics: shared-memory budget of the plane phase
+      const char* e = getenv("GSGPC_CG_PLANE_KB");
+      return e ? static_cast<int64_t>(atoi(e)) : int64_t{48};
+    }();
+    if (need * 8 <= plane_kb * 1024) {
       a.mm_plane = 1;
       a.mp_ys = static_cast<int>(ys);
       a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 296 / n0)));
+      if (const char* e = getenv("GSGPC_CG_PLANE_PARTS")) a.mp_parts = std::max(1, atoi(e));  // diagnostics
       mp_smem = static_cast<size_t>(need * 8);
     }
   }
