@@ -21,7 +21,10 @@ namespace gsgpc {
 // neighbours around it, mostly by the same block.  This is also correct inside the
 // persistent EFCG kernel, which rewrites v between grid barriers: grid.sync() invalidates
 // L1 (CCTL.IVALL in the SASS).  Measured: config 3 SpMV phase 52 → 47.5 µs, config 5
-// 102 → 91 µs, versus L2-only (ld.global.cg) loads.
+// 102 → 91 µs, versus L2-only (ld.global.cg) loads.  The batched stencil loads are streaming
+// (ld.global.cs, evict-first) — both the forward and the mirrored one: 47.6 → 44.8 µs
+// (config 3), 90.5 → 86.2 µs (config 5); only one of the two streaming, or both
+// ld.global.cg, measured no gain.
 template <int SMIN, typename OFF, int U = 8>
 __device__ __forceinline__ double stencil_row_dot(int m, const double* __restrict__ A, const double* __restrict__ v,
                                                   int a, OFF off) {
@@ -37,8 +40,8 @@ __device__ __forceinline__ double stencil_row_dot(int m, const double* __restric
       const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
       const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
       const double* As = A + static_cast<int64_t>(s + q) * m;
-      af[q] = __ldg(As + a);
-      ab[q] = okb ? __ldg(As + b) : 0.0;
+      af[q] = __ldcs(As + a);
+      ab[q] = okb ? __ldcs(As + b) : 0.0;
       vf[q] = okf ? ldv(f) : 0.0;
       vb[q] = okb ? ldv(b) : 0.0;
     }
