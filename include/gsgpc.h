@@ -140,9 +140,20 @@ gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* stats, const char
 /* Accumulate probe images of the reference's Rademacher probes (rademacher_probe,
  * gp.cpp:16-25: std::seed_seq{seed_lo, seed_hi, p_lo, p_hi} + std::mt19937_64, one draw per
  * row in stream order) for p = 0..probes-1 in every following gsgpc_stats_add; the library
- * generates the streams itself (host threads), continuing across batches.  Call before the
- * first row is added.  probes <= 64. */
+ * generates the streams itself on the device (one block per probe and substream), continuing
+ * across batches.  Call before the first row is added.  probes <= 64. */
 gsgpc_status gsgpc_stats_enable_probes(gsgpc_ctx* ctx, gsgpc_stats* stats, int probes, uint64_t seed);
+/* The same streams positioned at draw `first_row`: for an accumulator (a rank's shard) whose
+ * rows are rows [first_row, first_row + n) of one global stream, so that shard probe images
+ * sum (merge / all-reduce) to the single-pass W^T v_p of rademacher_probe over the whole
+ * stream.  The streams are advanced by GF(2) jump-ahead (no draws are generated).  merge()
+ * of probe-seeded shards requires adjacent row ranges. */
+gsgpc_status gsgpc_stats_enable_probes_at(gsgpc_ctx* ctx, gsgpc_stats* stats, int probes, uint64_t seed,
+                                          int64_t first_row);
+/* Test hook (host only, needs no GPU): bit 0 of draws [offset, offset + n) of
+ * rademacher_probe's stream for (seed, p) (gp.cpp:16-25), reached by the library's jump-ahead
+ * (out[i] = 1 ↔ +1). */
+gsgpc_status gsgpc_probe_stream_bits(uint64_t seed, uint64_t p, uint64_t offset, int64_t n, uint8_t* out);
 /* Reset an accumulator to the freshly constructed state (no rows), keeping its buffers —
  * equivalent to constructing a new SufficientStatsAccumulator on the same grid. */
 gsgpc_status gsgpc_stats_reset(gsgpc_ctx* ctx, gsgpc_stats* stats);

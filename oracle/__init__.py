@@ -81,6 +81,9 @@ def lib():
         "orc_kernel_generator": (C.c_int, [_vp, _vp]),
         "orc_kg_dense": (C.c_int, [_vp, _vp, _i64]),
         "orc_next_fast_fft_size": (_i64, [_i64]),
+        "orc_kg_set_direct": (None, [_vp, C.c_int]),
+        "orc_set_threads": (None, [C.c_int]),
+        "orc_get_threads": (C.c_int, []),
         "orc_factorized_cg_grid_rhs": (C.c_int, [_vp, _vp, _vp, _d, _d, _d, C.c_int, _vp, _pi, _pi, _pd, _vp, _vp, _vp, _pd]),
         "orc_posterior_mean_gsgp": (C.c_int, [_vp, _vp, _d, _d, C.c_int, _vp, _pi, _pd]),
         "orc_predict_mean": (C.c_int, [C.c_int, _pd, _pd, _pi64, C.c_int, _vp, _vp, _i64, _vp]),
@@ -269,6 +272,11 @@ class ToeplitzOperator:
         _check(lib().orc_kg_apply(self._h, _ptr(v), _ptr(out)))
         return out
 
+    def set_direct(self, on=True):
+        """Sensitivity study only: direct separable Toeplitz sums instead of the circulant FFT
+        (same operator, different rounding)."""
+        lib().orc_kg_set_direct(self._h, 1 if on else 0)
+
     def generator(self):
         out = np.zeros(self.dim)
         _check(lib().orc_kernel_generator(self._h, _ptr(out)))
@@ -279,6 +287,12 @@ class ToeplitzOperator:
         out = np.zeros((m, m))
         _check(lib().orc_kg_dense(self._h, _ptr(out), max_points))
         return out
+
+
+def set_threads(n: int) -> None:
+    """Host threads for independent CSR rows, FFT lines and SLQ probes (results are identical
+    for every thread count: each reduction keeps its sequential order)."""
+    lib().orc_set_threads(int(n))
 
 
 def next_fast_fft_size(x):

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <exception>
 #include <limits>
 #include <random>
 #include <stdexcept>
@@ -50,6 +51,30 @@ struct SolverNonConvergence : std::runtime_error {
 };
 
 constexpr double kLog2Pi = 1.8378770664093453;  // gp.cpp:12
+
+// Host threads for the row/line-parallel loops below (orc_set_threads).  Only loops whose
+// iterations are independent (CSR rows, FFT lines, SLQ probes) run in parallel, and every
+// reduction keeps its sequential order, so results do not depend on the thread count.
+int g_threads = 1;
+thread_local bool g_in_par = false;
+
+template <class F>
+void par_for(int64_t n, F&& f, int64_t grain = 64) {  // f(lo, hi) over [0, n)
+  const int64_t nt = std::min<int64_t>(g_in_par ? 1 : g_threads, n / std::max<int64_t>(grain, 1));
+  if (nt <= 1) {
+    if (n > 0) f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t) {
+    th.emplace_back([&, t] {
+      g_in_par = true;
+      f(n * t / nt, n * (t + 1) / nt);
+      g_in_par = false;
+    });
+  }
+  for (auto& h : th) h.join();
+}
 
 // ---------------------------------------------------------------- grid.cpp:12-40
 struct Grid {
@@ -193,11 +218,13 @@ struct Stats {
 
   Vec apply_wtw(const Vec& v) const {  // Eigen RowMajor sparse * dense: per-row sequential
     Vec out(m, 0.0);
-    for (int64_t i = 0; i < m; ++i) {
-      double tmp = 0.0;
-      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) tmp += val[k] * v[col[k]];
-      out[i] = tmp;
-    }
+    par_for(m, [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        double tmp = 0.0;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) tmp += val[k] * v[col[k]];
+        out[i] = tmp;
+      }
+    });
     return out;
   }
 };
@@ -350,15 +377,17 @@ struct FFTN {
       const std::size_t len = shape[k];
       inner /= len;
       const std::size_t outer = total / (len * inner);
-      std::vector<cplx> line(len), res(len);
-      for (std::size_t o = 0; o < outer; ++o) {
-        for (std::size_t i = 0; i < inner; ++i) {
+      par_for(static_cast<int64_t>(outer * inner), [&](int64_t lo, int64_t hi) {
+        std::vector<cplx> line(len), res(len);
+        for (int64_t li = lo; li < hi; ++li) {
+          const std::size_t o = static_cast<std::size_t>(li) / inner;
+          const std::size_t i = static_cast<std::size_t>(li) % inner;
           const std::size_t base = o * len * inner + i;
           for (std::size_t j = 0; j < len; ++j) line[j] = a[base + j * inner];
           plans[k].run(line.data(), res.data(), inv);
           for (std::size_t j = 0; j < len; ++j) a[base + j * inner] = res[j];
         }
-      }
+      });
     }
   }
 };
@@ -424,6 +453,42 @@ struct Toeplitz {
   }
   ~Toeplitz() { delete fft; }
 
+  // Sensitivity-study mode (orc_kg_set_direct): K_G v as d direct Toeplitz mode products
+  // (K_G = T_0 ⊗ … ⊗ T_{d-1} for the separable SE kernel, kernels.cpp:43-55), summed in
+  // index order.  Same operator as the circulant FFT below up to rounding — a second valid
+  // rounding of the reference's math, used to measure how far CG traces and iteration counts
+  // move under O(1e-16) perturbations of K_G.  Not the reference's algorithm.
+  bool direct = false;
+  Vec apply_direct(const Vec& v) const {
+    const int d = grid.d;
+    Vec cur = v, nxt(grid.m);
+    int64_t inner = grid.m;
+    for (int k = 0; k < d; ++k) {
+      const int64_t len = shape[k];
+      inner /= len;
+      const int64_t outer = grid.m / (len * inner);
+      const double h = grid.sp[k];
+      Vec gen(len);
+      for (int64_t j = 0; j < len; ++j) {
+        const double q = static_cast<double>(j) * h / ls[k];
+        gen[j] = std::exp(-0.5 * q * q) * (k == 0 ? outputscale : 1.0);
+      }
+      par_for(outer * inner, [&](int64_t lo, int64_t hi) {
+        for (int64_t li = lo; li < hi; ++li) {
+          const int64_t o = li / inner, i = li % inner;
+          const int64_t base = o * len * inner + i;
+          for (int64_t a = 0; a < len; ++a) {
+            double s = 0.0;
+            for (int64_t j = 0; j < len; ++j) s += gen[a > j ? a - j : j - a] * cur[base + j * inner];
+            nxt[base + a * inner] = s;
+          }
+        }
+      });
+      std::swap(cur, nxt);
+    }
+    return cur;
+  }
+
   std::size_t eflat_of(int64_t flat) const {
     std::size_t e = 0;
     std::vector<int64_t> idx(grid.d);
@@ -439,6 +504,7 @@ struct Toeplitz {
     if (static_cast<int64_t>(v.size()) != grid.m) {
       throw std::invalid_argument("ToeplitzOperator::apply: length mismatch");
     }
+    if (direct) return apply_direct(v);
     std::vector<cplx> buf(embed_total, cplx(0.0, 0.0));
     const int d = grid.d;
     std::vector<int64_t> idx(d, 0);
@@ -771,18 +837,31 @@ std::pair<double, int> slq_logdet_ski_factorized(const Toeplitz& kg, const Stats
     throw std::invalid_argument("slq_logdet_ski_factorized: need at least one probe");
   }
   const int depth = static_cast<int>(std::min<int64_t>(max_depth, n));
+  // probes are independent (gp.cpp:94-108); they run on the host threads and are summed in
+  // probe order afterwards, as the reference's sequential loop does
+  std::vector<std::pair<double, int>> per(num_probes);
+  std::vector<std::exception_ptr> errs(num_probes);
+  par_for(num_probes, [&](int64_t lo, int64_t hi) {
+    for (int64_t p = lo; p < hi; ++p) {
+      try {
+        const Vec v = rademacher_probe(n, seed, static_cast<uint64_t>(p));
+        const Vec wt = wt_apply(grid, scheme, x, n, v);
+        const Vec kgwt = kg.apply(wt);
+        const double z0_sq = dot(v, v);
+        const Tridiag t =
+            factorized_lanczos_fused(kg, stats, kgwt, wt, z0_sq, sigma * sigma, depth, false);
+        per[p] = quadrature_logdet(t.alpha, t.beta, z0_sq, quad_tol);
+      } catch (...) {
+        errs[p] = std::current_exception();
+      }
+    }
+  }, 1);
   double total = 0.0;
   int max_used = 0;
   for (int p = 0; p < num_probes; ++p) {
-    const Vec v = rademacher_probe(n, seed, p);
-    const Vec wt = wt_apply(grid, scheme, x, n, v);
-    const Vec kgwt = kg.apply(wt);
-    const double z0_sq = dot(v, v);
-    const Tridiag t =
-        factorized_lanczos_fused(kg, stats, kgwt, wt, z0_sq, sigma * sigma, depth, false);
-    const auto q = quadrature_logdet(t.alpha, t.beta, z0_sq, quad_tol);
-    total += q.first;
-    max_used = std::max(max_used, q.second);
+    if (errs[p]) std::rethrow_exception(errs[p]);
+    total += per[p].first;
+    max_used = std::max(max_used, per[p].second);
   }
   return {total / num_probes, max_used};
 }
@@ -958,7 +1037,15 @@ Stats run_stats(const Grid& grid, int scheme, const T* x, const T* y, int64_t n,
                       bad_msg[t]);
     }
   }
-  for (int t = 1; t < nthreads; ++t) accs[0]->merge(*accs[t]);
+  // merge() (interp.cpp:202-210) as a pairwise tree over the shards, independent pairs on
+  // their own threads (a sum, so only the order of the hash-map additions changes)
+  for (int stride = 1; stride < nthreads; stride *= 2) {
+    std::vector<std::thread> th;
+    for (int t = 0; t + stride < nthreads; t += 2 * stride) {
+      th.emplace_back([&, t, stride] { accs[t]->merge(*accs[t + stride]); });
+    }
+    for (auto& h : th) h.join();
+  }
   Stats s = accs[0]->finalize();
   for (auto* a : accs) delete a;
   return s;
@@ -1304,6 +1391,11 @@ int orc_kg_dense(const orc_kg* k, double* out, int64_t max_points) {  // grid.cp
 }
 
 int64_t orc_next_fast_fft_size(int64_t x) { return next_fast_fft_size(x); }
+
+void orc_kg_set_direct(orc_kg* k, int direct) { k->t->direct = direct != 0; }
+
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int orc_get_threads(void) { return g_threads; }
 
 int orc_factorized_cg_grid_rhs(const orc_kg* kg, const orc_stats* st, const double* rhat0,
                                double sigma, double eps_abs, double rel_tol, int maxiter,

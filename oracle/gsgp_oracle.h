@@ -86,6 +86,12 @@ int orc_kg_apply(const orc_kg* k, const double* v, double* out);
 int orc_kernel_generator(const orc_kg* k, double* out);
 int orc_kg_dense(const orc_kg* k, double* out, int64_t max_points);
 int64_t orc_next_fast_fft_size(int64_t x);
+/* Sensitivity study only: K_G v by direct separable Toeplitz sums instead of the circulant
+ * FFT (same operator, different rounding).  Not the reference algorithm. */
+void orc_kg_set_direct(orc_kg* k, int direct);
+/* Host threads for independent rows / FFT lines / SLQ probes (results do not depend on it). */
+void orc_set_threads(int n);
+int orc_get_threads(void);
 
 /* factorized_cg_grid_rhs (solvers.cpp:271-336).  Traces need room for maxiter+1. */
 int orc_factorized_cg_grid_rhs(const orc_kg* kg, const orc_stats* st, const double* rhat0,

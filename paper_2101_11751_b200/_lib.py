@@ -72,6 +72,8 @@ SIGNATURES = {
     "gsgpc_stats_merge": (_i, [_vp, _vp, _vp]),
     "gsgpc_stats_reset": (_i, [_vp, _vp]),
     "gsgpc_stats_enable_probes": (_i, [_vp, _vp, _i, C.c_uint64]),
+    "gsgpc_stats_enable_probes_at": (_i, [_vp, _vp, _i, C.c_uint64, _i64]),
+    "gsgpc_probe_stream_bits": (_i, [C.c_uint64, C.c_uint64, C.c_uint64, _i64, _vp]),
     "gsgpc_diag_fp64_peak": (_i, [_vp, _P(_d)]),
     "gsgpc_diag_fp64_tensor": (_i, [_vp, _P(_d), _P(_d)]),
     "gsgpc_stats_finalize": (_i, [_vp, _vp]),

@@ -157,6 +157,7 @@ struct gsgpc_stats {
   // seeded Rademacher probes (gsgpc_stats_enable_probes): one generator per probe
   bool probe_seeded = false;
   uint64_t probe_seed = 0;
+  int64_t probe_first_row = 0;  // global row index of this accumulator's first row (stream offset)
   DBuf rng;  // probe_seeded: per probe the MT19937-64 state (312 words) + index, on the device
   int64_t fin_count() const { return static_cast<int64_t>(S_min) * g.m + g.m + static_cast<int64_t>(probes) * g.m + 2; }
   double* stencil() const { return fin.as<double>(); }
@@ -686,15 +687,33 @@ void gen_probe_words(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t rows) {
   st.ensure(sizeof(uint64_t) * rows);
   DBuf& planes = ctx->buf("probe_planes");
   planes.ensure(static_cast<size_t>(s->probes) * std::min(rows, probe_rng_slab()));
-  run_probe_rng(ctx->L(), s->rng.as<uint64_t>(), s->probes, rows, planes.as<uint8_t>(), st.as<uint64_t>());
+  DBuf& scr = ctx->buf("probe_rng_scratch");
+  scr.ensure(sizeof(uint64_t) * probe_rng_scratch_words(s->probes));
+  run_probe_rng(ctx->L(), s->rng.as<uint64_t>(), s->probes, rows, planes.as<uint8_t>(), st.as<uint64_t>(),
+                scr.as<uint64_t>());
 }
 
-// initial generator states of rademacher_probe(·, seed, p), p < probes
+// Generator states of rademacher_probe(·, seed, p), p < probes, positioned at draw
+// probe_first_row (the accumulator's first global row): a fresh stream for row 0, else the
+// seeded state advanced by the GF(2) jump-ahead (mt_jump.cu) — 312·q draws as a block jump,
+// the remainder r as the generator's index.
 void seed_probe_streams(gsgpc_ctx* ctx, gsgpc_stats* s) {
   std::vector<uint64_t> h(static_cast<size_t>(s->probes) * 313);
   for (int p = 0; p < s->probes; ++p) mt_seed_state(s->probe_seed, static_cast<uint64_t>(p), h.data() + p * 313);
   s->rng.ensure(sizeof(uint64_t) * h.size());
-  GSGPC_CUDA(cudaMemcpyAsync(s->rng.p, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+  const uint64_t o = static_cast<uint64_t>(s->probe_first_row);
+  if (o == 0) {
+    GSGPC_CUDA(cudaMemcpyAsync(s->rng.p, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+  } else {
+    const uint64_t a = 312 + o;  // a seeded generator sits at index 312 (its first draw twists)
+    for (int p = 0; p < s->probes; ++p) h[static_cast<size_t>(p) * 313 + 312] = a % 312;
+    DBuf& tmp = ctx->buf("probe_seed_tmp");
+    tmp.ensure(sizeof(uint64_t) * (h.size() + 312));
+    GSGPC_CUDA(cudaMemcpyAsync(tmp.p, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+    run_mt_jump(ctx->L(), tmp.as<uint64_t>(), s->probes, {a / 312}, tmp.as<uint64_t>() + h.size(),
+                s->rng.as<uint64_t>());
+  }
   GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -705,6 +724,33 @@ extern "C" {
 
 const char* gsgpc_version(void) {
   return "gsgpc sm_100a " GSGPC_GIT " (precompute: cell-sorted polynomial moments; K_G: Kronecker Toeplitz)";
+}
+
+gsgpc_status gsgpc_probe_stream_bits(uint64_t seed, uint64_t p, uint64_t offset, int64_t n, uint8_t* out) {
+  if (n < 0 || (n > 0 && !out)) return GSGPC_INVALID_ARGUMENT;
+  return guard(nullptr, [&] {
+    uint64_t st[313];
+    mt_seed_state(seed, p, st);
+    mt_jump_host(st, offset);
+    // sequential draws from the jumped generator (std::mt19937_64 semantics, [rand.eng.mers])
+    constexpr uint64_t A = 0xB5026F5AA96619E9ull, UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+    uint64_t idx = st[312];
+    for (int64_t i = 0; i < n; ++i) {
+      if (idx >= 312) {
+        for (int k = 0; k < 312; ++k) {
+          const uint64_t x = (st[k] & UM) | (st[(k + 1) % 312] & LM);
+          st[k] = st[(k + 156) % 312] ^ (x >> 1) ^ ((x & 1ull) ? A : 0ull);
+        }
+        idx = 0;
+      }
+      uint64_t y = st[idx++];
+      y ^= (y >> 29) & 0x5555555555555555ull;
+      y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+      y ^= (y << 37) & 0xFFF7EEE000000000ull;
+      y ^= y >> 43;
+      out[i] = static_cast<uint8_t>(y & 1u);
+    }
+  });
 }
 
 gsgpc_status gsgpc_ctx_create(int device, gsgpc_ctx** out) {
@@ -1159,13 +1205,20 @@ gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* s, const char* pa
 }
 
 gsgpc_status gsgpc_stats_enable_probes(gsgpc_ctx* ctx, gsgpc_stats* s, int probes, uint64_t seed) {
+  return gsgpc_stats_enable_probes_at(ctx, s, probes, seed, 0);
+}
+
+gsgpc_status gsgpc_stats_enable_probes_at(gsgpc_ctx* ctx, gsgpc_stats* s, int probes, uint64_t seed,
+                                          int64_t first_row) {
   return guard(ctx, [&] {
     if (!s) invalid("stats is NULL");
     if (probes < 1 || probes > 64) throw Error(GSGPC_UNSUPPORTED, "probes must be in [1, 64]");
+    if (first_row < 0) invalid("gsgpc_stats_enable_probes_at: first_row must be >= 0");
     if (s->n > 0 || s->probes > 0) invalid("gsgpc_stats_enable_probes: call before the first row is added");
     s->probes = probes;
     s->probe_seeded = true;
     s->probe_seed = seed;
+    s->probe_first_row = first_row;
     seed_probe_streams(ctx, s);  // rademacher_probe (gp.cpp:16-25) streams, generated on the device
     s->pmom.ensure(sizeof(double) * s->g.cells * probes * s->QY);
     GSGPC_CUDA(cudaMemsetAsync(s->pmom.p, 0, sizeof(double) * s->g.cells * probes * s->QY, ctx->stream));
@@ -1199,6 +1252,20 @@ gsgpc_status gsgpc_stats_merge(gsgpc_ctx* ctx, gsgpc_stats* dst, const gsgpc_sta
              dst->grid.max[k] == src->grid.max[k];
     }
     if (!same) invalid("SufficientStatsAccumulator::merge: mismatched shards");
+    // seeded probe images are sums over global rows: shards merge only when their rows are
+    // adjacent in the one stream order ([first, first + n) intervals touching)
+    bool src_after = true;
+    if (dst->probe_seeded || src->probe_seeded) {
+      if (!(dst->probe_seeded && src->probe_seeded) || dst->probe_seed != src->probe_seed) {
+        invalid("SufficientStatsAccumulator::merge: shards carry different probe streams");
+      }
+      src_after = src->probe_first_row == dst->probe_first_row + dst->n;
+      const bool src_before = dst->probe_first_row == src->probe_first_row + src->n;
+      if (!src_after && !src_before) {
+        invalid("SufficientStatsAccumulator::merge: probe-seeded shards must cover adjacent row ranges "
+                "(gsgpc_stats_enable_probes_at first_row)");
+      }
+    }
     const Launch L = ctx->L();
     const int64_t nm = dst->g.cells * dst->Q;
     run_axpby(L, nm, 1.0, dst->mom.as<double>(), 1.0, src->mom.as<double>(), dst->mom.as<double>());
@@ -1208,6 +1275,14 @@ gsgpc_status gsgpc_stats_merge(gsgpc_ctx* ctx, gsgpc_stats* dst, const gsgpc_sta
       run_axpby(L, np, 1.0, dst->pmom.as<double>(), 1.0, src->pmom.as<double>(), dst->pmom.as<double>());
     }
     run_axpby(L, 1, 1.0, dst->yty.as<double>(), 1.0, src->yty.as<double>(), dst->yty.as<double>());
+    if (dst->probe_seeded) {
+      if (src_after) {  // continue from the end of src's rows
+        GSGPC_CUDA(cudaMemcpyAsync(dst->rng.p, src->rng.p, sizeof(uint64_t) * dst->probes * 313,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        dst->probe_first_row = src->probe_first_row;
+      }
+    }
     dst->n += src->n;
     dst->finalized = false;
     GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1404,7 +1479,6 @@ gsgpc_status gsgpc_stats_apply_wtw(gsgpc_ctx* ctx, gsgpc_stats* s, const double*
     if (!s) invalid("stats is NULL");
     finalize_stats(ctx, s);
     const StencilDesc sd = stencil_desc(s);
-    upload_stencil_offsets(sd, ctx->stream);
     const double* dv = dev_in(ctx, v, sd.m, "wtw_in");
     DevOut o(ctx, out, sd.m, "wtw_out");
     DBuf& fl = ctx->buf("wtw_flag");
@@ -1713,7 +1787,6 @@ CgOutcome run_efcg(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, const double* r
   CgCache& c = cg_setup(ctx, s, kg, maxiter);
   const CgBufs b = cg_bufs(c);
   const StencilDesc sd = stencil_desc(s);
-  upload_stencil_offsets(sd, ctx->stream);
   const Launch L = ctx->L();
   CgState st0{};
   st0.eps_abs = eps_abs;
@@ -2274,7 +2347,6 @@ gsgpc_status gsgpc_posterior_cov_lowrank(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_k
     if (rank > 0 && n > 0) {
       // start direction ĝ = WᵀW 1 / ‖WᵀW 1‖ (gp.cpp:446-452)
       const StencilDesc sd = stencil_desc(s);
-      upload_stencil_offsets(sd, ctx->stream);
       DBuf& a = ctx->buf("lr_a");
       DBuf& b = ctx->buf("lr_b");
       DBuf& c = ctx->buf("lr_c");

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "internal.cuh"
 #include "precompute.cuh"
@@ -25,8 +27,6 @@ constexpr int PCG_NT = 256;
 #ifndef PCG_MINB
 #define PCG_MINB 2  // resident blocks per SM (register cap 65536 / (256 · MINB))
 #endif
-
-__constant__ int c_pcg_off[172];
 
 struct PcgMode {
   int64_t n, inner, L;
@@ -53,6 +53,7 @@ struct PcgArgs {
   int mm_plane;              // d = 3: modes 2 and 1 fused per x0-plane on the tensor cores (pcg_plane_mma)
   int mp_parts, mp_ys;       // pcg_plane_mma: parts per plane, row stride of the mode-2 image
   unsigned long long* tbuf;  // optional phase trace: tbuf[iter * 8 + phase] = %globaltimer (ns)
+  int off[kMaxSmin];         // flat stencil offsets o_s (per launch: no module-global table)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -76,13 +77,14 @@ __device__ __forceinline__ double grid_reduce(const double* part, int np, double
 }
 
 struct PcgOff {
-  __device__ __forceinline__ int operator()(int s) const { return c_pcg_off[s]; }
+  const int* o;  // → PcgArgs::off of the launch's __grid_constant__ parameter
+  __device__ __forceinline__ int operator()(int s) const { return o[s]; }
 };
 
 template <int SMIN>
 __device__ __forceinline__ double pcg_spmv_node(int m, const double* __restrict__ A, const double* __restrict__ v,
-                                                int a) {
-  return stencil_row_dot<SMIN, PcgOff, PCG_SPMV_U>(m, A, v, a, PcgOff{});
+                                                int a, const int* off) {
+  return stencil_row_dot<SMIN, PcgOff, PCG_SPMV_U>(m, A, v, a, PcgOff{off});
 }
 
 // One Toeplitz mode product (grid-stride over line tiles × output chunks).  EPI: fused
@@ -441,7 +443,7 @@ __device__ __forceinline__ void pcg_plane_modes(const PcgArgs& a, double* smem) 
 }
 
 template <int SMIN>
-__global__ void __launch_bounds__(PCG_NT, PCG_MINB) k_efcg_persistent(PcgArgs a) {
+__global__ void __launch_bounds__(PCG_NT, PCG_MINB) k_efcg_persistent(const __grid_constant__ PcgArgs a) {
   extern __shared__ double smem[];
   __shared__ double sh[8];
   __shared__ double sh1;
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(PCG_NT, PCG_MINB) k_efcg_persistent(PcgArgs a)
   auto spmv_phase = [&]() {
     double dot = 0.0;
     for (int node = tid; node < m; node += nthr) {
-      const double u = pcg_spmv_node<SMIN>(m, a.A, a.r, node);
+      const double u = pcg_spmv_node<SMIN>(m, a.A, a.r, node, a.off);
       a.u[node] = u;
       dot = fma(u, __ldcg(a.r + node), dot);
     }
@@ -627,24 +629,34 @@ static PcgMode mode_cfg(const KgDev& kg, int k) {
   return c;
 }
 
+// Persistent grid size per (device, kernel, dynamic smem): SMs × resident blocks (≤ 4), cached
+// under a lock (each device configures its own function attributes).
+template <int SMIN>
+static int pcg_grid(size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, int> cache;
+  int dev = 0;
+  GSGPC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, smem});
+  if (it != cache.end()) return it->second;
+  int sms = 0, per_sm = 0;
+  GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+  // smallest shared-memory carveout that holds two blocks: the rest is L1
+  const int pct = static_cast<int>(std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+  GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
+  if (per_sm < 1) throw Error(GSGPC_CUDA_ERROR, "persistent EFCG kernel cannot be resident");
+  const int grid = sms * std::min(per_sm, 4);
+  cache[{dev, smem}] = grid;
+  return grid;
+}
+
 template <int SMIN>
 static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
-  static int grid = 0;
-  static size_t grid_smem = 0;
-  if (grid == 0 || grid_smem != smem) {
-    int dev = 0, sms = 0, per_sm = 0;
-    GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
-    // smallest shared-memory carveout that holds two blocks: the rest is L1
-    const int pct = static_cast<int>(std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
-    GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    GSGPC_CUDA(cudaGetDevice(&dev));
-    GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
-    if (per_sm < 1) throw Error(GSGPC_CUDA_ERROR, "persistent EFCG kernel cannot be resident");
-    grid = sms * std::min(per_sm, 4);
-    grid_smem = smem;
-  }
+  const int grid = pcg_grid<SMIN>(smem);
   // small grids: about one node per thread, at least 32 blocks — every grid barrier costs
   // more with more blocks (config 1, m = 1000: 296 blocks 0.064, 32 blocks 0.032 ms/iteration;
   // 16 blocks 0.048)
@@ -661,30 +673,13 @@ static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
   L.count();
 }
 
-int pcg_max_blocks() { return 148 * 4 + 64; }
-
 void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
                          int init, unsigned long long* tbuf) {
-  int o32[172];
-  {
-    const int E = 2 * sd.W - 1;
-    int S = 1;
-    for (int k = 0; k < sd.d; ++k) S *= E;
-    const int c0 = (S - 1) / 2;
-    for (int s2 = 0; s2 < sd.S_min; ++s2) {
-      int q = c0 + s2;
-      int dig[3] = {0, 0, 0};
-      for (int k = sd.d - 1; k >= 0; --k) {
-        dig[k] = q % E - (sd.W - 1);
-        q /= E;
-      }
-      long long f = 0;
-      for (int k = 0; k < sd.d; ++k) f = f * sd.sz[k] + dig[k];
-      o32[s2] = static_cast<int>(f);
-    }
-  }
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pcg_off, o32, sizeof(int) * sd.S_min, 0, cudaMemcpyHostToDevice, L.s));
   PcgArgs a{};
+  {
+    const StencilOffsets off = make_stencil_offsets(sd);
+    for (int s2 = 0; s2 < sd.S_min; ++s2) a.off[s2] = off.o32[s2];
+  }
   a.m = static_cast<int>(sd.m);
   a.d = sd.d;
   a.A = A;

@@ -29,62 +29,6 @@ namespace cg = cooperative_groups;
 constexpr int EF_NT = 256;
 constexpr int EF_MAXP = 32;
 
-// stencil offsets for this translation unit (no relocatable device code)
-__constant__ long long c_off_flat[172];
-__constant__ signed char c_off_d[172][4];
-__constant__ int c_pen_ob[49];
-__constant__ int c_pen_s[49][7];
-
-static void ef_upload_offsets(const StencilDesc& sd, cudaStream_t s) {
-  const int E = 2 * sd.W - 1;
-  int S = 1;
-  for (int k = 0; k < sd.d; ++k) S *= E;
-  const int c0 = (S - 1) / 2;
-  long long flat[172];
-  signed char dd[172][4] = {};
-  for (int s2 = 0; s2 < sd.S_min; ++s2) {
-    int q = c0 + s2;
-    int dig[3] = {0, 0, 0};
-    for (int k = sd.d - 1; k >= 0; --k) {
-      dig[k] = q % E - (sd.W - 1);
-      q /= E;
-    }
-    long long f = 0;
-    for (int k = 0; k < sd.d; ++k) {
-      f = f * sd.sz[k] + dig[k];
-      dd[s2][k] = static_cast<signed char>(dig[k]);
-    }
-    flat[s2] = f;
-  }
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_flat, flat, sizeof(long long) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_d, dd, sizeof(dd[0]) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
-  // pencils of the full stencil along the last dimension (k_spmm_pencil): base flat offset of
-  // pencil q (last digit 0) and, per last-dimension shift, the stored half index (≥ 0: the
-  // entry sits at the node itself) or −(index + 1) (mirrored: at the partner node)
-  int npen = 1;
-  for (int k = 0; k + 1 < sd.d; ++k) npen *= E;
-  int pen_ob[49];
-  int pen_s[49][7];
-  for (int q = 0; q < npen; ++q) {
-    int dig[3] = {0, 0, 0};
-    int r = q;
-    for (int k = sd.d - 2; k >= 0; --k) {
-      dig[k] = r % E - (sd.W - 1);
-      r /= E;
-    }
-    long long f = 0;
-    for (int k = 0; k < sd.d; ++k) f = f * sd.sz[k] + (k + 1 < sd.d ? dig[k] : 0);
-    pen_ob[q] = static_cast<int>(f);
-    for (int t = 0; t < E; ++t) {
-      int full = 0;
-      for (int k = 0; k < sd.d; ++k) full = full * E + (k + 1 < sd.d ? dig[k] : t - (sd.W - 1)) + (sd.W - 1);
-      pen_s[q][t] = full >= c0 ? full - c0 : -((S - 1 - full) - c0) - 1;
-    }
-  }
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pen_ob, pen_ob, sizeof(int) * npen, 0, cudaMemcpyHostToDevice, s));
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_pen_s, pen_s, sizeof(pen_s[0]) * npen, 0, cudaMemcpyHostToDevice, s));
-}
-
 struct EfScal {
   double cq, cqp, bprev, e, alpha, scale, b;
   int done, order;
@@ -244,7 +188,8 @@ __global__ void __launch_bounds__(EF_NT) k_ef_g2(int64_t m, int i, int k, const 
 // once and applied to every probe.
 template <int PB, int SMIN>
 __global__ void __launch_bounds__(128) k_spmm(int64_t m, const double* __restrict__ A, const double* __restrict__ x,
-                                              double* __restrict__ out, int P, const EfScal* sc) {
+                                              double* __restrict__ out, int P, const EfScal* sc,
+                                              const __grid_constant__ StencilOffsets off) {
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a >= m) return;
   double acc[PB];
@@ -254,7 +199,7 @@ __global__ void __launch_bounds__(128) k_spmm(int64_t m, const double* __restric
   // check-free: off-grid partners hit exactly-zero stencil entries (see operators.cu)
 #pragma unroll 2
   for (int s = 1; s < SMIN; ++s) {
-    const int64_t o = c_off_flat[s];
+    const int64_t o = off.flat[s];
     const int64_t f = a + o, b = a - o;
     if (f >= 0 && f < m) {
       const double v = A[s * m + a];
@@ -288,7 +233,7 @@ constexpr int PEN_T = 128;
 template <int PB, int W>
 __global__ void __launch_bounds__(PEN_T) k_spmm_pencil(int m, int npen, const double* __restrict__ A,
                                                        const double* __restrict__ x, double* __restrict__ out, int P,
-                                                       const EfScal* sc) {
+                                                       const EfScal* sc, const __grid_constant__ PencilTables pt) {
   constexpr int E = 2 * W - 1, WL = PEN_T + 2 * (W - 1);
   extern __shared__ double win[];  // [P][WL]
   const int a0 = blockIdx.x * PEN_T;
@@ -297,7 +242,7 @@ __global__ void __launch_bounds__(PEN_T) k_spmm_pencil(int m, int npen, const do
 #pragma unroll
   for (int p = 0; p < PB; ++p) acc[p] = 0.0;
   for (int q = 0; q < npen; ++q) {
-    const int ob = c_pen_ob[q];
+    const int ob = pt.ob[q];
     __syncthreads();
     for (int i = threadIdx.x; i < P * WL; i += PEN_T) {
       const int p = i / WL, t = i - p * WL;
@@ -308,7 +253,7 @@ __global__ void __launch_bounds__(PEN_T) k_spmm_pencil(int m, int npen, const do
     if (a < m) {
 #pragma unroll
       for (int t = 0; t < E; ++t) {
-        const int sidx = c_pen_s[q][t];
+        const int sidx = pt.s[q][t];
         const int o = ob + t - (W - 1);
         double c;
         if (sidx >= 0) {
@@ -339,7 +284,8 @@ constexpr int PEN2_T = 128;  // threads per block (2 · 128 nodes)
 template <int PH, int W>
 __global__ void __launch_bounds__(PEN2_T) k_spmm_pencil2(int m, int npen, const double* __restrict__ A,
                                                          const double* __restrict__ x, double* __restrict__ out,
-                                                         int P, const EfScal* sc) {
+                                                         int P, const EfScal* sc,
+                                                         const __grid_constant__ PencilTables pt) {
   constexpr int E = 2 * W - 1, NT = 2 * PEN2_T, WL = NT + 2 * (W - 1) + 2;  // even row length
   extern __shared__ __align__(16) double win2[];  // [PH][WL]
   const int p0 = blockIdx.y * PH;
@@ -353,7 +299,7 @@ __global__ void __launch_bounds__(PEN2_T) k_spmm_pencil2(int m, int npen, const 
 #pragma unroll
   for (int p = 0; p < PH; ++p) acc0[p] = acc1[p] = 0.0;
   for (int q = 0; q < npen; ++q) {
-    const int ob = c_pen_ob[q];
+    const int ob = pt.ob[q];
     __syncthreads();
     for (int i = threadIdx.x; i < np * WL; i += PEN2_T) {
       const int p = i / WL, t = i - p * WL;
@@ -364,7 +310,7 @@ __global__ void __launch_bounds__(PEN2_T) k_spmm_pencil2(int m, int npen, const 
     double c0[E], c1[E];
 #pragma unroll
     for (int t = 0; t < E; ++t) {
-      const int sidx = c_pen_s[q][t];
+      const int sidx = pt.s[q][t];
       const int o = ob + t - (W - 1);
       c0[t] = c1[t] = 0.0;
       if (sidx >= 0) {
@@ -419,6 +365,7 @@ static void launch_spmm(const Launch& L, const StencilDesc& sd, const double* A,
     return e && e[0] == '1';
   }();
   if (!grid_stride && sd.d >= 2 && sd.m < (int64_t{1} << 31)) {
+    const PencilTables pt = make_pencil_tables(sd);
     int npen = 1;
     for (int k = 0; k + 1 < sd.d; ++k) npen *= 2 * sd.W - 1;
     const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, PEN_T));
@@ -432,34 +379,27 @@ static void launch_spmm(const Launch& L, const StencilDesc& sd, const double* A,
       constexpr int PH = 16, WL2 = 2 * PEN2_T + 6 + 2;
       const size_t sm2 = sizeof(double) * PH * WL2;
       const dim3 g2(static_cast<unsigned>(ceil_div(sd.m, 2 * PEN2_T)), static_cast<unsigned>(ceil_div(P, PH)));
-      k_spmm_pencil2<PH, 4><<<g2, PEN2_T, sm2, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+      k_spmm_pencil2<PH, 4><<<g2, PEN2_T, sm2, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc, pt);
     } else if (sd.W == 4) {
-      static bool attr = false;
-      if (!attr) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_spmm_pencil<EF_MAXP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 6))));
-        attr = true;
-      }
-      k_spmm_pencil<EF_MAXP, 4><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_spmm_pencil<EF_MAXP, 4>),
+                           static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 6)));
+      k_spmm_pencil<EF_MAXP, 4><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc, pt);
     } else {
-      static bool attr = false;
-      if (!attr) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_spmm_pencil<EF_MAXP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 2))));
-        attr = true;
-      }
-      k_spmm_pencil<EF_MAXP, 2><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc);
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_spmm_pencil<EF_MAXP, 2>),
+                           static_cast<int>(sizeof(double) * EF_MAXP * (PEN_T + 2)));
+      k_spmm_pencil<EF_MAXP, 2><<<blocks, PEN_T, smem, L.s>>>(static_cast<int>(sd.m), npen, A, x, out, P, sc, pt);
     }
     return;
   }
   const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, 128));
+  const StencilOffsets off = make_stencil_offsets(sd);
   switch (sd.S_min) {
-    case 172: k_spmm<EF_MAXP, 172><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
-    case 25: k_spmm<EF_MAXP, 25><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
-    case 4: k_spmm<EF_MAXP, 4><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
-    case 14: k_spmm<EF_MAXP, 14><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
-    case 5: k_spmm<EF_MAXP, 5><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
-    default: k_spmm<EF_MAXP, 2><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc); break;
+    case 172: k_spmm<EF_MAXP, 172><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
+    case 25: k_spmm<EF_MAXP, 25><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
+    case 4: k_spmm<EF_MAXP, 4><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
+    case 14: k_spmm<EF_MAXP, 14><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
+    case 5: k_spmm<EF_MAXP, 5><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
+    default: k_spmm<EF_MAXP, 2><<<blocks, 128, 0, L.s>>>(sd.m, A, x, out, P, sc, off); break;
   }
 }
 
@@ -603,7 +543,6 @@ EflaOut efla_run(const Launch& L, const StencilDesc& sd, const double* A, const 
   k_ef_init<<<gv, EF_NT, 0, L.s>>>(m, P, z0sq_dev, wt_in, kwt_in, wt.d(), kwt.d());
   k_ef_scal_init<<<1, 32, 0, L.s>>>(P, sc, dv.d(), k);
   L.count(2);
-  ef_upload_offsets(sd, L.s);
   for (int i = 0; i < k; ++i) {
     k_ef_s1<<<gv, EF_NT, 0, L.s>>>(m, sc, sbar.d(), kwt.d(), qprev.d(), wv.d(), pcur.d(), wt.d(), part.d(), nblk);
     k_ef_reduce<<<P * 2, EF_NT, 0, L.s>>>(part.d(), nblk, dots.d());
@@ -966,7 +905,6 @@ BatchedOp sym_op(const Launch& L, const StencilDesc& sd, const double* A, const 
                  double* ku, double* wku, double* t0, double* t1) {
   return [=](const double* in, double* out) {
     run_kg_batched(L, kg, P, in, ku, t0, t1);
-    ef_upload_offsets(sd, L.s);
     launch_spmm(L, sd, A, ku, wku, P, nullptr);
     run_kg_batched(L, kg, P, wku, out, t0, t1);
     const int64_t n = static_cast<int64_t>(P) * sd.m;
@@ -1010,11 +948,12 @@ __global__ void k_dense_kg(int64_t m, KgDev kg, double* K) {
 }
 
 // dense WᵀW from the half stencil: row a, offset s ≥ 0: (a, a+o_s) and (a+o_s, a)
-__global__ void k_dense_wtw(int64_t m, int S_min, const double* A, double* D) {
+__global__ void k_dense_wtw(int64_t m, int S_min, const double* A, double* D,
+                            const __grid_constant__ StencilOffsets off) {
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a >= m) return;
   for (int s2 = 0; s2 < S_min; ++s2) {
-    const int64_t b = a + c_off_flat[s2];
+    const int64_t b = a + off.flat[s2];
     if (b < 0 || b >= m) continue;
     const double v = A[static_cast<int64_t>(s2) * m + a];
     if (v == 0.0) continue;
@@ -1137,8 +1076,8 @@ double dense_logdet_grid_system(const Launch& L, const StencilDesc& sd, const do
   DevMem K(MM), D(MM), S(MM);
   GSGPC_CUDA(cudaMemsetAsync(D.p, 0, MM, L.s));
   k_dense_kg<<<static_cast<unsigned>(ceil_div(m * m, 256)), 256, 0, L.s>>>(m, kg, K.d());
-  ef_upload_offsets(sd, L.s);
-  k_dense_wtw<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(m, sd.S_min, A, D.d());
+  k_dense_wtw<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(m, sd.S_min, A, D.d(),
+                                                                      make_stencil_offsets(sd));
   const dim3 gg(static_cast<unsigned>(ceil_div(m, 32)), static_cast<unsigned>(ceil_div(m, 32)));
   k_dgemm_shift<<<gg, 256, 0, L.s>>>(static_cast<int>(m), K.d(), D.d(), sigma_sq, S.d());
   L.count(3);
@@ -1301,7 +1240,6 @@ BcgOut bcg_run(const Launch& L, const StencilDesc& sd, const double* A, const Kg
   const unsigned gl = static_cast<unsigned>(ceil_div(pm, EF_NT));
   GSGPC_CUDA(cudaMemcpyAsync(r.p, rhat0, V, cudaMemcpyDeviceToDevice, L.s));
   GSGPC_CUDA(cudaMemsetAsync(x, 0, V, L.s));
-  ef_upload_offsets(sd, L.s);
   launch_spmm(L, sd, A, r.d(), u.d(), P, nullptr);
   run_kg_batched(L, kg, P, u.d(), v.d(), t0.d(), t1.d());
   k_bcg_init_dir<<<gl, EF_NT, 0, L.s>>>(pm, s2, r.d(), u.d(), v.d(), sdir.d(), z.d());
@@ -1412,7 +1350,6 @@ void cov_sub_abt(const Launch& L, int n, int64_t m, const double* A, const doubl
 }
 
 void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const double* x, double* out, int P) {
-  ef_upload_offsets(sd, L.s);
   for (int p0 = 0; p0 < P; p0 += EF_MAXP) {
     const int pb = std::min(EF_MAXP, P - p0);
     launch_spmm(L, sd, A, x + static_cast<int64_t>(p0) * sd.m, out + static_cast<int64_t>(p0) * sd.m, pb, nullptr);

@@ -9,7 +9,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <stdexcept>
+#include <utility>
 #include <string>
 
 #include "../../include/gsgpc.h"
@@ -33,6 +36,21 @@ struct Error : std::runtime_error {
   } while (0)
 
 inline void invalid(const std::string& m) { throw Error(GSGPC_INVALID_ARGUMENT, m); }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device property of a kernel: keep
+// what was set per (device, kernel), under a lock, so every device (and every thread) sees
+// the attribute before its first launch needing it.
+inline void set_max_dynamic_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  GSGPC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[{dev, func}];
+  if (bytes <= cur || bytes <= 48 * 1024) return;
+  GSGPC_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cur = bytes;
+}
 
 // ------------------------------------------------------------------ grid descriptor
 struct GridDev {

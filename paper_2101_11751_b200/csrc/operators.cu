@@ -23,18 +23,12 @@
 
 namespace gsgpc {
 
-constexpr int MAX_SMIN = 172;  // (7^3 + 1) / 2
-__constant__ long long c_off_flat[MAX_SMIN];
-__constant__ int c_off32[MAX_SMIN];
-__constant__ signed char c_off_d[MAX_SMIN][4];
-
-void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
+StencilOffsets make_stencil_offsets(const StencilDesc& sd) {
+  StencilOffsets t{};
   const int E = 2 * sd.W - 1;
   int S = 1;
   for (int k = 0; k < sd.d; ++k) S *= E;
   const int c0 = (S - 1) / 2;
-  long long flat[MAX_SMIN];
-  signed char dd[MAX_SMIN][4] = {};
   for (int s2 = 0; s2 < sd.S_min; ++s2) {
     int q = c0 + s2;
     long long f = 0;
@@ -45,16 +39,39 @@ void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
     }
     for (int k = 0; k < sd.d; ++k) {
       f = f * sd.sz[k] + dig[k];
-      dd[s2][k] = static_cast<signed char>(dig[k]);
+      t.d[s2][k] = static_cast<signed char>(dig[k]);
     }
-    flat[s2] = f;
+    t.flat[s2] = f;
+    t.o32[s2] = static_cast<int>(f);
   }
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_flat, flat, sizeof(long long) * sd.S_min, 0,
-                                     cudaMemcpyHostToDevice, s));
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off_d, dd, sizeof(dd[0]) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
-  int o32[MAX_SMIN];
-  for (int i = 0; i < sd.S_min; ++i) o32[i] = static_cast<int>(flat[i]);
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_off32, o32, sizeof(int) * sd.S_min, 0, cudaMemcpyHostToDevice, s));
+  return t;
+}
+
+PencilTables make_pencil_tables(const StencilDesc& sd) {
+  PencilTables t{};
+  const int E = 2 * sd.W - 1;
+  int S = 1;
+  for (int k = 0; k < sd.d; ++k) S *= E;
+  const int c0 = (S - 1) / 2;
+  int npen = 1;
+  for (int k = 0; k + 1 < sd.d; ++k) npen *= E;
+  for (int q = 0; q < npen; ++q) {
+    int dig[3] = {0, 0, 0};
+    int r = q;
+    for (int k = sd.d - 2; k >= 0; --k) {
+      dig[k] = r % E - (sd.W - 1);
+      r /= E;
+    }
+    long long f = 0;
+    for (int k = 0; k < sd.d; ++k) f = f * sd.sz[k] + (k + 1 < sd.d ? dig[k] : 0);
+    t.ob[q] = static_cast<int>(f);
+    for (int tt = 0; tt < E; ++tt) {
+      int full = 0;
+      for (int k = 0; k < sd.d; ++k) full = full * E + (k + 1 < sd.d ? dig[k] : tt - (sd.W - 1)) + (sd.W - 1);
+      t.s[q][tt] = full >= c0 ? full - c0 : -((S - 1 - full) - c0) - 1;
+    }
+  }
+  return t;
 }
 
 // ------------------------------------------------------------------ K3 stencil SpMV
@@ -66,25 +83,26 @@ void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s) {
 // the same unrolled loop (no divergence) and the blocks stay in step, which keeps the
 // mirrored-half reads in L2.
 struct OpOff {
-  __device__ __forceinline__ int operator()(int s) const { return c_off32[s]; }
+  const int* o;  // → the launch's __grid_constant__ StencilOffsets::o32
+  __device__ __forceinline__ int operator()(int s) const { return o[s]; }
 };
 
 template <int SMIN>
 __device__ __forceinline__ double spmv_node_fast(int64_t m64, const double* __restrict__ A,
-                                                 const double* __restrict__ v, int64_t a64) {
+                                                 const double* __restrict__ v, int64_t a64, const int* o32) {
   // 32-bit indexing: S_min·m < 2^31 is checked on the host
-  return stencil_row_dot<SMIN>(static_cast<int>(m64), A, v, static_cast<int>(a64), OpOff{});
+  return stencil_row_dot<SMIN>(static_cast<int>(m64), A, v, static_cast<int>(a64), OpOff{o32});
 }
 
 __device__ __forceinline__ double spmv_node_any(const StencilDesc& sd, const double* __restrict__ A,
-                                                const double* __restrict__ v, int64_t a) {
+                                                const double* __restrict__ v, int64_t a, const int* o32) {
   switch (sd.S_min) {
-    case 172: return spmv_node_fast<172>(sd.m, A, v, a);
-    case 25: return spmv_node_fast<25>(sd.m, A, v, a);
-    case 4: return spmv_node_fast<4>(sd.m, A, v, a);
-    case 14: return spmv_node_fast<14>(sd.m, A, v, a);
-    case 5: return spmv_node_fast<5>(sd.m, A, v, a);
-    default: return spmv_node_fast<2>(sd.m, A, v, a);
+    case 172: return spmv_node_fast<172>(sd.m, A, v, a, o32);
+    case 25: return spmv_node_fast<25>(sd.m, A, v, a, o32);
+    case 4: return spmv_node_fast<4>(sd.m, A, v, a, o32);
+    case 14: return spmv_node_fast<14>(sd.m, A, v, a, o32);
+    case 5: return spmv_node_fast<5>(sd.m, A, v, a, o32);
+    default: return spmv_node_fast<2>(sd.m, A, v, a, o32);
   }
 }
 
@@ -97,17 +115,18 @@ __device__ __forceinline__ double spmv_node_any(const StencilDesc& sd, const dou
 template <int SMIN>
 __global__ void __launch_bounds__(256) k_spmv(StencilDesc sd, const double* __restrict__ A,
                                               const double* __restrict__ v, double* __restrict__ out,
-                                              int* __restrict__ flag) {
+                                              int* __restrict__ flag, const __grid_constant__ StencilOffsets off) {
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a >= sd.m) return;
-  const double acc = spmv_node_fast<SMIN>(sd.m, A, v, a);
+  const double acc = spmv_node_fast<SMIN>(sd.m, A, v, a, off.o32);
   if (flag && !isfinite(acc)) *flag = 1;
   out[a] = acc;
 }
 
 __global__ void __launch_bounds__(256) k_spmv_touched(StencilDesc sd, const double* __restrict__ A,
                                                       const double* __restrict__ v, const uint8_t* __restrict__ touched,
-                                                      double* __restrict__ out) {
+                                                      double* __restrict__ out,
+                                                      const __grid_constant__ StencilOffsets off) {
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (a >= sd.m || isfinite(out[a])) return;
   int64_t co[3] = {0, 0, 0};
@@ -122,12 +141,12 @@ __global__ void __launch_bounds__(256) k_spmv_touched(StencilDesc sd, const doub
   const int64_t m = sd.m;
   double acc = touched[a] ? A[a] * v[a] : 0.0;
   for (int s = 1; s < sd.S_min; ++s) {
-    const int64_t o = c_off_flat[s];
+    const int64_t o = off.flat[s];
     bool fwd = true, bwd = true;
 #pragma unroll
     for (int k = 0; k < GSGPC_MAX_DIM; ++k) {
       if (k < sd.d) {
-        const int64_t dk = c_off_d[s][k];
+        const int64_t dk = off.d[s][k];
         fwd = fwd && co[k] + dk >= 0 && co[k] + dk < sd.sz[k];
         bwd = bwd && co[k] - dk >= 0 && co[k] - dk < sd.sz[k];
       }
@@ -140,13 +159,14 @@ __global__ void __launch_bounds__(256) k_spmv_touched(StencilDesc sd, const doub
 
 void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out, int* flag) {
   const unsigned blocks = static_cast<unsigned>(ceil_div(sd.m, 256));
+  const StencilOffsets off = make_stencil_offsets(sd);
   switch (sd.S_min) {
-    case 172: k_spmv<172><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
-    case 25: k_spmv<25><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
-    case 4: k_spmv<4><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
-    case 14: k_spmv<14><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
-    case 5: k_spmv<5><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
-    default: k_spmv<2><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag); break;
+    case 172: k_spmv<172><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
+    case 25: k_spmv<25><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
+    case 4: k_spmv<4><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
+    case 14: k_spmv<14><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
+    case 5: k_spmv<5><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
+    default: k_spmv<2><<<blocks, 256, 0, L.s>>>(sd, A, v, out, flag, off); break;
   }
   L.count();
   GSGPC_CUDA(cudaGetLastError());
@@ -154,7 +174,8 @@ void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const dou
 
 void run_spmv_touched(const Launch& L, const StencilDesc& sd, const double* A, const double* v,
                       const uint8_t* touched, double* out) {
-  k_spmv_touched<<<static_cast<unsigned>(ceil_div(sd.m, 256)), 256, 0, L.s>>>(sd, A, v, touched, out);
+  k_spmv_touched<<<static_cast<unsigned>(ceil_div(sd.m, 256)), 256, 0, L.s>>>(sd, A, v, touched, out,
+                                                                              make_stencil_offsets(sd));
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -269,14 +290,10 @@ static void toep_config(int64_t n, int64_t inner, int64_t outer, ToepArgs& t, di
 
 static void launch_toep(const Launch& L, int mode, ToepArgs t, dim3 grid, size_t smem, CgEpi e) {
   if (mode == 0) {
-    if (smem > 48 * 1024) {
-      GSGPC_CUDA(cudaFuncSetAttribute(k_toep<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    }
+    if (smem > 48 * 1024) set_max_dynamic_smem(reinterpret_cast<const void*>(k_toep<0>), 64 * 1024);
     k_toep<0><<<grid, 256, smem, L.s>>>(t, e);
   } else {
-    if (smem > 48 * 1024) {
-      GSGPC_CUDA(cudaFuncSetAttribute(k_toep<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    }
+    if (smem > 48 * 1024) set_max_dynamic_smem(reinterpret_cast<const void*>(k_toep<1>), 64 * 1024);
     k_toep<1><<<grid, 256, smem, L.s>>>(t, e);
   }
   L.count();
@@ -349,14 +366,15 @@ __global__ void __launch_bounds__(256) k_cg_update(CgBufs b, int64_t m) {
 }
 
 template <int INIT>
-__global__ void __launch_bounds__(256) k_cg_spmv(StencilDesc sd, const double* __restrict__ A, CgBufs b) {
+__global__ void __launch_bounds__(256) k_cg_spmv(StencilDesc sd, const double* __restrict__ A, CgBufs b,
+                                                 const __grid_constant__ StencilOffsets off) {
   CgState* st = b.st;
   if (st->done) return;
   __shared__ double sh[8];
   const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double d = 0.0;
   if (a < sd.m) {
-    const double u = spmv_node_any(sd, A, b.r, a);
+    const double u = spmv_node_any(sd, A, b.r, a, off.o32);
     b.u[a] = u;
     d = u * b.r[a];
   }
@@ -395,7 +413,7 @@ __global__ void __launch_bounds__(256) k_cg_spmv(StencilDesc sd, const double* _
 
 void run_cg_init(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
                  int64_t m) {
-  k_cg_spmv<1><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b);
+  k_cg_spmv<1><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b, make_stencil_offsets(sd));
   L.count();
   CgEpi e{b.r, b.u, b.s, b.z, b.part_b, b.st};
   kg_chain(L, kg, b.u, nullptr, b.kt0, b.kt1, 1, e);
@@ -405,7 +423,7 @@ void run_cg_init(const Launch& L, const StencilDesc& sd, const double* A, const 
 void run_cg_iter(const Launch& L, const StencilDesc& sd, const double* A, const KgDev& kg, const CgBufs& b,
                  int64_t m) {
   k_cg_update<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(b, m);
-  k_cg_spmv<0><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b);
+  k_cg_spmv<0><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, L.s>>>(sd, A, b, make_stencil_offsets(sd));
   L.count(2);
   CgEpi e{b.r, b.u, b.s, b.z, b.part_b, b.st};
   kg_chain(L, kg, b.u, nullptr, b.kt0, b.kt1, 1, e);

@@ -1526,7 +1526,7 @@ static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, c
   Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
   const size_t sm = static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 2 * sizeof(int) * bd.nb;
   auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT> : k_partition<T, false, RPT>;
-  GSGPC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(sm));
   k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, bbase, gcur, r1, cid1, pw_in, nw, pw1, gate);
 }
 
@@ -1585,23 +1585,13 @@ void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells
             static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
     } else if (dtype == GSGPC_F32) {
       const size_t ssm = slice_scatter_smem<float>(nbin, nw);
-      static size_t set_f = 0;
-      if (ssm > set_f) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_slice_scatter<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ssm)));
-        set_f = ssm;
-      }
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_scatter<float>), static_cast<int>(ssm));
       k_slice_scatter<float><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
           static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
           static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
     } else {
       const size_t ssm = slice_scatter_smem<double>(nbin, nw);
-      static size_t set_d = 0;
-      if (ssm > set_d) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_slice_scatter<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ssm)));
-        set_d = ssm;
-      }
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_scatter<double>), static_cast<int>(ssm));
       k_slice_scatter<double><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
           static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
           static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
@@ -1923,20 +1913,10 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
     double* yB = bufB + half / 2;
     const unsigned blocks = static_cast<unsigned>(lines * f.tiles);
     if (W == 4) {
-      static bool attr = false;
-      if (!attr) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_xform_first<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kFirstSmem)));
-        attr = true;
-      }
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_xform_first<4>), static_cast<int>(kFirstSmem));
       k_xform_first<4><<<blocks, 256, smem, L.s>>>(mom, bufA, yA, f);
     } else {
-      static bool attr = false;
-      if (!attr) {
-        GSGPC_CUDA(cudaFuncSetAttribute(k_xform_first<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kFirstSmem)));
-        attr = true;
-      }
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k_xform_first<2>), static_cast<int>(kFirstSmem));
       k_xform_first<2><<<blocks, 256, smem, L.s>>>(mom, bufA, yA, f);
     }
     L.count();

@@ -73,7 +73,22 @@ struct StencilDesc {
   int64_t sz[GSGPC_MAX_DIM];
   int64_t m;
 };
-void upload_stencil_offsets(const StencilDesc& sd, cudaStream_t s);
+// Stencil offset tables.  Kernels receive them BY VALUE as __grid_constant__ parameters (the
+// launch's own constant bank, read like __constant__ memory): no module-global table that two
+// contexts, streams or threads could overwrite under each other's in-flight kernels.
+constexpr int kMaxSmin = 172;  // (7^3 + 1) / 2
+constexpr int kMaxPen = 49;    // 7^2 pencils along the last dimension
+struct StencilOffsets {
+  long long flat[kMaxSmin];     // flat offset o_s of half-stencil entry s
+  int o32[kMaxSmin];            // the same in 32 bits (S_min·m < 2^31 checked by the callers)
+  signed char d[kMaxSmin][4];   // per-dimension displacements
+};
+struct PencilTables {           // the full stencil as E^(d−1) pencils along the last dimension
+  int ob[kMaxPen];              // base flat offset of pencil q (last digit 0)
+  int s[kMaxPen][7];            // per last-dimension shift: half index (≥ 0) or −(index + 1) (mirrored)
+};
+StencilOffsets make_stencil_offsets(const StencilDesc& sd);
+PencilTables make_pencil_tables(const StencilDesc& sd);
 // out = (W^T W) v ; if dot_out != nullptr also dot(out, dotv) via deterministic partials.
 // flag (optional, device int): set to 1 when some row's sum is not finite (see k_spmv)
 void run_spmv(const Launch& L, const StencilDesc& sd, const double* A, const double* v, double* out,
@@ -171,8 +186,17 @@ void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const
 // ---- probe_rng.cu: rademacher_probe streams (std::mt19937_64 per probe) on the device
 void mt_seed_state(uint64_t seed, uint64_t p, uint64_t* st /*313*/);
 int64_t probe_rng_slab();
+int64_t probe_rng_scratch_words(int P);
 // next `rows` draws of every probe: states P × 313 (device), planes ≥ P × slab bytes scratch,
-// words[rows] (bit p = probe p is +1)
-void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words);
+// words[rows] (bit p = probe p is +1), scratch ≥ probe_rng_scratch_words(P) device words
+void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words,
+                   uint64_t* scratch);
+// ---- mt_jump.cu: GF(2) jump-ahead of the MT19937-64 streams
+// out[s·K + k] = stream s (in: S × 313, window + index) advanced by 312·q[k] draws; polys_dev
+// ≥ K × 312 device words of scratch.  Synchronises the stream (host staging).
+void run_mt_jump(const Launch& L, const uint64_t* in, int S, const std::vector<uint64_t>& q, uint64_t* polys_dev,
+                 uint64_t* out);
+// host restatement: st (313 words) advanced by `draws` draws
+void mt_jump_host(uint64_t* st, uint64_t draws);
 
 }  // namespace gsgpc

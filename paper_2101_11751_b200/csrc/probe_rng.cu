@@ -7,7 +7,10 @@
 // old state; n−m ≤ i < n−1 from the new words i−(n−m); i = n−1 last), 32 words at a time, and
 // the tempered outputs of a block are written one byte per row (coalesced).  The default is
 // the block-per-probe variant below (k_probe_rng_blk: state in registers, one barrier per
-// twist; config 5's 30 × 5e7 draws 112 → 44 ms); GSGPC_PROBE_RNG_WARP=1 selects this one.  A second kernel
+// twist; config 5's 30 × 5e7 draws 112 → 44 ms), run over substreams of 1,048,320 draws each
+// started by the GF(2) jump-ahead of mt_jump.cu (30 probes × 16 substreams per slab instead
+// of 30 blocks on 148 SMs); GSGPC_PROBE_RNG_WARP=1 selects the warp kernel,
+// GSGPC_PROBE_RNG_NOSPLIT=1 one block per probe.  A second kernel
 // packs the bytes into one 64-bit word per row (bit p = probe p), the layout the binning
 // carries with the rows.  The initial state is built on the host exactly as
 // mersenne_twister_engine(seed_seq&) does ([rand.eng.mers]: generate 2n 32-bit words,
@@ -135,15 +138,19 @@ __global__ void __launch_bounds__(32) k_probe_rng(uint64_t* __restrict__ states,
 // then every thread tempers its two new words into the byte planes.
 constexpr int MT_BT = 160;  // 5 warps; threads ≥ 156 only help with the global state copy
 
-__global__ void __launch_bounds__(MT_BT) k_probe_rng_blk(uint64_t* __restrict__ states, int64_t rows,
-                                                         uint8_t* __restrict__ planes) {
+// Substreams: block b = (probe b / K, substream k = b % K) owns states[b] and draws
+// rows [k·Ls, min((k + 1)·Ls, total)) of its probe's `total` (K = 1: Ls = total).
+__global__ void __launch_bounds__(MT_BT) k_probe_rng_blk(uint64_t* __restrict__ states, int64_t total, int K,
+                                                         int64_t Ls, uint8_t* __restrict__ planes) {
   __shared__ uint64_t xa[2][MT_M + 1], xb[2][MT_M + 1];
-  const int p = blockIdx.x, j = threadIdx.x;
+  const int p = blockIdx.x / K, sk = blockIdx.x % K, j = threadIdx.x;
   const bool act = j < MT_M;
-  uint64_t* st = states + static_cast<int64_t>(p) * (MT_N + 1);
+  uint64_t* st = states + static_cast<int64_t>(blockIdx.x) * (MT_N + 1);
   uint64_t wa = act ? st[j] : 0ull, wb = act ? st[MT_M + j] : 0ull;
   int idx = static_cast<int>(st[MT_N]);
-  uint8_t* out = planes + static_cast<int64_t>(p) * rows;
+  const int64_t r0 = static_cast<int64_t>(sk) * Ls;
+  const int64_t rows = imin64(Ls, total - r0);
+  uint8_t* out = planes + static_cast<int64_t>(p) * total + r0;
   int64_t done = 0;
   if (idx < MT_N) {  // draws left in the current state
     const int k = static_cast<int>(imin64(MT_N - idx, rows));
@@ -200,20 +207,54 @@ __global__ void __launch_bounds__(256) k_probe_pack(const uint8_t* __restrict__ 
   words[i] = w;
 }
 
-int64_t probe_rng_slab() { return int64_t{1} << 24; }
+// dst[p] = src[p·K + K − 1] (the last substream's end state is the probe's new position)
+__global__ void k_probe_take_last(const uint64_t* __restrict__ src, int K, uint64_t* __restrict__ dst) {
+  const int p = blockIdx.x;
+  for (int i = threadIdx.x; i <= MT_N; i += blockDim.x)
+    dst[static_cast<int64_t>(p) * (MT_N + 1) + i] = src[(static_cast<int64_t>(p) * K + K - 1) * (MT_N + 1) + i];
+}
 
-void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words) {
+// Substream length: a whole number of 312-word blocks (so every substream start is a
+// block jump x^{312 q} with q = k · 3360, whatever the base index), and 16 of them per slab.
+constexpr int64_t kSubRows = int64_t{MT_N} * 3360;  // 1,048,320 draws
+constexpr int kMaxSub = 16;
+
+int64_t probe_rng_slab() { return kSubRows * kMaxSub; }
+int64_t probe_rng_scratch_words(int P) { return static_cast<int64_t>(P) * kMaxSub * (MT_N + 1) + kMaxSub * 312; }
+
+void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words,
+                   uint64_t* scratch) {
   const int64_t slab = probe_rng_slab();
+  static const bool warp_rng = [] {
+    const char* e = getenv("GSGPC_PROBE_RNG_WARP");
+    return e && e[0] == '1';
+  }();
+  static const bool no_split = [] {
+    const char* e = getenv("GSGPC_PROBE_RNG_NOSPLIT");
+    return e && e[0] == '1';
+  }();
   for (int64_t r0 = 0; r0 < rows; r0 += slab) {
     const int64_t nr = std::min(slab, rows - r0);
-    static const bool warp_rng = [] {
-      const char* e = getenv("GSGPC_PROBE_RNG_WARP");
-      return e && e[0] == '1';
-    }();
-    if (warp_rng) k_probe_rng<<<P, 32, 0, L.s>>>(states, nr, planes);
-    else k_probe_rng_blk<<<P, MT_BT, 0, L.s>>>(states, nr, planes);
+    const int K = (warp_rng || no_split) ? 1 : static_cast<int>(ceil_div(nr, kSubRows));
+    if (warp_rng) {
+      k_probe_rng<<<P, 32, 0, L.s>>>(states, nr, planes);
+      L.count(1);
+    } else if (K == 1) {
+      k_probe_rng_blk<<<P, MT_BT, 0, L.s>>>(states, nr, 1, nr, planes);
+      L.count(1);
+    } else {
+      // substream k of every probe starts k · kSubRows draws after the probe's position
+      uint64_t* sub = scratch;
+      uint64_t* polys = scratch + static_cast<int64_t>(P) * kMaxSub * (MT_N + 1);
+      std::vector<uint64_t> q(K);
+      for (int k = 0; k < K; ++k) q[k] = static_cast<uint64_t>(k) * (kSubRows / MT_N);
+      run_mt_jump(L, states, P, q, polys, sub);
+      k_probe_rng_blk<<<P * K, MT_BT, 0, L.s>>>(sub, nr, K, kSubRows, planes);
+      k_probe_take_last<<<P, 128, 0, L.s>>>(sub, K, states);
+      L.count(2);
+    }
     k_probe_pack<<<static_cast<unsigned>(ceil_div(nr, 256)), 256, 0, L.s>>>(planes, P, nr, words + r0);
-    L.count(2);
+    L.count(1);
   }
   GSGPC_CUDA(cudaGetLastError());
 }

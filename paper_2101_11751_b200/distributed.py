@@ -36,13 +36,19 @@ def stats_pattern_tensor(stats, device=None) -> torch.Tensor:
 
 def allreduce_stats(stats, group=None):
     """Sum the finalized statistics of every rank in place (all ranks end with the merged
-    statistics) and mark the object reduced."""
-    buf = stats_buffer_tensor(stats)
-    pat = stats_pattern_tensor(stats)
+    statistics) and mark the object reduced.
+
+    `stats` exposes reduce_tensor() / pattern_tensor() (views of the library's device buffers
+    for SufficientStats), context.synchronize() and mark_reduced(); the CPU tests hand in the
+    same buffers, as the library wrote them on a B200, held in host tensors (gloo)."""
+    buf = stats.reduce_tensor()
+    pat = stats.pattern_tensor()
     stats.context.synchronize()
-    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True)
     dist.all_reduce(pat, op=dist.ReduceOp.MAX, group=group)
-    torch.cuda.current_stream(buf.device).synchronize()
+    work.wait()
+    if buf.is_cuda:
+        torch.cuda.current_stream(buf.device).synchronize()
     stats.mark_reduced()
     return stats
 
@@ -98,9 +104,3 @@ def log_likelihood_gsgp_sharded(stats, kg, sigma, opts=None, group=None):
     return out
 
 
-def merge_buffers_host(buffers):
-    """Host restatement of the combine step (used by the gloo CPU tests)."""
-    out = buffers[0].clone()
-    for b in buffers[1:]:
-        out += b
-    return out

@@ -549,6 +549,18 @@ class SufficientStats:
         self._ctx.check(_L.load().gsgpc_stats_pattern_buffer(self._ctx.handle, self._h, C.byref(p), C.byref(c)))
         return int(p.value), int(c.value)
 
+    def reduce_tensor(self):
+        """torch view (no copy) of reduce_buffer() on the context's device."""
+        from .distributed import stats_buffer_tensor
+
+        return stats_buffer_tensor(self)
+
+    def pattern_tensor(self):
+        """torch view (no copy) of pattern_buffer() on the context's device."""
+        from .distributed import stats_pattern_tensor
+
+        return stats_pattern_tensor(self)
+
     def mark_reduced(self):
         self._ctx.check(_L.load().gsgpc_stats_mark_reduced(self._ctx.handle, self._h))
 
@@ -603,10 +615,13 @@ class SufficientStatsAccumulator:
         self._rows += rows.value
         return rows.value
 
-    def enable_probes(self, probes: int = 30, seed: int = 0):
+    def enable_probes(self, probes: int = 30, seed: int = 0, first_row: int = 0):
         """Accumulate W^T v_p for the reference's Rademacher probes p < probes (gp.cpp:16-25),
-        generated in stream order by the library; call before adding rows."""
-        self._ctx.check(_L.load().gsgpc_stats_enable_probes(self._ctx.handle, self._h, int(probes), int(seed)))
+        generated in stream order by the library; call before adding rows.  first_row: the
+        global index of this accumulator's first row (a shard of one stream: the probe streams
+        start there, by jump-ahead, so shard images sum to the single-pass images)."""
+        self._ctx.check(_L.load().gsgpc_stats_enable_probes_at(self._ctx.handle, self._h, int(probes), int(seed),
+                                                               int(first_row)))
 
     def reset(self):
         """Back to the freshly constructed state (buffers kept)."""
@@ -671,6 +686,16 @@ class BinaryRowStream:
 
 
 DATA_MAGIC = b"GSGPDAT1"
+
+
+def probe_stream_bits(seed: int, p: int, offset: int, n: int) -> np.ndarray:
+    """Bit 0 of draws [offset, offset + n) of rademacher_probe's (seed, p) stream (gp.cpp:16-25)
+    reached by the library's GF(2) jump-ahead (host only; 1 = +1)."""
+    out = np.zeros(max(int(n), 0), np.uint8)
+    code = _L.load().gsgpc_probe_stream_bits(int(seed), int(p), int(offset), int(n), out.ctypes.data)
+    if code != 0:
+        raise InvalidArgument(f"gsgpc_probe_stream_bits failed ({code})")
+    return out
 
 
 def write_dataset_binary(path, x, y):

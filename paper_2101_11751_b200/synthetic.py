@@ -115,16 +115,21 @@ def generate(cfg_id: int, n: Optional[int] = None, seed: Optional[int] = None):
 
 
 # ---------------------------------------------------------------- torch (device) generators
+GEN_CHUNK = 1 << 24
+
 def generate_torch(cfg_id: int, n: Optional[int] = None, device="cuda", seed: int = 0, packed: bool = True,
-                   chunk: int = 1 << 24):
-    """Full-size rows generated on `device`; packed → (n, d+1) rows (x..., y)."""
+                   start: int = 0):
+    """Rows [start, start + n) of config `cfg_id`'s global synthetic stream, generated on
+    `device`; packed → (n, d+1) rows (x..., y).  The stream is cut into fixed chunks of 2^24
+    rows, chunk c drawn from its own seeded generator, so a rank's shard [start, start + n) is
+    the same rows whatever the number of ranks (strong scaling splits one dataset)."""
     import torch
 
     cfg = CONFIGS[cfg_id]
     n = cfg.n if n is None else int(n)
+    chunk = GEN_CHUNK
     dt = torch.float32 if cfg.dtype == "f32" else torch.float64
     g = torch.Generator(device=device)
-    g.manual_seed(7919 * cfg_id + seed)
     out = torch.empty((n, cfg.d + 1), dtype=dt, device=device)
     if cfg_id == 3:
         centres, bc, bw, ba = (torch.as_tensor(a, device=device, dtype=torch.float64)
@@ -132,8 +137,9 @@ def generate_torch(cfg_id: int, n: Optional[int] = None, device="cuda", seed: in
     if cfg_id == 5:
         om, ph, am = (torch.as_tensor(a, device=device, dtype=torch.float64)
                       for a in _rff_params(np.random.default_rng(5101)))
-    for s in range(0, n, chunk):
-        k = min(chunk, n - s)
+    for c in range(start // chunk, -(-(start + n) // chunk)):
+        g.manual_seed(7919 * cfg_id + seed + 1_000_003 * c)
+        k = chunk
         if cfg_id == 1:
             x = torch.rand((k, 1), generator=g, device=device, dtype=torch.float64) * 20.0 - 10.0
             y = torch.sin(x[:, 0]) + 0.1 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
@@ -148,6 +154,7 @@ def generate_torch(cfg_id: int, n: Optional[int] = None, device="cuda", seed: in
             # Beta(2,5) via the order-statistic construction: the 2nd smallest of 6 uniforms
             u = torch.rand((k, 6), generator=g, device=device, dtype=torch.float64)
             x3 = u.kthvalue(2, dim=1).values
+            del u
             x = torch.cat([x12, x3[:, None]], dim=1)
             y = torch.zeros(k, device=device, dtype=torch.float64)
             for j in range(50):
@@ -161,8 +168,15 @@ def generate_torch(cfg_id: int, n: Optional[int] = None, device="cuda", seed: in
             x = torch.rand((k, 3), generator=g, device=device, dtype=torch.float64)
             y = np.sqrt(2.0 / om.shape[0]) * (torch.cos(x @ om.T + ph) @ am) + \
                 0.1 * torch.randn(k, generator=g, device=device, dtype=torch.float64)
-        out[s:s + k, : cfg.d] = x.to(dt)
-        out[s:s + k, cfg.d] = y.to(dt)
+        lo, hi = max(start, c * chunk), min(start + n, (c + 1) * chunk)
+        out[lo - start: hi - start, : cfg.d] = x[lo - c * chunk: hi - c * chunk].to(dt)
+        out[lo - start: hi - start, cfg.d] = y[lo - c * chunk: hi - c * chunk].to(dt)
+        del x, y
     if packed:
         return out
     return out[:, : cfg.d].contiguous(), out[:, cfg.d].contiguous()
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Rows [lo, hi) of rank `rank` when n rows are split over `world` ranks (strong scaling)."""
+    return n * rank // world, n * (rank + 1) // world

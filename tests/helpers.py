@@ -93,3 +93,37 @@ def dense_W(grid_mins, grid_maxs, sizes, x, W=4):
             if w != 0.0:
                 Wm[i, np.ravel_multi_index(idx, sizes)] += w
     return Wm
+
+
+def write_gsgpsst1(path, sizes_mins_maxs, scheme, rp, col, val, wty, yty, n):
+    """Write statistics in the reference's save_stats layout (io.cpp:192-221): magic
+    "GSGPSST1", u64 d, per dimension (f64 min, f64 max, u64 size), u64 scheme, u64 m, u64 n,
+    u64 nnz, f64 yty, m × f64 W^T y, nnz × (u64 row, u64 col, f64 value) in CSR row order.
+    Used to hand the ORACLE's statistics to the GPU (gsgpc_stats_load), so both solvers run on
+    identical statistics."""
+    mins, maxs, sizes = sizes_mins_maxs
+    d = len(sizes)
+    m = int(np.prod(sizes))
+    with open(path, "wb") as f:
+        f.write(b"GSGPSST1")
+        f.write(np.array([d], np.uint64).tobytes())
+        for k in range(d):
+            f.write(np.array([mins[k], maxs[k]], np.float64).tobytes())
+            f.write(np.array([sizes[k]], np.uint64).tobytes())
+        f.write(np.array([int(scheme), m, int(n), len(val)], np.uint64).tobytes())
+        f.write(np.array([yty], np.float64).tobytes())
+        f.write(np.ascontiguousarray(wty, np.float64).tobytes())
+        rows = np.repeat(np.arange(m), np.diff(rp))
+        trip = np.zeros(len(val), dtype=[("r", "<u8"), ("c", "<u8"), ("v", "<f8")])
+        trip["r"], trip["c"], trip["v"] = rows, col, val
+        f.write(trip.tobytes())
+
+
+def oracle_stats_from_gpu(gs):
+    """The GPU's statistics as an oracle SufficientStats (CSR export → orc_stats_from_csr):
+    the other direction of the identical-statistics handoff, for prefixes where the oracle's
+    own hash-map precompute would take minutes."""
+    import oracle as O
+
+    rp, col, val = gs.csr()
+    return O.SufficientStats.from_csr(gs.grid_size(), rp, col, val, gs.wty(), gs.yty(), gs.n())

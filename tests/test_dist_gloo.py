@@ -96,13 +96,87 @@ def test_gloo_allreduce_equals_merge(tmp_path):
         assert np.array_equal(got, full_mask)  # structure of the union = OR of the shards'
 
 
-def test_host_merge_helper():
-    pytest.importorskip("torch")
-    from paper_2101_11751_b200.distributed import merge_buffers_host
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "dist_shards.npz")
 
-    a = torch.arange(5, dtype=torch.float64)
-    b = torch.ones(5, dtype=torch.float64)
-    assert torch.equal(merge_buffers_host([a, b]), a + b)
+
+class _LibraryBuffers:
+    """A rank's statistics as libgsgpc wrote them on a B200 (tests/golden/make_dist_golden.py):
+    the reduce buffer [stencil | W^T y | probe images | yty | n] and the per-cell pattern bytes,
+    in host tensors, with the interface distributed.allreduce_stats drives."""
+
+    class _Ctx:
+        def synchronize(self):
+            pass
+
+    def __init__(self, buf, pat):
+        self.buf = torch.from_numpy(buf.copy())
+        self.pat = torch.from_numpy(pat.copy())
+        self.context = self._Ctx()
+        self.reduced = False
+
+    def reduce_tensor(self):
+        return self.buf
+
+    def pattern_tensor(self):
+        return self.pat
+
+    def mark_reduced(self):
+        self.reduced = True
+
+
+def _lib_worker(rank, world, port, out_path):
+    from paper_2101_11751_b200.distributed import allreduce_stats
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    z = np.load(GOLD)
+    st = _LibraryBuffers(z[f"buf{rank}"], z[f"pat{rank}"])
+    allreduce_stats(st)
+    assert st.reduced
+    np.save(f"{out_path}.{rank}.npy", st.buf.numpy())
+    np.save(f"{out_path}.pat.{rank}.npy", st.pat.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not os.path.exists(GOLD), reason="tests/golden/dist_shards.npz not generated")
+def test_allreduce_stats_on_library_buffers(tmp_path):
+    """distributed.allreduce_stats (the function the NCCL ranks call) over gloo, on the library's
+    own shard buffers: two row shards of one stream, their probe streams positioned by
+    enable_probes(first_row).  The all-reduced buffers equal the library's single pass over all
+    rows (values to 1e-12, n exact, structure bytes identical), and the stencil / W^T y part
+    equals the oracle's merge() of the same rows."""
+    world = 2
+    port = _free_port()
+    out = str(tmp_path / "lib")
+    mp.start_processes(_lib_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    z = np.load(GOLD)
+    full, pfull = z["buf_full"], z["pat_full"]
+    sizes = [int(v) for v in z["sizes"]]
+    m = int(np.prod(sizes))
+    s_min = int(z["s_min"])
+    for r in range(world):
+        got = np.load(f"{out}.{r}.npy")
+        assert got[-1] == full[-1] == z["x"].shape[0]  # n exact
+        np.testing.assert_allclose(got, full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+        assert np.array_equal(np.load(f"{out}.pat.{r}.npy"), pfull)
+    # against the oracle's statistics of all rows (stencil, W^T y, yty)
+    g = O.fit_grid_to_data([0, 0], [1, 1], sizes)
+    ost = O.sufficient_stats(g, z["x"], z["y"])
+    rp, col, val, wty = ost.csr()
+    ref = csr_to_half_stencil(rp, col, val, sizes, 4).reshape(-1)
+    got = np.load(f"{out}.0.npy")
+    assert np.abs(got[: s_min * m] - ref).max() <= 1e-10 * np.abs(ref).max()
+    assert np.abs(got[s_min * m: s_min * m + m] - wty).max() <= 1e-10 * np.abs(wty).max()
+    assert abs(got[-2] - ost.yty) <= 1e-12 * ost.yty
+    # probe images of the shards sum to the single-stream images of rademacher_probe
+    P = int(z["probes"])
+    img = got[s_min * m + m: s_min * m + m + P * m].reshape(P, m)
+    for p in range(P):
+        v = O.rademacher_probe(z["x"].shape[0], int(z["seed"]), p)
+        ri = O.wt_apply(g, z["x"], v)
+        assert np.abs(img[p] - ri).max() <= 1e-10 * np.abs(ri).max()
 
 
 def test_probe_shards_cover_the_probe_set():
