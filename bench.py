@@ -418,7 +418,7 @@ def run_ours(args):
               "time_to_solution": {"seconds": wall, "loop_seconds": model.loop_seconds,
                                    "prep_seconds": wall - model.loop_seconds, "iterations": model.solve_iterations,
                                    "converged": True,
-                                   "relative_residual": float(np.sqrt(model.residual_sq / st.yty())),
+                                   "relative_residual": float(np.sqrt(model.solve_residual_sq / st.yty())),
                                    "what": "posterior_mean_gsgp(stats, K_G, tol) through the public API, converged "
                                            "(eps = tol²·yᵀy, gp.cpp:326-352), best of 2"},
               "roofline": {"bound": "hbm", "kernel": "k_efcg_persistent (K3 stencil SpMV + K4 K_G modes + updates)",

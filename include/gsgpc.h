@@ -209,6 +209,15 @@ gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** ou
  * (kernels.hpp:11-47: noise_std, lengthscales[dim], outputscale). */
 gsgpc_status gsgpc_kg_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* lengthscales,
                              double outputscale, double noise_std, gsgpc_kg** out);
+/* The same with the K_G route chosen per dimension: dimensions with >= fft_min_nodes nodes
+ * apply T_k by the reference's circulant embedding + FFT (grid.cpp:94-151, 193-235: zero-pad
+ * to next_fast_fft_size(2 n_k − 1), r2c, spectrum product, c2r, 1/e scaling — per factor of
+ * the separable kernel), the others by tensor-core Toeplitz mode products.  fft_min_nodes <= 0:
+ * the default, 2041 (the mode products hold up to 2040 nodes per dimension). */
+gsgpc_status gsgpc_kg_create_ex(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* lengthscales,
+                                double outputscale, double noise_std, int64_t fft_min_nodes, gsgpc_kg** out);
+/* next_fast_fft_size (grid.cpp:73-82): the smallest 5-smooth integer >= x (1 for x < 1). */
+int64_t gsgpc_next_fast_fft_size(int64_t x);
 void gsgpc_kg_destroy(gsgpc_kg* kg);
 /* ToeplitzOperator::apply (grid.hpp:82-83, grid.cpp:193-235): out = K_G v. */
 gsgpc_status gsgpc_kg_apply(gsgpc_ctx* ctx, gsgpc_kg* kg, const double* v, double* out);

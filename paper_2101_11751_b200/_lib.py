@@ -92,6 +92,8 @@ SIGNATURES = {
     "gsgpc_stats_save": (_i, [_vp, _vp, C.c_char_p]),
     "gsgpc_stats_load": (_i, [_vp, C.c_char_p, _P(_vp)]),
     "gsgpc_kg_create": (_i, [_vp, _P(Grid_t), _vp, _d, _d, _P(_vp)]),
+    "gsgpc_kg_create_ex": (_i, [_vp, _P(Grid_t), _vp, _d, _d, _i64, _P(_vp)]),
+    "gsgpc_next_fast_fft_size": (_i64, [_i64]),
     "gsgpc_kg_destroy": (None, [_vp]),
     "gsgpc_kg_apply": (_i, [_vp, _vp, _vp, _vp]),
     "gsgpc_kg_info": (_i, [_vp, _P(_i64), _P(_d)]),

@@ -173,6 +173,7 @@ struct gsgpc_kg {
   double noise_std = 1.0;
   DBuf gen[GSGPC_MAX_DIM];
   KgDev dev{};
+  std::shared_ptr<KgFft> fft;  // circulant-FFT route of the long dimensions (operators.cu)
 };
 
 // LowRankCov (gp.hpp:148-167): R (k × m, row j = column j of the reference's r_), the
@@ -188,6 +189,7 @@ struct gsgpc_lowrank {
   std::vector<double> alpha, beta;
   DBuf gen[GSGPC_MAX_DIM];
   KgDev kg{};
+  std::shared_ptr<KgFft> fft;
 };
 
 struct CgCache {
@@ -583,13 +585,16 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     cid1.ensure(sizeof(int) * nvalid);
     DBuf& pw1 = ctx->buf("bin_probe");
     if (nw) pw1.ensure(sizeof(uint64_t) * nw * nvalid);
-    DBuf& gcur = ctx->buf("bin_cursor");
-    gcur.ensure(sizeof(int) * bd.nb);
+    DBuf& spv = ctx->buf("k1_split_v");
+    DBuf& spc = ctx->buf("k1_split_c");
+    const int64_t spw = split_rec_warps(nvalid), spr = split_rec_doubles(g, probes);
+    spv.ensure(sizeof(double) * spw * spr);
+    spc.ensure(sizeof(int64_t) * spw);
+    const SplitBuf sb{spv.as<double>(), spc.as<int64_t>(), spw, spr};
     DBuf& scnt = ctx->buf("bin_scnt");
     scnt.ensure(sizeof(int) * std::max<int64_t>(1, nslices) * (int64_t{1} << bd.bsh));
     h = pt.begin(2);
-    GSGPC_CUDA(cudaMemsetAsync(gcur.p, 0, sizeof(int) * bd.nb, ctx->stream));
-    run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), bbase.as<int64_t>(), gcur.as<int>(), rows1.p,
+    run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), tcnt.as<int>(), rows1.p,
                   cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr, errp);
     const int64_t* rows_end = bbase.as<int64_t>() + bd.nb;
     if (G == 1) {
@@ -599,10 +604,10 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
       pt.end(h);
       const int hk = pt.begin(3);
       run_moments(L, dtype, pay.p, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
-                  s->pat.as<uint8_t>(), errp, rows_end);
+                  s->pat.as<uint8_t>(), errp, sb, rows_end);
       if (probes > 0) {
         run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
-                          s->pmom.as<double>(), errp, rows_end);
+                          s->pmom.as<double>(), errp, sb, rows_end);
       }
       pt.end(hk);
     } else {
@@ -643,10 +648,10 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
         const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
         const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
         run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>(),
-                    s->pat.as<uint8_t>(), errp);
+                    s->pat.as<uint8_t>(), errp, sb);
         if (probes > 0) {
           run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
-                            probes, s->pmom.as<double>(), errp);
+                            probes, s->pmom.as<double>(), errp, sb);
         }
       }
       pt.end(h);
@@ -1657,6 +1662,13 @@ gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** ou
 // ---------------------------------------------------------------- K_G
 gsgpc_status gsgpc_kg_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* ls, double outputscale,
                              double noise_std, gsgpc_kg** out) {
+  return gsgpc_kg_create_ex(ctx, grid, ls, outputscale, noise_std, 0, out);
+}
+
+int64_t gsgpc_next_fast_fft_size(int64_t x) { return next_fast_fft_size(x); }
+
+gsgpc_status gsgpc_kg_create_ex(gsgpc_ctx* ctx, const gsgpc_grid* grid, const double* ls, double outputscale,
+                                double noise_std, int64_t fft_min_nodes, gsgpc_kg** out) {
   return guard(ctx, [&] {
     if (!out || !ls) invalid("NULL argument");
     const GridDev g = make_grid(grid, GSGPC_CUBIC);
@@ -1689,6 +1701,8 @@ gsgpc_status gsgpc_kg_create(gsgpc_ctx* ctx, const gsgpc_grid* grid, const doubl
       kg->dev.gen[k] = kg->gen[k].as<double>();
     }
     GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
+    kg->fft = kg_fft_create(kg->dev, fft_min_nodes > 0 ? fft_min_nodes : kKgFftMinNodes, ctx->stream);
+    kg->dev.fft = kg->fft.get();
     *out = kg.release();
   });
 }
@@ -1809,7 +1823,9 @@ CgOutcome run_efcg(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_kg* kg, const double* r
   GSGPC_CUDA(cudaEventCreate(&e0));
   GSGPC_CUDA(cudaEventCreate(&e1));
   CgState h{};
-  if (!use_graph) {
+  // the persistent kernel runs the tensor-core mode products only: an FFT-route K_G (a grid
+  // dimension > 2040 nodes) takes the per-phase kernels + cuFFT, graph-replayed
+  if (!use_graph && !kg->dev.fft) {
     // one cooperative launch runs the whole solve (efcg_persistent.cu)
     static const bool trace = [] {
       const char* e = getenv("GSGPC_CG_TRACE");
@@ -2336,6 +2352,7 @@ gsgpc_status gsgpc_posterior_cov_lowrank(gsgpc_ctx* ctx, gsgpc_stats* s, gsgpc_k
     lr->scheme = s->scheme;
     lr->m = m;
     lr->kg = kg->dev;
+    lr->fft = kg->fft;  // the spectra do not depend on the generator copies below
     for (int k = 0; k < kg->dev.d; ++k) {
       const size_t b = sizeof(double) * kg->dev.sz[k];
       lr->gen[k].ensure(b);

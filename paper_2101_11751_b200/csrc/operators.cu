@@ -12,8 +12,12 @@
 //                            (factorized_cg_grid_rhs, solvers.cpp:271-336); dots use
 //                            per-block partials + a last-block reduction (deterministic).
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <algorithm>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "internal.cuh"
@@ -300,6 +304,197 @@ static void launch_toep(const Launch& L, int mode, ToepArgs t, dim3 grid, size_t
   GSGPC_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------ K4' Toeplitz mode by FFT
+// Dimensions too long for the shared-memory / tensor-core mode products (the reference takes
+// any grid): the product with T_k runs as the reference's circulant embedding
+// (grid.cpp:94-151, 193-235) restricted to one factor of the separable SE kernel — every line
+// along k is zero-padded to e_k = next_fast_fft_size(2 n_k − 1), transformed (batched r2c,
+// cuFFT), multiplied by the spectrum of T_k's embedded first column, transformed back (c2r)
+// and scaled by 1/e_k.  O(m log e_k) per mode instead of O(m n_k).
+int64_t next_fast_fft_size(int64_t x) {
+  if (x < 1) return 1;
+  for (int64_t n = x;; ++n) {
+    int64_t r = n;
+    while (r % 2 == 0) r /= 2;
+    while (r % 3 == 0) r /= 3;
+    while (r % 5 == 0) r /= 5;
+    if (r == 1) return n;
+  }
+}
+
+#define GSGPC_CUFFT(expr)                                                                          \
+  do {                                                                                             \
+    const cufftResult _r = (expr);                                                                 \
+    if (_r != CUFFT_SUCCESS)                                                                       \
+      throw ::gsgpc::Error(GSGPC_CUDA_ERROR, std::string(#expr " failed: cufftResult ") + std::to_string(_r)); \
+  } while (0)
+
+struct KgFft {
+  int d = 0;
+  int device = 0;
+  bool on[GSGPC_MAX_DIM] = {};
+  int64_t n[GSGPC_MAX_DIM] = {}, e[GSGPC_MAX_DIM] = {};
+  double2* spec[GSGPC_MAX_DIM] = {};
+  std::map<std::pair<int, int64_t>, std::pair<cufftHandle, cufftHandle>> plans;  // (dim, lines) → r2c, c2r
+  double* rbuf = nullptr;
+  double2* cbuf = nullptr;
+  size_t rcap = 0, ccap = 0;
+  std::mutex mu;
+  ~KgFft() {
+    cudaSetDevice(device);
+    for (auto& kv : plans) {
+      cufftDestroy(kv.second.first);
+      cufftDestroy(kv.second.second);
+    }
+    for (auto* p : spec) cudaFree(p);
+    cudaFree(rbuf);
+    cudaFree(cbuf);
+  }
+  // plans + scratch for `lines` lines of dimension k (not inside a stream capture)
+  std::pair<cufftHandle, cufftHandle> plan(int k, int64_t lines) {
+    auto it = plans.find({k, lines});
+    if (it != plans.end()) return it->second;
+    const size_t need_r = static_cast<size_t>(lines) * e[k], need_c = static_cast<size_t>(lines) * (e[k] / 2 + 1);
+    if (need_r > rcap) {
+      cudaFree(rbuf);
+      rbuf = nullptr;
+      GSGPC_CUDA(cudaMalloc(&rbuf, sizeof(double) * need_r));
+      rcap = need_r;
+    }
+    if (need_c > ccap) {
+      cudaFree(cbuf);
+      cbuf = nullptr;
+      GSGPC_CUDA(cudaMalloc(&cbuf, sizeof(double2) * need_c));
+      ccap = need_c;
+    }
+    int nn = static_cast<int>(e[k]);
+    const int hc = static_cast<int>(e[k] / 2 + 1);
+    cufftHandle f, b;
+    GSGPC_CUFFT(cufftPlanMany(&f, 1, &nn, nullptr, 1, nn, nullptr, 1, hc, CUFFT_D2Z, static_cast<int>(lines)));
+    GSGPC_CUFFT(cufftPlanMany(&b, 1, &nn, nullptr, 1, hc, nullptr, 1, nn, CUFFT_Z2D, static_cast<int>(lines)));
+    plans[{k, lines}] = {f, b};
+    return {f, b};
+  }
+};
+
+bool kg_fft_dim(const KgDev& kg, int k) { return kg.fft != nullptr && kg.fft->on[k]; }
+
+// circulant embedding of a symmetric Toeplitz column: c[j] = g[δ(j)], δ = j (j < n),
+// e − j (e − j < n), else none (grid.cpp:120-138)
+__global__ void k_fft_embed_gen(const double* __restrict__ gen, int64_t n, int64_t e, double* __restrict__ c) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= e) return;
+  c[j] = j < n ? gen[j] : (e - j < n ? gen[e - j] : 0.0);
+}
+
+// lines of X ([outer][n][inner]) → zero-padded rows rb[l][0..e), l = o·inner + i
+__global__ void k_fft_scatter(const double* __restrict__ X, int64_t n, int64_t inner, int64_t lines, int64_t e,
+                              double* __restrict__ rb, const CgState* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= lines * e) return;
+  const int64_t l = q / e, j = q - l * e;
+  const int64_t o = l / inner, i = l - o * inner;
+  rb[q] = j < n ? X[(o * n + j) * inner + i] : 0.0;
+}
+
+__global__ void k_fft_mul(double2* __restrict__ cb, const double2* __restrict__ spec, int64_t hc, int64_t total,
+                          const CgState* st) {
+  if (st != nullptr && st->done) return;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= total) return;
+  const double2 a = cb[q], b = spec[q % hc];
+  cb[q] = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// rb[l][a] / e → Y in [outer][n][inner] order; MODE 1: the CG epilogue of k_toep
+template <int MODE>
+__global__ void __launch_bounds__(256) k_fft_gather(const double* __restrict__ rb, int64_t n, int64_t inner,
+                                                    int64_t total, int64_t e, double scale, double* __restrict__ Y,
+                                                    CgEpi ep) {
+  if (ep.st != nullptr && ep.st->done) return;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double dot = 0.0;
+  if (g < total) {
+    const int64_t i = g % inner, t = g / inner, a = t % n, o = t / n;
+    const double acc = rb[(o * inner + i) * e + a] * scale;
+    if (MODE == 0) {
+      Y[g] = acc;
+    } else {
+      const double beta = ep.st->beta;
+      const double v = acc + ep.st->sigma_sq * ep.r[g];
+      const double s = ep.u[g] + beta * ep.s[g];
+      const double z = v + beta * ep.z[g];
+      ep.s[g] = s;
+      ep.z[g] = z;
+      dot = s * z;
+    }
+  }
+  if (MODE == 1) {
+    __shared__ double sh[8];
+    const double bs = block_sum<256>(dot, sh);
+    if (threadIdx.x == 0) ep.part[blockIdx.x] = bs;
+    if (arrive_last(&ep.st->cnt_b)) {
+      const double pap = reduce_partials<256>(ep.part, gridDim.x, sh);
+      if (threadIdx.x == 0) {
+        ep.st->pap = pap;
+        ep.st->cnt_b = 0;
+      }
+    }
+  }
+}
+
+std::shared_ptr<KgFft> kg_fft_create(const KgDev& kg, int64_t min_nodes, cudaStream_t s) {
+  bool any = false;
+  for (int k = 0; k < kg.d; ++k) any = any || kg.sz[k] >= min_nodes;
+  if (!any) return nullptr;
+  auto f = std::make_shared<KgFft>();
+  f->d = kg.d;
+  GSGPC_CUDA(cudaGetDevice(&f->device));
+  for (int k = 0; k < kg.d; ++k) {
+    if (kg.sz[k] < min_nodes) continue;
+    f->on[k] = true;
+    f->n[k] = kg.sz[k];
+    f->e[k] = next_fast_fft_size(2 * kg.sz[k] - 1);
+    const int64_t e = f->e[k], hc = e / 2 + 1;
+    GSGPC_CUDA(cudaMalloc(&f->spec[k], sizeof(double2) * hc));
+    double* col = nullptr;
+    GSGPC_CUDA(cudaMalloc(&col, sizeof(double) * e));
+    k_fft_embed_gen<<<static_cast<unsigned>(ceil_div(e, 256)), 256, 0, s>>>(kg.gen[k], kg.sz[k], e, col);
+    cufftHandle p;
+    int nn = static_cast<int>(e);
+    GSGPC_CUFFT(cufftPlan1d(&p, nn, CUFFT_D2Z, 1));
+    GSGPC_CUFFT(cufftSetStream(p, s));
+    GSGPC_CUFFT(cufftExecD2Z(p, col, f->spec[k]));
+    GSGPC_CUDA(cudaStreamSynchronize(s));
+    cufftDestroy(p);
+    cudaFree(col);
+    f->plan(k, kg.m / kg.sz[k]);  // one m-vector (the solvers' case; ready before any graph capture)
+  }
+  GSGPC_CUDA(cudaGetLastError());
+  return f;
+}
+
+static void fft_mode(const Launch& L, KgFft& f, int k, const double* X, double* Y, int64_t inner, int64_t outer,
+                     int mode, CgEpi e) {
+  std::lock_guard<std::mutex> lk(f.mu);
+  const int64_t n = f.n[k], E = f.e[k], hc = E / 2 + 1, lines = inner * outer;
+  const auto pl = f.plan(k, lines);
+  const CgState* st = e.st;
+  k_fft_scatter<<<static_cast<unsigned>(ceil_div(lines * E, 256)), 256, 0, L.s>>>(X, n, inner, lines, E, f.rbuf, st);
+  GSGPC_CUFFT(cufftSetStream(pl.first, L.s));
+  GSGPC_CUFFT(cufftExecD2Z(pl.first, f.rbuf, f.cbuf));
+  k_fft_mul<<<static_cast<unsigned>(ceil_div(lines * hc, 256)), 256, 0, L.s>>>(f.cbuf, f.spec[k], hc, lines * hc, st);
+  GSGPC_CUFFT(cufftSetStream(pl.second, L.s));
+  GSGPC_CUFFT(cufftExecZ2D(pl.second, f.cbuf, f.rbuf));
+  const int64_t total = lines * n;
+  const unsigned gb = static_cast<unsigned>(ceil_div(total, 256));
+  if (mode == 0) k_fft_gather<0><<<gb, 256, 0, L.s>>>(f.rbuf, n, inner, total, E, 1.0 / static_cast<double>(E), Y, e);
+  else k_fft_gather<1><<<gb, 256, 0, L.s>>>(f.rbuf, n, inner, total, E, 1.0 / static_cast<double>(E), Y, e);
+  L.count(3);
+  GSGPC_CUDA(cudaGetLastError());
+}
+
 // Applies T_{d-1}, ..., T_1 (plain) and T_0 (MODE, possibly with the CG epilogue).
 // batch > 1: `batch` contiguous m-vectors, the batch index an extra outermost dimension.
 static void kg_chain(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1,
@@ -309,13 +504,18 @@ static void kg_chain(const Launch& L, const KgDev& kg, const double* v, double* 
     int64_t inner = 1, outer = batch;
     for (int j = k + 1; j < kg.d; ++j) inner *= kg.sz[j];
     for (int j = 0; j < k; ++j) outer *= kg.sz[j];
+    double* dst = k == 0 ? out : (cur == tmp0 ? tmp1 : tmp0);
+    if (kg_fft_dim(kg, k)) {
+      fft_mode(L, *kg.fft, k, cur, dst, inner, outer, k == 0 ? last_mode : 0, e);
+      cur = dst;
+      continue;
+    }
     ToepArgs t{};
     dim3 grid;
     size_t smem;
     toep_config(kg.sz[k], inner, outer, t, grid, smem);
     t.X = cur;
     t.gen = kg.gen[k];
-    double* dst = k == 0 ? out : (cur == tmp0 ? tmp1 : tmp0);
     t.Y = dst;
     launch_toep(L, k == 0 ? last_mode : 0, t, grid, smem, e);
     cur = dst;

@@ -166,6 +166,43 @@ struct BinGate {
   }
 };
 
+// ------------------------------------------------------------------ deterministic ranks
+// The counting sorts of the binning hand out slots from shared-memory atomicAdd cursors in
+// arrival order, so the rows of a cell reached K1 — and the fp64 sums — in a different order
+// every run.  Deterministic ranks without per-item block barriers:
+//   1. warp_rank: each warp ranks its own items per key against its own row of a per-warp
+//      count table (u16, nkeys per warp): __match_any_sync gives the rank inside a round, the
+//      row the warp's earlier rounds;
+//   2. after one block barrier, col_prefix turns every key's column into the exclusive prefix
+//      over the warps and returns the key's total.
+// An item's slot = key start + prefix[warp][key] + rank: order (warp, round, lane), fixed.
+__device__ __forceinline__ int warp_rank(int key, uint16_t* __restrict__ row) {
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int leader = __ffs(peers) - 1;
+  int base = 0;
+  if (key >= 0 && lane == leader) {
+    base = row[key];
+    row[key] = static_cast<uint16_t>(base + __popc(peers));
+  }
+  base = __shfl_sync(0xffffffffu, base, leader);
+  __syncwarp();
+  return key >= 0 ? base + __popc(peers & ((1u << lane) - 1u)) : -1;
+}
+
+// column key of the [NW][nkeys] table → exclusive prefix over warps (+ add), returns the total
+template <int NW>
+__device__ __forceinline__ int col_prefix(uint16_t* __restrict__ tab, int nkeys, int key, int add) {
+  int run = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int v = tab[w * nkeys + key];
+    tab[w * nkeys + key] = static_cast<uint16_t>(run + add);
+    run += v;
+  }
+  return run;
+}
+
 // ------------------------------------------------------------------ K2 binning
 // Two-level counting sort, no per-row global atomics.  Rows are cut into tiles of
 // TILE_ROWS; cells into buckets of 2^bsh consecutive (row-major) cells, nb ≤ ~1024 buckets.
@@ -189,7 +226,7 @@ constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threa
 // Build-time knobs (B200, config 3, partition + slice sort = 2.20 ms with the defaults):
 // 512-thread partition blocks ×2 per SM 2.32 ms.
 #ifndef PART_NT_DEF
-#define PART_NT_DEF 1024
+#define PART_NT_DEF 512
 #endif
 #ifndef PART_MINB
 #define PART_MINB 1
@@ -298,7 +335,7 @@ __device__ __forceinline__ int64_t block_exscan_1024(int64_t v, int64_t* wsum, i
 }
 
 // One block (1024 threads), nb ≤ 8 · 1024.
-__global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ gsum, int64_t ngroups, int nb,
+__global__ void __launch_bounds__(1024) k_tscan_buckets(int* __restrict__ gsum, int64_t ngroups, int nb,
                                                         int64_t* __restrict__ bbase, int64_t* __restrict__ sbase) {
   __shared__ int64_t wsum[32];
   const int per = (nb + 1023) / 1024;
@@ -310,7 +347,11 @@ __global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ 
     const int b = b0 + q;
     if (q < per && b < nb) {
       int64_t run = 0;
-      for (int64_t gi = 0; gi < ngroups; ++gi) run += gsum[gi * nb + b];
+      for (int64_t gi = 0; gi < ngroups; ++gi) {  // in place: exclusive prefix over the groups
+        const int v = gsum[gi * nb + b];
+        gsum[gi * nb + b] = static_cast<int>(run);
+        run += v;
+      }
       tots[q] = run;
       rows_local += run;
       slices_local += (run + SLICE_ROWS - 1) / SLICE_ROWS;
@@ -335,6 +376,26 @@ __global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ 
   }
 }
 
+// Tile offsets: tcnt[tile][b] ← first output row of tile's bucket-b rows = bbase[b] + rows
+// of bucket b in earlier tiles (the groups' exclusive prefix from k_tscan_buckets plus the
+// earlier tiles of the group) — every tile's runs are placed by row order, not by which block
+// claimed a cursor first.
+__global__ void k_tile_offsets(int* __restrict__ tcnt, int64_t ntiles, int nb, const int* __restrict__ gpre,
+                               const int64_t* __restrict__ bbase) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ngroups = (ntiles + TSCAN_G - 1) / TSCAN_G;
+  if (idx >= ngroups * nb) return;
+  const int64_t gi = idx / nb;
+  const int b = static_cast<int>(idx - gi * nb);
+  int run = static_cast<int>(bbase[b]) + gpre[idx];
+  const int64_t t1 = imin64((gi + 1) * TSCAN_G, ntiles);
+  for (int64_t t = gi * TSCAN_G; t < t1; ++t) {
+    const int v = tcnt[t * nb + b];
+    tcnt[t * nb + b] = run;
+    run += v;
+  }
+}
+
 // K2c.  Rows are taken in sub-tiles of R rows (R = rows_per_thread · PART_NT): each
 // sub-tile is counting-sorted by bucket in shared memory, claims one run per bucket from
 // the bucket's global cursor (one atomic per (sub-tile, bucket)), and is written out
@@ -342,101 +403,122 @@ __global__ void __launch_bounds__(1024) k_tscan_buckets(const int* __restrict__ 
 // registers (every lane of a warp in a different bucket, 1e3 buckets spread over 2 GB)
 // ran at ~1.1 TB/s whatever the DRAM traffic: the stores' address spread, not the bytes,
 // was the limit.
-template <typename T, bool PACKED, int RPT>
+template <typename T, bool PACKED, int RPT, bool DET>
 __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts, int64_t n, int d,
                                                           const int* __restrict__ cellid, int bsh, int nb,
-                                                          const int64_t* __restrict__ bbase, int* __restrict__ gcur,
+                                                          const int* __restrict__ toff,
                                                           Row4<T>* __restrict__ rows1, int* __restrict__ cid1,
                                                           const uint64_t* __restrict__ pw_in, int nw,
                                                           uint64_t* __restrict__ pw1, BinGate gate) {
   constexpr int R = RPT * PART_NT;
+  constexpr int NW = PART_NT / 32;
+  static_assert(TILE_ROWS % R == 0, "a tile is a whole number of sub-tiles");
   if (gate.closed()) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
   int* stage_c = reinterpret_cast<int*>(stage + R);
-  int* cnt = stage_c + R;   // per-bucket count, then cursor
-  int* goff = cnt + nb;     // global slot of stage row j = goff[bucket] + j
+  uint16_t* tab = reinterpret_cast<uint16_t*>(stage_c + R);   // [NW][nb] per-warp counts (det ranks)
+  int* cnt = reinterpret_cast<int*>(tab + (DET ? ((nb * NW + 1) & ~1) : 0));  // per-bucket count, then local start
+  int* goff = cnt + nb;    // global slot of stage row j = goff[bucket] + j
+  int* gcur = goff + nb;   // next global slot of each bucket in this tile
   __shared__ int wsum[32];
   __shared__ int total_s;
-  const int64_t nsub = (n + R - 1) / R;
-  for (int64_t sub = blockIdx.x; sub < nsub; sub += gridDim.x) {
-    const int64_t base = sub * R;
-    for (int j = threadIdx.x; j < nb; j += PART_NT) cnt[j] = 0;
-    __syncthreads();
-    Row4<T> r[RPT];
-    int c[RPT], rank[RPT];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (DET)
+    for (int j = threadIdx.x; j < nb * NW / 2; j += PART_NT) reinterpret_cast<int*>(tab)[j] = 0;
+  const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int j = threadIdx.x; j < nb; j += PART_NT) gcur[j] = toff[tile * nb + j];
+    for (int sub = 0; sub < TILE_ROWS / R; ++sub) {
+      const int64_t base = tile * TILE_ROWS + static_cast<int64_t>(sub) * R;
+      if (base >= n) break;
+      for (int j = threadIdx.x; j < nb; j += PART_NT) cnt[j] = 0;
+      __syncthreads();
+      Row4<T> r[RPT];
+      int c[RPT], rank[RPT];
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
-      c[u] = -1;
-      if (i < n) {
-        c[u] = __ldcs(cellid + i);
-        load_row<T, PACKED>(pts, d, i, r[u].v);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) rank[u] = c[u] >= 0 ? atomicAdd(&cnt[c[u] >> bsh], 1) : 0;
-    __syncthreads();
-    // exclusive scan of cnt over the buckets (each thread a contiguous segment)
-    const int per = (nb + PART_NT - 1) / PART_NT;
-    const int j0 = threadIdx.x * per;
-    int local = 0;
-    for (int q = 0; q < per; ++q)
-      if (j0 + q < nb) local += cnt[j0 + q];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      int x = lane < PART_NT / 32 ? wsum[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      wsum[lane] = x;
-      if (lane == 31) total_s = x;
-    }
-    __syncthreads();
-    int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
-    for (int q = 0; q < per; ++q) {
-      const int j = j0 + q;
-      if (j < nb) {
-        const int k = cnt[j];
-        goff[j] = k > 0 ? static_cast<int>(bbase[j]) + atomicAdd(&gcur[j], k) - run : 0;
-        cnt[j] = run;  // local start
-        run += k;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      if (c[u] >= 0) {
-        const int bk = c[u] >> bsh;
-        const int lp = cnt[bk] + rank[u];
-        stage[lp] = r[u];
-        stage_c[lp] = c[u];
-        if (nw) {
-          const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
-          const int64_t gp = goff[bk] + lp;
-          for (int q = 0; q < nw; ++q) pw1[gp * nw + q] = pw_in[i * nw + q];
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
+        c[u] = -1;
+        if (i < n) {
+          c[u] = __ldcs(cellid + i);
+          load_row<T, PACKED>(pts, d, i, r[u].v);
         }
       }
+      // ranks within each bucket: deterministic (warp table) or shared-atomic cursors
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int key = c[u] >= 0 ? c[u] >> bsh : -1;
+        if (DET) rank[u] = warp_rank(key, tab + w * nb);
+        else rank[u] = key >= 0 ? atomicAdd(&cnt[key], 1) : 0;
+      }
+      __syncthreads();
+      if (DET)
+        for (int j = threadIdx.x; j < nb; j += PART_NT) cnt[j] = col_prefix<NW>(tab, nb, j, 0);
+      __syncthreads();
+      // exclusive scan of cnt over the buckets (each thread a contiguous segment)
+      const int per = (nb + PART_NT - 1) / PART_NT;
+      const int j0 = threadIdx.x * per;
+      int local = 0;
+      for (int q = 0; q < per; ++q)
+        if (j0 + q < nb) local += cnt[j0 + q];
+      int incl = local;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[w] = incl;
+      __syncthreads();
+      if (w == 0) {
+        int x = lane < PART_NT / 32 ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        wsum[lane] = x;
+        if (lane == 31) total_s = x;
+      }
+      __syncthreads();
+      int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+      for (int q = 0; q < per; ++q) {
+        const int j = j0 + q;
+        if (j < nb) {
+          const int k = cnt[j];
+          goff[j] = gcur[j] - run;  // the tile's next slots of bucket j, in row order
+          gcur[j] += k;
+          cnt[j] = run;  // local start
+          run += k;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        if (c[u] >= 0) {
+          const int bk = c[u] >> bsh;
+          const int lp = cnt[bk] + rank[u] + (DET ? tab[w * nb + bk] : 0);
+          stage[lp] = r[u];
+          stage_c[lp] = c[u];
+          if (nw) {
+            const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
+            const int64_t gp = goff[bk] + lp;
+            for (int q = 0; q < nw; ++q) pw1[gp * nw + q] = pw_in[i * nw + q];
+          }
+        }
+      }
+      __syncthreads();
+      const int tot = total_s;
+      for (int j = threadIdx.x; j < tot; j += PART_NT) {
+        const int cc = stage_c[j];
+        const int64_t gp = goff[cc >> bsh] + j;
+        rows1[gp] = stage[j];
+        cid1[gp] = cc;
+      }
+      if (DET)
+        for (int j = threadIdx.x; j < nb * NW / 2; j += PART_NT) reinterpret_cast<int*>(tab)[j] = 0;
+      __syncthreads();
     }
-    __syncthreads();
-    const int tot = total_s;
-    for (int j = threadIdx.x; j < tot; j += PART_NT) {
-      const int cc = stage_c[j];
-      const int64_t gp = goff[cc >> bsh] + j;
-      rows1[gp] = stage[j];
-      cid1[gp] = cc;
-    }
-    __syncthreads();
   }
 }
 
@@ -537,7 +619,7 @@ __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, con
 // anyway and the staged kernel's extra block barriers cost more (B200: config 3 2.20 vs
 // 2.29 ms, config 5 1.55 vs 1.64 ms, config 2 0.27 vs 0.28 ms; config 4, 8-row runs: staged
 // 2.29 vs direct 3.03 ms).
-template <typename T>
+template <typename T, bool DET>
 __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
                                                        const int64_t* __restrict__ bbase,
                                                        const int64_t* __restrict__ sbase, int bsh, int nb,
@@ -546,38 +628,63 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* 
                                                        const uint64_t* __restrict__ pw1, int nw,
                                                        uint64_t* __restrict__ pws, int64_t s0, BinGate gate) {
   constexpr int UNR = sizeof(T) == 4 ? 8 : 4;
-  extern __shared__ int cur[];
+  constexpr int NW = 256 / 32;
+  extern __shared__ __align__(16) int cur[];
   const int64_t sl = s0 + blockIdx.x;
   if (gate.closed() || sl >= sbase[nb]) return;
   const int b = slice_bucket(sbase, nb, sl);
   const int nbin = 1 << bsh;
+  int* tot = cur + nbin;                                    // per cell: rows of this chunk
+  uint16_t* tab = reinterpret_cast<uint16_t*>(tot + nbin);  // [NW][nbin] per-warp counts (det ranks)
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
   const int ncell = static_cast<int>(imin64(nbin, cells - c0));
   const int64_t r0 = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
   const int64_t r1 = imin64(r0 + SLICE_ROWS, bbase[b + 1]);
   for (int j = threadIdx.x; j < ncell; j += blockDim.x)
     cur[j] = static_cast<int>(off[c0 + j]) + scnt[sl * nbin + j];  // rows per add < 2^31
+  if (DET)
+    for (int j = threadIdx.x; j < nbin * NW; j += blockDim.x) tab[j] = 0;
   __syncthreads();
-  for (int64_t i0 = r0 + threadIdx.x; i0 < r1; i0 += 256 * UNR) {
+  const int w = threadIdx.x >> 5;
+  for (int64_t base = r0; base < r1; base += 256 * UNR) {  // uniform trip count (block barriers)
     int cc[UNR];
     Row4<T> rr[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t i = i0 + u * 256;
+      const int64_t i = base + u * 256 + threadIdx.x;
       cc[u] = -1;
       if (i < r1) {
         cc[u] = __ldcs(cid1 + i);
         rr[u] = rows1[i];
       }
     }
+    int rank[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int key = cc[u] >= 0 ? static_cast<int>(cc[u] - c0) : -1;
+      if (DET) rank[u] = warp_rank(key, tab + w * nbin);
+      else rank[u] = key >= 0 ? atomicAdd(&cur[key], 1) : 0;
+    }
+    if (DET) {  // per cell: each warp's slots start at cur + the earlier warps' counts
+      __syncthreads();
+      for (int j = threadIdx.x; j < ncell; j += blockDim.x) tot[j] = col_prefix<NW>(tab, nbin, j, 0);
+      __syncthreads();
+    }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       if (cc[u] >= 0) {
-        const int64_t pos = atomicAdd(&cur[cc[u] - c0], 1);
+        const int key = static_cast<int>(cc[u] - c0);
+        const int pos = DET ? cur[key] + tab[w * nbin + key] + rank[u] : rank[u];
         out[pos] = rr[u];
-        const int64_t i = i0 + u * 256;
-        for (int w2 = 0; w2 < nw; ++w2) pws[pos * nw + w2] = pw1[i * nw + w2];
+        const int64_t i = base + u * 256 + threadIdx.x;
+        for (int w2 = 0; w2 < nw; ++w2) pws[static_cast<int64_t>(pos) * nw + w2] = pw1[i * nw + w2];
       }
+    }
+    if (DET) {
+      __syncthreads();
+      for (int j = threadIdx.x; j < ncell; j += blockDim.x) cur[j] += tot[j];
+      for (int j = threadIdx.x; j < nbin * NW; j += blockDim.x) tab[j] = 0;
+      __syncthreads();
     }
   }
 }
@@ -592,13 +699,13 @@ template <typename T>
 __host__ __device__ constexpr int ss_sub() { return sizeof(T) == 4 ? 4096 : 2048; }
 
 template <typename T>
-size_t slice_scatter_smem(int nbin, int nw) {
+size_t slice_scatter_smem(int nbin, int nw, bool det) {
   const size_t R = ss_sub<T>();
   return R * sizeof(Row4<T>) + R * sizeof(uint64_t) * (nw > 0 ? 1 : 0) + R * 2 * sizeof(uint16_t) +
-         2 * sizeof(int) * (static_cast<size_t>(nbin) + 1);
+         2 * sizeof(int) * (static_cast<size_t>(nbin) + 1) + (det ? sizeof(uint16_t) * static_cast<size_t>(nbin) * (SS_NT / 32) : 0);
 }
 
-template <typename T>
+template <typename T, bool DET>
 __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
                                                             const int64_t* __restrict__ bbase,
                                                             const int64_t* __restrict__ sbase, int bsh, int nb,
@@ -620,11 +727,15 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __res
   uint16_t* stage_i = stage_c + R;
   int* cnt = reinterpret_cast<int*>(stage_i + R);  // per cell: count, then local start; [ncell] = total
   int* gcur = cnt + nbin + 1;                      // per cell: next global slot
+  constexpr int NW = SS_NT / 32;
+  uint16_t* tab = reinterpret_cast<uint16_t*>(gcur + nbin + 1);  // [NW][nbin] per-warp counts (det ranks)
   __shared__ int wsum[SS_NT / 32];
   const int64_t r0s = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
   const int64_t r1s = imin64(r0s + SLICE_ROWS, bbase[b + 1]);
   for (int j = threadIdx.x; j < ncell; j += SS_NT)
     gcur[j] = static_cast<int>(off[c0 + j]) + scnt[sl * nbin + j];  // rows per add < 2^31
+  if (DET)
+    for (int j = threadIdx.x; j < nbin * NW; j += SS_NT) tab[j] = 0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t r0 = r0s; r0 < r1s; r0 += R) {
     const int nr = static_cast<int>(imin64(R, r1s - r0));
@@ -642,8 +753,15 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __res
       }
     }
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) rank[u] = lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0;
+    for (int u = 0; u < RPT; ++u) {  // ranks within each cell: deterministic (warp table) or atomic
+      if (DET) rank[u] = warp_rank(lc[u], tab + w * nbin);
+      else rank[u] = lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0;
+    }
     __syncthreads();
+    if (DET) {
+      for (int j = threadIdx.x; j < ncell; j += SS_NT) cnt[j] = col_prefix<NW>(tab, nbin, j, 0);
+      __syncthreads();
+    }
     // exclusive scan of cnt[0..ncell) (each thread a contiguous segment)
     const int per = (ncell + SS_NT - 1) / SS_NT;
     const int j0 = threadIdx.x * per;
@@ -682,7 +800,7 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __res
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
       if (lc[u] >= 0) {
-        const int lp = cnt[lc[u]] + rank[u];
+        const int lp = cnt[lc[u]] + rank[u] + (DET ? tab[w * nbin + lc[u]] : 0);
         stage[lp] = rr[u];
         stage_c[lp] = static_cast<uint16_t>(lc[u]);
         stage_i[lp] = static_cast<uint16_t>(u * SS_NT + threadIdx.x);
@@ -697,6 +815,8 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __res
     }
     __syncthreads();
     for (int j = threadIdx.x; j < ncell; j += SS_NT) gcur[j] += cnt[j + 1] - cnt[j];
+    if (DET)
+      for (int j = threadIdx.x; j < nbin * NW; j += SS_NT) tab[j] = 0;
     __syncthreads();  // cnt is reset by the next sub-slice
   }
 }
@@ -778,6 +898,42 @@ __device__ __forceinline__ void row_t(const GridDev& g, const Row4<T>& r, double
 // (config 3, 2.56e6 rows: K1 1.65 → 0.49 ms; the 1.2e8-row step is unchanged).
 __device__ __forceinline__ void flush_val(double* p, double v) { atomicAdd(p, v); }
 
+// Bitwise-reproducible flushes.  Rows reach K1 in a fixed order (deterministic binning), each
+// warp sums its fixed row range in that order, and every cell gets exactly ONE add per launch:
+//   * a segment whose cell starts inside the warp's range is flushed as before (one RED per
+//     entry — the only add of this launch to those addresses, so old + v is order-free);
+//   * the first segment of a range whose cell started in an earlier warp's range stores its
+//     partial in the warp's split record sv[warp] (scell[warp] = the cell) instead;
+//   * k_split_fix then adds each split cell's chain of records, in warp order, with one add.
+// (RED flushes from several warps into one cell summed in arrival order: run-to-run
+// differences of ~1e-14, enough to move CG iteration counts on ill-conditioned systems.)
+struct SplitRec {
+  double* v;        // nwarps × rec doubles
+  int64_t* cell;    // nwarps: the cell of the warp's stored partial, or −1
+  __device__ __forceinline__ void none(int64_t warp, int lane) const {
+    if (lane == 0) cell[warp] = -1;
+  }
+};
+
+// chain heads: warps whose record continues cell c and whose predecessor's record is not c
+__global__ void __launch_bounds__(128) k_split_fix(const double* __restrict__ sv, const int64_t* __restrict__ scell,
+                                                   int64_t nwarps, int rec, int qv, double* __restrict__ M,
+                                                   int64_t mstride, int64_t mbase, BinGate gate) {
+  if (gate.closed()) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nwarps) return;
+  const int64_t c = scell[w];
+  if (c < 0 || (w > 0 && scell[w - 1] == c)) return;
+  int64_t e = w + 1;
+  while (e < nwarps && scell[e] == c) ++e;
+  for (int q = lane; q < qv; q += 32) {
+    double s2 = 0.0;
+    for (int64_t k = w; k < e; ++k) s2 += sv[k * rec + q];
+    M[c * mstride + mbase + q] += s2;
+  }
+}
+
 // ------------------------------------------------------------------ W^T W structure
 // The reference's W^T W holds an entry for every node pair to which some point gives two
 // nonzero weights (interp.cpp:188-200; zero weights are dropped, interp.cpp:94-99), however
@@ -831,11 +987,12 @@ template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
                                                             int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, double* __restrict__ mom,
-                                                            uint8_t* __restrict__ pat, int64_t range) {
+                                                            uint8_t* __restrict__ pat, int64_t range, SplitRec sp) {
   __shared__ __align__(16) double sm[4][32 * D3C_STRIDE];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
   if (gate.closed()) return;
+  sp.none(warp, lane);
   nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
@@ -860,6 +1017,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
   // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
+  bool first = true;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
@@ -909,8 +1067,15 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
       __syncwarp();
       cur_row = next_row;
     }
-    // flush this lane's fragment entries
-    double* M = mom + c * D3C_Q;
+    // flush this lane's fragment entries (a cell continued from the previous warp's range:
+    // into the split record, see SplitRec)
+    const bool split = first && off[c] < r0;
+    first = false;
+    double* M = split ? sp.v + warp * D3C_Q : mom + c * D3C_Q;
+    auto put = [&](int q, double v) {
+      if (split) M[q] = v;
+      else flush_val(M + q, v);
+    };
 #pragma unroll
     for (int tt = 0; tt < 7; ++tt) {
 #pragma unroll
@@ -918,9 +1083,9 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
         const int col = cb + i;
         if (col < 7) {
           if (r < 7) {
-            flush_val(M + r * 49 + tt * 7 + col, dx[tt][i]);
+            put(r * 49 + tt * 7 + col, dx[tt][i]);
           } else if (tt < 4 && col < 4) {
-            flush_val(M + D3C_QX + tt * 4 + col, dx[tt][i]);  // Y[a=0][b=tt][c=col]
+            put(D3C_QX + tt * 4 + col, dx[tt][i]);  // Y[a=0][b=tt][c=col]
           }
         }
         dx[tt][i] = 0.0;
@@ -929,9 +1094,10 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int col = cb + i;
-      if (yrow) flush_val(M + D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i]);
+      if (yrow) put(D3C_QX + ya * 16 + (ybh + (col >> 2)) * 4 + (col & 3), dy[i]);
       dy[i] = 0.0;
     }
+    if (split && lane == 0) sp.cell[warp] = c;
     flush_pat(pat, c, 27, pm, lane);
     pm = 0;
     p = seg_end;
@@ -991,11 +1157,12 @@ template <typename T>
 __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay, int64_t nvalid,
                                                          int64_t row0, BinGate gate, GridDev g,
                                                          double* __restrict__ mom, uint8_t* __restrict__ pat,
-                                                         int64_t range) {
+                                                         int64_t range, SplitRec sp) {
   __shared__ __align__(16) double sm[4][32 * 16];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 4 + wib;
   if (gate.closed()) return;
+  sp.none(warp, lane);
   nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
@@ -1005,18 +1172,33 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
   double dx0 = 0.0, dx1 = 0.0, dy0 = 0.0, dy1 = 0.0;
   int open = -1;   // cell held in the fragments
   unsigned pm = 0;  // its rows' zero-weight patterns (W^T W structure)
+  // the cell of the row before the range: a first cell equal to it continues the previous
+  // warp's range (its partial goes to the split record, see SplitRec)
+  int prev_cell = -1;
+  if (r0 > row0) {
+    double t0[3] = {0.0, 0.0, 0.0}, y0 = 0.0;
+    prev_cell = row_tc<T>(g, pay[r0 - 1], t0, y0);
+  }
+  bool first = true;
   auto flush = [&]() {
     flush_pat(pat, open, 9, pm, lane);
     pm = 0;
-    double* M = mom + static_cast<int64_t>(open) * D2C_Q;
+    const bool split = first && open == prev_cell;
+    first = false;
+    double* M = split ? sp.v + warp * D2C_Q : mom + static_cast<int64_t>(open) * D2C_Q;
+    auto put = [&](int q, double v) {
+      if (split) M[q] = v;
+      else flush_val(M + q, v);
+    };
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int col = cb + i;
       const double vx = i == 0 ? dx0 : dx1, vy = i == 0 ? dy0 : dy1;
-      if (col < 7 && r < 7) flush_val(M + r * 7 + col, vx);
-      else if (r == 7 && col < 4) flush_val(M + D2C_QX + col, vx);  // Y[0][col]
-      if (r < 3 && col < 4) flush_val(M + D2C_QX + (r + 1) * 4 + col, vy);
+      if (col < 7 && r < 7) put(r * 7 + col, vx);
+      else if (r == 7 && col < 4) put(D2C_QX + col, vx);  // Y[0][col]
+      if (r < 3 && col < 4) put(D2C_QX + (r + 1) * 4 + col, vy);
     }
+    if (split && lane == 0) sp.cell[warp] = open;
     dx0 = dx1 = dy0 = dy1 = 0.0;
   };
   // the next batch's row is loaded one batch ahead (its latency hides under this batch)
@@ -1078,7 +1260,7 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
     __syncwarp();
     cur = nxt;
   }
-  // the open cell may continue in the next warp's range: its part is added atomically too
+  // the open cell may continue in the next warp's range: that warp records its own part
   if (open >= 0) flush();
 }
 
@@ -1090,7 +1272,8 @@ template <int D, int W, typename T>
 __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict__ pay,
                                                      const int64_t* __restrict__ off, int64_t cells,
                                                      int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
-                                                     double* __restrict__ mom, uint8_t* __restrict__ pat, int64_t range) {
+                                                     double* __restrict__ mom, uint8_t* __restrict__ pat, int64_t range,
+                                                     SplitRec sp) {
   constexpr int E = 2 * W - 1;
   constexpr int NP = D == 1 ? 3 : (D == 2 ? 9 : 27);
   constexpr int QX = D == 1 ? E : (D == 2 ? E * E : E * E * E);
@@ -1099,6 +1282,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   const int lane = threadIdx.x & 31;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gate.closed()) return;
+  sp.none(warp, lane);
   nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
@@ -1108,6 +1292,7 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
   for (int q = 0; q < Q; ++q) acc[q] = 0.0;
   int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
+  bool first = true;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
@@ -1166,12 +1351,18 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
     // butterfly reduce, then lane l writes moments l, l+32, ...
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = warp_sum(acc[q]);
-    double* M = mom + c * Q;
+    const bool split = first && off[c] < r0;
+    first = false;
+    double* M = split ? sp.v + warp * Q : mom + c * Q;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      if ((q & 31) == lane) flush_val(M + q, acc[q]);
+      if ((q & 31) == lane) {
+        if (split) M[q] = acc[q];
+        else flush_val(M + q, acc[q]);
+      }
       acc[q] = 0.0;
     }
+    if (split && lane == 0) sp.cell[warp] = c;
     flush_pat(pat, c, NP, __reduce_or_sync(0xffffffffu, pl), lane);
     p = seg_end;
   }
@@ -1186,12 +1377,13 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
                                                       const int64_t* __restrict__ off, int64_t cells,
                                                       int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, int probes,
                                                       double* __restrict__ pmom /*cells × P × QY*/,
-                                                      int64_t range, int pbase) {
+                                                      int64_t range, int pbase, SplitRec sp) {
   constexpr int QY = D == 1 ? W : (D == 2 ? W * W : W * W * W);
   __shared__ __align__(16) double sm[2][32 * (QY + 1)];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 2 + wib;
   if (gate.closed()) return;
+  sp.none(warp, lane);
   nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
@@ -1206,6 +1398,7 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
   for (int q = 0; q < QY; ++q) acc[q] = 0.0;
   int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
+  bool first = true;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
@@ -1250,11 +1443,17 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
       }
       __syncwarp();
     }
-    if (plive) {
-      double* M = pmom + (c * probes + pj) * QY;
+    const bool split = first && off[c] < r0;
+    first = false;
+    if (plive) {  // split record: 32 probes × QY per warp
+      double* M = split ? sp.v + (warp * 32 + lane) * QY : pmom + (c * probes + pj) * QY;
 #pragma unroll
-      for (int q = 0; q < QY; ++q) flush_val(M + q, acc[q]);
+      for (int q = 0; q < QY; ++q) {
+        if (split) M[q] = acc[q];
+        else flush_val(M + q, acc[q]);
+      }
     }
+    if (split && lane == 0) sp.cell[warp] = c;
 #pragma unroll
     for (int q = 0; q < QY; ++q) acc[q] = 0.0;
     p = seg_end;
@@ -1508,55 +1707,75 @@ void run_sum_partials(const Launch& L, const double* part, int np, double* acc) 
   GSGPC_CUDA(cudaGetLastError());
 }
 
-void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, const int* tcnt, int* gsum, int64_t* bbase,
+void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, int* tcnt, int* gsum, int64_t* bbase,
                        int64_t* sbase) {
   const int64_t nt = bin_tiles(n), ng = bin_groups(n);
-  k_tscan_groups<<<static_cast<unsigned>(ceil_div(ng * bd.nb, 256)), 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum);
+  const unsigned gb = static_cast<unsigned>(ceil_div(ng * bd.nb, 256));
+  k_tscan_groups<<<gb, 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum);
   k_tscan_buckets<<<1, 1024, 0, L.s>>>(gsum, ng, bd.nb, bbase, sbase);
-  L.count(2);
+  k_tile_offsets<<<gb, 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum, bbase);  // tcnt → per-tile offsets
+  L.count(3);
   GSGPC_CUDA(cudaGetLastError());
 }
 
 int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd) { return ceil_div(nvalid, SLICE_ROWS) + bd.nb; }
 
+// Deterministic ranks while the per-warp count table fits next to the staged sub-tile (bucket
+// count nb ≤ 1280: every grid up to ~2e7 cells); beyond that the shared-atomic cursors.
+constexpr int DET_MAX_NB = 1280;
+
 template <typename T, int RPT>
-static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                               const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                               const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk, BinGate gate) {
-  Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
-  const size_t sm = static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 2 * sizeof(int) * bd.nb;
-  auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT> : k_partition<T, false, RPT>;
-  set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(sm));
-  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, bbase, gcur, r1, cid1, pw_in, nw, pw1, gate);
+static size_t partition_smem(const BinDesc& bd, bool det) {
+  return static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 3 * sizeof(int) * bd.nb +
+         (det ? sizeof(uint16_t) * ((static_cast<size_t>(bd.nb) * (PART_NT / 32) + 1) & ~size_t{1}) : 0);
 }
 
-// rows per thread so that the staged sub-tile + 2 nb counters fit the shared memory
-template <typename T>
-static void launch_partition(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                             const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                             const uint64_t* pw_in, int nw, uint64_t* pw1, int nblk, BinGate gate) {
-  const size_t budget = 200 * 1024 / PART_MINB - 2 * sizeof(int) * bd.nb;
-  const size_t per_rpt = PART_NT * (sizeof(Row4<T>) + sizeof(int));
-  if (budget >= 8 * per_rpt)
-    launch_partition_r<T, 8>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else if (budget >= 4 * per_rpt)
-    launch_partition_r<T, 4>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else if (budget >= 2 * per_rpt)
-    launch_partition_r<T, 2>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+template <typename T, int RPT, bool DET>
+static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                               const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in,
+                               int nw, uint64_t* pw1, int nblk, BinGate gate) {
+  Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
+  const size_t sm = partition_smem<T, RPT>(bd, DET);
+  auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT, DET> : k_partition<T, false, RPT, DET>;
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(sm));
+  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, toff, r1, cid1, pw_in, nw, pw1, gate);
+}
+
+// rows per thread so that the staged sub-tile + per-bucket counters (+ rank tables) fit the
+// shared memory
+template <typename T, bool DET>
+static void launch_partition_d(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
+                               const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in,
+                               int nw, uint64_t* pw1, int nblk, BinGate gate) {
+  const size_t budget = 220 * 1024 / PART_MINB;
+  if (partition_smem<T, 16>(bd, DET) <= budget)
+    launch_partition_r<T, 16, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  else if (partition_smem<T, 8>(bd, DET) <= budget)
+    launch_partition_r<T, 8, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  else if (partition_smem<T, 4>(bd, DET) <= budget)
+    launch_partition_r<T, 4, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  else if (partition_smem<T, 2>(bd, DET) <= budget)
+    launch_partition_r<T, 2, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
   else
-    launch_partition_r<T, 1>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+    launch_partition_r<T, 1, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
 }
 
 void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                   const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                   const uint64_t* pw_in, int nw, uint64_t* pw1, const unsigned long long* err) {
+                   const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in, int nw,
+                   uint64_t* pw1, const unsigned long long* err) {
   const BinGate gate{err, nullptr};
   int dev = 0, sms = 148;
   GSGPC_CUDA(cudaGetDevice(&dev));
   GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, PART_NT), sms * PART_MINB)));
-  if (dtype == GSGPC_F32) launch_partition<float>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else launch_partition<double>(L, p, n, g, bd, cellid, bbase, gcur, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(bin_tiles(n), sms * PART_MINB)));
+  const bool det = bd.nb <= DET_MAX_NB;
+  if (dtype == GSGPC_F32) {
+    if (det) launch_partition_d<float, true>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+    else launch_partition_d<float, false>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  } else {
+    if (det) launch_partition_d<double, true>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+    else launch_partition_d<double, false>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  }
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1575,26 +1794,34 @@ void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells
   if (ns > 0) {
     const int nbin = 1 << bd.bsh;
     if (SLICE_ROWS / nbin >= 32) {
+      // deterministic ranks: cursors + a byte table of 8 warps per cell (nbin ≤ 256 here)
+      const size_t smd = 2 * sizeof(int) * static_cast<size_t>(nbin) + sizeof(uint16_t) * static_cast<size_t>(nbin) * 8;
       if (dtype == GSGPC_F32)
-        k_slice_scatter_direct<float><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+        k_slice_scatter_direct<float, true><<<static_cast<unsigned>(ns), 256, smd, L.s>>>(
             static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
             static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
       else
-        k_slice_scatter_direct<double><<<static_cast<unsigned>(ns), 256, sm, L.s>>>(
+        k_slice_scatter_direct<double, true><<<static_cast<unsigned>(ns), 256, smd, L.s>>>(
             static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
             static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
-    } else if (dtype == GSGPC_F32) {
-      const size_t ssm = slice_scatter_smem<float>(nbin, nw);
-      set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_scatter<float>), static_cast<int>(ssm));
-      k_slice_scatter<float><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
-          static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
     } else {
-      const size_t ssm = slice_scatter_smem<double>(nbin, nw);
-      set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_scatter<double>), static_cast<int>(ssm));
-      k_slice_scatter<double><<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
-          static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-          static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
+      // deterministic ranks while the per-warp table (16 warps × cells, u16) fits: 2^bsh ≤ 2048
+      const bool det = nbin <= 2048;
+      if (dtype == GSGPC_F32) {
+        const size_t ssm = slice_scatter_smem<float>(nbin, nw, det);
+        auto k = det ? k_slice_scatter<float, true> : k_slice_scatter<float, false>;
+        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
+        k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
+            static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+            static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
+      } else {
+        const size_t ssm = slice_scatter_smem<double>(nbin, nw, det);
+        auto k = det ? k_slice_scatter<double, true> : k_slice_scatter<double, false>;
+        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
+        k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
+            static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+            static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
+      }
     }
   }
   L.count(3);
@@ -1611,52 +1838,85 @@ int moments_per_cell(int d, int W) {
   return qx + qy;
 }
 
+static int64_t k1_range_d3() {  // rows per warp of the d = 3 cubic K1 (GSGPC_K1_RANGE: diagnostics)
+  static const int64_t range = [] {
+    const char* e = getenv("GSGPC_K1_RANGE");
+    return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
+  }();
+  return range;
+}
+
+// Split records (SplitRec) of one K1 / K1p launch: warps ≤ rows / min range + a block's slack.
+int64_t split_rec_warps(int64_t rows) { return ceil_div(rows, std::min<int64_t>(512, k1_range_d3())) + 8; }
+int64_t split_rec_doubles(const GridDev& g, int probes) {
+  int64_t q = moments_per_cell(g.d, g.W);
+  int QY = 1;
+  for (int k = 0; k < g.d; ++k) QY *= g.W;
+  if (probes > 0) q = std::max<int64_t>(q, int64_t{32} * QY);
+  return q;
+}
+
+static void split_fix(const Launch& L, const SplitBuf& sb, int64_t nwarps, int rec, int qv, double* M,
+                      int64_t mstride, int64_t mbase, BinGate gate) {
+  if (nwarps <= 0) return;
+  if (nwarps > sb.warps || rec > sb.rec) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
+  k_split_fix<<<static_cast<unsigned>(ceil_div(nwarps, 4)), 128, 0, L.s>>>(sb.v, sb.cell, nwarps, rec, qv, M, mstride,
+                                                                           mbase, gate);
+  L.count();
+}
+
 template <typename T>
 static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, BinGate gate) {
+                           int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, BinGate gate,
+                           const SplitBuf& sb) {
   if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
+  const SplitRec sp{sb.v, sb.cell};
+  const int Q = moments_per_cell(g.d, g.W);
   if (g.d == 3 && g.W == 4) {
-    static const int64_t range = [] {  // rows per warp (GSGPC_K1_RANGE: diagnostics)
-      const char* e = getenv("GSGPC_K1_RANGE");
-      return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
-    }();
+    const int64_t range = k1_range_d3();
     const int64_t warps = ceil_div(nvalid - row0, range);
     static const int minb = [] {
       const char* e = getenv("GSGPC_K1_MINB");
       return e ? atoi(e) : 5;  // resident blocks/SM (B200, config 3, row prefetch): 5 → 5.36, 6 → 5.39, 7 → 5.45 ms
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
-#define GSGPC_D3(MB) k_moments_d3c_mma<T, MB><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range)
+    if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
+#define GSGPC_D3(MB) k_moments_d3c_mma<T, MB><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp)
     if (minb >= 8) GSGPC_D3(8);
     else if (minb == 7) GSGPC_D3(7);
     else if (minb == 6) GSGPC_D3(6);
     else if (minb == 5) GSGPC_D3(5);
     else GSGPC_D3(4);
 #undef GSGPC_D3
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
   } else if (g.d == 2 && g.W == 4) {
     const int64_t range = 512;
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
-    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range);
+    if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
+    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range, sp);
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid - row0, range);
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
+    if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
 #define GSGPC_LM(DD, WW)                                                                          \
   if (g.d == DD && g.W == WW) {                                                                 \
-    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range); \
+    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp); \
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
   }
 }
 
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
                  int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err,
-                 const int64_t* rows_end) {
+                 const SplitBuf& sb, const int64_t* rows_end) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate);
-  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate);
+  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
   if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1675,13 +1935,14 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
                                                           const int64_t* __restrict__ off, int64_t cells,
                                                           int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate,
                                                           GridDev g, int probes, double* __restrict__ pmom,
-                                                          int64_t range, int pbase) {
+                                                          int64_t range, int pbase, SplitRec sp) {
   constexpr int QY = 64;
   __shared__ __align__(16) double sm[2][32 * QY];
   __shared__ uint64_t swd[2][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * 2 + wib;
   if (gate.closed()) return;
+  sp.none(warp, lane);
   nvalid = gate.rows(nvalid);
   const int64_t r0 = row0 + warp * range;
   if (r0 >= nvalid) return;
@@ -1697,6 +1958,7 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
     for (int b = 0; b < PMM_PT; ++b) d[a][b][0] = d[a][b][1] = 0.0;
   int64_t c = first_cell(off, c_lo, cells, r0, lane);
   int64_t p = r0;
+  bool first = true;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
@@ -1755,7 +2017,10 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
       }
       __syncwarp();
     }
-    // flush: D[r][cb + i] = monomial 8 ta + r of probe pbase + 8 tb + cb + i
+    // flush: D[r][cb + i] = monomial 8 ta + r of probe pbase + 8 tb + cb + i (split record:
+    // 8·PMM_PT probes × QY per warp)
+    const bool split = first && off[c] < r0;
+    first = false;
 #pragma unroll
     for (int ta = 0; ta < 8; ++ta)
 #pragma unroll
@@ -1763,9 +2028,13 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int pj = pbase + 8 * tb + cb + i;
-          if (pj < probes) flush_val(pmom + (c * probes + pj) * QY + 8 * ta + r, d[ta][tb][i]);
+          if (pj < probes) {
+            if (split) sp.v[(warp * 8 * PMM_PT + (pj - pbase)) * QY + 8 * ta + r] = d[ta][tb][i];
+            else flush_val(pmom + (c * probes + pj) * QY + 8 * ta + r, d[ta][tb][i]);
+          }
           d[ta][tb][i] = 0.0;
         }
+    if (split && lane == 0) sp.cell[warp] = c;
     p = seg_end;
   }
 }
@@ -1773,9 +2042,12 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
 template <typename T>
 static void launch_probe_moments(const Launch& L, const void* pay, const uint64_t* pw, const int64_t* off,
                                  int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
-                                 int probes, double* pmom, BinGate gate) {
+                                 int probes, double* pmom, BinGate gate, const SplitBuf& sb) {
   if (nvalid <= row0) return;
   const Row4<T>* P = static_cast<const Row4<T>*>(pay);
+  const SplitRec sp{sb.v, sb.cell};
+  int QY = 1;
+  for (int k = 0; k < g.d; ++k) QY *= g.W;
   const int64_t range = 1024;
   const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 2));
   static const bool lane_pm = [] {
@@ -1785,30 +2057,36 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
   if (g.d == 3 && g.W == 4 && !lane_pm) {
     const int64_t rng = 512;
     const unsigned blk = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, rng), 2));
+    if (static_cast<int64_t>(blk) * 2 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1p split records undersized");
     for (int pb = 0; pb < probes; pb += 8 * PMM_PT) {
       k_probe_moments_mma<T><<<blk, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, rng,
-                                                   pb);
+                                                   pb, sp);
       L.count();
+      split_fix(L, sb, static_cast<int64_t>(blk) * 2, 8 * PMM_PT * 64, std::min(8 * PMM_PT, probes - pb) * 64, pmom,
+                static_cast<int64_t>(probes) * 64, static_cast<int64_t>(pb) * 64, gate);
     }
     return;
   }
+  if (static_cast<int64_t>(blocks) * 2 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1p split records undersized");
   for (int pb = 0; pb < probes; pb += 32) {
 #define GSGPC_PM(DD, WW)                                                                                  \
   if (g.d == DD && g.W == WW) {                                                                         \
-    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, range, pb); \
+    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, range, pb, sp); \
   }
     GSGPC_PM(1, 2) GSGPC_PM(1, 4) GSGPC_PM(2, 2) GSGPC_PM(2, 4) GSGPC_PM(3, 2) GSGPC_PM(3, 4)
 #undef GSGPC_PM
     L.count();
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 2, 32 * QY, std::min(32, probes - pb) * QY, pmom,
+              static_cast<int64_t>(probes) * QY, static_cast<int64_t>(pb) * QY, gate);
   }
 }
 
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
                        int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom, const unsigned long long* err, const int64_t* rows_end) {
+                       double* pmom, const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate);
-  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate);
+  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
+  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
   GSGPC_CUDA(cudaGetLastError());
 }
 

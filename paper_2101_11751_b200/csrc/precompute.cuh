@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <functional>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -33,15 +34,18 @@ void run_classify(const Launch& L, int dtype, const PointsDev& p, int64_t n, int
                   const BinDesc& bd, int* tcnt, unsigned long long* err, double* part, int nblk, int* cellid);
 void run_sum_partials(const Launch& L, const double* part, int np, double* acc);
 // bucket sizes: bbase[nb + 1] (row offsets), sbase[nb + 1] (slice offsets); gsum scratch [groups][nb]
-void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, const int* tcnt, int* gsum, int64_t* bbase,
+// bucket totals → bbase / sbase; tcnt (per-tile bucket counts) becomes the per-tile output
+// offsets the partition places each tile's runs at (row order: deterministic)
+void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, int* tcnt, int* gsum, int64_t* bbase,
                        int64_t* sbase);
 int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd);
-// rows → bucket-contiguous rows1 / cid1 / pw1 (gcur: nb zeroed cursors)
+// rows → bucket-contiguous rows1 / cid1 / pw1, in row order within each bucket (toff: the
+// per-tile offsets from run_bucket_totals)
 // Kernels that commit take the device error word of the classify pass (err) and return at
 // once when it records an out-of-grid row; rows_end (device) bounds the rows binned.
 void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                   const int* cellid, const int64_t* bbase, int* gcur, void* rows1, int* cid1,
-                   const uint64_t* pw_in, int nw, uint64_t* pw1, const unsigned long long* err);
+                   const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in, int nw,
+                   uint64_t* pw1, const unsigned long long* err);
 // dst += src unless err records an error
 void run_commit_add(const Launch& L, const unsigned long long* err, const double* src, double* dst);
 // bucket-contiguous → cell-sorted rows (out, pws) and off[] for buckets [b0, b1) = slices [s0, s1)
@@ -50,13 +54,24 @@ void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells
                     int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
                     int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws,
                     const unsigned long long* err);
+// K1 split records (bitwise-reproducible flushes of cells split across warp ranges, see
+// precompute.cu SplitRec): device scratch of warps × rec doubles + warps int64
+struct SplitBuf {
+  double* v;
+  int64_t* cell;
+  int64_t warps;
+  int64_t rec;
+};
+int64_t split_rec_warps(int64_t rows);
+int64_t split_rec_doubles(const GridDev& g, int probes);
 // K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there)
 void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err = nullptr,
-                 const int64_t* rows_end = nullptr);
+                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err,
+                 const SplitBuf& sb, const int64_t* rows_end = nullptr);
 void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
                        int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom, const unsigned long long* err = nullptr, const int64_t* rows_end = nullptr);
+                       double* pmom, const unsigned long long* err, const SplitBuf& sb,
+                       const int64_t* rows_end = nullptr);
 // W^T W structure: touched[S_min][m] (0/1) from the per-cell zero-weight patterns
 // (cells × 3^d bytes written by K1); byte-wise OR for merges.
 void run_touched(const Launch& L, const GridDev& g, int S_min, const uint8_t* pat, uint8_t* out);
@@ -98,12 +113,25 @@ void run_spmv_touched(const Launch& L, const StencilDesc& sd, const double* A, c
                       const uint8_t* touched, double* out);
 
 // Kronecker K_G (Toeplitz mode products)
+struct KgFft;  // operators.cu: circulant-embedding FFT route for large dimensions
 struct KgDev {
   int d;
   int64_t sz[GSGPC_MAX_DIM];
   int64_t m;
   const double* gen[GSGPC_MAX_DIM];  // per-dim generator columns (outputscale folded into dim 0)
+  KgFft* fft;                        // host object (never read on the device); nullptr: no FFT dims
 };
+// next_fast_fft_size (grid.cpp:73-82): smallest 5-smooth integer ≥ x
+int64_t next_fast_fft_size(int64_t x);
+// default: dimensions with more nodes than the tensor-core mode products hold (2040) take the
+// circulant FFT route
+constexpr int64_t kKgFftMinNodes = 2041;
+// Builds the FFT route for the dimensions of kg with ≥ min_nodes nodes (nullptr if none):
+// per dimension the spectrum of T_k's circulant embedding (size next_fast_fft_size(2 n_k − 1),
+// grid.cpp:94-151 restricted to one factor of the separable kernel) and cuFFT plans for one
+// m-vector.  Synchronises the stream.
+std::shared_ptr<KgFft> kg_fft_create(const KgDev& kg, int64_t min_nodes, cudaStream_t s);
+bool kg_fft_dim(const KgDev& kg, int k);
 void run_kg_apply(const Launch& L, const KgDev& kg, const double* v, double* out, double* tmp0, double* tmp1);
 // `batch` contiguous m-vectors at once (tmp0 / tmp1 hold batch·m doubles)
 void run_kg_apply_batched(const Launch& L, const KgDev& kg, int64_t batch, const double* v, double* out,

@@ -688,6 +688,11 @@ class BinaryRowStream:
 DATA_MAGIC = b"GSGPDAT1"
 
 
+def next_fast_fft_size(x: int) -> int:
+    """grid.cpp:73-82: the smallest 5-smooth integer >= x (the circulant embedding size)."""
+    return int(_L.load().gsgpc_next_fast_fft_size(int(x)))
+
+
 def probe_stream_bits(seed: int, p: int, offset: int, n: int) -> np.ndarray:
     """Bit 0 of draws [offset, offset + n) of rademacher_probe's (seed, p) stream (gp.cpp:16-25)
     reached by the library's GF(2) jump-ahead (host only; 1 = +1)."""
@@ -761,7 +766,9 @@ def load_stats(path: str, ctx: Optional[Context] = None) -> StatsFile:
 class ToeplitzOperator:
     """K_G on the grid for the SE-ARD kernel (grid.hpp:58-90)."""
 
-    def __init__(self, grid: Grid, spec: KernelSpec, ctx: Optional[Context] = None):
+    def __init__(self, grid: Grid, spec: KernelSpec, ctx: Optional[Context] = None, fft_min_nodes: int = 0):
+        """fft_min_nodes: dimensions with at least this many nodes apply T_k by the reference's
+        circulant embedding + FFT (0: the default, dimensions above 2040 nodes)."""
         self._ctx = ctx or default_context()
         if spec.hyper.dim() != grid.dim():
             raise InvalidArgument("build_toeplitz_operator: kernel/grid dimension mismatch")
@@ -770,9 +777,9 @@ class ToeplitzOperator:
         ls = np.asarray(spec.hyper.lengthscales, dtype=np.float64)
         h = C.c_void_p()
         g = grid._c()
-        self._ctx.check(_L.load().gsgpc_kg_create(self._ctx.handle, C.byref(g), ls.ctypes.data,
-                                                  float(spec.hyper.outputscale), float(spec.hyper.noise_std),
-                                                  C.byref(h)))
+        self._ctx.check(_L.load().gsgpc_kg_create_ex(self._ctx.handle, C.byref(g), ls.ctypes.data,
+                                                     float(spec.hyper.outputscale), float(spec.hyper.noise_std),
+                                                     int(fft_min_nodes), C.byref(h)))
         self._h = h
         self._count = 0
 

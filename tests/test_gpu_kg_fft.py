@@ -1,0 +1,115 @@
+"""K_G for grid dimensions beyond the tensor-core mode products (> 2040 nodes): the reference's
+circulant embedding + FFT route (grid.cpp:73-82, 94-151, 193-235), per factor of the separable
+SE kernel, against the oracle's restated circulant FFT — apply, and EFCG on identical
+statistics (the GPU's, exported to the oracle)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2101_11751_b200 as G
+from helpers import oracle_stats_from_gpu, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _threads():
+    O.set_threads(os.cpu_count() or 8)
+    yield
+
+
+def ogrid(g):
+    return O.Grid([g.min(k) for k in range(g.dim())], [g.max(k) for k in range(g.dim())],
+                  [g.size(k) for k in range(g.dim())])
+
+
+@pytest.mark.parametrize("sizes,ls", [((37,), [0.1]), ((40, 23), [0.08, 0.2]), ((12, 11, 9), [0.2, 0.3, 0.25]),
+                                      ((64, 64, 64), [0.1, 0.1, 0.1])])
+def test_fft_route_matches_oracle_and_mode_products(sizes, ls):
+    """Every dimension forced onto the FFT route (fft_min_nodes = 2): K_G v against the oracle's
+    circulant FFT and against the tensor-core mode products."""
+    d = len(sizes)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    spec = G.KernelSpec(G.Hyperparams(0.1, ls, 1.3))
+    v = np.random.default_rng(1).standard_normal(g.num_points())
+    fft = G.ToeplitzOperator(g, spec, fft_min_nodes=2)
+    mma = G.ToeplitzOperator(g, spec)
+    okg = O.ToeplitzOperator(ogrid(g), ls, 1.3, 0.1)
+    ref = okg.apply(v)
+    assert rel_err(fft.apply(v), ref) <= 1e-12
+    assert rel_err(fft.apply(v), mma.apply(v)) <= 1e-12
+
+
+def _efcg_case(g, ls, sigma, n, seed, fft_min=0, iters=None, tol=1e-8):
+    d = g.dim()
+    rng = np.random.default_rng(seed)
+    x = rng.random((n, d))
+    y = np.sin(6 * x).sum(axis=1) + 0.1 * rng.standard_normal(n)
+    gst = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    ost = oracle_stats_from_gpu(gst)
+    spec = G.KernelSpec(G.Hyperparams(sigma, ls, 1.0))
+    kg = G.ToeplitzOperator(g, spec, fft_min_nodes=fft_min)
+    okg = O.ToeplitzOperator(ogrid(g), ls, 1.0, sigma)
+    wty = gst.wty()
+    assert rel_err(kg.apply(wty), okg.apply(wty)) <= 1e-12
+    r0 = -okg.apply(wty) / (sigma * sigma)
+    if iters:
+        ores = O.factorized_cg_grid_rhs(okg, ost, r0, sigma, eps_abs=1e-30, maxiter=iters)
+        gres = G.factorized_cg_grid_rhs(kg, gst, r0, sigma, G.GridRhsTolerance(eps_abs=1e-30), iters)
+    else:
+        ores = O.factorized_cg_grid_rhs(okg, ost, r0, sigma, rel_tol=tol, maxiter=3000)
+        gres = G.factorized_cg_grid_rhs(kg, gst, r0, sigma, G.GridRhsTolerance(rel_tol=tol), 3000)
+    return gres, ores
+
+
+def test_1d_grid_10000_nodes():
+    """A 1-D grid of 10,000 nodes (embedding 19,999 → 20,000): apply, and the posterior-mean
+    EFCG on identical statistics — iterations ±1, x̂_d to 1e-6, leading traces to 1e-10."""
+    g = G.fit_grid_to_data([0.0], [1.0], [10_000])
+    gres, ores = _efcg_case(g, [0.0004], 0.5, 400_000, 5)
+    assert ores.converged and gres.converged and ores.iterations < 1500
+    assert abs(gres.iterations - ores.iterations) <= 1
+    assert rel_err(gres.xhat_d, ores.xhat_d) <= 1e-6
+    n = min(20, len(ores.alphas))
+    assert np.max(np.abs(gres.alphas[:n] - ores.alphas[:n]) / np.abs(ores.alphas[:n])) <= 1e-10
+
+
+def test_2d_grid_3000_by_3000():
+    """A 3000 × 3000 grid (9e6 nodes, embedding 6000 × 6000 per the reference's
+    next_fast_fft_size): K_G apply and a 4-iteration EFCG window on identical statistics (the
+    oracle's full complex FFT of 3.6e7 points takes seconds per apply)."""
+    g = G.fit_grid_to_data(np.zeros(2), np.ones(2), (3000, 3000))
+    gres, ores = _efcg_case(g, [0.002, 0.003], 0.3, 200_000, 6, iters=4)
+    assert gres.iterations == ores.iterations == 4
+    for name in ("alphas", "betas", "residual_trace"):
+        a, b = np.asarray(getattr(gres, name)), np.asarray(getattr(ores, name))
+        assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-10, name
+    assert rel_err(gres.xhat_d, ores.xhat_d) <= 1e-8
+
+
+def test_fft_route_posterior_mean_and_loglik():
+    """The FFT route inside posterior_mean_gsgp and the SkiOperator log-likelihood (batched K_G
+    over probes) equals the tensor-core route to round-off."""
+    d, sizes = 2, (48, 40)
+    g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
+    rng = np.random.default_rng(2)
+    x = rng.random((50_000, d))
+    y = np.cos(5 * x).sum(axis=1) + 0.1 * rng.standard_normal(50_000)
+    acc = G.SufficientStatsAccumulator(g)
+    acc.enable_probes(6, seed=4)
+    acc.add(x, y)
+    st = acc.finalize()
+    spec = G.KernelSpec(G.Hyperparams(0.2, [0.1, 0.12], 1.0))
+    kf = G.ToeplitzOperator(g, spec, fft_min_nodes=2)
+    km = G.ToeplitzOperator(g, spec)
+    mf = G.posterior_mean_gsgp(st, kf, spec, G.InterpScheme.Cubic, 0.2, 1e-8, 3000)
+    mm = G.posterior_mean_gsgp(st, km, spec, G.InterpScheme.Cubic, 0.2, 1e-8, 3000)
+    assert abs(mf.solve_iterations - mm.solve_iterations) <= max(1, mm.solve_iterations // 20)
+    assert rel_err(mf.mean_coeffs, mm.mean_coeffs) <= 1e-6
+    opts = G.LoglikOptions(solve_tol=1e-8, probes=6, slq=G.SlqOptions(25, 0.0), seed=4, maxiter=3000,
+                           route=G.LogdetRoute.SkiOperator)
+    lf = G.log_likelihood_gsgp(st, kf, 0.2, opts)
+    lm = G.log_likelihood_gsgp(st, km, 0.2, opts)
+    assert abs(lf.loglik - lm.loglik) <= 1e-6 * abs(lm.loglik)

@@ -28,3 +28,9 @@ def test_substream_boundaries():
     for k in (1, 2, 3):
         got = G.probe_stream_bits(0, 5, k * L - 32, 64)
         assert np.array_equal(got.astype(bool), full[k * L - 32: k * L + 32])
+
+
+def test_next_fast_fft_size_matches_oracle():
+    """grid.cpp:73-82 through the C ABI (host only) against the oracle's restatement."""
+    for x in list(range(-2, 400)) + [1999, 2047, 4095, 5999, 19999, 123457]:
+        assert G.next_fast_fft_size(x) == O.next_fast_fft_size(x), x
