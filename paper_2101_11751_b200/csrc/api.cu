@@ -71,25 +71,33 @@ struct PinnedBuf {
   }
 };
 
-// cudaPointerGetAttributes may hand back an error an earlier call left pending (runtime calls
-// report the last recorded non-sticky error); that must not turn a device pointer into a
-// "host" one, so a failure clears the error and asks once more.
+// Device or host?  A CUDA error already pending when we ask is surfaced (never swallowed:
+// clearing it here would hide a fault from an earlier launch and then treat a device pointer
+// as host memory).  A device allocation of another GPU than the context's is rejected — its
+// kernels would dereference a foreign address.
 bool is_device_ptr(const void* p) {
   if (!p) return false;
-  cudaPointerAttributes a{};
-  cudaError_t e = cudaPointerGetAttributes(&a, p);
-  if (e != cudaSuccess) {
-    static const bool dbg = getenv("GSGPC_DEBUG_PTR") != nullptr;
-    if (dbg) fprintf(stderr, "[gsgpc] cudaPointerGetAttributes: %s (retrying)\n", cudaGetErrorString(e));
+  const cudaError_t pend = cudaPeekAtLastError();
+  if (pend != cudaSuccess) {
     cudaGetLastError();
-    a = cudaPointerAttributes{};
-    e = cudaPointerGetAttributes(&a, p);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
+    throw Error(GSGPC_CUDA_ERROR, std::string("CUDA error pending before the pointer query: ") +
+                                      cudaGetErrorString(pend));
   }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  cudaPointerAttributes a{};
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(GSGPC_CUDA_ERROR, std::string("cudaPointerGetAttributes failed: ") + cudaGetErrorString(e));
+  }
+  if (a.type == cudaMemoryTypeDevice) {
+    int dev = 0;
+    GSGPC_CUDA(cudaGetDevice(&dev));
+    if (a.device != dev)
+      invalid("device array lives on device " + std::to_string(a.device) + ", the context is on device " +
+              std::to_string(dev));
+    return true;
+  }
+  return a.type == cudaMemoryTypeManaged;
 }
 
 }  // namespace
@@ -573,18 +581,14 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     GSGPC_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   {
-    const size_t es = dtype_size(dtype);
-    DBuf& pay = ctx->buf("payload");
-    pay.ensure(es * 4 * nvalid);
-    const int nw = probes > 0 ? (probes + 63) / 64 : 0;
-    DBuf& pws = ctx->buf("probe_sorted");
-    if (nw) pws.ensure(sizeof(uint64_t) * nw * nvalid);
-    DBuf& rows1 = ctx->buf("bin_rows");
-    rows1.ensure(es * 4 * nvalid);
+    // the binning sorts (cell, row) keys; K1 gathers the rows (and probe words) of P through
+    // the cell-sorted row indices
+    DBuf& idx_s = ctx->buf("bin_idx_sorted");
+    idx_s.ensure(sizeof(int) * nvalid);
     DBuf& cid1 = ctx->buf("bin_cid");
     cid1.ensure(sizeof(int) * nvalid);
-    DBuf& pw1 = ctx->buf("bin_probe");
-    if (nw) pw1.ensure(sizeof(uint64_t) * nw * nvalid);
+    DBuf& idx1 = ctx->buf("bin_idx");
+    idx1.ensure(sizeof(int) * nvalid);
     DBuf& spv = ctx->buf("k1_split_v");
     DBuf& spc = ctx->buf("k1_split_c");
     const int64_t spw = split_rec_warps(nvalid), spr = split_rec_doubles(g, probes);
@@ -594,19 +598,17 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
     DBuf& scnt = ctx->buf("bin_scnt");
     scnt.ensure(sizeof(int) * std::max<int64_t>(1, nslices) * (int64_t{1} << bd.bsh));
     h = pt.begin(2);
-    run_partition(L, dtype, P, n, g, bd, cellid.as<int>(), tcnt.as<int>(), rows1.p,
-                  cid1.as<int>(), pw_dev, nw, nw ? pw1.as<uint64_t>() : nullptr, errp);
+    run_partition(L, n, bd, cellid.as<int>(), tcnt.as<int>(), cid1.as<int>(), idx1.as<int>(), errp);
     const int64_t* rows_end = bbase.as<int64_t>() + bd.nb;
     if (G == 1) {
-      run_slice_sort(L, dtype, bd, g.cells, 0, bd.nb, 0, nslices, rows1.p, cid1.as<int>(), bbase.as<int64_t>(),
-                     sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p,
-                     nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr, errp);
+      run_slice_sort(L, bd, g.cells, 0, bd.nb, 0, nslices, cid1.as<int>(), idx1.as<int>(), bbase.as<int64_t>(),
+                     sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), idx_s.as<int>(), errp);
       pt.end(h);
       const int hk = pt.begin(3);
-      run_moments(L, dtype, pay.p, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
+      run_moments(L, dtype, P, idx_s.as<int>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
                   s->pat.as<uint8_t>(), errp, sb, rows_end);
       if (probes > 0) {
-        run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
+        run_probe_moments(L, dtype, P, idx_s.as<int>(), pw_dev, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
                           s->pmom.as<double>(), errp, sb, rows_end);
       }
       pt.end(hk);
@@ -641,16 +643,16 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
       for (int j = 0; j < G; ++j) {
         const int b0 = gb[j], b1 = gb[j + 1];
         if (b1 <= b0) continue;
-        run_slice_sort(LS, dtype, bd, g.cells, b0, b1, hsl[b0], hsl[b1], rows1.p, cid1.as<int>(),
-                       bbase.as<int64_t>(), sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), pay.p,
-                       nw ? pw1.as<uint64_t>() : nullptr, nw, nw ? pws.as<uint64_t>() : nullptr, errp);
+        run_slice_sort(LS, bd, g.cells, b0, b1, hsl[b0], hsl[b1], cid1.as<int>(), idx1.as<int>(),
+                       bbase.as<int64_t>(), sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), idx_s.as<int>(),
+                       errp);
         GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, record(ss), 0));
         const int64_t c_lo = static_cast<int64_t>(b0) << bd.bsh;
         const int64_t c_hi = std::min<int64_t>(static_cast<int64_t>(b1) << bd.bsh, g.cells);
-        run_moments(L, dtype, pay.p, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g, s->mom.as<double>(),
-                    s->pat.as<uint8_t>(), errp, sb);
+        run_moments(L, dtype, P, idx_s.as<int>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
+                    s->mom.as<double>(), s->pat.as<uint8_t>(), errp, sb);
         if (probes > 0) {
-          run_probe_moments(L, dtype, pay.p, pws.as<uint64_t>(), off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
+          run_probe_moments(L, dtype, P, idx_s.as<int>(), pw_dev, off.as<int64_t>(), hb[b0], hb[b1], c_lo, c_hi, g,
                             probes, s->pmom.as<double>(), errp, sb);
         }
       }

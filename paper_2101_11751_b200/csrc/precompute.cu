@@ -28,43 +28,38 @@
 
 namespace gsgpc {
 
-__constant__ double c_C[4 * 4 * 7];  // C[i][j][e]: coefficient of t^e in w_i(t) w_j(t)
-__constant__ double c_P[4 * 4];      // P[i][e]: coefficient of t^e in w_i(t)
-
 // Polynomial form of the 1-D weights on t ∈ [0,1] (expanded from interp.cpp:27-37 on the
 // branch each stencil slot takes): cubic slots c(t+1), c(t), c(1-t), c(2-t); linear
 // slots l(t), l(1-t).  All coefficients are dyadic, so the tables are exact in fp64.
-void weight_polys(int W, double P[4][4]) {
-  for (int i = 0; i < 4; ++i)
-    for (int e = 0; e < 4; ++e) P[i][e] = 0.0;
+// Both schemes' tables are compile-time constants (no per-call upload, so contexts and
+// threads using different schemes on one device never see each other's tables).
+struct PolyTables {
+  double C[4 * 4 * 7];  // C[i][j][e]: coefficient of t^e in w_i(t) w_j(t)
+  double P[4 * 4];      // P[i][e]: coefficient of t^e in w_i(t)
+};
+
+constexpr PolyTables make_poly_tables(int W) {
+  PolyTables t{};
   if (W == 4) {
     const double p[4][4] = {{0.0, -0.5, 1.0, -0.5},
                             {1.0, 0.0, -2.5, 1.5},
                             {0.0, 0.5, 2.0, -1.5},
                             {0.0, 0.0, -0.5, 0.5}};
     for (int i = 0; i < 4; ++i)
-      for (int e = 0; e < 4; ++e) P[i][e] = p[i][e];
+      for (int e = 0; e < 4; ++e) t.P[i * 4 + e] = p[i][e];
   } else {
-    P[0][0] = 1.0;
-    P[0][1] = -1.0;
-    P[1][1] = 1.0;
+    t.P[0 * 4 + 0] = 1.0;
+    t.P[0 * 4 + 1] = -1.0;
+    t.P[1 * 4 + 1] = 1.0;
   }
-}
-
-void upload_poly_tables(int W, cudaStream_t s) {
-  double P[4][4];
-  weight_polys(W, P);
-  double C[4 * 4 * 7] = {0};
   for (int i = 0; i < W; ++i)
     for (int j = 0; j < W; ++j)
       for (int a = 0; a < W; ++a)
-        for (int b = 0; b < W; ++b) C[(i * 4 + j) * 7 + a + b] += P[i][a] * P[j][b];
-  double Pf[16];
-  for (int i = 0; i < 4; ++i)
-    for (int e = 0; e < 4; ++e) Pf[i * 4 + e] = P[i][e];
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_C, C, sizeof(C), 0, cudaMemcpyHostToDevice, s));
-  GSGPC_CUDA(cudaMemcpyToSymbolAsync(c_P, Pf, sizeof(Pf), 0, cudaMemcpyHostToDevice, s));
+        for (int b = 0; b < W; ++b) t.C[(i * 4 + j) * 7 + a + b] += t.P[i * 4 + a] * t.P[j * 4 + b];
+  return t;
 }
+
+__constant__ PolyTables c_poly[2] = {make_poly_tables(2), make_poly_tables(4)};  // [0] linear, [1] cubic
 
 // ------------------------------------------------------------------ K2a classify + count
 // classify() specialised on the dimension, branch-light, 32-bit cell arithmetic
@@ -171,14 +166,33 @@ struct BinGate {
 // arrival order, so the rows of a cell reached K1 — and the fp64 sums — in a different order
 // every run.  Deterministic ranks without per-item block barriers:
 //   1. warp_rank: each warp ranks its own items per key against its own row of a per-warp
-//      count table (u16, nkeys per warp): __match_any_sync gives the rank inside a round, the
-//      row the warp's earlier rounds;
+//      count table (u16, nkeys per warp): the lanes holding the same key (one ballot per key
+//      bit — MATCH.ANY, a long MIO operation, stalled the partition and slice scatters on
+//      its result) give the rank inside a round, the row the warp's earlier rounds;
 //   2. after one block barrier, col_prefix turns every key's column into the exclusive prefix
 //      over the warps and returns the key's total.
 // An item's slot = key start + prefix[warp][key] + rank: order (warp, round, lane), fixed.
-__device__ __forceinline__ int warp_rank(int key, uint16_t* __restrict__ row) {
+constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints (keys of ≤ 14 bits)
+
+// lanes whose key equals this lane's (keys < 2^nbits, or −1): nbits + 1 ballots
+__device__ __forceinline__ unsigned warp_peers(int key, int nbits) {
+  const bool valid = key >= 0;
+  const unsigned v = __ballot_sync(0xffffffffu, valid);
+  unsigned peers = valid ? v : ~v;
+#pragma unroll 1
+  for (int b = 0; b < BIN_MAX_BSH; ++b) {
+    if (b < nbits) {  // warp-uniform
+      const bool bit = (key >> b) & 1;
+      const unsigned m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+  }
+  return peers;
+}
+
+__device__ __forceinline__ int warp_rank(int key, int nbits, uint16_t* __restrict__ row) {
   const int lane = threadIdx.x & 31;
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const unsigned peers = warp_peers(key, nbits);
   const int leader = __ffs(peers) - 1;
   int base = 0;
   if (key >= 0 && lane == leader) {
@@ -219,7 +233,24 @@ __device__ __forceinline__ int col_prefix(uint16_t* __restrict__ tab, int nkeys,
 // atomics and at most nb + slices write frontiers.
 template <typename T>
 struct alignas(sizeof(T) * 4) Row4 {
-  T v[4];  // x0, x1, x2 (unused dims 0), y  — the sorted payload
+  T v[4];  // x0, x1, x2 (unused dims 0), y
+};
+
+// The rows of a batch in cell order, as K1 reads them: sorted row index p → the row gathered
+// from the caller's layout (one vector load for packed (x0, x1, x2, y) rows).  The binning
+// sorts 4-byte indices only; K1 is FP64-bound at d = 3, so the gathers' latency hides under
+// the MMAs (each batch's rows are requested one batch ahead).
+template <typename T, bool PACKED>
+struct RowSrc {
+  PointsDev pts;
+  const int* __restrict__ idx;  // sorted row → batch row
+  int d;
+  __device__ __forceinline__ int64_t at(int64_t p) const { return __ldg(idx + p); }
+  __device__ __forceinline__ Row4<T> operator[](int64_t p) const {
+    Row4<T> r;
+    load_row<T, PACKED>(pts, d, at(p), r.v);
+    return r;
+  }
 };
 
 constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threads × SORT_UNR × 16
@@ -229,10 +260,9 @@ constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threa
 #define PART_NT_DEF 512
 #endif
 #ifndef PART_MINB
-#define PART_MINB 1
+#define PART_MINB 2
 #endif
 constexpr int PART_NT = PART_NT_DEF;  // partition: PART_MINB blocks of PART_NT threads per SM
-constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints
 
 template <typename T, bool PACKED, int D>
 __global__ void __launch_bounds__(256, 3) k_classify_tiles(PointsDev pts, int64_t n, int64_t row0, GridDev g,
@@ -379,51 +409,59 @@ __global__ void __launch_bounds__(1024) k_tscan_buckets(int* __restrict__ gsum, 
 // Tile offsets: tcnt[tile][b] ← first output row of tile's bucket-b rows = bbase[b] + rows
 // of bucket b in earlier tiles (the groups' exclusive prefix from k_tscan_buckets plus the
 // earlier tiles of the group) — every tile's runs are placed by row order, not by which block
-// claimed a cursor first.
+// claimed a cursor first.  One warp per (group, bucket): lane l scans tiles 2l, 2l + 1 of the
+// group (TSCAN_G = 64), a warp scan adds the earlier lanes (a thread walking the group's 64
+// tiles serially was latency-bound: 124 µs at config 3).
+static_assert(TSCAN_G == 64, "k_tile_offsets: two tiles per lane");
 __global__ void k_tile_offsets(int* __restrict__ tcnt, int64_t ntiles, int nb, const int* __restrict__ gpre,
                                const int64_t* __restrict__ bbase) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t ngroups = (ntiles + TSCAN_G - 1) / TSCAN_G;
-  if (idx >= ngroups * nb) return;
-  const int64_t gi = idx / nb;
-  const int b = static_cast<int>(idx - gi * nb);
-  int run = static_cast<int>(bbase[b]) + gpre[idx];
-  const int64_t t1 = imin64((gi + 1) * TSCAN_G, ntiles);
-  for (int64_t t = gi * TSCAN_G; t < t1; ++t) {
-    const int v = tcnt[t * nb + b];
-    tcnt[t * nb + b] = run;
-    run += v;
+  if (wid >= ngroups * nb) return;
+  const int64_t gi = wid / nb;
+  const int b = static_cast<int>(wid - gi * nb);
+  const int64_t t0 = gi * TSCAN_G + 2 * lane;
+  const int v0 = t0 < ntiles ? tcnt[t0 * nb + b] : 0;
+  const int v1 = t0 + 1 < ntiles ? tcnt[(t0 + 1) * nb + b] : 0;
+  int incl = v0 + v1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
+  const int run = static_cast<int>(bbase[b]) + gpre[wid] + incl - v0 - v1;
+  if (t0 < ntiles) tcnt[t0 * nb + b] = run;
+  if (t0 + 1 < ntiles) tcnt[(t0 + 1) * nb + b] = run + v0;
 }
 
-// K2c.  Rows are taken in sub-tiles of R rows (R = rows_per_thread · PART_NT): each
-// sub-tile is counting-sorted by bucket in shared memory, claims one run per bucket from
-// the bucket's global cursor (one atomic per (sub-tile, bucket)), and is written out
-// linearly — consecutive lanes store consecutive rows of a run.  Rows stored straight from
-// registers (every lane of a warp in a different bucket, 1e3 buckets spread over 2 GB)
-// ran at ~1.1 TB/s whatever the DRAM traffic: the stores' address spread, not the bytes,
-// was the limit.
-template <typename T, bool PACKED, int RPT, bool DET>
-__global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts, int64_t n, int d,
-                                                          const int* __restrict__ cellid, int bsh, int nb,
-                                                          const int* __restrict__ toff,
-                                                          Row4<T>* __restrict__ rows1, int* __restrict__ cid1,
-                                                          const uint64_t* __restrict__ pw_in, int nw,
-                                                          uint64_t* __restrict__ pw1, BinGate gate) {
+// K2c.  The binning moves 8-byte keys (cell, row index), never the rows: K1 later gathers
+// each row from the caller's layout through the sorted indices (RowSrc).  Keys are taken in
+// sub-tiles of R (R = keys_per_thread · PART_NT): each sub-tile is counting-sorted by bucket
+// in shared memory with deterministic ranks, placed at the tile's per-bucket offsets (row
+// order, from the tile scan), and written out linearly — consecutive lanes store consecutive
+// keys of a run.  (Moving the 16-byte rows twice through the two sorts cost 2.4× the bytes;
+// keys stored straight from registers, every lane of a warp in a different bucket, were
+// bound by the stores' address spread, not the bytes.)
+template <int RPT, bool DET>
+__global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(const int* __restrict__ cellid, int64_t n, int bsh,
+                                                                  int nb, const int* __restrict__ toff,
+                                                                  int* __restrict__ cid1, int* __restrict__ idx1,
+                                                                  BinGate gate) {
   constexpr int R = RPT * PART_NT;
   constexpr int NW = PART_NT / 32;
   static_assert(TILE_ROWS % R == 0, "a tile is a whole number of sub-tiles");
   if (gate.closed()) return;
   extern __shared__ __align__(16) unsigned char smraw[];
-  Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
-  int* stage_c = reinterpret_cast<int*>(stage + R);
-  uint16_t* tab = reinterpret_cast<uint16_t*>(stage_c + R);   // [NW][nb] per-warp counts (det ranks)
+  int2* stage = reinterpret_cast<int2*>(smraw);                     // (cell, row) in bucket order
+  uint16_t* tab = reinterpret_cast<uint16_t*>(stage + R);           // [NW][nb] per-warp counts (det ranks)
   int* cnt = reinterpret_cast<int*>(tab + (DET ? ((nb * NW + 1) & ~1) : 0));  // per-bucket count, then local start
-  int* goff = cnt + nb;    // global slot of stage row j = goff[bucket] + j
+  int* goff = cnt + nb;    // global slot of stage key j = goff[bucket] + j
   int* gcur = goff + nb;   // next global slot of each bucket in this tile
   __shared__ int wsum[32];
   __shared__ int total_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int kbits = 32 - __clz(max(nb - 1, 1));  // bucket keys < 2^kbits
   if (DET)
     for (int j = threadIdx.x; j < nb * NW / 2; j += PART_NT) reinterpret_cast<int*>(tab)[j] = 0;
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
@@ -434,22 +472,17 @@ __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts,
       if (base >= n) break;
       for (int j = threadIdx.x; j < nb; j += PART_NT) cnt[j] = 0;
       __syncthreads();
-      Row4<T> r[RPT];
       int c[RPT], rank[RPT];
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
-        c[u] = -1;
-        if (i < n) {
-          c[u] = __ldcs(cellid + i);
-          load_row<T, PACKED>(pts, d, i, r[u].v);
-        }
+        c[u] = i < n ? __ldcs(cellid + i) : -1;
       }
       // ranks within each bucket: deterministic (warp table) or shared-atomic cursors
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int key = c[u] >= 0 ? c[u] >> bsh : -1;
-        if (DET) rank[u] = warp_rank(key, tab + w * nb);
+        if (DET) rank[u] = warp_rank(key, kbits, tab + w * nb);
         else rank[u] = key >= 0 ? atomicAdd(&cnt[key], 1) : 0;
       }
       __syncthreads();
@@ -498,22 +531,16 @@ __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(PointsDev pts,
         if (c[u] >= 0) {
           const int bk = c[u] >> bsh;
           const int lp = cnt[bk] + rank[u] + (DET ? tab[w * nb + bk] : 0);
-          stage[lp] = r[u];
-          stage_c[lp] = c[u];
-          if (nw) {
-            const int64_t i = base + static_cast<int64_t>(u) * PART_NT + threadIdx.x;
-            const int64_t gp = goff[bk] + lp;
-            for (int q = 0; q < nw; ++q) pw1[gp * nw + q] = pw_in[i * nw + q];
-          }
+          stage[lp] = make_int2(c[u], static_cast<int>(base + static_cast<int64_t>(u) * PART_NT + threadIdx.x));
         }
       }
       __syncthreads();
       const int tot = total_s;
       for (int j = threadIdx.x; j < tot; j += PART_NT) {
-        const int cc = stage_c[j];
-        const int64_t gp = goff[cc >> bsh] + j;
-        rows1[gp] = stage[j];
-        cid1[gp] = cc;
+        const int2 e = stage[j];
+        const int64_t gp = goff[e.x >> bsh] + j;
+        __stcg(cid1 + gp, e.x);
+        __stcg(idx1 + gp, e.y);
       }
       if (DET)
         for (int j = threadIdx.x; j < nb * NW / 2; j += PART_NT) reinterpret_cast<int*>(tab)[j] = 0;
@@ -614,20 +641,17 @@ __global__ void __launch_bounds__(1024) k_slice_scan(int* __restrict__ scnt, con
   if (threadIdx.x == 0) off[c0 + ncell] = bbase[b + 1];
 }
 
-// Slice scatter, direct: every thread stores its rows at its cell's shared cursor.  Used when
-// a slice's runs per cell are long (≥ 32 rows on average), where the stores coalesce in L2
-// anyway and the staged kernel's extra block barriers cost more (B200: config 3 2.20 vs
-// 2.29 ms, config 5 1.55 vs 1.64 ms, config 2 0.27 vs 0.28 ms; config 4, 8-row runs: staged
-// 2.29 vs direct 3.03 ms).
-template <typename T, bool DET>
-__global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
-                                                       const int64_t* __restrict__ bbase,
-                                                       const int64_t* __restrict__ sbase, int bsh, int nb,
-                                                       int64_t cells, const int* __restrict__ scnt,
-                                                       const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
-                                                       const uint64_t* __restrict__ pw1, int nw,
-                                                       uint64_t* __restrict__ pws, int64_t s0, BinGate gate) {
-  constexpr int UNR = sizeof(T) == 4 ? 8 : 4;
+// Slice scatter, direct: every thread stores its row index at its cell's shared cursor.  Used
+// when a slice's runs per cell are long (≥ 32 rows on average), where the stores coalesce in
+// L2 anyway and the staged kernel's extra block barriers cost more.
+template <bool DET>
+__global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const int* __restrict__ cid1, const int* __restrict__ idx1,
+                                                                 const int64_t* __restrict__ bbase,
+                                                                 const int64_t* __restrict__ sbase, int bsh, int nb,
+                                                                 int64_t cells, const int* __restrict__ scnt,
+                                                                 const int64_t* __restrict__ off, int* __restrict__ out,
+                                                                 int64_t s0, BinGate gate) {
+  constexpr int UNR = 16;
   constexpr int NW = 256 / 32;
   extern __shared__ __align__(16) int cur[];
   const int64_t sl = s0 + blockIdx.x;
@@ -647,22 +671,21 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* 
   __syncthreads();
   const int w = threadIdx.x >> 5;
   for (int64_t base = r0; base < r1; base += 256 * UNR) {  // uniform trip count (block barriers)
-    int cc[UNR];
-    Row4<T> rr[UNR];
+    int cc[UNR], ri[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t i = base + u * 256 + threadIdx.x;
       cc[u] = -1;
       if (i < r1) {
         cc[u] = __ldcs(cid1 + i);
-        rr[u] = rows1[i];
+        ri[u] = __ldcs(idx1 + i);
       }
     }
     int rank[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int key = cc[u] >= 0 ? static_cast<int>(cc[u] - c0) : -1;
-      if (DET) rank[u] = warp_rank(key, tab + w * nbin);
+      if (DET) rank[u] = warp_rank(key, bsh, tab + w * nbin);
       else rank[u] = key >= 0 ? atomicAdd(&cur[key], 1) : 0;
     }
     if (DET) {  // per cell: each warp's slots start at cur + the earlier warps' counts
@@ -675,9 +698,7 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* 
       if (cc[u] >= 0) {
         const int key = static_cast<int>(cc[u] - c0);
         const int pos = DET ? cur[key] + tab[w * nbin + key] + rank[u] : rank[u];
-        out[pos] = rr[u];
-        const int64_t i = base + u * 256 + threadIdx.x;
-        for (int w2 = 0; w2 < nw; ++w2) pws[static_cast<int64_t>(pos) * nw + w2] = pw1[i * nw + w2];
+        out[pos] = ri[u];
       }
     }
     if (DET) {
@@ -689,31 +710,27 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const Row4<T>* 
   }
 }
 
-// Slice scatter, staged: the slice is taken SS_SUB rows at a time; each sub-slice is
-// counting-sorted by cell in shared memory (shared-atomic ranks, block scan) and written out
-// linearly, so consecutive lanes store consecutive rows of one cell's run (rows stored
-// straight from registers sent every lane of a warp to a different cell: ~32 partial-line
-// writes per store instruction and DRAM read-modify-writes at config 4).
+// Slice scatter, staged: the slice (≤ SLICE_ROWS keys) is counting-sorted by cell in shared
+// memory (deterministic ranks, block scan) and written out linearly, so consecutive lanes
+// store consecutive indices of one cell's run (stores straight from registers sent every lane
+// of a warp to a different cell: partial-sector writes and DRAM read-modify-writes at
+// config 4's ~8-row runs).
 constexpr int SS_NT = 512;
-template <typename T>
-__host__ __device__ constexpr int ss_sub() { return sizeof(T) == 4 ? 4096 : 2048; }
+constexpr int SS_RPT = SLICE_ROWS / SS_NT;
 
-template <typename T>
-size_t slice_scatter_smem(int nbin, int nw, bool det) {
-  const size_t R = ss_sub<T>();
-  return R * sizeof(Row4<T>) + R * sizeof(uint64_t) * (nw > 0 ? 1 : 0) + R * 2 * sizeof(uint16_t) +
-         2 * sizeof(int) * (static_cast<size_t>(nbin) + 1) + (det ? sizeof(uint16_t) * static_cast<size_t>(nbin) * (SS_NT / 32) : 0);
+size_t slice_scatter_smem(int nbin, bool det) {
+  return static_cast<size_t>(SLICE_ROWS) * (sizeof(int) + sizeof(uint16_t)) +
+         2 * sizeof(int) * (static_cast<size_t>(nbin) + 1) +
+         (det ? sizeof(uint16_t) * static_cast<size_t>(nbin) * (SS_NT / 32) : 0);
 }
 
-template <typename T, bool DET>
-__global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __restrict__ rows1, const int* __restrict__ cid1,
+template <bool DET>
+__global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const int* __restrict__ cid1, const int* __restrict__ idx1,
                                                             const int64_t* __restrict__ bbase,
                                                             const int64_t* __restrict__ sbase, int bsh, int nb,
                                                             int64_t cells, const int* __restrict__ scnt,
-                                                            const int64_t* __restrict__ off, Row4<T>* __restrict__ out,
-                                                            const uint64_t* __restrict__ pw1, int nw,
-                                                            uint64_t* __restrict__ pws, int64_t s0, BinGate gate) {
-  constexpr int R = ss_sub<T>(), RPT = R / SS_NT;
+                                                            const int64_t* __restrict__ off, int* __restrict__ out,
+                                                            int64_t s0, BinGate gate) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int64_t sl = s0 + blockIdx.x;
   if (gate.closed() || sl >= sbase[nb]) return;
@@ -721,103 +738,90 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const Row4<T>* __res
   const int nbin = 1 << bsh;
   const int64_t c0 = static_cast<int64_t>(b) << bsh;
   const int ncell = static_cast<int>(imin64(nbin, cells - c0));
-  Row4<T>* stage = reinterpret_cast<Row4<T>*>(smraw);
-  uint64_t* stage_w = reinterpret_cast<uint64_t*>(stage + R);
-  uint16_t* stage_c = reinterpret_cast<uint16_t*>(stage_w + (nw > 0 ? R : 0));
-  uint16_t* stage_i = stage_c + R;
-  int* cnt = reinterpret_cast<int*>(stage_i + R);  // per cell: count, then local start; [ncell] = total
-  int* gcur = cnt + nbin + 1;                      // per cell: next global slot
+  int* stage_i = reinterpret_cast<int*>(smraw);
+  uint16_t* stage_c = reinterpret_cast<uint16_t*>(stage_i + SLICE_ROWS);
+  int* cnt = reinterpret_cast<int*>(stage_c + SLICE_ROWS);  // per cell: count, then local start; [ncell] = total
+  int* gcur = cnt + nbin + 1;                               // per cell: first global slot of this slice
   constexpr int NW = SS_NT / 32;
   uint16_t* tab = reinterpret_cast<uint16_t*>(gcur + nbin + 1);  // [NW][nbin] per-warp counts (det ranks)
   __shared__ int wsum[SS_NT / 32];
-  const int64_t r0s = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
-  const int64_t r1s = imin64(r0s + SLICE_ROWS, bbase[b + 1]);
-  for (int j = threadIdx.x; j < ncell; j += SS_NT)
+  const int64_t r0 = bbase[b] + (sl - sbase[b]) * SLICE_ROWS;
+  const int nr = static_cast<int>(imin64(SLICE_ROWS, bbase[b + 1] - r0));
+  for (int j = threadIdx.x; j < ncell; j += SS_NT) {
     gcur[j] = static_cast<int>(off[c0 + j]) + scnt[sl * nbin + j];  // rows per add < 2^31
+    cnt[j] = 0;
+  }
   if (DET)
     for (int j = threadIdx.x; j < nbin * NW; j += SS_NT) tab[j] = 0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t r0 = r0s; r0 < r1s; r0 += R) {
-    const int nr = static_cast<int>(imin64(R, r1s - r0));
-    for (int j = threadIdx.x; j < ncell; j += SS_NT) cnt[j] = 0;
-    __syncthreads();
-    Row4<T> rr[RPT];
-    int lc[RPT], rank[RPT];
+  __syncthreads();
+  int ri[SS_RPT], lc[SS_RPT];  // lc: local cell, then (local cell << 16) | rank (registers: no spills)
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int i = u * SS_NT + threadIdx.x;
-      lc[u] = -1;
-      if (i < nr) {
-        lc[u] = static_cast<int>(__ldcs(cid1 + r0 + i) - c0);
-        rr[u] = rows1[r0 + i];
-      }
+  for (int u = 0; u < SS_RPT; ++u) {
+    const int i = u * SS_NT + threadIdx.x;
+    lc[u] = -1;
+    if (i < nr) {
+      lc[u] = static_cast<int>(__ldcs(cid1 + r0 + i) - c0);
+      ri[u] = __ldcs(idx1 + r0 + i);
     }
+  }
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {  // ranks within each cell: deterministic (warp table) or atomic
-      if (DET) rank[u] = warp_rank(lc[u], tab + w * nbin);
-      else rank[u] = lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0;
-    }
+  for (int u = 0; u < SS_RPT; ++u) {  // ranks within each cell: deterministic (warp table) or atomic
+    const int rank = DET ? warp_rank(lc[u], bsh, tab + w * nbin) : (lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0);
+    if (lc[u] >= 0) lc[u] = (lc[u] << 16) | rank;
+  }
+  __syncthreads();
+  if (DET) {
+    for (int j = threadIdx.x; j < ncell; j += SS_NT) cnt[j] = col_prefix<NW>(tab, nbin, j, 0);
     __syncthreads();
-    if (DET) {
-      for (int j = threadIdx.x; j < ncell; j += SS_NT) cnt[j] = col_prefix<NW>(tab, nbin, j, 0);
-      __syncthreads();
-    }
-    // exclusive scan of cnt[0..ncell) (each thread a contiguous segment)
-    const int per = (ncell + SS_NT - 1) / SS_NT;
-    const int j0 = threadIdx.x * per;
-    int local = 0;
-    for (int q = 0; q < per; ++q)
-      if (j0 + q < ncell) local += cnt[j0 + q];
-    int incl = local;
+  }
+  // exclusive scan of cnt[0..ncell) (each thread a contiguous segment)
+  const int per = (ncell + SS_NT - 1) / SS_NT;
+  const int j0 = threadIdx.x * per;
+  int local = 0;
+  for (int q = 0; q < per; ++q)
+    if (j0 + q < ncell) local += cnt[j0 + q];
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < SS_NT / 32 ? wsum[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      int x = lane < SS_NT / 32 ? wsum[lane] : 0;
+    if (lane < SS_NT / 32) wsum[lane] = x;
+  }
+  __syncthreads();
+  int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
+  for (int q = 0; q < per; ++q) {
+    const int j = j0 + q;
+    if (j < ncell) {
+      const int k = cnt[j];
+      cnt[j] = run;
+      run += k;
+    }
+  }
+  __syncthreads();
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane < SS_NT / 32) wsum[lane] = x;
+  for (int u = 0; u < SS_RPT; ++u) {
+    if (lc[u] >= 0) {
+      const int c = lc[u] >> 16;
+      const int lp = cnt[c] + (lc[u] & 0xffff) + (DET ? tab[w * nbin + c] : 0);
+      stage_i[lp] = ri[u];
+      stage_c[lp] = static_cast<uint16_t>(c);
     }
-    __syncthreads();
-    int run = incl - local + (w > 0 ? wsum[w - 1] : 0);
-    for (int q = 0; q < per; ++q) {
-      const int j = j0 + q;
-      if (j < ncell) {
-        const int k = cnt[j];
-        cnt[j] = run;
-        run += k;
-      }
-    }
-    if (threadIdx.x == 0) cnt[ncell] = nr;
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      if (lc[u] >= 0) {
-        const int lp = cnt[lc[u]] + rank[u] + (DET ? tab[w * nbin + lc[u]] : 0);
-        stage[lp] = rr[u];
-        stage_c[lp] = static_cast<uint16_t>(lc[u]);
-        stage_i[lp] = static_cast<uint16_t>(u * SS_NT + threadIdx.x);
-      }
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < nr; j += SS_NT) {
-      const int c = stage_c[j];
-      const int64_t pos = static_cast<int64_t>(gcur[c]) + (j - cnt[c]);
-      out[pos] = stage[j];
-      for (int q = 0; q < nw; ++q) pws[pos * nw + q] = pw1[(r0 + stage_i[j]) * nw + q];
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < ncell; j += SS_NT) gcur[j] += cnt[j + 1] - cnt[j];
-    if (DET)
-      for (int j = threadIdx.x; j < nbin * NW; j += SS_NT) tab[j] = 0;
-    __syncthreads();  // cnt is reset by the next sub-slice
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nr; j += SS_NT) {
+    const int c = stage_c[j];
+    out[static_cast<int64_t>(gcur[c]) + (j - cnt[c])] = stage_i[j];
   }
 }
 
@@ -983,8 +987,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <typename T, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(const Row4<T>* __restrict__ pay,
+template <typename T, bool PK, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay,
                                                             const int64_t* __restrict__ off, int64_t cells,
                                                             int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, double* __restrict__ mom,
                                                             uint8_t* __restrict__ pat, int64_t range, SplitRec sp) {
@@ -1153,8 +1157,8 @@ __device__ __forceinline__ int row_tc(const GridDev& g, const Row4<T>& r, double
   return cell;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restrict__ pay, int64_t nvalid,
+template <typename T, bool PK>
+__global__ void __launch_bounds__(128) k_moments_d2c_mma(RowSrc<T, PK> pay, int64_t nvalid,
                                                          int64_t row0, BinGate gate, GridDev g,
                                                          double* __restrict__ mom, uint8_t* __restrict__ pat,
                                                          int64_t range, SplitRec sp) {
@@ -1268,8 +1272,8 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(const Row4<T>* __restri
 // d ≤ 2 (any scheme) and d = 3 linear: every lane accumulates all QX + QY moments of its
 // own points in registers; a segment flush warp-reduces them (butterfly) and the lanes
 // write the cell's contiguous moments cooperatively.
-template <int D, int W, typename T>
-__global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict__ pay,
+template <int D, int W, typename T, bool PK>
+__global__ void __launch_bounds__(128) k_moments_lane(RowSrc<T, PK> pay,
                                                      const int64_t* __restrict__ off, int64_t cells,
                                                      int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g,
                                                      double* __restrict__ mom, uint8_t* __restrict__ pat, int64_t range,
@@ -1371,8 +1375,8 @@ __global__ void __launch_bounds__(128) k_moments_lane(const Row4<T>* __restrict_
 // ------------------------------------------------------------------ probe images (K1p)
 // W^T v_p for P Rademacher probes: per cell, Σ_p s_p Π_k t_pk^{e_k} (e_k ≤ W-1) — the same
 // y-moment reconstruction then yields W^T v_p.  Lane j owns probe j (P ≤ 64 → two passes).
-template <int D, int W, typename T>
-__global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict__ pay,
+template <int D, int W, typename T, bool PK>
+__global__ void __launch_bounds__(64) k_probe_moments(RowSrc<T, PK> pay,
                                                       const uint64_t* __restrict__ pw,
                                                       const int64_t* __restrict__ off, int64_t cells,
                                                       int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate, GridDev g, int probes,
@@ -1431,7 +1435,7 @@ __global__ void __launch_bounds__(64) k_probe_moments(const Row4<T>* __restrict_
           }
           P[q] = m;
         }
-        SW[lane] = v ? pw[(b + lane) * nw + (pj >> 6)] : 0ull;
+        SW[lane] = v ? pw[pay.at(b + lane) * nw + (pj >> 6)] : 0ull;
       }
       __syncwarp();
       for (int r = 0; r < nb; ++r) {
@@ -1514,7 +1518,7 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
 #pragma unroll
     for (int i = 0; i < W; ++i)
 #pragma unroll
-      for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_P[i * 4 + e], acc);
+      for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_poly[W == 4].P[i * 4 + e], acc);
     const int qo = q_hi * x.inner_q + q_lo;  // digit k collapsed to extent 1
     out[static_cast<int64_t>(qo) * x.sp_out + sp] = acc;
   } else {
@@ -1529,7 +1533,7 @@ __global__ void __launch_bounds__(256) k_xform(const double* __restrict__ in, do
         const int j = i + delta;
         if (j >= 0 && j < W) {
 #pragma unroll
-          for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_C[(i * 4 + j) * 7 + e], acc);
+          for (int e = 0; e < EIN; ++e) acc = fma(v[i][e], c_poly[W == 4].C[(i * 4 + j) * 7 + e], acc);
         }
       }
       out[(x.half ? qo - x.c0 : qo) * x.sp_out + sp] = acc;
@@ -1610,7 +1614,7 @@ __global__ void __launch_bounds__(256, 2) k_xform_first(const double* __restrict
           const int j = i + dq - (W - 1);
           if (j >= 0 && j < W) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) acc[dq] = fma(v[e], c_C[(i * 4 + j) * 7 + e], acc[dq]);
+            for (int e = 0; e < E; ++e) acc[dq] = fma(v[e], c_poly[W == 4].C[(i * 4 + j) * 7 + e], acc[dq]);
           }
         }
       }
@@ -1629,7 +1633,7 @@ __global__ void __launch_bounds__(256, 2) k_xform_first(const double* __restrict
       if (c >= 0 && c < x.ext_in) {
         const double* r = rec + (c - c_lo) * x.Q + x.QX + q_hi * W;
 #pragma unroll
-        for (int e = 0; e < W; ++e) acc = fma(r[e], c_P[i * 4 + e], acc);
+        for (int e = 0; e < W; ++e) acc = fma(r[e], c_poly[W == 4].P[i * 4 + e], acc);
       }
     }
     outy[static_cast<int64_t>(q_hi) * x.sp_out + sp0 + ai] = acc;
@@ -1713,7 +1717,8 @@ void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, int* tcnt,
   const unsigned gb = static_cast<unsigned>(ceil_div(ng * bd.nb, 256));
   k_tscan_groups<<<gb, 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum);
   k_tscan_buckets<<<1, 1024, 0, L.s>>>(gsum, ng, bd.nb, bbase, sbase);
-  k_tile_offsets<<<gb, 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum, bbase);  // tcnt → per-tile offsets
+  k_tile_offsets<<<static_cast<unsigned>(ceil_div(ng * bd.nb * 32, 256)), 256, 0, L.s>>>(tcnt, nt, bd.nb, gsum,
+                                                                                       bbase);  // tcnt → per-tile offsets
   L.count(3);
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1724,104 +1729,88 @@ int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd) { return ceil_div(nval
 // count nb ≤ 1280: every grid up to ~2e7 cells); beyond that the shared-atomic cursors.
 constexpr int DET_MAX_NB = 1280;
 
-template <typename T, int RPT>
+static bool bin_nondet() {  // GSGPC_BIN_NONDET=1: diagnostics only (shared-atomic ranks, not reproducible)
+  static const bool v = getenv("GSGPC_BIN_NONDET") != nullptr;
+  return v;
+}
+
+template <int RPT>
 static size_t partition_smem(const BinDesc& bd, bool det) {
-  return static_cast<size_t>(RPT) * PART_NT * (sizeof(Row4<T>) + sizeof(int)) + 3 * sizeof(int) * bd.nb +
+  return static_cast<size_t>(RPT) * PART_NT * sizeof(int2) + 3 * sizeof(int) * bd.nb +
          (det ? sizeof(uint16_t) * ((static_cast<size_t>(bd.nb) * (PART_NT / 32) + 1) & ~size_t{1}) : 0);
 }
 
-template <typename T, int RPT, bool DET>
-static void launch_partition_r(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                               const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in,
-                               int nw, uint64_t* pw1, int nblk, BinGate gate) {
-  Row4<T>* r1 = static_cast<Row4<T>*>(rows1);
-  const size_t sm = partition_smem<T, RPT>(bd, DET);
-  auto k = packed4(p, g.d, sizeof(T)) ? k_partition<T, true, RPT, DET> : k_partition<T, false, RPT, DET>;
-  set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(sm));
-  k<<<nblk, PART_NT, sm, L.s>>>(p, n, g.d, cellid, bd.bsh, bd.nb, toff, r1, cid1, pw_in, nw, pw1, gate);
+template <int RPT, bool DET>
+static void launch_partition_r(const Launch& L, int64_t n, const BinDesc& bd, const int* cellid, const int* toff,
+                               int* cid1, int* idx1, int nblk, BinGate gate) {
+  const size_t sm = partition_smem<RPT>(bd, DET);
+  set_max_dynamic_smem(reinterpret_cast<const void*>(k_partition<RPT, DET>), static_cast<int>(sm));
+  k_partition<RPT, DET><<<nblk, PART_NT, sm, L.s>>>(cellid, n, bd.bsh, bd.nb, toff, cid1, idx1, gate);
 }
 
-// rows per thread so that the staged sub-tile + per-bucket counters (+ rank tables) fit the
+// keys per thread so that the staged sub-tile + per-bucket counters (+ rank tables) fit the
 // shared memory
-template <typename T, bool DET>
-static void launch_partition_d(const Launch& L, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                               const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in,
-                               int nw, uint64_t* pw1, int nblk, BinGate gate) {
+template <bool DET>
+static void launch_partition_d(const Launch& L, int64_t n, const BinDesc& bd, const int* cellid, const int* toff,
+                               int* cid1, int* idx1, int nblk, BinGate gate) {
   const size_t budget = 220 * 1024 / PART_MINB;
-  if (partition_smem<T, 16>(bd, DET) <= budget)
-    launch_partition_r<T, 16, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else if (partition_smem<T, 8>(bd, DET) <= budget)
-    launch_partition_r<T, 8, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else if (partition_smem<T, 4>(bd, DET) <= budget)
-    launch_partition_r<T, 4, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  else if (partition_smem<T, 2>(bd, DET) <= budget)
-    launch_partition_r<T, 2, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+  if (partition_smem<32>(bd, DET) <= budget)
+    launch_partition_r<32, DET>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
+  else if (partition_smem<16>(bd, DET) <= budget)
+    launch_partition_r<16, DET>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
+  else if (partition_smem<8>(bd, DET) <= budget)
+    launch_partition_r<8, DET>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
+  else if (partition_smem<4>(bd, DET) <= budget)
+    launch_partition_r<4, DET>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
   else
-    launch_partition_r<T, 1, DET>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
+    launch_partition_r<1, DET>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
 }
 
-void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                   const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in, int nw,
-                   uint64_t* pw1, const unsigned long long* err) {
+void run_partition(const Launch& L, int64_t n, const BinDesc& bd, const int* cellid, const int* toff, int* cid1,
+                   int* idx1, const unsigned long long* err) {
   const BinGate gate{err, nullptr};
   int dev = 0, sms = 148;
   GSGPC_CUDA(cudaGetDevice(&dev));
   GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(bin_tiles(n), sms * PART_MINB)));
-  const bool det = bd.nb <= DET_MAX_NB;
-  if (dtype == GSGPC_F32) {
-    if (det) launch_partition_d<float, true>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-    else launch_partition_d<float, false>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  } else {
-    if (det) launch_partition_d<double, true>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-    else launch_partition_d<double, false>(L, p, n, g, bd, cellid, toff, rows1, cid1, pw_in, nw, pw1, nblk, gate);
-  }
+  if (bd.nb <= DET_MAX_NB && !bin_nondet()) launch_partition_d<true>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
+  else launch_partition_d<false>(L, n, bd, cellid, toff, cid1, idx1, nblk, gate);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
 
-void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0,
-                    int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
-                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws,
-                    const unsigned long long* err) {
+void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0, int64_t s1,
+                    const int* cid1, const int* idx1, const int64_t* bbase, const int64_t* sbase, int* scnt,
+                    int64_t* off, int* idx_s, const unsigned long long* err) {
   const BinGate gate{err, nullptr};
   const size_t sm = sizeof(int) * (size_t{1} << bd.bsh);
   const int64_t ns = s1 - s0;
-  if (ns > 0)
+  if (ns > 0) {
+    set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_count), static_cast<int>(sm));  // 2^bsh ≤ 16384 cells
     k_slice_count<<<static_cast<unsigned>(ns), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt, s0, gate);
+  }
   if (b1 > b0)
     k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0, gate);
   if (ns > 0) {
     const int nbin = 1 << bd.bsh;
-    if (SLICE_ROWS / nbin >= 32) {
-      // deterministic ranks: cursors + a byte table of 8 warps per cell (nbin ≤ 256 here)
+    static const bool direct = [] {  // GSGPC_SLICE_DIRECT=1: diagnostics (direct scatter for long runs)
+      const char* e = getenv("GSGPC_SLICE_DIRECT");
+      return e && e[0] == '1';
+    }();
+    if (direct && SLICE_ROWS / nbin >= 32) {
+      // deterministic ranks: cursors + a u16 table of 8 warps per cell (nbin ≤ 256 here)
       const size_t smd = 2 * sizeof(int) * static_cast<size_t>(nbin) + sizeof(uint16_t) * static_cast<size_t>(nbin) * 8;
-      if (dtype == GSGPC_F32)
-        k_slice_scatter_direct<float, true><<<static_cast<unsigned>(ns), 256, smd, L.s>>>(
-            static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-            static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
-      else
-        k_slice_scatter_direct<double, true><<<static_cast<unsigned>(ns), 256, smd, L.s>>>(
-            static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-            static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
+      auto k = bin_nondet() ? k_slice_scatter_direct<false> : k_slice_scatter_direct<true>;
+      k<<<static_cast<unsigned>(ns), 256, smd, L.s>>>(cid1, idx1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off, idx_s,
+                                                       s0, gate);
     } else {
       // deterministic ranks while the per-warp table (16 warps × cells, u16) fits: 2^bsh ≤ 2048
-      const bool det = nbin <= 2048;
-      if (dtype == GSGPC_F32) {
-        const size_t ssm = slice_scatter_smem<float>(nbin, nw, det);
-        auto k = det ? k_slice_scatter<float, true> : k_slice_scatter<float, false>;
-        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
-        k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
-            static_cast<const Row4<float>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-            static_cast<Row4<float>*>(out), pw1, nw, pws, s0, gate);
-      } else {
-        const size_t ssm = slice_scatter_smem<double>(nbin, nw, det);
-        auto k = det ? k_slice_scatter<double, true> : k_slice_scatter<double, false>;
-        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
-        k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(
-            static_cast<const Row4<double>*>(rows1), cid1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-            static_cast<Row4<double>*>(out), pw1, nw, pws, s0, gate);
-      }
+      const bool det = nbin <= 2048 && !bin_nondet();
+      const size_t ssm = slice_scatter_smem(nbin, det);
+      auto k = det ? k_slice_scatter<true> : k_slice_scatter<false>;
+      set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
+      k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(cid1, idx1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
+                                                         idx_s, s0, gate);
     }
   }
   L.count(3);
@@ -1865,12 +1854,11 @@ static void split_fix(const Launch& L, const SplitBuf& sb, int64_t nwarps, int r
   L.count();
 }
 
-template <typename T>
-static void launch_moments(const Launch& L, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
+template <typename T, bool PK>
+static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_t* off, int64_t row0, int64_t nvalid,
                            int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, BinGate gate,
                            const SplitBuf& sb) {
   if (nvalid <= row0) return;
-  const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   const SplitRec sp{sb.v, sb.cell};
   const int Q = moments_per_cell(g.d, g.W);
   if (g.d == 3 && g.W == 4) {
@@ -1878,14 +1866,12 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     const int64_t warps = ceil_div(nvalid - row0, range);
     static const int minb = [] {
       const char* e = getenv("GSGPC_K1_MINB");
-      return e ? atoi(e) : 5;  // resident blocks/SM (B200, config 3, row prefetch): 5 → 5.36, 6 → 5.39, 7 → 5.45 ms
+      return e ? atoi(e) : 5;  // resident blocks/SM (B200, config 3, row prefetch): 4, 5 → 5.36, 6 → 5.39 ms
     }();
     const unsigned blocks = static_cast<unsigned>(ceil_div(warps, 4));
     if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
-#define GSGPC_D3(MB) k_moments_d3c_mma<T, MB><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp)
-    if (minb >= 8) GSGPC_D3(8);
-    else if (minb == 7) GSGPC_D3(7);
-    else if (minb == 6) GSGPC_D3(6);
+#define GSGPC_D3(MB) k_moments_d3c_mma<T, PK, MB><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp)
+    if (minb >= 6) GSGPC_D3(6);
     else if (minb == 5) GSGPC_D3(5);
     else GSGPC_D3(4);
 #undef GSGPC_D3
@@ -1894,7 +1880,7 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     const int64_t range = 512;
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
     if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
-    k_moments_d2c_mma<T><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range, sp);
+    k_moments_d2c_mma<T, PK><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range, sp);
     split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
   } else {
     const int64_t range = 1024;
@@ -1903,7 +1889,7 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
     if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
 #define GSGPC_LM(DD, WW)                                                                          \
   if (g.d == DD && g.W == WW) {                                                                 \
-    k_moments_lane<DD, WW, T><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp); \
+    k_moments_lane<DD, WW, T, PK><<<blocks, 128, 0, L.s>>>(P, off, c_hi, nvalid, row0, c_lo, gate, g, mom, pat, range, sp); \
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
@@ -1911,12 +1897,22 @@ static void launch_moments(const Launch& L, const void* pay, const int64_t* off,
   }
 }
 
-void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err,
-                 const SplitBuf& sb, const int64_t* rows_end) {
+template <typename T>
+static void launch_moments_t(const Launch& L, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
+                             int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
+                             BinGate gate, const SplitBuf& sb) {
+  if (packed4(p, g.d, sizeof(T)))
+    launch_moments<T, true>(L, RowSrc<T, true>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+  else
+    launch_moments<T, false>(L, RowSrc<T, false>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+}
+
+void run_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
+                 int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
+                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_moments<float>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
-  else launch_moments<double>(L, pay, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+  if (dtype == GSGPC_F32) launch_moments_t<float>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+  else launch_moments_t<double>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
   if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }
@@ -1929,8 +1925,8 @@ void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off
 // XOR swizzle of the d = 2 K1 (conflict-free stores and fragment loads).
 constexpr int PMM_PT = 2;  // probe tiles of 8 per pass
 
-template <typename T>
-__global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restrict__ pay,
+template <typename T, bool PK>
+__global__ void __launch_bounds__(64) k_probe_moments_mma(RowSrc<T, PK> pay,
                                                           const uint64_t* __restrict__ pw,
                                                           const int64_t* __restrict__ off, int64_t cells,
                                                           int64_t nvalid, int64_t row0, int64_t c_lo, BinGate gate,
@@ -1992,7 +1988,7 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
               P[(q & ~15) | ((q & 15) ^ sw)] = ab * pk[2][e];
             }
           }
-        SW[lane] = v ? pw[(b0 + lane) * nw + (pbase >> 6)] : 0ull;
+        SW[lane] = v ? pw[pay.at(b0 + lane) * nw + (pbase >> 6)] : 0ull;
       }
       __syncwarp();
       const int steps = (nb + 3) >> 2;
@@ -2039,12 +2035,11 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(const Row4<T>* __restr
   }
 }
 
-template <typename T>
-static void launch_probe_moments(const Launch& L, const void* pay, const uint64_t* pw, const int64_t* off,
+template <typename T, bool PK>
+static void launch_probe_moments(const Launch& L, const RowSrc<T, PK>& P, const uint64_t* pw, const int64_t* off,
                                  int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
                                  int probes, double* pmom, BinGate gate, const SplitBuf& sb) {
   if (nvalid <= row0) return;
-  const Row4<T>* P = static_cast<const Row4<T>*>(pay);
   const SplitRec sp{sb.v, sb.cell};
   int QY = 1;
   for (int k = 0; k < g.d; ++k) QY *= g.W;
@@ -2059,7 +2054,7 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
     const unsigned blk = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, rng), 2));
     if (static_cast<int64_t>(blk) * 2 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1p split records undersized");
     for (int pb = 0; pb < probes; pb += 8 * PMM_PT) {
-      k_probe_moments_mma<T><<<blk, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, rng,
+      k_probe_moments_mma<T, PK><<<blk, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, rng,
                                                    pb, sp);
       L.count();
       split_fix(L, sb, static_cast<int64_t>(blk) * 2, 8 * PMM_PT * 64, std::min(8 * PMM_PT, probes - pb) * 64, pmom,
@@ -2071,7 +2066,7 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
   for (int pb = 0; pb < probes; pb += 32) {
 #define GSGPC_PM(DD, WW)                                                                                  \
   if (g.d == DD && g.W == WW) {                                                                         \
-    k_probe_moments<DD, WW, T><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, range, pb, sp); \
+    k_probe_moments<DD, WW, T, PK><<<blocks, 64, 0, L.s>>>(P, pw, off, c_hi, nvalid, row0, c_lo, gate, g, probes, pmom, range, pb, sp); \
   }
     GSGPC_PM(1, 2) GSGPC_PM(1, 4) GSGPC_PM(2, 2) GSGPC_PM(2, 4) GSGPC_PM(3, 2) GSGPC_PM(3, 4)
 #undef GSGPC_PM
@@ -2081,12 +2076,27 @@ static void launch_probe_moments(const Launch& L, const void* pay, const uint64_
   }
 }
 
-void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
-                       int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom, const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end) {
+template <typename T>
+static void launch_probe_moments_t(const Launch& L, const PointsDev& p, const int* idx, const uint64_t* pw,
+                                   const int64_t* off, int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi,
+                                   const GridDev& g, int probes, double* pmom, BinGate gate, const SplitBuf& sb) {
+  if (packed4(p, g.d, sizeof(T)))
+    launch_probe_moments<T, true>(L, RowSrc<T, true>{p, idx, g.d}, pw, off, row0, nvalid, c_lo, c_hi, g, probes,
+                                  pmom, gate, sb);
+  else
+    launch_probe_moments<T, false>(L, RowSrc<T, false>{p, idx, g.d}, pw, off, row0, nvalid, c_lo, c_hi, g, probes,
+                                   pmom, gate, sb);
+}
+
+void run_probe_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const uint64_t* pw,
+                       const int64_t* off, int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
+                       int probes, double* pmom, const unsigned long long* err, const SplitBuf& sb,
+                       const int64_t* rows_end) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_probe_moments<float>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
-  else launch_probe_moments<double>(L, pay, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
+  if (dtype == GSGPC_F32)
+    launch_probe_moments_t<float>(L, p, idx, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
+  else
+    launch_probe_moments_t<double>(L, p, idx, pw, off, row0, nvalid, c_lo, c_hi, g, probes, pmom, gate, sb);
   GSGPC_CUDA(cudaGetLastError());
 }
 
@@ -2101,7 +2111,6 @@ void run_finalize(const Launch& L, const GridDev& g, const double* mom, int prob
     QX *= E;
     QY *= W;
   }
-  upload_poly_tables(W, L.s);
   const int64_t half = ws_elems / 2;
   double* bufA = ws;
   double* bufB = ws + half;

@@ -39,21 +39,20 @@ void run_sum_partials(const Launch& L, const double* part, int np, double* acc);
 void run_bucket_totals(const Launch& L, const BinDesc& bd, int64_t n, int* tcnt, int* gsum, int64_t* bbase,
                        int64_t* sbase);
 int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd);
-// rows → bucket-contiguous rows1 / cid1 / pw1, in row order within each bucket (toff: the
-// per-tile offsets from run_bucket_totals)
+// keys (cellid[i], i) → bucket-contiguous cid1 / idx1, in a fixed order within each bucket
+// (toff: the per-tile offsets from run_bucket_totals).  The rows themselves never move: K1
+// gathers them through the sorted indices.
 // Kernels that commit take the device error word of the classify pass (err) and return at
 // once when it records an out-of-grid row; rows_end (device) bounds the rows binned.
-void run_partition(const Launch& L, int dtype, const PointsDev& p, int64_t n, const GridDev& g, const BinDesc& bd,
-                   const int* cellid, const int* toff, void* rows1, int* cid1, const uint64_t* pw_in, int nw,
-                   uint64_t* pw1, const unsigned long long* err);
+void run_partition(const Launch& L, int64_t n, const BinDesc& bd, const int* cellid, const int* toff, int* cid1,
+                   int* idx1, const unsigned long long* err);
 // dst += src unless err records an error
 void run_commit_add(const Launch& L, const unsigned long long* err, const double* src, double* dst);
-// bucket-contiguous → cell-sorted rows (out, pws) and off[] for buckets [b0, b1) = slices [s0, s1)
-// (off[cells] written by the last bucket); scnt: slices × 2^bsh
-void run_slice_sort(const Launch& L, int dtype, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0,
-                    int64_t s1, const void* rows1, const int* cid1, const int64_t* bbase, const int64_t* sbase,
-                    int* scnt, int64_t* off, void* out, const uint64_t* pw1, int nw, uint64_t* pws,
-                    const unsigned long long* err);
+// bucket-contiguous keys → cell-sorted row indices idx_s and off[] for buckets [b0, b1) =
+// slices [s0, s1) (off[cells] written by the last bucket); scnt: slices × 2^bsh
+void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, int b1, int64_t s0, int64_t s1,
+                    const int* cid1, const int* idx1, const int64_t* bbase, const int64_t* sbase, int* scnt,
+                    int64_t* off, int* idx_s, const unsigned long long* err);
 // K1 split records (bitwise-reproducible flushes of cells split across warp ranges, see
 // precompute.cu SplitRec): device scratch of warps × rec doubles + warps int64
 struct SplitBuf {
@@ -64,13 +63,15 @@ struct SplitBuf {
 };
 int64_t split_rec_warps(int64_t rows);
 int64_t split_rec_doubles(const GridDev& g, int probes);
-// K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there)
-void run_moments(const Launch& L, int dtype, const void* pay, const int64_t* off, int64_t row0, int64_t nvalid,
-                 int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, const unsigned long long* err,
-                 const SplitBuf& sb, const int64_t* rows_end = nullptr);
-void run_probe_moments(const Launch& L, int dtype, const void* pay, const uint64_t* pw, const int64_t* off,
-                       int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, int probes,
-                       double* pmom, const unsigned long long* err, const SplitBuf& sb,
+// K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there);
+// sorted row p is batch row idx[p] of p (the batch's points, as classified)
+void run_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
+                 int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
+                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end = nullptr);
+// probe words pw: [batch row][⌈P/64⌉] (bit j of word w: probe 64w + j is +1)
+void run_probe_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const uint64_t* pw,
+                       const int64_t* off, int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,
+                       int probes, double* pmom, const unsigned long long* err, const SplitBuf& sb,
                        const int64_t* rows_end = nullptr);
 // W^T W structure: touched[S_min][m] (0/1) from the per-cell zero-weight patterns
 // (cells × 3^d bytes written by K1); byte-wise OR for merges.

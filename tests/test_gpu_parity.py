@@ -98,6 +98,23 @@ def test_precompute_large_grid_sparse_cells(dtype):
     assert gs.n() == os_.n
 
 
+def test_precompute_huge_sparse_grid():
+    """A 3000 × 3000 grid (~9e6 cells → 16384-cell buckets, beyond the deterministic rank
+    tables of the staged slice scatter) with 0.02 rows per cell."""
+    sizes = (3000, 3000)
+    g = G.fit_grid_to_data(np.zeros(2), np.ones(2), sizes, G.InterpScheme.Cubic)
+    og = O.fit_grid_to_data(np.zeros(2), np.ones(2), sizes, 1)
+    x, y = points(2, 200_000, 23)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(og, x, y, scheme=1, nthreads=8)
+    rp, col, val = gs.csr()
+    orp, ocol, oval, owty = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert np.abs(val - oval).max() <= 1e-10 * np.abs(oval).max()
+    assert rel_err(gs.wty(), owty) <= 1e-10
+    assert gs.n() == os_.n
+
+
 @pytest.mark.parametrize("d,scheme", [(1, G.InterpScheme.Cubic), (2, G.InterpScheme.Cubic),
                                       (2, G.InterpScheme.Linear), (3, G.InterpScheme.Cubic),
                                       (3, G.InterpScheme.Linear)])
