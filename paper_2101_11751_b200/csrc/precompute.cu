@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -190,9 +191,10 @@ __device__ __forceinline__ unsigned warp_peers(int key, int nbits) {
   return peers;
 }
 
+// nbits < 0: the peers from MATCH.ANY instead of ballots
 __device__ __forceinline__ int warp_rank(int key, int nbits, uint16_t* __restrict__ row) {
   const int lane = threadIdx.x & 31;
-  const unsigned peers = warp_peers(key, nbits);
+  const unsigned peers = nbits < 0 ? __match_any_sync(0xffffffffu, key) : warp_peers(key, nbits);
   const int leader = __ffs(peers) - 1;
   int base = 0;
   if (key >= 0 && lane == leader) {
@@ -447,7 +449,7 @@ template <int RPT, bool DET>
 __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(const int* __restrict__ cellid, int64_t n, int bsh,
                                                                   int nb, const int* __restrict__ toff,
                                                                   int* __restrict__ cid1, int* __restrict__ idx1,
-                                                                  BinGate gate) {
+                                                                  int kbits, BinGate gate) {
   constexpr int R = RPT * PART_NT;
   constexpr int NW = PART_NT / 32;
   static_assert(TILE_ROWS % R == 0, "a tile is a whole number of sub-tiles");
@@ -461,7 +463,6 @@ __global__ void __launch_bounds__(PART_NT, PART_MINB) k_partition(const int* __r
   __shared__ int wsum[32];
   __shared__ int total_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int kbits = 32 - __clz(max(nb - 1, 1));  // bucket keys < 2^kbits
   if (DET)
     for (int j = threadIdx.x; j < nb * NW / 2; j += PART_NT) reinterpret_cast<int*>(tab)[j] = 0;
   const int64_t ntiles = (n + TILE_ROWS - 1) / TILE_ROWS;
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const int* __re
                                                                  const int64_t* __restrict__ sbase, int bsh, int nb,
                                                                  int64_t cells, const int* __restrict__ scnt,
                                                                  const int64_t* __restrict__ off, int* __restrict__ out,
-                                                                 int64_t s0, BinGate gate) {
+                                                                 int64_t s0, int kbits, BinGate gate) {
   constexpr int UNR = 16;
   constexpr int NW = 256 / 32;
   extern __shared__ __align__(16) int cur[];
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(256, 3) k_slice_scatter_direct(const int* __re
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int key = cc[u] >= 0 ? static_cast<int>(cc[u] - c0) : -1;
-      if (DET) rank[u] = warp_rank(key, bsh, tab + w * nbin);
+      if (DET) rank[u] = warp_rank(key, kbits, tab + w * nbin);
       else rank[u] = key >= 0 ? atomicAdd(&cur[key], 1) : 0;
     }
     if (DET) {  // per cell: each warp's slots start at cur + the earlier warps' counts
@@ -730,7 +731,7 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const int* __restric
                                                             const int64_t* __restrict__ sbase, int bsh, int nb,
                                                             int64_t cells, const int* __restrict__ scnt,
                                                             const int64_t* __restrict__ off, int* __restrict__ out,
-                                                            int64_t s0, BinGate gate) {
+                                                            int64_t s0, int kbits, BinGate gate) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int64_t sl = s0 + blockIdx.x;
   if (gate.closed() || sl >= sbase[nb]) return;
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(SS_NT, 2) k_slice_scatter(const int* __restric
   }
 #pragma unroll
   for (int u = 0; u < SS_RPT; ++u) {  // ranks within each cell: deterministic (warp table) or atomic
-    const int rank = DET ? warp_rank(lc[u], bsh, tab + w * nbin) : (lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0);
+    const int rank = DET ? warp_rank(lc[u], kbits, tab + w * nbin) : (lc[u] >= 0 ? atomicAdd(&cnt[lc[u]], 1) : 0);
     if (lc[u] >= 0) lc[u] = (lc[u] << 16) | rank;
   }
   __syncthreads();
@@ -1655,7 +1656,7 @@ BinDesc bin_desc(int64_t cells) {
   BinDesc bd{};
   static const int64_t target = [] {  // GSGPC_BIN_BUCKETS: diagnostics override
     const char* e = getenv("GSGPC_BIN_BUCKETS");
-    return e ? std::max<int64_t>(1, atoll(e)) : int64_t{1024};
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t{512};  // B200, config 3 partition + slice sort: 1024 2.89, 512 2.57, 256 2.58, 128 2.66 ms
   }();
   bd.bsh = 0;
   while (((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh) > target && bd.bsh < BIN_MAX_BSH) ++bd.bsh;
@@ -1729,6 +1730,18 @@ int64_t bin_slices_max(int64_t nvalid, const BinDesc& bd) { return ceil_div(nval
 // count nb ≤ 1280: every grid up to ~2e7 cells); beyond that the shared-atomic cursors.
 constexpr int DET_MAX_NB = 1280;
 
+// Deterministic ranks: lanes sharing a key from ballots (one per key bit) or from MATCH.ANY
+// (GSGPC_RANK_MATCH = "part", "slice", "both" or "none" selects MATCH.ANY per pass).
+static int rank_bits(bool partition, int keybits) {
+  static const int mode = [] {
+    const char* e = getenv("GSGPC_RANK_MATCH");
+    if (!e) return 1;  // default: MATCH.ANY in the partition, ballots in the slice scatter
+    const std::string v(e);
+    return v == "part" ? 1 : v == "slice" ? 2 : v == "both" ? 3 : 0;
+  }();
+  return (mode & (partition ? 1 : 2)) ? -1 : keybits;
+}
+
 static bool bin_nondet() {  // GSGPC_BIN_NONDET=1: diagnostics only (shared-atomic ranks, not reproducible)
   static const bool v = getenv("GSGPC_BIN_NONDET") != nullptr;
   return v;
@@ -1745,7 +1758,8 @@ static void launch_partition_r(const Launch& L, int64_t n, const BinDesc& bd, co
                                int* cid1, int* idx1, int nblk, BinGate gate) {
   const size_t sm = partition_smem<RPT>(bd, DET);
   set_max_dynamic_smem(reinterpret_cast<const void*>(k_partition<RPT, DET>), static_cast<int>(sm));
-  k_partition<RPT, DET><<<nblk, PART_NT, sm, L.s>>>(cellid, n, bd.bsh, bd.nb, toff, cid1, idx1, gate);
+  const int kbits = rank_bits(true, 32 - __builtin_clz(static_cast<unsigned>(std::max(bd.nb - 1, 1))));
+  k_partition<RPT, DET><<<nblk, PART_NT, sm, L.s>>>(cellid, n, bd.bsh, bd.nb, toff, cid1, idx1, kbits, gate);
 }
 
 // keys per thread so that the staged sub-tile + per-bucket counters (+ rank tables) fit the
@@ -1802,7 +1816,7 @@ void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, i
       const size_t smd = 2 * sizeof(int) * static_cast<size_t>(nbin) + sizeof(uint16_t) * static_cast<size_t>(nbin) * 8;
       auto k = bin_nondet() ? k_slice_scatter_direct<false> : k_slice_scatter_direct<true>;
       k<<<static_cast<unsigned>(ns), 256, smd, L.s>>>(cid1, idx1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off, idx_s,
-                                                       s0, gate);
+                                                       s0, rank_bits(false, bd.bsh), gate);
     } else {
       // deterministic ranks while the per-warp table (16 warps × cells, u16) fits: 2^bsh ≤ 2048
       const bool det = nbin <= 2048 && !bin_nondet();
@@ -1810,7 +1824,7 @@ void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, i
       auto k = det ? k_slice_scatter<true> : k_slice_scatter<false>;
       set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(ssm));
       k<<<static_cast<unsigned>(ns), SS_NT, ssm, L.s>>>(cid1, idx1, bbase, sbase, bd.bsh, bd.nb, cells, scnt, off,
-                                                         idx_s, s0, gate);
+                                                         idx_s, s0, rank_bits(false, bd.bsh), gate);
     }
   }
   L.count(3);
