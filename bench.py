@@ -55,6 +55,10 @@ def parse():
     p.add_argument("--cpu-rows", type=int, default=200_000,
                    help="single-thread CPU baseline: prefix rows per trial (SURVEY §8(d): >= 2e5 at d = 3)")
     p.add_argument("--cpu-trials", type=int, default=3)
+    p.add_argument("--ref-rows", type=int, default=100_000,
+                   help="--impl reference: prefix rows per step (one pinned thread, ~17 s per step at d = 3)")
+    p.add_argument("--cpu-sharded", action="store_true",
+                   help="also time the oracle sharded over all host threads (merge(); labelled separately)")
     p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                    help="strong: the config's n rows split over the ranks (north star); weak: n rows per rank")
     p.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "traffic.json"))
@@ -208,6 +212,10 @@ def oracle_grid(grid):
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference's CPU path on this box: the oracle restatement of sufficient_stats (one
+    std::unordered_map accumulator in stream order, interp.cpp:179-221 — the reference's
+    precompute is single-threaded, so one thread pinned to one core is all the threads it can
+    use), each step a bounded prefix sample of the bench workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -216,36 +224,39 @@ def run_reference(args):
 
     O.build()
     cfg = S.CONFIGS[args.config]
-    n_sample_max = 4_000_000
-    x, y = S.generate(args.config, n=min(cfg.n, n_sample_max))
+    rows = min(cfg.n, args.ref_rows)
+    x, y = S.generate(args.config, n=rows)
     grid = S.grid_for(cfg)
     og = oracle_grid(grid)
-    threads = os.cpu_count() or 1
-    # size one step: ~target seconds of all-core work
-    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    rate, s, el = cpu_rate(x, y, og, 1, threads, per_step)
+    old = os.sched_getaffinity(0)
+    core = max(old)
+    os.sched_setaffinity(0, {core})
     times = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        st = O.sufficient_stats(og, x[:s], y[:s], scheme=1, nthreads=threads)
-        el = time.perf_counter() - t0
-        del st
-        if i >= args.warmup:
-            times.append(el)
+    try:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            st = O.sufficient_stats(og, x, y, scheme=1, nthreads=1)
+            el = time.perf_counter() - t0
+            del st
+            if i >= args.warmup:
+                times.append(el)
+    finally:
+        os.sched_setaffinity(0, old)
     ms = 1e3 * float(np.mean(times))
-    value = s / (ms / 1e3)
-    _, ci = mean_ci([s / t for t in times])
+    value = rows / (ms / 1e3)
+    _, ci = mean_ci([rows / t for t in times])
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": value / PUBLISHED_PTS_PER_S, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{args.config} ({cfg.name}) prefix sample", "sample_rows": s,
+        "config": {"workload": f"config{args.config} ({cfg.name}) prefix sample", "sample_rows": rows,
                    "grid": list(cfg.sizes), "scheme": "cubic"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "threads": threads, "kind": "port",
-                         "ci95": ci, "cpu": cpu_lscpu(),
-                         "sample": f"sharded, {threads} cores: first {s} rows of config {args.config} per step "
-                                   f"(oracle restatement: one std::unordered_map accumulator per thread, "
-                                   f"interp.cpp:179-221; threads shard rows and merge(), interp.cpp:202-210)"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "threads": 1, "kind": "port", "ci95": ci,
+                         "cpu": cpu_lscpu(), "trials": [round(t, 3) for t in times],
+                         "sample": f"first {rows} rows of config {args.config} per step, one thread pinned to core "
+                                   f"{core} (oracle restatement of sufficient_stats: one std::unordered_map "
+                                   f"accumulator in stream order, interp.cpp:179-221; the reference precompute is "
+                                   f"single-threaded)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -475,12 +486,13 @@ def run_ours(args):
         og = oracle_grid(grid)
         cpu = cpu_single_thread(samp[:, : cfg.d], samp[:, cfg.d], og, args.cpu_rows, args.cpu_trials)
         cpu["cpu"] = cpu_lscpu()
-        threads = os.cpu_count() or 1
-        rate, s_all, el_all = cpu_rate(samp[:, : cfg.d], samp[:, cfg.d], og, 1, threads, args.cpu_seconds)
-        cpu["sharded_all_cores"] = {
-            "value": rate, "unit": "points/s", "cores": threads,
-            "sample": f"sharded, {threads} cores: first {s_all} rows ({el_all:.1f} s; one accumulator per thread, "
-                      f"merge(), interp.cpp:202-210)"}
+        if args.cpu_sharded:
+            threads = os.cpu_count() or 1
+            rate, s_all, el_all = cpu_rate(samp[:, : cfg.d], samp[:, cfg.d], og, 1, threads, args.cpu_seconds)
+            cpu["sharded_all_cores"] = {
+                "value": rate, "unit": "points/s", "cores": threads,
+                "sample": f"sharded, {threads} cores: first {s_all} rows ({el_all:.1f} s; one accumulator per "
+                          f"thread, merge(), interp.cpp:202-210)"}
 
     if rank == 0:
         line = {

@@ -170,6 +170,36 @@ def test_interp_weights_bit_exact(d):
             assert np.array_equal(w[i, : nnz[i]], ow), (i, x[i])
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_classify_near_node_rows(dtype):
+    """Rows a few ulp .. 1e-4 of a spacing from a node and rows inside the 1e-9 snap band, on a
+    grid with u up to 1029: statistics equal the oracle's (structure, values ≤ 1e-10).  Offsets
+    t ∈ (1e-9, ~3e-8) are left out: there the reference's fp64 Keys weight c(2 − t) ≈ −t²/2
+    rounds to exactly 0 and drops node pairs the moment structure keeps."""
+    sizes = (40, 1030)
+    g = G.fit_grid_to_data(np.zeros(2), np.ones(2), sizes)
+    og = ogrid(g)
+    rng = np.random.default_rng(11)
+    n = 60_000
+    k = np.column_stack([rng.integers(10, sizes[0] - 3, n), rng.integers(250, sizes[1] - 3, n)])
+    base = np.array([g.min(0), g.min(1)]) + k * np.array([g.spacing(0), g.spacing(1)])
+    rel = rng.choice([0.0, 1e-12, -1e-12, 5e-10, -5e-10, 1e-6, -2e-6, 2e-5, -1e-4, 3e-4, 0.37], size=(n, 2))
+    x = (base + rel * np.array([g.spacing(0), g.spacing(1)])).astype(dtype)
+    xf = x.astype(np.float64)
+    for j in range(1, 6):  # neighbouring fp32/fp64 values of node coordinates
+        x[j::11, 0] = np.nextafter(x[j::11, 0], np.inf if j % 2 else -np.inf)
+        x[j::13, 1] = np.nextafter(x[j::13, 1], np.inf if j % 2 else -np.inf)
+    y = (np.cos(3 * xf).sum(axis=1)).astype(dtype)
+    gs = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
+    os_ = O.sufficient_stats(og, x, y, scheme=1, nthreads=8)
+    rp, col, val = gs.csr()
+    orp, ocol, oval, owty = os_.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert np.abs(val - oval).max() <= 1e-10 * np.abs(oval).max()
+    assert rel_err(gs.wty(), owty) <= 1e-10
+    assert gs.n() == os_.n
+
+
 def test_out_of_grid_errors_report_first_row():
     g = G.Grid([G.GridDim(0.0, 10.0, 11)])
     x = np.array([[2.0], [3.3], [0.5], [11.0], [-1.0]] + [[5.0]] * 10)
