@@ -81,6 +81,17 @@ typedef struct {
 
 /* ---------------------------------------------------------------- context */
 gsgpc_status gsgpc_ctx_create(int device, gsgpc_ctx** out);
+/* Several GPUs from one process (SURVEY §8(b) gsgpc_ctx_create(device_ids[], ngpu)): one
+ * context per listed device plus, for distinct devices, an NCCL communicator over them
+ * (libnccl resolved at run time; a group listing a device twice exchanges through peer
+ * copies).  gsgpc_group_ctx(g, r) is device r's context (owned by the group). */
+typedef struct gsgpc_group gsgpc_group;
+gsgpc_status gsgpc_group_create(const int* device_ids, int ngpu, gsgpc_group** out);
+gsgpc_status gsgpc_group_destroy(gsgpc_group* group);
+gsgpc_status gsgpc_group_info(const gsgpc_group* group, int* ngpu, int* uses_nccl);
+gsgpc_ctx* gsgpc_group_ctx(gsgpc_group* group, int rank);
+const char* gsgpc_group_last_error(const gsgpc_group* group);
+int64_t gsgpc_group_last_error_row(const gsgpc_group* group);
 void gsgpc_ctx_destroy(gsgpc_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own one. */
 gsgpc_status gsgpc_ctx_set_stream(gsgpc_ctx* ctx, void* cuda_stream);
@@ -200,6 +211,19 @@ gsgpc_status gsgpc_stats_reduce_buffer(gsgpc_ctx* ctx, gsgpc_stats* stats, doubl
 gsgpc_status gsgpc_stats_pattern_buffer(gsgpc_ctx* ctx, gsgpc_stats* stats, uint8_t** dev_ptr,
                                         int64_t* count);
 gsgpc_status gsgpc_stats_mark_reduced(gsgpc_ctx* ctx, gsgpc_stats* stats);
+/* sufficient_stats (interp.cpp:244-263) sharded over a group's devices: device r takes rows
+ * [r*n/G, (r+1)*n/G) of pts (host or device memory), the shards' statistics are finalized and
+ * combined with one all-reduce — merge() semantics (interp.cpp:202-210): W^T W, W^T y, yty, n
+ * summed, W^T W structure united — so out[r] (device r) each hold the full statistics.
+ * probes > 0: Rademacher probe images with the reference's streams (gp.cpp:16-25), each shard
+ * starting its streams at its first row.  OUT_OF_GRID reports the first bad row of the whole
+ * batch (gsgpc_group_last_error_row).  out: ngpu handles. */
+gsgpc_status gsgpc_group_sufficient_stats(gsgpc_group* group, const gsgpc_grid* grid, int scheme,
+                                          const gsgpc_points* pts, int64_t n, int probes, uint64_t seed,
+                                          gsgpc_stats** out);
+/* The exchange step alone: stats[r] (finalized, on device r, same grid and scheme) become their
+ * sum (merge(), interp.cpp:202-210) on every device. */
+gsgpc_status gsgpc_group_allreduce_stats(gsgpc_group* group, gsgpc_stats** stats);
 /* save_stats / load_stats (io.hpp:82-97, io.cpp:192-262), "GSGPSST1" layout. */
 gsgpc_status gsgpc_stats_save(gsgpc_ctx* ctx, gsgpc_stats* stats, const char* path);
 gsgpc_status gsgpc_stats_load(gsgpc_ctx* ctx, const char* path, gsgpc_stats** out);

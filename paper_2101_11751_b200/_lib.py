@@ -53,6 +53,14 @@ _P = C.POINTER
 SIGNATURES = {
     "gsgpc_version": (C.c_char_p, []),
     "gsgpc_ctx_create": (_i, [_i, _P(_vp)]),
+    "gsgpc_group_create": (_i, [_P(_i), _i, _P(_vp)]),
+    "gsgpc_group_destroy": (_i, [_vp]),
+    "gsgpc_group_info": (_i, [_vp, _P(_i), _P(_i)]),
+    "gsgpc_group_ctx": (_vp, [_vp, _i]),
+    "gsgpc_group_last_error": (C.c_char_p, [_vp]),
+    "gsgpc_group_last_error_row": (_i64, [_vp]),
+    "gsgpc_group_sufficient_stats": (_i, [_vp, _P(Grid_t), _i, _P(Points_t), _i64, _i, C.c_uint64, _P(_vp)]),
+    "gsgpc_group_allreduce_stats": (_i, [_vp, _P(_vp)]),
     "gsgpc_ctx_destroy": (None, [_vp]),
     "gsgpc_ctx_set_stream": (_i, [_vp, _vp]),
     "gsgpc_ctx_stream": (_vp, [_vp]),

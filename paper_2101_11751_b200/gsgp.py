@@ -136,7 +136,19 @@ class Context:
     def reset_phase_times(self):
         self.check(_L.load().gsgpc_ctx_reset_phase_times(self._h))
 
+    @classmethod
+    def _borrowed(cls, handle, device: int, owner):
+        """A context owned by someone else (a DeviceGroup): never destroyed here."""
+        c = cls.__new__(cls)
+        c._h = handle
+        c.device = int(device)
+        c._owner = owner
+        return c
+
     def close(self):
+        if getattr(self, "_owner", None) is not None:
+            self._h = None
+            return
         if getattr(self, "_h", None):
             _L.load().gsgpc_ctx_destroy(self._h)
             self._h = None
@@ -735,6 +747,84 @@ def sufficient_stats(grid: Grid, scheme, x, y=None, ctx: Optional[Context] = Non
     g = grid._c()
     ctx.check(_L.load().gsgpc_sufficient_stats(ctx.handle, C.byref(g), int(scheme), C.byref(p), n, C.byref(h)))
     return SufficientStats(h, grid, scheme, ctx)
+
+
+class DeviceGroup:
+    """Several GPUs driven from one process (gsgpc_group: SURVEY §8(b)'s
+    gsgpc_ctx_create(device_ids[], ngpu)).  One context per device; `sufficient_stats` shards
+    the rows over the devices and combines the per-device statistics with one all-reduce
+    (NCCL for distinct devices) — the reference's merge() (interp.cpp:202-210) — so every
+    device holds the full statistics for a replicated solve."""
+
+    def __init__(self, devices):
+        lib = _L.load()
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise InvalidArgument("DeviceGroup: need at least one device")
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        code = lib.gsgpc_group_create(arr, len(devs), C.byref(h))
+        if code != _L.OK:
+            raise GsgpcCudaError(f"gsgpc_group_create({devs}) failed with status {code}")
+        self._h = h
+        self.devices = devs
+        self._ctx = [Context._borrowed(lib.gsgpc_group_ctx(h, r), d, self) for r, d in enumerate(devs)]
+
+    def __len__(self):
+        return len(self.devices)
+
+    def context(self, rank: int) -> Context:
+        return self._ctx[rank]
+
+    @property
+    def uses_nccl(self) -> bool:
+        n, u = C.c_int(), C.c_int()
+        _L.load().gsgpc_group_info(self._h, C.byref(n), C.byref(u))
+        return bool(u.value)
+
+    def _check(self, code):
+        if code != _L.OK:
+            lib = _L.load()
+            msg = lib.gsgpc_group_last_error(self._h).decode()
+            row = int(lib.gsgpc_group_last_error_row(self._h))
+            if code in (_L.INVALID_ARGUMENT, _L.OUT_OF_GRID):
+                raise InvalidArgument(msg, row)
+            if code == _L.UNSUPPORTED:
+                raise NotImplementedError(msg)
+            if code == _L.CUDA_ERROR:
+                raise GsgpcCudaError(msg)
+            raise RuntimeError(msg)
+
+    def sufficient_stats(self, grid: Grid, scheme, x, y=None, probes: int = 0, seed: int = 0):
+        """interp.cpp:244-263 over the group: device r takes rows [r·n/G, (r+1)·n/G); returns one
+        SufficientStats per device, each the merged statistics of all rows."""
+        p, n, keep = _points(x, y, grid.dim())
+        g = grid._c()
+        out = (C.c_void_p * len(self.devices))()
+        self._check(_L.load().gsgpc_group_sufficient_stats(self._h, C.byref(g), int(scheme), C.byref(p), n,
+                                                           int(probes), int(seed), out))
+        del keep
+        return [SufficientStats(C.c_void_p(out[r]), grid, scheme, self._ctx[r]) for r in range(len(self.devices))]
+
+    def allreduce(self, stats):
+        """The exchange step alone: per-device finalized statistics become their sum."""
+        if len(stats) != len(self.devices):
+            raise InvalidArgument("DeviceGroup.allreduce: one stats object per device")
+        arr = (C.c_void_p * len(stats))(*[s.handle.value if hasattr(s.handle, "value") else s.handle for s in stats])
+        self._check(_L.load().gsgpc_group_allreduce_stats(self._h, arr))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            for c in self._ctx:
+                c._h = None
+            _L.load().gsgpc_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def save_stats(path: str, stats: SufficientStats, grid: Grid = None, scheme=None):
