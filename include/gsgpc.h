@@ -102,7 +102,8 @@ int64_t gsgpc_last_error_row(const gsgpc_ctx* ctx);
 /* Number of library kernels launched on this context so far (instrumentation). */
 uint64_t gsgpc_ctx_launch_count(const gsgpc_ctx* ctx);
 /* Per-phase device timing (CUDA events on the context stream), off by default.
- * Phases: 0 classify/count, 1 scan, 2 scatter, 3 moments (K1), 4 finalize, 5 H2D. */
+ * Phases: 0 classify/count, 1 scan, 2 scatter, 3 moments (K1), 4 finalize, 5 H2D, 6 K1 split
+ * fix-up, 7 probe moments. */
 gsgpc_status gsgpc_ctx_enable_phase_timing(gsgpc_ctx* ctx, int enable);
 gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out /*[8]*/, int64_t* calls_out /*[8]*/);
 gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx);

@@ -604,9 +604,15 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
       run_slice_sort(L, bd, g.cells, 0, bd.nb, 0, nslices, cid1.as<int>(), idx1.as<int>(), bbase.as<int64_t>(),
                      sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), idx_s.as<int>(), errp);
       pt.end(h);
-      const int hk = pt.begin(3);
+      int hk = pt.begin(3);
+      SplitFixJob fix{};
       run_moments(L, dtype, P, idx_s.as<int>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
-                  s->pat.as<uint8_t>(), errp, sb, rows_end);
+                  s->pat.as<uint8_t>(), errp, sb, rows_end, &fix);
+      pt.end(hk);
+      hk = pt.begin(6);
+      run_split_fix(L, sb, fix);
+      pt.end(hk);
+      hk = pt.begin(7);
       if (probes > 0) {
         run_probe_moments(L, dtype, P, idx_s.as<int>(), pw_dev, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
                           s->pmom.as<double>(), errp, sb, rows_end);

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -28,6 +29,22 @@
 #include "precompute.cuh"
 
 namespace gsgpc {
+
+bool debug_sync_enabled() {
+  static const bool on = getenv("GSGPC_DEBUG_SYNC") != nullptr;
+  return on;
+}
+
+void debug_sync_check(cudaStream_t s, uint64_t ordinal) {
+  const cudaError_t e = cudaStreamSynchronize(s);
+  const cudaError_t l = cudaGetLastError();
+  if (e != cudaSuccess || l != cudaSuccess) {
+    fprintf(stderr, "[gsgpc debug] launch #%llu failed: %s\n", static_cast<unsigned long long>(ordinal),
+            cudaGetErrorString(e != cudaSuccess ? e : l));
+    throw Error(GSGPC_CUDA_ERROR, std::string("launch #") + std::to_string(ordinal) + " failed: " +
+                                      cudaGetErrorString(e != cudaSuccess ? e : l));
+  }
+}
 
 // Polynomial form of the 1-D weights on t ∈ [0,1] (expanded from interp.cpp:27-37 on the
 // branch each stencil slot takes): cubic slots c(t+1), c(t), c(1-t), c(2-t); linear
@@ -174,6 +191,7 @@ struct BinGate {
 //      over the warps and returns the key's total.
 // An item's slot = key start + prefix[warp][key] + rank: order (warp, round, lane), fixed.
 constexpr int BIN_MAX_BSH = 14;  // bucket-sort shared counters: 2^14 ints (keys of ≤ 14 bits)
+constexpr int64_t BIN_MAX_NB = 8192;  // buckets: k_tscan_buckets handles 8 per thread
 
 // lanes whose key equals this lane's (keys < 2^nbits, or −1): nbits + 1 ballots
 __device__ __forceinline__ unsigned warp_peers(int key, int nbits) {
@@ -248,11 +266,12 @@ struct RowSrc {
   const int* __restrict__ idx;  // sorted row → batch row
   int d;
   __device__ __forceinline__ int64_t at(int64_t p) const { return __ldg(idx + p); }
-  __device__ __forceinline__ Row4<T> operator[](int64_t p) const {
+  __device__ __forceinline__ Row4<T> row(int64_t i) const {  // by batch row index
     Row4<T> r;
-    load_row<T, PACKED>(pts, d, at(p), r.v);
+    load_row<T, PACKED>(pts, d, i, r.v);
     return r;
   }
+  __device__ __forceinline__ Row4<T> operator[](int64_t p) const { return row(at(p)); }
 };
 
 constexpr int TILE_ROWS = 32768;  // classify tile (bucket histogram): 256 threads × SORT_UNR × 16
@@ -1022,6 +1041,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay
   // rows are consumed in order; the next batch's row is loaded one batch ahead so its DRAM
   // latency hides under the current batch's MMAs (the batch after [b, b+nb) starts at b+nb)
   Row4<T> cur_row = pay[imin64(r0 + lane, rend - 1)];
+  int64_t inx = pay.at(imin64(r0 + 32 + lane, rend - 1));  // the next batch's row index
   bool first = true;
   while (p < rend) {
     c = next_cell(off, c, p, cells, lane);
@@ -1029,7 +1049,10 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay
     const int64_t seg_end = min(ce, rend);
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
-      const Row4<T> next_row = pay[imin64(b + nb + lane, rend - 1)];
+      // the batch after [b, b + nb) starts at b + nb: its index was loaded ahead when that is
+      // b + 32 (full batch); a short batch (cell end) re-reads it
+      const Row4<T> next_row = nb == 32 ? pay.row(inx) : pay[imin64(b + nb + lane, rend - 1)];
+      inx = pay.at(imin64(b + nb + 32 + lane, rend - 1));
       {
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
@@ -1206,11 +1229,17 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(RowSrc<T, PK> pay, int6
     if (split && lane == 0) sp.cell[warp] = open;
     dx0 = dx1 = dy0 = dy1 = 0.0;
   };
-  // the next batch's row is loaded one batch ahead (its latency hides under this batch)
+  // rows are gathered two batches ahead and their indices three batches ahead: each batch
+  // waits on no load issued in it, and every lane keeps two row gathers in flight (the
+  // memory-bound d = 2 K1 was latency-bound on one gather per lane: config 4 2.98 ms per
+  // 1.25e8 rows with one batch of look-ahead)
   Row4<T> cur = pay[imin64(r0 + lane, rend - 1)];
+  Row4<T> nxt = pay[imin64(r0 + 32 + lane, rend - 1)];
+  int64_t inx = pay.at(imin64(r0 + 64 + lane, rend - 1));
   for (int64_t b = r0; b < rend; b += 32) {
     const int nb = static_cast<int>(imin64(32, rend - b));
-    const Row4<T> nxt = pay[imin64(b + 32 + lane, rend - 1)];
+    const Row4<T> nxt2 = pay.row(inx);
+    inx = pay.at(imin64(b + 96 + lane, rend - 1));
     const bool v = lane < nb;
     int cell = 0x7fffffff;
     unsigned bit = 0;
@@ -1264,6 +1293,7 @@ __global__ void __launch_bounds__(128) k_moments_d2c_mma(RowSrc<T, PK> pay, int6
     }
     __syncwarp();
     cur = nxt;
+    nxt = nxt2;
   }
   // the open cell may continue in the next warp's range: that warp records its own part
   if (open >= 0) flush();
@@ -1658,9 +1688,14 @@ BinDesc bin_desc(int64_t cells) {
     const char* e = getenv("GSGPC_BIN_BUCKETS");
     return e ? std::max<int64_t>(1, atoll(e)) : int64_t{512};  // B200, config 3 partition + slice sort: 1024 2.89, 512 2.57, 256 2.58, 128 2.66 ms
   }();
+  // ≥ cells / 1024 buckets: the staged slice scatter's per-warp rank tables stay ≤ 32 KB
+  // (config 4, 1024² nodes: 2048-cell buckets cost 3.6 vs 1024-cell ~2.7 ms per 1.25e8 rows)
+  const int64_t tgt = std::min<int64_t>(BIN_MAX_NB, std::max<int64_t>(target, (cells + 1023) / 1024));
   bd.bsh = 0;
-  while (((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh) > target && bd.bsh < BIN_MAX_BSH) ++bd.bsh;
+  while (((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh) > tgt && bd.bsh < BIN_MAX_BSH) ++bd.bsh;
   bd.nb = static_cast<int>((cells + (int64_t{1} << bd.bsh) - 1) >> bd.bsh);
+  if (bd.nb > BIN_MAX_NB)  // k_tscan_buckets: ≤ 8 buckets per thread of one 1024-thread block
+    throw Error(GSGPC_UNSUPPORTED, "sufficient_stats: grids above 2^14 · 8192 cells are not supported by this build");
   return bd;
 }
 
@@ -1802,9 +1837,13 @@ void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, i
   if (ns > 0) {
     set_max_dynamic_smem(reinterpret_cast<const void*>(k_slice_count), static_cast<int>(sm));  // 2^bsh ≤ 16384 cells
     k_slice_count<<<static_cast<unsigned>(ns), 256, sm, L.s>>>(cid1, bbase, sbase, bd.bsh, bd.nb, scnt, s0, gate);
+    L.count();
   }
   if (b1 > b0)
+  {
     k_slice_scan<<<static_cast<unsigned>(b1 - b0), 1024, 0, L.s>>>(scnt, bbase, sbase, bd.bsh, bd.nb, cells, off, b0, gate);
+    L.count();
+  }
   if (ns > 0) {
     const int nbin = 1 << bd.bsh;
     static const bool direct = [] {  // GSGPC_SLICE_DIRECT=1: diagnostics (direct scatter for long runs)
@@ -1827,7 +1866,7 @@ void run_slice_sort(const Launch& L, const BinDesc& bd, int64_t cells, int b0, i
                                                          idx_s, s0, rank_bits(false, bd.bsh), gate);
     }
   }
-  L.count(3);
+  L.count(ns > 0 ? 1 : 0);
   GSGPC_CUDA(cudaGetLastError());
 }
 
@@ -1860,7 +1899,11 @@ int64_t split_rec_doubles(const GridDev& g, int probes) {
 }
 
 static void split_fix(const Launch& L, const SplitBuf& sb, int64_t nwarps, int rec, int qv, double* M,
-                      int64_t mstride, int64_t mbase, BinGate gate) {
+                      int64_t mstride, int64_t mbase, BinGate gate, SplitFixJob* defer = nullptr) {
+  if (defer) {  // the caller runs it (run_split_fix), e.g. to time it apart from K1
+    *defer = SplitFixJob{nwarps, rec, qv, M, mstride, mbase, gate.err, gate.rows_end, true};
+    return;
+  }
   if (nwarps <= 0) return;
   if (nwarps > sb.warps || rec > sb.rec) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
   k_split_fix<<<static_cast<unsigned>(ceil_div(nwarps, 4)), 128, 0, L.s>>>(sb.v, sb.cell, nwarps, rec, qv, M, mstride,
@@ -1871,7 +1914,7 @@ static void split_fix(const Launch& L, const SplitBuf& sb, int64_t nwarps, int r
 template <typename T, bool PK>
 static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_t* off, int64_t row0, int64_t nvalid,
                            int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat, BinGate gate,
-                           const SplitBuf& sb) {
+                           const SplitBuf& sb, SplitFixJob* defer) {
   if (nvalid <= row0) return;
   const SplitRec sp{sb.v, sb.cell};
   const int Q = moments_per_cell(g.d, g.W);
@@ -1889,13 +1932,13 @@ static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_
     else if (minb == 5) GSGPC_D3(5);
     else GSGPC_D3(4);
 #undef GSGPC_D3
-    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate, defer);
   } else if (g.d == 2 && g.W == 4) {
     const int64_t range = 512;
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
     if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
     k_moments_d2c_mma<T, PK><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range, sp);
-    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate, defer);
   } else {
     const int64_t range = 1024;
     const int64_t warps = ceil_div(nvalid - row0, range);
@@ -1907,26 +1950,34 @@ static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_
   }
     GSGPC_LM(1, 2) GSGPC_LM(1, 4) GSGPC_LM(2, 2) GSGPC_LM(2, 4) GSGPC_LM(3, 2)
 #undef GSGPC_LM
-    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate);
+    split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate, defer);
   }
 }
 
 template <typename T>
 static void launch_moments_t(const Launch& L, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
                              int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
-                             BinGate gate, const SplitBuf& sb) {
+                             BinGate gate, const SplitBuf& sb, SplitFixJob* defer) {
   if (packed4(p, g.d, sizeof(T)))
-    launch_moments<T, true>(L, RowSrc<T, true>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+    launch_moments<T, true>(L, RowSrc<T, true>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb,
+                            defer);
   else
-    launch_moments<T, false>(L, RowSrc<T, false>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+    launch_moments<T, false>(L, RowSrc<T, false>{p, idx, g.d}, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb,
+                             defer);
+}
+
+void run_split_fix(const Launch& L, const SplitBuf& sb, const SplitFixJob& j) {
+  if (!j.pending) return;
+  split_fix(L, sb, j.nwarps, j.rec, j.qv, j.M, j.mstride, j.mbase, BinGate{j.err, j.rows_end});
+  GSGPC_CUDA(cudaGetLastError());
 }
 
 void run_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
                  int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
-                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end) {
+                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end, SplitFixJob* defer) {
   const BinGate gate{err, rows_end};
-  if (dtype == GSGPC_F32) launch_moments_t<float>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
-  else launch_moments_t<double>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb);
+  if (dtype == GSGPC_F32) launch_moments_t<float>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb, defer);
+  else launch_moments_t<double>(L, p, idx, off, row0, nvalid, c_lo, c_hi, g, mom, pat, gate, sb, defer);
   if (nvalid > row0) L.count();
   GSGPC_CUDA(cudaGetLastError());
 }

@@ -14,10 +14,17 @@
 namespace gsgpc {
 
 // Stream + launch counter (every library kernel launch is counted: gsgpc_ctx_launch_count).
+// GSGPC_DEBUG_SYNC=1 (diagnostics): synchronize after every counted launch and report the
+// first failing one by its ordinal.
+bool debug_sync_enabled();
+void debug_sync_check(cudaStream_t s, uint64_t ordinal);
 struct Launch {
   cudaStream_t s;
   uint64_t* counter;
-  void count(int k = 1) const { *counter += static_cast<uint64_t>(k); }
+  void count(int k = 1) const {
+    *counter += static_cast<uint64_t>(k);
+    if (debug_sync_enabled()) debug_sync_check(s, *counter);
+  }
 };
 
 // ---- precompute.cu
@@ -63,11 +70,26 @@ struct SplitBuf {
 };
 int64_t split_rec_warps(int64_t rows);
 int64_t split_rec_doubles(const GridDev& g, int probes);
+// The split-record fix-up of a K1 launch (adds the partials of cells continued across warp
+// ranges, in warp order).  run_moments runs it itself unless asked to hand it back.
+struct SplitFixJob {
+  int64_t nwarps;
+  int rec, qv;
+  double* M;
+  int64_t mstride, mbase;
+  const unsigned long long* err;
+  const int64_t* rows_end;
+  bool pending;
+};
+void run_split_fix(const Launch& L, const SplitBuf& sb, const SplitFixJob& job);
 // K1 over sorted rows [row0, nvalid) whose cells lie in [c_lo, c_hi) (off[] read only there);
-// sorted row p is batch row idx[p] of p (the batch's points, as classified)
+// sorted row p is batch row idx[p] of p (the batch's points, as classified).  defer: the split
+// fix-up is returned there instead of launched (the caller runs run_split_fix before the next
+// K1 launch that uses the same split records).
 void run_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const int64_t* off, int64_t row0,
                  int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g, double* mom, uint8_t* pat,
-                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end = nullptr);
+                 const unsigned long long* err, const SplitBuf& sb, const int64_t* rows_end = nullptr,
+                 SplitFixJob* defer = nullptr);
 // probe words pw: [batch row][⌈P/64⌉] (bit j of word w: probe 64w + j is +1)
 void run_probe_moments(const Launch& L, int dtype, const PointsDev& p, const int* idx, const uint64_t* pw,
                        const int64_t* off, int64_t row0, int64_t nvalid, int64_t c_lo, int64_t c_hi, const GridDev& g,

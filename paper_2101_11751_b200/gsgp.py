@@ -119,7 +119,7 @@ class Context:
         ms = (C.c_double * 8)()
         calls = (C.c_int64 * 8)()
         self.check(_L.load().gsgpc_ctx_phase_times(self._h, ms, calls))
-        names = ["classify", "scan", "scatter", "moments", "finalize", "h2d", "p6", "p7"]
+        names = ["classify", "scan", "scatter", "moments", "finalize", "h2d", "split_fix", "probe_moments"]
         return {names[i]: (ms[i], calls[i]) for i in range(8) if calls[i]}
 
     def fp64_peak_tflops(self) -> float:
