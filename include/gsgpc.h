@@ -103,9 +103,9 @@ int64_t gsgpc_last_error_row(const gsgpc_ctx* ctx);
 uint64_t gsgpc_ctx_launch_count(const gsgpc_ctx* ctx);
 /* Per-phase device timing (CUDA events on the context stream), off by default.
  * Phases: 0 classify/count, 1 scan, 2 scatter, 3 moments (K1), 4 finalize, 5 H2D, 6 K1 split
- * fix-up, 7 probe moments. */
+ * fix-up, 7 probe moments, 8 probe streams (device MT19937-64), 9 reserved. */
 gsgpc_status gsgpc_ctx_enable_phase_timing(gsgpc_ctx* ctx, int enable);
-gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out /*[8]*/, int64_t* calls_out /*[8]*/);
+gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out /*[10]*/, int64_t* calls_out /*[10]*/);
 gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx);
 /* Diagnostics: measured FP64 FMA throughput of this GPU (TFLOP/s, 2 flops per DFMA) from a
  * register-resident DFMA loop over all SMs — the denominator of the precompute's FP64 roofline. */

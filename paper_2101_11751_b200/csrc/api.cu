@@ -104,6 +104,7 @@ bool is_device_ptr(const void* p) {
 
 // ------------------------------------------------------------------ handles
 struct CgCache;
+constexpr int kPhases = 10;  // gsgpc_ctx_phase_times
 
 struct gsgpc_ctx {
   int device = 0;
@@ -113,8 +114,8 @@ struct gsgpc_ctx {
   int64_t err_row = 0;
   uint64_t launches = 0;
   bool timing = false;
-  double phase_ms[8] = {0};
-  int64_t phase_calls[8] = {0};
+  double phase_ms[kPhases] = {0};
+  int64_t phase_calls[kPhases] = {0};
   std::map<std::string, std::unique_ptr<DBuf>> bufs;
   PinnedBuf pin;
   std::unique_ptr<CgCache> cg;
@@ -834,7 +835,7 @@ gsgpc_status gsgpc_ctx_enable_phase_timing(gsgpc_ctx* ctx, int enable) {
 
 gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out, int64_t* calls_out) {
   if (!ctx) return GSGPC_INVALID_ARGUMENT;
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kPhases; ++i) {
     if (ms_out) ms_out[i] = ctx->phase_ms[i];
     if (calls_out) calls_out[i] = ctx->phase_calls[i];
   }
@@ -843,7 +844,7 @@ gsgpc_status gsgpc_ctx_phase_times(gsgpc_ctx* ctx, double* ms_out, int64_t* call
 
 gsgpc_status gsgpc_ctx_reset_phase_times(gsgpc_ctx* ctx) {
   if (!ctx) return GSGPC_INVALID_ARGUMENT;
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kPhases; ++i) {
     ctx->phase_ms[i] = 0;
     ctx->phase_calls[i] = 0;
   }
@@ -1067,7 +1068,10 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
         }
         const uint64_t* pw = nullptr;
         if (s->probe_seeded && !probe_words) {
+          PhaseTimer ptr(ctx);
+          const int hr = ptr.begin(8);
           gen_probe_words(ctx, s, r1 - r0);
+          ptr.end(hr);
           pw = ctx->buf("probe_stage").as<uint64_t>();
         } else if (nw) {
           if (pw_dev) {

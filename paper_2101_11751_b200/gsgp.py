@@ -116,11 +116,12 @@ class Context:
         self.check(_L.load().gsgpc_ctx_enable_phase_timing(self._h, 1 if on else 0))
 
     def phase_times(self):
-        ms = (C.c_double * 8)()
-        calls = (C.c_int64 * 8)()
+        ms = (C.c_double * 10)()
+        calls = (C.c_int64 * 10)()
         self.check(_L.load().gsgpc_ctx_phase_times(self._h, ms, calls))
-        names = ["classify", "scan", "scatter", "moments", "finalize", "h2d", "split_fix", "probe_moments"]
-        return {names[i]: (ms[i], calls[i]) for i in range(8) if calls[i]}
+        names = ["classify", "scan", "scatter", "moments", "finalize", "h2d", "split_fix", "probe_moments",
+                 "probe_rng", "p9"]
+        return {names[i]: (ms[i], calls[i]) for i in range(10) if calls[i]}
 
     def fp64_peak_tflops(self) -> float:
         v = C.c_double()
