@@ -549,7 +549,7 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   cellid.ensure(sizeof(int) * n);
   DBuf& err = ctx->buf("err");
   err.ensure(sizeof(unsigned long long) * 2);
-  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, 148 * 6)));
+  const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count() * 6)));
   DBuf& part = ctx->buf("yty_part");
   part.ensure(sizeof(double) * nblk);
   DBuf& ychunk = ctx->buf("yty_chunk");

@@ -721,7 +721,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
       mma = false;
       break;
     }
-    const int64_t target = 296;  // one block task per resident block (2 per SM), one wave
+    const int64_t target = 2 * sm_count();  // one block task per resident block (2 per SM), one wave
     const int64_t nlt = ceil_div(c.L, 8);
     const int64_t cw = std::max<int64_t>(1, std::min<int64_t>(cwmax, ceil_div(nlt, target)));
     const int64_t nlb = ceil_div(nlt, cw);
@@ -752,7 +752,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     if (need * 8 <= plane_kb * 1024) {
       a.mm_plane = 1;
       a.mp_ys = static_cast<int>(ys);
-      a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 296 / n0)));
+      a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 2 * sm_count() / n0)));
       if (const char* e = getenv("GSGPC_CG_PLANE_PARTS")) a.mp_parts = std::max(1, atoi(e));  // diagnostics
       mp_smem = static_cast<size_t>(need * 8);
     }

@@ -40,6 +40,21 @@ inline void invalid(const std::string& m) { throw Error(GSGPC_INVALID_ARGUMENT, 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device property of a kernel: keep
 // what was set per (device, kernel), under a lock, so every device (and every thread) sees
 // the attribute before its first launch needing it.
+// Streaming multiprocessors of the current device (148 on B200), cached per device.
+inline int sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  cache[dev] = n;
+  return n;
+}
+
 inline void set_max_dynamic_smem(const void* func, int bytes) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, int> done;

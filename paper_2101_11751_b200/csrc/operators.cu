@@ -285,7 +285,7 @@ static void toep_config(int64_t n, int64_t inner, int64_t outer, ToepArgs& t, di
   TL = std::max<int64_t>(1, std::min<int64_t>(TL, t.L));
   t.TL = static_cast<int>(TL);
   const int64_t tiles = ceil_div(t.L, TL);
-  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(296, tiles), ceil_div(n, 32)));
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * sm_count(), tiles), ceil_div(n, 32)));
   t.TA = static_cast<int>(ceil_div(n, chunks));
   chunks = ceil_div(n, t.TA);
   grid = dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));

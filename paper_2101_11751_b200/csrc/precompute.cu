@@ -2368,7 +2368,7 @@ __global__ void k_touched(GridDev g, int64_t total, const uint8_t* __restrict__ 
 
 void run_touched(const Launch& L, const GridDev& g, int S_min, const uint8_t* pat, uint8_t* out) {
   const int64_t total = static_cast<int64_t>(S_min) * g.m;
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 16)));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), sm_count() * 16)));
   k_touched<<<blocks, 256, 0, L.s>>>(g, total, pat, out);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
@@ -2382,7 +2382,7 @@ __global__ void k_or_bytes(int64_t n, uint8_t* __restrict__ dst, const uint8_t* 
 
 void run_or_bytes(const Launch& L, int64_t n, uint8_t* dst, const uint8_t* src) {
   if (n <= 0) return;
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), sm_count() * 8)));
   k_or_bytes<<<blocks, 256, 0, L.s>>>(n, dst, src);
   L.count();
   GSGPC_CUDA(cudaGetLastError());
