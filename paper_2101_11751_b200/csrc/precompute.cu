@@ -985,7 +985,8 @@ __device__ __forceinline__ void flush_pat(uint8_t* __restrict__ pat, int64_t c, 
 
 // ------------------------------------------------------------------ K1, d = 3 cubic
 // Moment record per cell: 343 x-moments + 64 y-moments; the row's powers t^0..t^6 per
-// dimension are staged in shared memory (stride 26 doubles).
+// dimension are staged in shared memory (stride 26 doubles).  (Staging the y-tile operand
+// products as well — stride 28 — measured slower: 5.43 vs 5.19 ms at config 3.)
 constexpr int D3C_QX = 343, D3C_QY = 64, D3C_Q = 407;
 static_assert(D3C_Q == D3C_QX + D3C_QY, "moment record = x-moments + y-moments");
 constexpr int D3C_STRIDE = 26;
@@ -1005,6 +1006,32 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// The in-cell offsets of a row whose cell (digits i0[k], as doubles) is known — every row K1
+// reads: t_k = (x_k − min_k)·(1/h_k) − i0_k with one rounding after the product (an FMA), to
+// within 2^-52·size of the reference's (x − min)/h − i0.  Rows within 4e-9 of a cell face,
+// where the reference's 1e-9 snap (interp.cpp:48-50) decides t ∈ {0, 1}, take the exact
+// division.  (Re-classifying every row from scratch — rint, band test, floor, clamp — was
+// ~36 FP64 instructions per row competing with the DMMAs for the FP64 pipe.)
+__device__ __forceinline__ double t_exact(const GridDev& g, int k, double x) {
+  int64_t i0 = 0;
+  double t = 0.0;
+  stencil_dim(x, g.mn[k], g.sp[k], g.sz[k], i0, t);
+  return t;
+}
+
+template <typename T>
+__device__ __forceinline__ void row_t_cell(const GridDev& g, const double* i0d, const Row4<T>& r, double* t,
+                                           double& y) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x = static_cast<double>(r.v[k]);
+    double tk = fma(__dsub_rn(x, g.mn[k]), g.isp[k], -i0d[k]);
+    if (fabs(tk - 0.5) > 0.5 - 4e-9) tk = t_exact(g, k, x);
+    t[k] = tk;
+  }
+  y = static_cast<double>(r.v[3]);
 }
 
 template <typename T, bool PK, int MINB>
@@ -1047,6 +1074,14 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
+    double i0d[3];  // the segment's cell digits (row-major over nc[k])
+    {
+      const int64_t c12 = c / g.nc[2];
+      i0d[2] = static_cast<double>(c - c12 * g.nc[2]);
+      const int64_t c0 = c12 / g.nc[1];
+      i0d[1] = static_cast<double>(c12 - c0 * g.nc[1]);
+      i0d[0] = static_cast<double>(c0);
+    }
     for (int64_t b = p; b < seg_end; b += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b));
       // the batch after [b, b + nb) starts at b + nb: its index was loaded ahead when that is
@@ -1056,7 +1091,7 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay
       {
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
-        if (v) row_t<T>(g, cur_row, t, y);
+        if (v) row_t_cell<T>(g, i0d, cur_row, t, y);
         pm |= __reduce_or_sync(0xffffffffu, v ? pat_bit<3>(t) : 0u);
         double* P = S + lane * D3C_STRIDE;
         double q0 = v ? 1.0 : 0.0, q1 = q0, q2 = q0;
