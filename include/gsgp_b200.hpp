@@ -75,6 +75,8 @@ class Context {
     static Context ctx(0);
     return ctx;
   }
+  // A context owned by someone else (a DeviceGroup), kept alive through `owner`.
+  Context(std::shared_ptr<void> owner, gsgpc_ctx* borrowed) : h_(std::move(owner), borrowed) {}
 
  private:
   std::shared_ptr<gsgpc_ctx> h_;
@@ -290,6 +292,61 @@ class SufficientStats {
   InterpScheme scheme_ = InterpScheme::Cubic;
   Context ctx_{Context::default_context()};
   mutable int64_t wtw_count_ = 0;
+};
+
+// ---------------------------------------------------------------- several GPUs, one process
+// gsgpc_group_* (SURVEY §8(b) gsgpc_ctx_create(device_ids[], ngpu)): sufficient_stats sharded
+// by rows over the devices and combined with one all-reduce — merge() semantics
+// (interp.cpp:202-210) — so every device holds the full statistics.
+class DeviceGroup {
+ public:
+  explicit DeviceGroup(const std::vector<int>& devices) {
+    gsgpc_group* g = nullptr;
+    if (devices.empty() || gsgpc_group_create(devices.data(), static_cast<int>(devices.size()), &g) != GSGPC_OK)
+      throw std::runtime_error("gsgpc: cannot create a device group");
+    h_.reset(g, gsgpc_group_destroy);
+  }
+  int size() const {
+    int n = 0;
+    gsgpc_group_info(h_.get(), &n, nullptr);
+    return n;
+  }
+  bool uses_nccl() const {
+    int u = 0;
+    gsgpc_group_info(h_.get(), nullptr, &u);
+    return u != 0;
+  }
+  Context context(int rank) const { return Context(h_, gsgpc_group_ctx(h_.get(), rank)); }
+  // x: n × d row-major coordinates, y: n responses.
+  std::vector<SufficientStats> sufficient_stats(const Grid& grid, InterpScheme scheme, const std::vector<double>& x,
+                                                const std::vector<double>& y, int probes = 0,
+                                                uint64_t seed = 0) const {
+    const int d = grid.dim();
+    if (static_cast<int64_t>(x.size()) != static_cast<int64_t>(y.size()) * d)
+      throw std::invalid_argument("sufficient_stats: stream/grid dimension mismatch");
+    gsgpc_points p{};
+    p.dtype = GSGPC_F64;
+    p.x = x.data();
+    p.x_row_stride = d;
+    for (int k = 0; k < d; ++k) p.x_col_offset[k] = k;
+    p.y = y.data();
+    p.y_stride = 1;
+    const gsgpc_grid g = grid.c();
+    std::vector<gsgpc_stats*> out(size(), nullptr);
+    const gsgpc_status st =
+        gsgpc_group_sufficient_stats(h_.get(), &g, scheme == InterpScheme::Linear ? GSGPC_LINEAR : GSGPC_CUBIC, &p,
+                                     static_cast<int64_t>(y.size()), probes, seed, out.data());
+    if (st == GSGPC_INVALID_ARGUMENT || st == GSGPC_OUT_OF_GRID)
+      throw std::invalid_argument(gsgpc_group_last_error(h_.get()));
+    if (st != GSGPC_OK) throw std::runtime_error(gsgpc_group_last_error(h_.get()));
+    std::vector<SufficientStats> res;
+    for (int r = 0; r < static_cast<int>(out.size()); ++r)
+      res.emplace_back(std::shared_ptr<gsgpc_stats>(out[r], gsgpc_stats_destroy), grid, scheme, context(r));
+    return res;
+  }
+
+ private:
+  std::shared_ptr<gsgpc_group> h_;
 };
 
 // Row-at-a-time data source (interp.hpp:150-155).  sufficient_stats() drains it in

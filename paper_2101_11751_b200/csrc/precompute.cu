@@ -2059,12 +2059,20 @@ __global__ void __launch_bounds__(64) k_probe_moments_mma(RowSrc<T, PK> pay,
     c = next_cell(off, c, p, cells, lane);
     const int64_t ce = off[c + 1];
     const int64_t seg_end = min(ce, rend);
+    double i0d[3];  // the segment's cell digits
+    {
+      const int64_t c12 = c / g.nc[2];
+      i0d[2] = static_cast<double>(c - c12 * g.nc[2]);
+      const int64_t c0 = c12 / g.nc[1];
+      i0d[1] = static_cast<double>(c12 - c0 * g.nc[1]);
+      i0d[0] = static_cast<double>(c0);
+    }
     for (int64_t b0 = p; b0 < seg_end; b0 += 32) {
       const int nb = static_cast<int>(imin64(32, seg_end - b0));
       {
         double t[3] = {0.0, 0.0, 0.0}, y = 0.0;
         const bool v = lane < nb;
-        if (v) row_t<T>(g, pay[b0 + lane], t, y);
+        if (v) row_t_cell<T>(g, i0d, pay[b0 + lane], t, y);
         double pk[3][4];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {

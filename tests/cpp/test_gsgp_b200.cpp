@@ -132,6 +132,21 @@ int main() {
   const StatsFile sf = load_stats("/tmp/gsgp_b200_test.gsgpsst");
   CHECK(sf.stats.n() == n && sf.stats.wtw().val == csr.val, "stats round trip");
 
+  // several GPUs from one process: a group listing device 0 twice (one GPU per test box) —
+  // the merged statistics equal the oracle's on all rows, on every device
+  {
+    const DeviceGroup group({0, 0});
+    CHECK(group.size() == 2, "group size");
+    const std::vector<SufficientStats> gs = group.sufficient_stats(grid, InterpScheme::Cubic, x, y);
+    for (const SufficientStats& st : gs) {
+      CHECK(st.n() == n, "group n");
+      CHECK(max_rel(st.wty(), owty) <= 1e-10, "group wty");
+      const auto gc = st.wtw();
+      CHECK(gc.row_ptr == rp && gc.col == col, "group wtw structure");
+      CHECK(max_rel(gc.val, val) <= 1e-10, "group wtw values");
+    }
+  }
+
   orc_stats_destroy(os);
   orc_kg_destroy(okg);
   if (failures == 0) std::printf("cpp api OK: iters=%d (oracle %d)\n", model.solve_iterations, oit);
