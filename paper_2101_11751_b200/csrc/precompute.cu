@@ -1950,16 +1950,25 @@ int moments_per_cell(int d, int W) {
   return qx + qy;
 }
 
-static int64_t k1_range_d3() {  // rows per warp of the d = 3 cubic K1 (GSGPC_K1_RANGE: diagnostics)
-  static const int64_t range = [] {
+// Rows per warp of the d = 3 cubic K1: large ranges mean fewer split records (one per range
+// that starts inside a cell) and fewer flushes, small ones a shorter tail.  Ranges double from
+// 512 up to 2048 while a launch still has ≥ 8 waves of 20 warps per SM (B200, config 3, K1 +
+// split fix-up: 512 → 5.52, 1024 → 5.35, 1536 → 5.29, 2048 → 5.28, 3072 → 5.27 ms; with rows
+// moved by the binning, round 1: 512 5.40, 1024 5.51 ms).  GSGPC_K1_RANGE: diagnostics.
+static int64_t k1_range_d3(int64_t rows) {
+  static const int64_t forced = [] {
     const char* e = getenv("GSGPC_K1_RANGE");
-    return e ? std::max<int64_t>(32, atoll(e)) : int64_t{512};  // B200 sweep: 128 5.84, 256 5.49, 512 5.40, 1024 5.51, 4096 6.02 ms
+    return e ? std::max<int64_t>(32, atoll(e)) : int64_t{0};
   }();
+  if (forced) return forced;
+  const int64_t target = rows / (static_cast<int64_t>(sm_count()) * 20 * 8);
+  int64_t range = 512;
+  while (range * 2 <= std::min<int64_t>(2048, target)) range *= 2;
   return range;
 }
 
 // Split records (SplitRec) of one K1 / K1p launch: warps ≤ rows / min range + a block's slack.
-int64_t split_rec_warps(int64_t rows) { return ceil_div(rows, std::min<int64_t>(512, k1_range_d3())) + 8; }
+int64_t split_rec_warps(int64_t rows) { return ceil_div(rows, std::min<int64_t>(512, k1_range_d3(rows))) + 8; }
 int64_t split_rec_doubles(const GridDev& g, int probes) {
   int64_t q = moments_per_cell(g.d, g.W);
   int QY = 1;
@@ -1989,7 +1998,7 @@ static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_
   const SplitRec sp{sb.v, sb.cell};
   const int Q = moments_per_cell(g.d, g.W);
   if (g.d == 3 && g.W == 4) {
-    const int64_t range = k1_range_d3();
+    const int64_t range = k1_range_d3(nvalid - row0);
     const int64_t warps = ceil_div(nvalid - row0, range);
     static const int minb = [] {
       const char* e = getenv("GSGPC_K1_MINB");
@@ -2004,7 +2013,7 @@ static void launch_moments(const Launch& L, const RowSrc<T, PK>& P, const int64_
 #undef GSGPC_D3
     split_fix(L, sb, static_cast<int64_t>(blocks) * 4, Q, Q, mom, Q, 0, gate, defer);
   } else if (g.d == 2 && g.W == 4) {
-    const int64_t range = 512;
+    const int64_t range = k1_range_d3(nvalid - row0);  // same trade-off as d = 3
     const unsigned blocks = static_cast<unsigned>(ceil_div(ceil_div(nvalid - row0, range), 4));
     if (static_cast<int64_t>(blocks) * 4 > sb.warps) throw Error(GSGPC_RUNTIME_ERROR, "K1 split records undersized");
     k_moments_d2c_mma<T, PK><<<blocks, 128, 0, L.s>>>(P, nvalid, row0, gate, g, mom, pat, range, sp);
