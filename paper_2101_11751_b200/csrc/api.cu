@@ -700,7 +700,7 @@ void gen_probe_words(gsgpc_ctx* ctx, gsgpc_stats* s, int64_t rows) {
   DBuf& st = ctx->buf("probe_stage");
   st.ensure(sizeof(uint64_t) * rows);
   DBuf& planes = ctx->buf("probe_planes");
-  planes.ensure(static_cast<size_t>(s->probes) * std::min(rows, probe_rng_slab()));
+  planes.ensure(static_cast<size_t>(s->probes) * std::min(rows, probe_rng_slab(s->probes)));
   DBuf& scr = ctx->buf("probe_rng_scratch");
   scr.ensure(sizeof(uint64_t) * probe_rng_scratch_words(s->probes));
   run_probe_rng(ctx->L(), s->rng.as<uint64_t>(), s->probes, rows, planes.as<uint8_t>(), st.as<uint64_t>(),
@@ -1017,8 +1017,12 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
       const char* e = getenv("GSGPC_HOST_CHUNK_LOG2");  // diagnostics: host staging chunk (rows)
       return e ? std::max(16, std::min(28, atoi(e))) : 23;  // B200 config 3 e2e: 2^22 37.5, 2^23 36.9, 2^24 37.3 ms
     }();
+    static const int dev_chunk_log2 = [] {
+      const char* e = getenv("GSGPC_DEV_CHUNK_LOG2");  // diagnostics: device-resident chunk (rows)
+      return e ? std::max(16, std::min(30, atoi(e))) : 27;
+    }();
     // host rows: equal chunks of at most 2^host_chunk_log2 rows (no short last chunk)
-    const int64_t CH0 = dev ? (int64_t{1} << 27) : (int64_t{1} << host_chunk_log2);
+    const int64_t CH0 = dev ? (int64_t{1} << dev_chunk_log2) : (int64_t{1} << host_chunk_log2);
     const int64_t CH = ceil_div(n, ceil_div(n, CH0));
     const int64_t nchunks = ceil_div(n, CH);
     StatsSnapshot snap(ctx, s, nchunks > 1);

@@ -198,59 +198,104 @@ constexpr int kJT = 320;  // threads per jump block (312 window words)
 
 // Block b = (stream s = b / K, jump k = b % K): out[s·K + k] = F^{312 q_k} in[s] (window
 // mt[0..311]; the index word is copied).  polys[k] = x^{312 q_k} mod φ (kPW words); a
-// polynomial equal to 1 copies the window.
+// polynomial equal to 1 copies the window.  The set coefficients of g are first compacted
+// into a list of positions (~10^4 for a random jump), so the correlation runs 8 independent
+// shared loads per step instead of a bit scan with one dependent load per set bit (the jump
+// kernel was the largest part of config 5's probe generation).
 __global__ void __launch_bounds__(kJT) k_mt_jump(const uint64_t* __restrict__ in, int K,
                                                  const uint64_t* __restrict__ polys, uint64_t* __restrict__ out) {
   extern __shared__ uint64_t smem[];
-  uint64_t* y = smem;           // kSeq words
-  uint64_t* g = smem + kSeq;    // kPW words
+  uint64_t* y = smem;                                        // kSeq words
+  uint64_t* g = smem + kSeq;                                 // kPW words
+  uint16_t* pos = reinterpret_cast<uint16_t*>(g + kPW);      // ≤ kDeg positions
+  __shared__ int wtot[kJT / 32 + 1];
   const int s = blockIdx.x / K, k = blockIdx.x % K, t = threadIdx.x;
+  const int lane = t & 31, wid = t >> 5;
   const uint64_t* st = in + static_cast<int64_t>(s) * (kN + 1);
   for (int i = t; i < kN; i += kJT) y[i] = st[i];
   for (int i = t; i < kPW; i += kJT) g[i] = polys[static_cast<int64_t>(k) * kPW + i];
   __syncthreads();
+  // positions of the set bits, in increasing order (thread t < kPW owns word t)
+  const uint64_t gw = t < kPW ? g[t] : 0ull;
+  const int c = __popcll(gw);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wtot[wid] = incl;
   // the sequence: words [base + 312, base + 468) depend only on words below base + 312
   for (int base = 0; base + kN < kSeq; base += kM) {
     const int i = base + t;
     if (t < kM && i + kN < kSeq) y[i + kN] = jmix(y[i], y[i + 1], y[i + kM]);
     __syncthreads();
   }
-  uint64_t acc = 0;
-  const int j = t < kN ? t : 0;
-  for (int w = 0; w < kPW; ++w) {
-    uint64_t bits = g[w];
+  if (t == 0) {
+    int run = 0;
+    for (int w = 0; w < kJT / 32; ++w) {
+      const int v = wtot[w];
+      wtot[w] = run;
+      run += v;
+    }
+    wtot[kJT / 32] = run;
+  }
+  __syncthreads();
+  {
+    int o = wtot[wid] + incl - c;
+    uint64_t bits = gw;
     while (bits) {
       const int b = __ffsll(static_cast<long long>(bits)) - 1;
       bits &= bits - 1;
-      acc ^= y[64 * w + b + j];
+      pos[o++] = static_cast<uint16_t>(64 * t + b);
     }
   }
+  __syncthreads();
+  const int np = wtot[kJT / 32];
+  const int j = t < kN ? t : 0;
+  uint64_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int i = 0;
+  for (; i + 8 <= np; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] ^= y[pos[i + u] + j];
+  }
+  for (; i < np; ++i) acc[0] ^= y[pos[i] + j];
+  const uint64_t r = ((acc[0] ^ acc[1]) ^ (acc[2] ^ acc[3])) ^ ((acc[4] ^ acc[5]) ^ (acc[6] ^ acc[7]));
   uint64_t* o = out + (static_cast<int64_t>(s) * K + k) * (kN + 1);
-  if (t < kN) o[t] = acc;
+  if (t < kN) o[t] = r;
   if (t == 0) o[kN] = st[kN];
 }
 
 }  // namespace
 
-// x^{312 q} mod φ (cached)
-static const Poly& jump_poly(uint64_t q) {
-  std::lock_guard<std::mutex> lk(g_poly_mu);
+// x^{312 q} mod φ (cached; caller holds g_poly_mu).  Substream starts are multiples N·q0 of
+// one unit (kJumpUnit blocks of 312 draws): x^{312 N q0} is the square of x^{312 (N/2) q0}
+// (N even) or x^{312 (N−1) q0} · x^{312 q0} (N odd) — a few squarings and multiplications per
+// new multiple instead of a full square-and-multiply chain.
+static const Poly& jump_poly_locked(uint64_t q) {
   auto& c = poly_cache();
   auto it = c.find(q);
   if (it != c.end()) return it->second;
-  // substream starts are multiples k·q0 of one step: x^{312 k q0} = x^{312 (k−1) q0} · x^{312 q0}
-  // (one multiplication instead of a square-and-multiply chain)
-  for (const uint64_t q0 : {uint64_t{3360}}) {
-    if (q > q0 && q % q0 == 0) {
-      auto a = c.find(q - q0), b = c.find(q0);
-      if (a != c.end() && b != c.end()) return c.emplace(q, field().mul(a->second, b->second)).first->second;
-    }
+  const uint64_t q0 = kJumpUnit;
+  Poly p;
+  if (q > q0 && q % q0 == 0) {
+    const uint64_t N = q / q0;
+    if (N % 2 == 0) p = field().sqr(jump_poly_locked(q / 2));
+    else p = field().mul(jump_poly_locked(q - q0), jump_poly_locked(q0));
+  } else {
+    p = field().xpow(312ull * q);
   }
-  const Poly p = field().xpow(312ull * q);
-  return c.emplace(q, p).first->second;
+  return c.emplace(q, std::move(p)).first->second;
 }
 
-int64_t mt_jump_smem_bytes() { return static_cast<int64_t>(sizeof(uint64_t)) * (kSeq + kPW); }
+static const Poly& jump_poly(uint64_t q) {
+  std::lock_guard<std::mutex> lk(g_poly_mu);
+  return jump_poly_locked(q);
+}
+
+int64_t mt_jump_smem_bytes() {
+  return static_cast<int64_t>(sizeof(uint64_t)) * (kSeq + kPW) + static_cast<int64_t>(sizeof(uint16_t)) * (kDeg + 1);
+}
 
 // Device: for S streams (states in: S × 313) and K block-jumps q[0..K) (q = 0: copy),
 // out[s·K + k] = stream s advanced by 312·q[k] draws (index word kept).  polys_dev: scratch

@@ -236,7 +236,10 @@ void spmm_batched(const Launch& L, const StencilDesc& sd, const double* A, const
 
 // ---- probe_rng.cu: rademacher_probe streams (std::mt19937_64 per probe) on the device
 void mt_seed_state(uint64_t seed, uint64_t p, uint64_t* st /*313*/);
-int64_t probe_rng_slab();
+// substream starts are multiples of kJumpUnit blocks of 312 draws (mt_jump.cu caches the
+// jump polynomials of those multiples)
+constexpr uint64_t kJumpUnit = 3360;
+int64_t probe_rng_slab(int P);
 int64_t probe_rng_scratch_words(int P);
 // next `rows` draws of every probe: states P × 313 (device), planes ≥ P × slab bytes scratch,
 // words[rows] (bit p = probe p is +1), scratch ≥ probe_rng_scratch_words(P) device words

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <random>
 #include <vector>
@@ -214,17 +215,26 @@ __global__ void k_probe_take_last(const uint64_t* __restrict__ src, int K, uint6
     dst[static_cast<int64_t>(p) * (MT_N + 1) + i] = src[(static_cast<int64_t>(p) * K + K - 1) * (MT_N + 1) + i];
 }
 
-// Substream length: a whole number of 312-word blocks (so every substream start is a
-// block jump x^{312 q} with q = k · 3360, whatever the base index), and 16 of them per slab.
-constexpr int64_t kSubRows = int64_t{MT_N} * 3360;  // 1,048,320 draws
-constexpr int kMaxSub = 16;
+// Substreams: every substream is a whole number of units of kSubRows draws (kJumpUnit blocks
+// of 312 words), so each start is a block jump x^{312 q} with q a multiple of kJumpUnit,
+// whatever the base index.  One slab holds as many rows as a 3 GB plane budget allows (config
+// 5: all 5e7 rows at once), cut into K substreams per probe so P·K ≈ 4 blocks per SM draw
+// concurrently — few jumps (each costs ~10^4 shared loads per thread) and enough blocks for
+// the latency-bound twist.  (Round 2 start: 16 fixed 1.05e6-draw substreams per 1.7e7-row slab,
+// 1440 jumps for config 5.)
+constexpr int64_t kSubRows = int64_t{MT_N} * static_cast<int64_t>(kJumpUnit);  // 1,048,320 draws
+constexpr int kMaxSub = 64;
+constexpr int64_t kPlaneBudget = int64_t{3} << 30;  // bytes of probe planes per slab
 
-int64_t probe_rng_slab() { return kSubRows * kMaxSub; }
+int64_t probe_rng_slab(int P) {
+  const int64_t units = std::max<int64_t>(1, kPlaneBudget / (std::max(1, P) * kSubRows));
+  return units * kSubRows;
+}
 int64_t probe_rng_scratch_words(int P) { return static_cast<int64_t>(P) * kMaxSub * (MT_N + 1) + kMaxSub * 312; }
 
 void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8_t* planes, uint64_t* words,
                    uint64_t* scratch) {
-  const int64_t slab = probe_rng_slab();
+  const int64_t slab = probe_rng_slab(P);
   static const bool warp_rng = [] {
     const char* e = getenv("GSGPC_PROBE_RNG_WARP");
     return e && e[0] == '1';
@@ -233,9 +243,20 @@ void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8
     const char* e = getenv("GSGPC_PROBE_RNG_NOSPLIT");
     return e && e[0] == '1';
   }();
+  static const int bps = [] {  // diagnostics: concurrent generator blocks per SM
+    const char* e = getenv("GSGPC_PROBE_RNG_BPS");
+    return e ? std::max(1, atoi(e)) : 4;  // B200, config 5 (30 probes × 5e7 draws): 1 → 10.4, 2 → 6.4, 4 → 5.1 ms
+  }();
   for (int64_t r0 = 0; r0 < rows; r0 += slab) {
     const int64_t nr = std::min(slab, rows - r0);
-    const int K = (warp_rng || no_split) ? 1 : static_cast<int>(ceil_div(nr, kSubRows));
+    int K = 1;
+    int64_t Ls = nr;
+    if (!warp_rng && !no_split) {
+      const int want = std::min<int>(kMaxSub, std::max<int>(1, static_cast<int>(ceil_div(sm_count() * bps, P))));
+      Ls = ceil_div(ceil_div(nr, want), kSubRows) * kSubRows;
+      K = static_cast<int>(ceil_div(nr, Ls));
+      if (K == 1) Ls = nr;
+    }
     if (warp_rng) {
       k_probe_rng<<<P, 32, 0, L.s>>>(states, nr, planes);
       L.count(1);
@@ -243,13 +264,13 @@ void run_probe_rng(const Launch& L, uint64_t* states, int P, int64_t rows, uint8
       k_probe_rng_blk<<<P, MT_BT, 0, L.s>>>(states, nr, 1, nr, planes);
       L.count(1);
     } else {
-      // substream k of every probe starts k · kSubRows draws after the probe's position
+      // substream k of every probe starts k · Ls draws after the probe's position
       uint64_t* sub = scratch;
       uint64_t* polys = scratch + static_cast<int64_t>(P) * kMaxSub * (MT_N + 1);
       std::vector<uint64_t> q(K);
-      for (int k = 0; k < K; ++k) q[k] = static_cast<uint64_t>(k) * (kSubRows / MT_N);
+      for (int k = 0; k < K; ++k) q[k] = static_cast<uint64_t>(k) * static_cast<uint64_t>(Ls / MT_N);
       run_mt_jump(L, states, P, q, polys, sub);
-      k_probe_rng_blk<<<P * K, MT_BT, 0, L.s>>>(sub, nr, K, kSubRows, planes);
+      k_probe_rng_blk<<<P * K, MT_BT, 0, L.s>>>(sub, nr, K, Ls, planes);
       k_probe_take_last<<<P, 128, 0, L.s>>>(sub, K, states);
       L.count(2);
     }
