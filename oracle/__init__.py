@@ -5,10 +5,13 @@ The oracle restates the reference hot path (arXiv 2101.11751 C++ reference,
 ``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import this module,
 and only as the checker / CPU baseline.  The product path never routes through it.
 
-Parity status: the reference cannot be built in this image (Eigen3/FFTW3 absent,
-SURVEY.md §0) and its own tests are empty, so this restatement is pinned against the
-SPEC.md known-answer examples and dense-algebra identities only ("parity unpinned" by
-reference outputs).
+Parity status: the reference's own build cannot run in this image (Eigen3, FFTW3 and
+nlohmann-json are absent), and its own tests are empty stubs.  The restatement is pinned
+(1) against the reference's OWN SOURCES compiled where they lie against self-written stand-ins
+for those headers (``oracle/refshim``, ``oracle/ref.py``, ``tests/test_ref_pin.py``: grids,
+weights, statistics, probes bit-exact; solves to round-off) and (2) against the SPEC.md
+known-answer examples and independent numpy fixtures (``tests/golden``).  What stays unpinned
+is the bit pattern of real Eigen's / FFTW's internal reductions.
 """
 from __future__ import annotations
 

@@ -6,11 +6,13 @@
  * bench.py (cpu_baseline leg and --impl reference) may load this library, and only as
  * the checker / CPU baseline — never as the product path.
  *
- * Parity status: the reference itself cannot be built in this image (Eigen3, FFTW3 and
- * the vendored headers are absent, and its CLI has a link defect), and its
- * own tests are empty stubs, so no reference golden vector exists.  This restatement is
- * pinned against the SPEC.md known-answer examples and dense-algebra identities
- * (tests/golden/, tests/test_oracle_*.py) — "parity unpinned" by reference outputs.
+ * Parity status: the reference's own build cannot run in this image (Eigen3, FFTW3 and
+ * nlohmann-json absent) and its own tests are empty stubs.  This restatement is
+ * pinned against (1) the reference's OWN SOURCES compiled where they lie against self-written
+ * stand-ins for those headers (oracle/refshim, oracle/_ref/libgsgp_ref.so exporting these same
+ * entry points; tests/test_ref_pin.py) and (2) the SPEC.md known-answer examples and
+ * independent numpy fixtures (tests/golden/).  Unpinned: the bit pattern of real Eigen's /
+ * FFTW's internal reductions.
  *
  * Every entry point cites the reference function it restates (file:line under
  * /root/reference/proj).  Errors are returned as codes (see ORC_*), never thrown across

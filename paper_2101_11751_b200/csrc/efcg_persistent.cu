@@ -643,8 +643,9 @@ static int pcg_grid(size_t smem) {
   int sms = 0, per_sm = 0;
   GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
-  // smallest shared-memory carveout that holds two blocks: the rest is L1
-  const int pct = static_cast<int>(std::min<size_t>(100, (2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+  // smallest shared-memory carveout that holds the resident blocks: the rest is L1
+  const int pct =
+      static_cast<int>(std::min<size_t>(100, (PCG_MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
   GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
@@ -721,7 +722,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
       mma = false;
       break;
     }
-    const int64_t target = 2 * sm_count();  // one block task per resident block (2 per SM), one wave
+    const int64_t target = PCG_MINB * sm_count();  // one block task per resident block, one wave
     const int64_t nlt = ceil_div(c.L, 8);
     const int64_t cw = std::max<int64_t>(1, std::min<int64_t>(cwmax, ceil_div(nlt, target)));
     const int64_t nlb = ceil_div(nlt, cw);
@@ -752,7 +753,7 @@ void run_efcg_persistent(const Launch& L, const StencilDesc& sd, const double* A
     if (need * 8 <= plane_kb * 1024) {
       a.mm_plane = 1;
       a.mp_ys = static_cast<int>(ys);
-      a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), 2 * sm_count() / n0)));
+      a.mp_parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n1, 8), PCG_MINB * sm_count() / n0)));
       if (const char* e = getenv("GSGPC_CG_PLANE_PARTS")) a.mp_parts = std::max(1, atoi(e));  // diagnostics
       mp_smem = static_cast<size_t>(need * 8);
     }

@@ -39,6 +39,9 @@ def _built():
     import oracle
 
     oracle.build()
+    import oracle.ref
+
+    oracle.ref.available()  # builds oracle/_ref when /root/reference is present
     from paper_2101_11751_b200 import build as B
 
     try:

@@ -1,0 +1,244 @@
+// spmv_variants.cu — diagnostic microbenchmark (not part of the library): the config-3 half-stencil
+// SpMV (80×80×20 grid, S_min = 172, offset-major A[s][node]) in several variants of the
+// register-batched kernel the persistent EFCG uses:
+//   base     : stencil_row_dot (8 offsets of loads in flight per thread), 2 blocks/SM
+//   pf<PD>   : + prefetch.global.L2 of the forward stencil element PD offsets ahead
+//   split<K> : the offsets of a 32-node group split over K warps (partials summed in order
+//              through shared memory), U offsets per batch, MINB blocks/SM
+//   l2win    : base with the first X MB of A under a persisting-L2 access-policy window
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_2101_11751_b200/csrc \
+//        -o tools/_spmv_variants tools/spmv_variants.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "stencil_spmv.cuh"
+
+using namespace gsgpc;
+
+constexpr int SMIN = 172;
+__constant__ int c_off[SMIN];
+struct Off {
+  __device__ __forceinline__ int operator()(int s) const { return c_off[s]; }
+};
+
+__global__ void __launch_bounds__(256, 2) k_base(int m, const double* __restrict__ A, const double* __restrict__ v,
+                                                 double* __restrict__ out) {
+  for (int a = blockIdx.x * 256 + threadIdx.x; a < m; a += gridDim.x * 256)
+    out[a] = stencil_row_dot<SMIN>(m, A, v, a, Off{});
+}
+
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// partial dot over offsets [s0, s1) (s0 ≥ 1), U per batch, optional L2 prefetch PD offsets ahead,
+// CS: streaming (evict-first) stencil loads
+template <int U, int PD, bool CS>
+__device__ __forceinline__ double part_dot(int m, const double* __restrict__ A, const double* __restrict__ v, int a,
+                                           int s0, int s1) {
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  auto lda = [&](const double* p) -> double { return CS ? __ldcs(p) : __ldg(p); };
+  if (PD > 0) {
+    for (int s = s0; s < min(s0 + PD, s1); ++s) pf_l2(A + static_cast<int64_t>(s) * m + a);
+  }
+  int s = s0;
+  for (; s + U <= s1; s += U) {
+    double af[U], ab[U], vf[U], vb[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int o = c_off[s + q];
+      const int f = a + o, b = a - o;
+      const bool okf = static_cast<unsigned>(f) < static_cast<unsigned>(m);
+      const bool okb = static_cast<unsigned>(b) < static_cast<unsigned>(m);
+      const double* As = A + static_cast<int64_t>(s + q) * m;
+      if (PD > 0 && s + q + PD < s1) pf_l2(As + static_cast<int64_t>(PD) * m + a);
+      af[q] = lda(As + a);
+      ab[q] = okb ? lda(As + b) : 0.0;
+      vf[q] = okf ? __ldca(v + f) : 0.0;
+      vb[q] = okb ? __ldca(v + b) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; q += 2) {
+      acc0 = fma(af[q], vf[q], acc0);
+      acc1 = fma(ab[q], vb[q], acc1);
+      if (q + 1 < U) {
+        acc2 = fma(af[q + 1], vf[q + 1], acc2);
+        acc3 = fma(ab[q + 1], vb[q + 1], acc3);
+      }
+    }
+  }
+  if (s < s1) {  // predicated tail batch
+    double af[U], ab[U], vf[U], vb[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const bool live = s + q < s1;
+      const int o = live ? c_off[s + q] : 0;
+      const int f = a + o, b = a - o;
+      const bool okf = live && static_cast<unsigned>(f) < static_cast<unsigned>(m);
+      const bool okb = live && static_cast<unsigned>(b) < static_cast<unsigned>(m);
+      const double* As = A + static_cast<int64_t>(live ? s + q : s0) * m;
+      af[q] = live ? lda(As + a) : 0.0;
+      ab[q] = okb ? lda(As + b) : 0.0;
+      vf[q] = okf ? __ldca(v + f) : 0.0;
+      vb[q] = okb ? __ldca(v + b) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      acc0 = fma(af[q], vf[q], acc0);
+      acc1 = fma(ab[q], vb[q], acc1);
+    }
+  }
+  return (acc0 + acc1) + (acc2 + acc3);
+}
+
+template <int U, int PD, bool CS, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_pf(int m, const double* __restrict__ A, const double* __restrict__ v,
+                                                  double* __restrict__ out) {
+  for (int a = blockIdx.x * 256 + threadIdx.x; a < m; a += gridDim.x * 256)
+    out[a] = __ldg(A + a) * __ldca(v + a) + part_dot<U, PD, CS>(m, A, v, a, 1, SMIN);
+}
+
+// K warps per 32-node group; a block of 8 warps covers 8/K groups per pass
+template <int K, int U, int PD, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_split(int m, const double* __restrict__ A, const double* __restrict__ v,
+                                                     double* __restrict__ out) {
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int GPB = 8 / K;  // groups per block pass
+  const int ngroups = (m + 31) >> 5;
+  constexpr int PER = (SMIN - 1 + K - 1) / K;
+  const int k = w % K, gl = w / K;
+  for (int g0 = blockIdx.x * GPB; g0 < ngroups; g0 += gridDim.x * GPB) {
+    const int g = g0 + gl;
+    const int a = g * 32 + lane;
+    double p = 0.0;
+    if (g < ngroups && a < m) {
+      const int s0 = 1 + k * PER, s1 = min(SMIN, s0 + PER);
+      p = part_dot<U, PD, true>(m, A, v, a, s0, s1);
+      if (k == 0) p += __ldg(A + a) * __ldca(v + a);
+    }
+    part[w][lane] = p;
+    __syncthreads();
+    if (k == 0 && g < ngroups && a < m) {
+      double s = part[w][lane];
+#pragma unroll
+      for (int j = 1; j < K; ++j) s += part[w + j][lane];
+      out[a] = s;
+    }
+    __syncthreads();
+  }
+}
+
+int main(int argc, char** argv) {
+  const int n0 = 80, n1 = 80, n2 = 20, m = n0 * n1 * n2;
+  std::vector<int> off;
+  for (int s = 0; s < SMIN; ++s) {
+    int q = 171 + s, d[3];
+    for (int k = 2; k >= 0; --k) {
+      d[k] = q % 7 - 3;
+      q /= 7;
+    }
+    off.push_back((d[0] * n1 + d[1]) * n2 + d[2]);
+  }
+  cudaMemcpyToSymbol(c_off, off.data(), sizeof(int) * SMIN);
+  std::vector<double> hA(static_cast<size_t>(SMIN) * m + 64), hv(m);
+  unsigned long long x = 88172645463325252ull;
+  auto rnd = [&] {
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    return (x >> 11) * 0x1.0p-53;
+  };
+  for (auto& e : hA) e = rnd();
+  for (auto& e : hv) e = rnd() - 0.5;
+  double *A, *v, *o1, *o2;
+  cudaMalloc(&A, sizeof(double) * hA.size());
+  cudaMalloc(&v, sizeof(double) * m);
+  cudaMalloc(&o1, sizeof(double) * m);
+  cudaMalloc(&o2, sizeof(double) * m);
+  cudaMemcpy(A, hA.data(), sizeof(double) * hA.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(v, hv.data(), sizeof(double) * m, cudaMemcpyHostToDevice);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<double> ref(m), got(m);
+  bool have_ref = false;
+  // back-to-back passes, as inside a CG solve (the stencil is 176 MB > L2)
+  auto run = [&](const char* name, auto launch) {
+    cudaMemsetAsync(o2, 0, sizeof(double) * m, st);
+    for (int r = 0; r < 5; ++r) launch();
+    float best = 1e30f;
+    const int reps = 5, inner = 20;
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(e0, st);
+      for (int i = 0; i < inner; ++i) launch();
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms / inner < best ? ms / inner : best;
+    }
+    cudaMemcpy(got.data(), o2, sizeof(double) * m, cudaMemcpyDeviceToHost);
+    double err = 0.0;
+    if (!have_ref) {
+      ref = got;
+      have_ref = true;
+    } else {
+      for (int i = 0; i < m; ++i) err = std::max(err, std::abs(ref[i] - got[i]));
+    }
+    std::printf("%-44s %6.1f us  (%.2f TB/s)  maxdiff %.2g  %s\n", name, best * 1e3,
+                double(SMIN) * m * 8 / (best * 1e-3) / 1e12, err, cudaGetErrorString(cudaGetLastError()));
+    std::fflush(stdout);
+  };
+  run("base U=8 2x256/SM", [&] { k_base<<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("base node/thread (500 blocks)", [&] { k_base<<<(m + 255) / 256, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=0 cs 2/SM", [&] { k_pf<8, 0, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=8 cs 2/SM", [&] { k_pf<8, 8, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=16 cs 2/SM", [&] { k_pf<8, 16, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=32 cs 2/SM", [&] { k_pf<8, 32, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=64 cs 2/SM", [&] { k_pf<8, 64, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=8 PD=32 ldg 2/SM", [&] { k_pf<8, 32, false, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=4 PD=0 cs 4/SM", [&] { k_pf<4, 0, true, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=4 PD=16 cs 4/SM", [&] { k_pf<4, 16, true, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=4 PD=32 cs 4/SM", [&] { k_pf<4, 32, true, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=6 PD=24 cs 3/SM", [&] { k_pf<6, 24, true, 3><<<3 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("pf U=2 PD=32 cs 6/SM", [&] { k_pf<2, 32, true, 6><<<6 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=2 U=8 2/SM", [&] { k_split<2, 8, 0, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=4 U=8 2/SM", [&] { k_split<4, 8, 0, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=4 U=4 4/SM", [&] { k_split<4, 4, 0, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=4 U=4 PD=16 4/SM", [&] { k_split<4, 4, 16, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=4 U=8 PD=16 2/SM", [&] { k_split<4, 8, 16, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  run("split K=8 U=4 PD=8 4/SM", [&] { k_split<8, 4, 8, 4><<<4 * sms, 256, 0, st>>>(m, A, v, o2); });
+  // persisting-L2 window over the first X MB of A (hitRatio 1), plain loads vs streaming loads
+  for (int mb : {32, 48, 64, 80}) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(mb) << 20);
+    cudaStreamAttrValue at{};
+    at.accessPolicyWindow.base_ptr = A;
+    at.accessPolicyWindow.num_bytes = size_t(mb) << 20;
+    at.accessPolicyWindow.hitRatio = 1.0f;
+    at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaError_t e = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at);
+    char nm[96];
+    std::snprintf(nm, sizeof nm, "l2win %d MB ldg 2/SM (%s)", mb, cudaGetErrorString(e));
+    run(nm, [&] { k_pf<8, 0, false, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+    std::snprintf(nm, sizeof nm, "l2win %d MB ldg PD=32 2/SM", mb);
+    run(nm, [&] { k_pf<8, 32, false, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  }
+  {
+    cudaStreamAttrValue at{};
+    at.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at);
+    cudaCtxResetPersistingL2Cache();
+  }
+  int l2 = 0, maxp = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0);
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0);
+  std::printf("L2 %d MB, max persisting %d MB\n", l2 >> 20, maxp >> 20);
+  return 0;
+}
