@@ -9,10 +9,11 @@ One JSON line on rank 0 (contract in the task prompt):
             D2H of W^T y, y^T y, n inside the timed region
   roofline— K1 (per-cell moments kernel) vs its binding peak: the FP64 tensor pipe at d = 3
             (DMMA peak measured live), HBM otherwise; the HBM view is kept as a sub-object
-  cpu_baseline — the oracle restatement of the reference (hash-map accumulation, all
-            host threads) on a bounded prefix sample of the same workload
-`--impl reference` times only the reference CPU path (the oracle port: the reference
-itself cannot be built here) on the same config.
+  cpu_baseline — the reference's own sufficient_stats (oracle/_ref: the reference sources
+            compiled against stand-in Eigen/FFTW headers, kind "reference"; the oracle
+            restatement, kind "port", only if that library is absent) on one pinned host
+            thread over a bounded prefix sample of the same workload
+`--impl reference` times only that CPU path on the same config.
 
 `--gpus N` (N > 1) starts N ranks itself under torch.distributed.run when no torchrun
 environment is present.  Default scaling is strong: the config's n rows are split over the ranks
@@ -133,10 +134,27 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-# ---------------------------------------------------------------- CPU (oracle) timing
-def cpu_rate(x, y, grid_o, scheme, nthreads, target_s):
-    """Points/s of the oracle restatement (reference algorithm) on a prefix sample."""
+# ---------------------------------------------------------------- CPU (reference / oracle) timing
+def cpu_checker():
+    """(front-end module, kind, what): the reference's own code when oracle/_ref is built
+    (it travels to the GPU box prebuilt), else the oracle restatement."""
     import oracle as O
+
+    try:
+        import oracle.ref as R
+
+        if R.available():
+            return R._mod, "reference", ("the reference's own sufficient_stats (interp.cpp:244-263; its sources compiled "
+                                         "against stand-in Eigen/FFTW headers, oracle/refshim)")
+    except Exception:  # noqa: BLE001
+        pass
+    O.build()
+    return O, "port", "oracle restatement of sufficient_stats (std::unordered_map accumulation, interp.cpp:179-221)"
+
+
+def cpu_rate(x, y, grid_o, scheme, nthreads, target_s):
+    """Points/s of the CPU checker (reference algorithm) on a prefix sample."""
+    O = cpu_checker()[0]
 
     n_all = x.shape[0]
     s = min(n_all, 2000 * nthreads)
@@ -166,7 +184,7 @@ def cpu_single_thread(x, y, grid_o, rows, trials):
     accumulator, interp.cpp:179-221) on ONE host thread pinned to one core (sched_setaffinity
     of the calling thread = taskset), 1 warm-up then `trials` timed runs over a `rows`-row prefix;
     sufficient_stats wall time → points/s, mean and 95 % CI."""
-    import oracle as O
+    O, kind, what = cpu_checker()
 
     rows = min(rows, x.shape[0])
     old = os.sched_getaffinity(0)
@@ -185,11 +203,10 @@ def cpu_single_thread(x, y, grid_o, rows, trials):
         os.sched_setaffinity(0, old)
     rates = [rows / t for t in times]
     mean, ci = mean_ci(rates)
-    return {"value": mean, "unit": "points/s", "cores": 1, "threads": 1, "kind": "port", "ci95": ci,
+    return {"value": mean, "unit": "points/s", "cores": 1, "threads": 1, "kind": kind, "ci95": ci,
             "trials": [round(t, 3) for t in times],
             "sample": f"first {rows} rows of the bench workload, 1 warm-up + {trials} trials, one thread pinned "
-                      f"to core {core} (oracle restatement of sufficient_stats: std::unordered_map accumulation, "
-                      f"interp.cpp:179-221)"}
+                      f"to core {core} ({what})"}
 
 
 def cpu_lscpu():
@@ -204,7 +221,7 @@ def cpu_lscpu():
 
 
 def oracle_grid(grid):
-    import oracle as O
+    O = cpu_checker()[0]
 
     d = grid.dim()
     return O.Grid([grid.min(k) for k in range(d)], [grid.max(k) for k in range(d)], [grid.size(k) for k in range(d)])
@@ -212,17 +229,17 @@ def oracle_grid(grid):
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
-    """The reference's CPU path on this box: the oracle restatement of sufficient_stats (one
-    std::unordered_map accumulator in stream order, interp.cpp:179-221 — the reference's
-    precompute is single-threaded, so one thread pinned to one core is all the threads it can
-    use), each step a bounded prefix sample of the bench workload."""
+    """The reference's CPU path on this box: its own sufficient_stats (oracle/_ref; the oracle
+    restatement if that library is absent) — one std::unordered_map accumulator in stream order,
+    interp.cpp:179-221; the reference's precompute is single-threaded, so one thread pinned to
+    one core is all the threads it can use — each step a bounded prefix sample of the bench
+    workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle as O
     from paper_2101_11751_b200 import synthetic as S
 
-    O.build()
+    O, kind, what = cpu_checker()
     cfg = S.CONFIGS[args.config]
     rows = min(cfg.n, args.ref_rows)
     x, y = S.generate(args.config, n=rows)
@@ -251,12 +268,10 @@ def run_reference(args):
         "scaling": args.scaling, "vs_baseline": value / PUBLISHED_PTS_PER_S, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config{args.config} ({cfg.name}) prefix sample", "sample_rows": rows,
                    "grid": list(cfg.sizes), "scheme": "cubic"},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "threads": 1, "kind": "port", "ci95": ci,
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "threads": 1, "kind": kind, "ci95": ci,
                          "cpu": cpu_lscpu(), "trials": [round(t, 3) for t in times],
                          "sample": f"first {rows} rows of config {args.config} per step, one thread pinned to core "
-                                   f"{core} (oracle restatement of sufficient_stats: one std::unordered_map "
-                                   f"accumulator in stream order, interp.cpp:179-221; the reference precompute is "
-                                   f"single-threaded)"},
+                                   f"{core} ({what}; the reference precompute is single-threaded)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -479,9 +494,6 @@ def run_ours(args):
     # thread, plus the all-core sharded figure labelled separately
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        import oracle as O
-
-        O.build()
         samp = rows[: min(n, max(args.cpu_rows, 4_000_000))].cpu().numpy()
         og = oracle_grid(grid)
         cpu = cpu_single_thread(samp[:, : cfg.d], samp[:, cfg.d], og, args.cpu_rows, args.cpu_trials)

@@ -311,37 +311,47 @@ class SparseMatrixBase {
   const Scalar* valuePtr() const { return val_.data(); }
   void makeCompressed() {}
 
-  // duplicates are summed in input order; explicit zeros are kept
+  // duplicates are summed in input order; explicit zeros are kept.  Linear time like the real
+  // library: a counting pass over the outer index, then a stable sort of each outer vector.
   template <typename It>
   void setFromTriplets(It first, It last) {
-    struct E {
-      StorageIndex o, i;
-      Scalar v;
-    };
-    std::vector<E> es;
-    for (It t = first; t != last; ++t) {
-      const StorageIndex o = Options == RowMajor ? t->row() : t->col();
-      const StorageIndex i = Options == RowMajor ? t->col() : t->row();
-      if (o < 0 || o >= outerSize() || i < 0 || i >= innerSize()) {
-        throw std::logic_error("eigen_stand_in: triplet out of range");
-      }
-      es.push_back({o, i, t->value()});
+    const Index no = outerSize(), ni = innerSize();
+    std::vector<std::size_t> start(static_cast<std::size_t>(no) + 1, 0);
+    std::size_t total = 0;
+    for (It t = first; t != last; ++t, ++total) {
+      const Index o = Options == RowMajor ? t->row() : t->col();
+      const Index i = Options == RowMajor ? t->col() : t->row();
+      if (o < 0 || o >= no || i < 0 || i >= ni) throw std::logic_error("eigen_stand_in: triplet out of range");
+      ++start[static_cast<std::size_t>(o) + 1];
     }
-    std::stable_sort(es.begin(), es.end(),
-                     [](const E& a, const E& b) { return a.o != b.o ? a.o < b.o : a.i < b.i; });
-    outer_.assign(static_cast<std::size_t>(outerSize()) + 1, 0);
+    for (Index o = 0; o < no; ++o) start[o + 1] += start[o];
+    std::vector<std::pair<StorageIndex, Scalar>> e(total);
+    {
+      std::vector<std::size_t> cur(start.begin(), start.end() - 1);
+      for (It t = first; t != last; ++t) {
+        const Index o = Options == RowMajor ? t->row() : t->col();
+        const StorageIndex i = Options == RowMajor ? t->col() : t->row();
+        e[cur[static_cast<std::size_t>(o)]++] = {i, t->value()};
+      }
+    }
+    outer_.assign(static_cast<std::size_t>(no) + 1, 0);
     inner_.clear();
     val_.clear();
-    for (std::size_t k = 0; k < es.size(); ++k) {
-      if (k > 0 && es[k].o == es[k - 1].o && es[k].i == es[k - 1].i) {
-        val_.back() += es[k].v;
-      } else {
-        inner_.push_back(es[k].i);
-        val_.push_back(es[k].v);
-        ++outer_[static_cast<std::size_t>(es[k].o) + 1];
+    inner_.reserve(total);
+    val_.reserve(total);
+    for (Index o = 0; o < no; ++o) {
+      auto b = e.begin() + static_cast<std::ptrdiff_t>(start[o]), en = e.begin() + static_cast<std::ptrdiff_t>(start[o + 1]);
+      std::stable_sort(b, en, [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (auto it = b; it != en; ++it) {
+        if (it != b && it->first == (it - 1)->first) {
+          val_.back() += it->second;
+        } else {
+          inner_.push_back(it->first);
+          val_.push_back(it->second);
+        }
       }
+      outer_[static_cast<std::size_t>(o) + 1] = static_cast<StorageIndex>(inner_.size());
     }
-    for (std::size_t o = 0; o + 1 < outer_.size(); ++o) outer_[o + 1] += outer_[o];
   }
 
   // drops entries with |v| <= ref (Eigen's prune(ref) with the default epsilon keeps |v| > 0 for ref = 0)
