@@ -629,35 +629,37 @@ static PcgMode mode_cfg(const KgDev& kg, int k) {
   return c;
 }
 
-// Persistent grid size per (device, kernel, dynamic smem): SMs × resident blocks (≤ 4), cached
-// under a lock (each device configures its own function attributes).
+// Launch of the persistent kernel.  The function attributes (dynamic shared-memory limit and
+// the shared-memory carveout) belong to the kernel, not to a launch, so they are set before
+// EVERY launch — a solve with another shared-memory size in between (another grid, another
+// context on the device) would otherwise leave a carveout under which the cached grid no longer
+// fits ("too many blocks in cooperative launch") — and attribute setting + launch run under one
+// lock per kernel instantiation.  The grid size per (device, dynamic smem) is cached.
 template <int SMIN>
-static int pcg_grid(size_t smem) {
+static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<int, size_t>, int> cache;
   int dev = 0;
   GSGPC_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find({dev, smem});
-  if (it != cache.end()) return it->second;
-  int sms = 0, per_sm = 0;
   GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
   // smallest shared-memory carveout that holds the resident blocks: the rest is L1
   const int pct =
       static_cast<int>(std::min<size_t>(100, (PCG_MINB * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
   GSGPC_CUDA(cudaFuncSetAttribute(k_efcg_persistent<SMIN>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-  GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
-  if (per_sm < 1) throw Error(GSGPC_CUDA_ERROR, "persistent EFCG kernel cannot be resident");
-  const int grid = sms * std::min(per_sm, 4);
-  cache[{dev, smem}] = grid;
-  return grid;
-}
-
-template <int SMIN>
-static void launch_pcg(const Launch& L, const PcgArgs& a, size_t smem) {
-  const int grid = pcg_grid<SMIN>(smem);
+  int grid = 0;
+  auto it = cache.find({dev, smem});
+  if (it != cache.end()) {
+    grid = it->second;
+  } else {
+    int sms = 0, per_sm = 0;
+    GSGPC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSGPC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_efcg_persistent<SMIN>, PCG_NT, smem));
+    if (per_sm < 1) throw Error(GSGPC_CUDA_ERROR, "persistent EFCG kernel cannot be resident");
+    grid = sms * std::min(per_sm, 4);
+    cache[{dev, smem}] = grid;
+  }
   // small grids: about one node per thread, at least 32 blocks — every grid barrier costs
   // more with more blocks (config 1, m = 1000: 296 blocks 0.064, 32 blocks 0.032 ms/iteration;
   // 16 blocks 0.048)

@@ -84,3 +84,31 @@ def test_foreign_device_pointer_rejected():
     with pytest.raises(G.InvalidArgument, match="device"):
         G.sufficient_stats(g, G.InterpScheme.Cubic, rows[:, :1].contiguous(), rows[:, 1].contiguous(),
                            ctx=G.Context(0))
+
+
+def test_persistent_cg_after_solves_with_other_shared_memory_sizes():
+    """The persistent CG kernel's function attributes (dynamic shared memory, carveout) are per
+    kernel, not per launch: a solve on a large grid must still launch after solves of the same
+    dimension on smaller grids changed them (regression: 'too many blocks in cooperative launch'
+    when the cached grid met another launch's carveout), with bitwise the same result."""
+    ctx = G.Context(0)
+    rng = np.random.default_rng(9)
+    spec = G.KernelSpec(G.Hyperparams(0.3, [0.05, 0.05], 1.0))
+
+    def solve(sizes, n):
+        x = np.random.default_rng(sizes[0]).random((n, 2))
+        y = np.sin(3.0 * x.sum(axis=1))
+        g = G.fit_grid_to_data(np.zeros(2), np.ones(2), sizes, G.InterpScheme.Cubic)
+        st = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y, ctx=ctx)
+        kg = G.ToeplitzOperator(g, spec, ctx=ctx)
+        r0 = -kg.apply(st.wty()) / 0.09
+        res = G.factorized_cg_grid_rhs(kg, st, r0, 0.3, G.GridRhsTolerance(eps_abs=1e-30), 12)
+        return res.xhat_d.copy(), res.residual_trace.copy()
+
+    first = solve((256, 256), 400_000)
+    for sizes in ((20, 17), (64, 48), (700, 30), (9, 300)):
+        solve(sizes, 20_000)
+    again = solve((256, 256), 400_000)
+    assert np.array_equal(first[0].view(np.uint64), again[0].view(np.uint64))
+    assert np.array_equal(first[1].view(np.uint64), again[1].view(np.uint64))
+    del rng

@@ -196,6 +196,7 @@ int main(int argc, char** argv) {
     std::fflush(stdout);
   };
   run("base U=8 2x256/SM", [&] { k_base<<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
+  if (argc > 1 && !std::strcmp(argv[1], "base")) return 0;  // for an ncu capture of the SpMV alone
   run("base node/thread (500 blocks)", [&] { k_base<<<(m + 255) / 256, 256, 0, st>>>(m, A, v, o2); });
   run("pf U=8 PD=0 cs 2/SM", [&] { k_pf<8, 0, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
   run("pf U=8 PD=8 cs 2/SM", [&] { k_pf<8, 8, true, 2><<<2 * sms, 256, 0, st>>>(m, A, v, o2); });
