@@ -128,6 +128,93 @@ __global__ void __launch_bounds__(288) k_tma(int m, const double* __restrict__ A
   }
 }
 
+// ---------------------------------------------------------------- TMA ring, lane-parallel issue
+// Same ring, but the producer warp issues the 2·TU2 bulk copies of a stage from 2·TU2 lanes at
+// once (one copy per lane) instead of one thread issuing them in turn.
+template <int TU2, int S>
+__global__ void __launch_bounds__(288) k_tma2(int m, const double* __restrict__ A, const double* __restrict__ v,
+                                              double* __restrict__ out) {
+  static_assert(2 * TU2 <= 32, "one copy per producer lane");
+  constexpr int NG2 = (SMIN - 1 + TU2 - 1) / TU2;
+  constexpr int STG = TU2 * (TN + TB);
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int ntiles = (m + TN - 1) / TN;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], TN / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= TN) {  // producer warp
+    const int lane = threadIdx.x - TN;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int base = tile * TN;
+      const int nn = min(TN, m - base);
+      const unsigned fbytes = static_cast<unsigned>(((nn + 1) & ~1) * 8);
+      for (int gI = 0; gI < NG2; ++gI, ++it) {
+        const int st = it % S;
+        if (lane == 0) mbar_wait(&empty[st], ((it / S) & 1) ^ 1);
+        __syncwarp();
+        double* buf = ring + st * STG;
+        const int nq = min(TU2, SMIN - 1 - gI * TU2);
+        if (lane == 0) mbar_expect(&full[st], static_cast<unsigned>(nq) * (fbytes + TB * 8));
+        __syncwarp();
+        const int q = lane >> 1, dir = lane & 1;
+        if (q < nq) {
+          const int s = 1 + gI * TU2 + q;
+          const double* row = A + static_cast<int64_t>(s) * m;
+          if (dir == 0) bulk_g2s(buf + q * TN, row + base, fbytes, &full[st]);
+          else bulk_g2s(buf + TU2 * TN + q * TB, row + bwd_start(base, c_off[s]), TB * 8, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  const int t = threadIdx.x;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int base = tile * TN;
+    const int a = base + t;
+    const bool live = a < m;
+    double acc0 = live ? __ldg(A + a) * __ldca(v + a) : 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    for (int gI = 0; gI < NG2; ++gI, ++it) {
+      const int st = it % S;
+      // v loads do not depend on the ring: issue them before waiting for the stage
+      double vf[TU2], vb[TU2];
+      int bo[TU2];
+#pragma unroll
+      for (int q = 0; q < TU2; ++q) {
+        const int s = 1 + gI * TU2 + q;
+        const int o = s < SMIN ? c_off[s] : 0;
+        const int f = a + o, b = a - o;
+        const bool okf = live && s < SMIN && static_cast<unsigned>(f) < static_cast<unsigned>(m);
+        const bool okb = live && s < SMIN && b >= 0;
+        vf[q] = okf ? __ldca(v + f) : 0.0;
+        vb[q] = okb ? __ldca(v + b) : 0.0;
+        bo[q] = okb ? b - bwd_start(base, o) : 0;
+      }
+      mbar_wait(&full[st], (it / S) & 1);
+      const double* buf = ring + st * STG;
+#pragma unroll
+      for (int q = 0; q < TU2; q += 2) {
+        acc0 = fma(buf[q * TN + t], vf[q], acc0);
+        acc1 = fma(buf[TU2 * TN + q * TB + bo[q]], vb[q], acc1);
+        if (q + 1 < TU2) {
+          acc2 = fma(buf[(q + 1) * TN + t], vf[q + 1], acc2);
+          acc3 = fma(buf[TU2 * TN + (q + 1) * TB + bo[q + 1]], vb[q + 1], acc3);
+        }
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[st]);
+    }
+    if (live) out[a] = (acc0 + acc1) + (acc2 + acc3);
+  }
+}
+
 int main() {
   const int n0 = 80, n1 = 80, n2 = 20, m = n0 * n1 * n2;
   std::vector<int> off;
@@ -204,5 +291,24 @@ int main() {
   tma(k_tma<8>, 8, 1, "tma S=8 1/SM");
   tma(k_tma<12>, 12, 1, "tma S=12 1/SM");
   tma(k_tma<4>, 4, 3, "tma S=4 3/SM");
+  auto tma2 = [&](auto kern, int TU2, int S, int per_sm, const char* name) {
+    const size_t smem = sizeof(double) * S * TU2 * (TN + TB);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    run(name, [&] { kern<<<per_sm * sms, 288, smem>>>(m, A, v, o2); });
+    std::vector<double> r1(m), r2(m);
+    cudaMemcpy(r1.data(), o1, sizeof(double) * m, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r2.data(), o2, sizeof(double) * m, cudaMemcpyDeviceToHost);
+    double err = 0.0;
+    for (int i = 0; i < m; ++i) err = std::max(err, std::abs(r1[i] - r2[i]));
+    std::printf("    max |tma2 - ldg| = %.3g\n", err);
+  };
+  tma2(k_tma2<4, 6>, 4, 6, 2, "tma2 TU=4 S=6 2/SM");
+  tma2(k_tma2<8, 3>, 8, 3, 2, "tma2 TU=8 S=3 2/SM");
+  tma2(k_tma2<8, 6>, 8, 6, 1, "tma2 TU=8 S=6 1/SM");
+  tma2(k_tma2<8, 4>, 8, 4, 1, "tma2 TU=8 S=4 1/SM");
+  tma2(k_tma2<16, 3>, 16, 3, 1, "tma2 TU=16 S=3 1/SM");
+  tma2(k_tma2<4, 4>, 4, 4, 3, "tma2 TU=4 S=4 3/SM");
+  tma2(k_tma2<8, 2>, 8, 2, 3, "tma2 TU=8 S=2 3/SM");
+  tma2(k_tma2<4, 3>, 4, 3, 4, "tma2 TU=4 S=3 4/SM");
   return 0;
 }
