@@ -527,38 +527,56 @@ static int bucket_groups(gsgpc_ctx* ctx, int64_t nvalid, int nb) {
   return std::min(env, nb);
 }
 
+// Device-resident batches of several chunks: the binning of chunk k + 1 (classify … slice sort,
+// on the high-priority sort stream) can overlap the moments kernel of chunk k (compute stream).
+// Each of the two scratch sets is reused once the K1 that read it has finished; every kernel
+// and every order of accumulation is the sequential path's, so the statistics are bitwise the
+// same.  Measured on B200 (GSGPC_CHUNK_PIPE=1): config 4, 1e9 rows in 8 chunks 58.7 → 68.9 ms
+// (the latency-bound d = 2 K1 and the sorts contend for the same DRAM queues); config 3 in four
+// 2^25-row chunks 11.03 → 10.54 ms (one chunk: 9.24 ms).  Off by default.
+struct ChunkPipe {
+  cudaStream_t bin = nullptr;
+  cudaEvent_t binned[2] = {nullptr, nullptr}, k1done[2] = {nullptr, nullptr};
+  int set = 0;
+  int64_t k = 0;
+};
+
 void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, int64_t n, int64_t row0,
-               const uint64_t* pw_dev, int probes) {
-  const Launch L = ctx->L();
+               const uint64_t* pw_dev, int probes, const ChunkPipe* pipe) {
+  const Launch LK = ctx->L();
+  const Launch L = pipe ? Launch{pipe->bin, &ctx->launches} : LK;  // binning launches
   const GridDev& g = s->g;
   PhaseTimer pt(ctx);
+  const std::string sfx = pipe && pipe->set ? "#1" : "";
+  auto sbuf = [&](const char* name) -> DBuf& { return ctx->buf(name + sfx); };
+  if (pipe && pipe->k >= 2) GSGPC_CUDA(cudaStreamWaitEvent(pipe->bin, pipe->k1done[pipe->set], 0));
   if (n >= (int64_t{1} << 31)) throw Error(GSGPC_INVALID_ARGUMENT, "sufficient_stats: batch too large");
   const BinDesc bd = bin_desc(g.cells);
   const int64_t ntiles = bin_tiles(n);
-  DBuf& tcnt = ctx->buf("bin_tcnt");
+  DBuf& tcnt = sbuf("bin_tcnt");
   tcnt.ensure(sizeof(int) * ntiles * bd.nb);
-  DBuf& gsum = ctx->buf("bin_gsum");
+  DBuf& gsum = sbuf("bin_gsum");
   gsum.ensure(sizeof(int) * bin_groups(n) * bd.nb);
-  DBuf& bbase = ctx->buf("bin_base");
+  DBuf& bbase = sbuf("bin_base");
   bbase.ensure(sizeof(int64_t) * (bd.nb + 1));
-  DBuf& sbase = ctx->buf("bin_sbase");
+  DBuf& sbase = sbuf("bin_sbase");
   sbase.ensure(sizeof(int64_t) * (bd.nb + 1));
-  DBuf& off = ctx->buf("off");
+  DBuf& off = sbuf("off");
   off.ensure(sizeof(int64_t) * (g.cells + 2));
-  DBuf& cellid = ctx->buf("cellid");
+  DBuf& cellid = sbuf("cellid");
   cellid.ensure(sizeof(int) * n);
   DBuf& err = ctx->buf("err");
   err.ensure(sizeof(unsigned long long) * 2);
   const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count() * 6)));
-  DBuf& part = ctx->buf("yty_part");
+  DBuf& part = sbuf("yty_part");
   part.ensure(sizeof(double) * nblk);
-  DBuf& ychunk = ctx->buf("yty_chunk");
+  DBuf& ychunk = sbuf("yty_chunk");
   ychunk.ensure(sizeof(double));
 
   // err: reset once per public call (stats_add / add_file), checked by the caller after the
   // whole batch — see BinGate (precompute.cu)
   int h = pt.begin(0);
-  GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), ctx->stream));
+  GSGPC_CUDA(cudaMemsetAsync(ychunk.p, 0, sizeof(double), L.s));
   run_classify(L, dtype, P, n, row0, g, bd, tcnt.as<int>(), err.as<unsigned long long>(), part.as<double>(), nblk,
                cellid.as<int>());
   run_sum_partials(L, part.as<double>(), nblk, ychunk.as<double>());
@@ -571,7 +589,7 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   // binning → moments without a host round trip: sizes are upper bounds (every row valid),
   // the kernels read the true counts from bbase / sbase
   const int64_t nvalid = n, nslices = bin_slices_max(n, bd);
-  const int G = bucket_groups(ctx, nvalid, bd.nb);
+  const int G = pipe ? 1 : bucket_groups(ctx, nvalid, bd.nb);
   std::vector<int64_t> hb, hsl;
   if (G > 1) {  // the optional overlap needs the bucket offsets on the host
     const int64_t NB1 = bd.nb + 1;
@@ -584,19 +602,19 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
   {
     // the binning sorts (cell, row) keys; K1 gathers the rows (and probe words) of P through
     // the cell-sorted row indices
-    DBuf& idx_s = ctx->buf("bin_idx_sorted");
+    DBuf& idx_s = sbuf("bin_idx_sorted");
     idx_s.ensure(sizeof(int) * nvalid);
-    DBuf& cid1 = ctx->buf("bin_cid");
+    DBuf& cid1 = sbuf("bin_cid");
     cid1.ensure(sizeof(int) * nvalid);
-    DBuf& idx1 = ctx->buf("bin_idx");
+    DBuf& idx1 = sbuf("bin_idx");
     idx1.ensure(sizeof(int) * nvalid);
-    DBuf& spv = ctx->buf("k1_split_v");
-    DBuf& spc = ctx->buf("k1_split_c");
+    DBuf& spv = sbuf("k1_split_v");
+    DBuf& spc = sbuf("k1_split_c");
     const int64_t spw = split_rec_warps(nvalid), spr = split_rec_doubles(g, probes);
     spv.ensure(sizeof(double) * spw * spr);
     spc.ensure(sizeof(int64_t) * spw);
     const SplitBuf sb{spv.as<double>(), spc.as<int64_t>(), spw, spr};
-    DBuf& scnt = ctx->buf("bin_scnt");
+    DBuf& scnt = sbuf("bin_scnt");
     scnt.ensure(sizeof(int) * std::max<int64_t>(1, nslices) * (int64_t{1} << bd.bsh));
     h = pt.begin(2);
     run_partition(L, n, bd, cellid.as<int>(), tcnt.as<int>(), cid1.as<int>(), idx1.as<int>(), errp);
@@ -605,20 +623,25 @@ void add_chunk(gsgpc_ctx* ctx, gsgpc_stats* s, int dtype, const PointsDev& P, in
       run_slice_sort(L, bd, g.cells, 0, bd.nb, 0, nslices, cid1.as<int>(), idx1.as<int>(), bbase.as<int64_t>(),
                      sbase.as<int64_t>(), scnt.as<int>(), off.as<int64_t>(), idx_s.as<int>(), errp);
       pt.end(h);
+      if (pipe) {  // K1 of this chunk waits for its binning; the next chunk's binning starts now
+        GSGPC_CUDA(cudaEventRecord(pipe->binned[pipe->set], pipe->bin));
+        GSGPC_CUDA(cudaStreamWaitEvent(ctx->stream, pipe->binned[pipe->set], 0));
+      }
       int hk = pt.begin(3);
       SplitFixJob fix{};
-      run_moments(L, dtype, P, idx_s.as<int>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
+      run_moments(LK, dtype, P, idx_s.as<int>(), off.as<int64_t>(), 0, nvalid, 0, g.cells, g, s->mom.as<double>(),
                   s->pat.as<uint8_t>(), errp, sb, rows_end, &fix);
       pt.end(hk);
       hk = pt.begin(6);
-      run_split_fix(L, sb, fix);
+      run_split_fix(LK, sb, fix);
       pt.end(hk);
       hk = pt.begin(7);
       if (probes > 0) {
-        run_probe_moments(L, dtype, P, idx_s.as<int>(), pw_dev, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
+        run_probe_moments(LK, dtype, P, idx_s.as<int>(), pw_dev, off.as<int64_t>(), 0, nvalid, 0, g.cells, g, probes,
                           s->pmom.as<double>(), errp, sb, rows_end);
       }
       pt.end(hk);
+      if (pipe) GSGPC_CUDA(cudaEventRecord(pipe->k1done[pipe->set], ctx->stream));
     } else {
       // bucket groups of ~equal rows; group j's K1 overlaps group j+1's slice sort
       const int64_t nv = hb[bd.nb];
@@ -1052,8 +1075,35 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
       if (trace) tkind.push_back(0);
       GSGPC_CUDA(cudaEventRecord(ctx->ev_copied[sl], ctx->copy));
     };
+    // device-resident rows in several chunks: binning of chunk k + 1 under K1 of chunk k (ChunkPipe)
+    static const int pipe_env = [] {
+      const char* e = getenv("GSGPC_CHUNK_PIPE");  // diagnostics: 1 = on (default off: measured slower at d = 2)
+      return e ? atoi(e) : 0;
+    }();
+    ChunkPipe pipe;
+    const bool piped = dev && nchunks > 1 && probes == 0 && !ctx->timing && pipe_env > 0;
+    struct PipeEvents {
+      ChunkPipe* p;
+      ~PipeEvents() {
+        for (int i = 0; i < 2; ++i) {
+          if (p->binned[i]) cudaEventDestroy(p->binned[i]);
+          if (p->k1done[i]) cudaEventDestroy(p->k1done[i]);
+        }
+      }
+    } pipe_events{&pipe};
     try {
       bin_error_reset(ctx);
+      if (piped) {
+        ctx->ensure_sort_stream();
+        pipe.bin = ctx->sort;
+        for (int i = 0; i < 2; ++i) {
+          GSGPC_CUDA(cudaEventCreateWithFlags(&pipe.binned[i], cudaEventDisableTiming));
+          GSGPC_CUDA(cudaEventCreateWithFlags(&pipe.k1done[i], cudaEventDisableTiming));
+        }
+        // fork: the binning stream starts after everything queued so far (snapshot, error reset)
+        GSGPC_CUDA(cudaEventRecord(pipe.binned[0], ctx->stream));
+        GSGPC_CUDA(cudaStreamWaitEvent(pipe.bin, pipe.binned[0], 0));
+      }
       if (!dev) {
         ctx->ensure_copy_stream();
         // the staging buffers may still be read by earlier work on the compute stream
@@ -1089,7 +1139,9 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
           }
         }
         tmark(ctx->stream);
-        add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes);
+        pipe.set = static_cast<int>(k & 1);
+        pipe.k = k;
+        add_chunk(ctx, s, pts->dtype, P, r1 - r0, s->n, pw, probes, piped ? &pipe : nullptr);
         tmark(ctx->stream);
         if (trace) tkind.push_back(1);
         if (!dev) GSGPC_CUDA(cudaEventRecord(ctx->ev_free[k & 1], ctx->stream));
@@ -1108,6 +1160,7 @@ gsgpc_status gsgpc_stats_add(gsgpc_ctx* ctx, gsgpc_stats* s, const gsgpc_points*
       bin_error_check(ctx);
     } catch (...) {
       if (ctx->copy) cudaStreamSynchronize(ctx->copy);
+      if (piped && pipe.bin) cudaStreamSynchronize(pipe.bin);
       snap.restore();
       throw;
     }
@@ -1201,7 +1254,7 @@ gsgpc_status gsgpc_stats_add_file(gsgpc_ctx* ctx, gsgpc_stats* s, const char* pa
             gen_probe_words(ctx, s, rows);
             pw = ctx->buf("probe_stage").as<uint64_t>();
           }
-          add_chunk(ctx, s, GSGPC_F64, P, rows, done, pw, s->probes);
+          add_chunk(ctx, s, GSGPC_F64, P, rows, done, pw, s->probes, nullptr);
           GSGPC_CUDA(cudaEventRecord(ctx->ev_free[sl], ctx->stream));
         } catch (...) {
           if (reader.joinable()) reader.join();
