@@ -81,3 +81,36 @@ def test_device_rows_over_several_chunks_and_rollback():
         acc.add(x, y)
     assert e.value.row == 1000 + bad + 1 and "outside grid" in str(e.value)
     _same(acc.finalize(), before, tol=0.0)
+
+
+def test_chunk_pipeline_gives_bitwise_the_sequential_statistics():
+    """GSGPC_CHUNK_PIPE=1 overlaps the binning of chunk k + 1 with the moments kernel of chunk k on
+    two scratch sets; kernels and accumulation order are the sequential path's, so the
+    statistics must be bit-identical (the knob is read once per process: two subprocesses)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, hashlib, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import torch, paper_2101_11751_b200 as G\n"
+        "g = torch.Generator(device='cuda').manual_seed(5)\n"
+        "for d, sizes in ((2, [64, 48]), (3, [20, 16, 12])):\n"
+        "    x = torch.rand((700_000, d), generator=g, device='cuda', dtype=torch.float32) * 0.9 + 0.05\n"
+        "    y = torch.sin(3 * x).sum(dim=1)\n"
+        "    grid = G.fit_grid_to_data([0.0] * d, [1.0] * d, sizes)\n"
+        "    st = G.sufficient_stats(grid, G.InterpScheme.Cubic, x, y)\n"
+        "    h = hashlib.sha256(st.stencil()[0].tobytes() + st.wty().tobytes() + np.float64(st.yty()).tobytes())\n"
+        "    print(d, st.n(), h.hexdigest())\n"
+    )
+    outs = []
+    for pipe in ("0", "1"):
+        env = dict(os.environ, GSGPC_CHUNK_PIPE=pipe, GSGPC_DEV_CHUNK_LOG2="16")  # 11 chunks
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout)
+    assert outs[0] == outs[1] and outs[0].count("\n") == 2
+    del hashlib
