@@ -244,6 +244,10 @@ def test_batches_merge_and_devices():
     d, sizes = 2, (31, 29)
     g = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes)
     x, y = points(d, 30000, 7)
+    # on-node rows (zero weights dropped: fewer W^T W entries) in ONE shard only, at cells no other
+    # row of that kind touches: the merged structure is the OR of the shards' structures
+    x[25000:25003] = np.array([[3, 5], [11, 2], [20, 17]]) / (np.array(sizes) - 5.0)
+    x[15000, 1] = 7 / (sizes[1] - 5.0)
     full = G.sufficient_stats(g, G.InterpScheme.Cubic, x, y)
     acc = G.SufficientStatsAccumulator(g)
     acc.add(x[:10000], y[:10000])
@@ -257,6 +261,34 @@ def test_batches_merge_and_devices():
     v1, _ = st.stencil()
     assert rel_err(v1, v0) <= 1e-12
     assert rel_err(st.wty(), full.wty()) <= 1e-12
+    # SufficientStatsAccumulator::merge (interp.cpp:202-210) against the checker's statistics of all
+    # rows: the same CSR structure (setFromTriplets of the merged map), values, W^T y, yᵀy, n
+    ost = O.sufficient_stats(ogrid(g), x, y, scheme=1)
+    rp, col, val = st.csr()
+    orp, ocol, oval, owty = ost.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert rel_err(val, oval) <= 1e-10 and rel_err(st.wty(), owty) <= 1e-10
+    assert abs(st.yty() - ost.yty) <= 1e-12 * ost.yty and st.max_row_nnz() == ost.max_row_nnz()
+    # sparse grid (most cells empty, some touched only by on-node rows of ONE shard): the merged
+    # structure is the union of the shards' structures, each strictly smaller than the merge
+    sizes2 = (60, 50)
+    g2 = G.fit_grid_to_data(np.zeros(d), np.ones(d), sizes2)
+    xs, ys = points(d, 900, 8, edge=False)
+    xs[800:830] = np.round(xs[800:830] * (np.array(sizes2) - 5.0)) / (np.array(sizes2) - 5.0)  # on nodes
+    xs[830:860, 0] = np.round(xs[830:860, 0] * (sizes2[0] - 5.0)) / (sizes2[0] - 5.0)          # on a node line
+    a, b = G.SufficientStatsAccumulator(g2), G.SufficientStatsAccumulator(g2)
+    a.add(xs[:450], ys[:450])
+    b.add(xs[450:], ys[450:])
+    nnz_a = len(G.sufficient_stats(g2, G.InterpScheme.Cubic, xs[:450], ys[:450]).csr()[2])
+    nnz_b = len(G.sufficient_stats(g2, G.InterpScheme.Cubic, xs[450:], ys[450:]).csr()[2])
+    a.merge(b)
+    sm = a.finalize()
+    om = O.sufficient_stats(ogrid(g2), xs, ys, scheme=1)
+    rp, col, val = sm.csr()
+    orp, ocol, oval, owty = om.csr()
+    assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    assert rel_err(val, oval) <= 1e-10 and rel_err(sm.wty(), owty) <= 1e-10 and sm.n() == om.n == 900
+    assert max(nnz_a, nnz_b) < len(val) < nnz_a + nnz_b
 
 
 @pytest.mark.parametrize("d", [1, 2, 3])
