@@ -56,8 +56,9 @@ def parse():
     p.add_argument("--cpu-rows", type=int, default=200_000,
                    help="single-thread CPU baseline: prefix rows per trial (SURVEY §8(d): >= 2e5 at d = 3)")
     p.add_argument("--cpu-trials", type=int, default=3)
-    p.add_argument("--ref-rows", type=int, default=100_000,
-                   help="--impl reference: prefix rows per step (one pinned thread, ~17 s per step at d = 3)")
+    p.add_argument("--ref-rows", type=int, default=0,
+                   help="rows per step of the reference arm (0 = sized so that steps + warmup take ~4 minutes "
+                        "at ~6e3 rows/s on one host thread, at most 1e5)")
     p.add_argument("--cpu-sharded", action="store_true",
                    help="also time the oracle sharded over all host threads (merge(); labelled separately)")
     p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -241,7 +242,8 @@ def run_reference(args):
 
     O, kind, what = cpu_checker()
     cfg = S.CONFIGS[args.config]
-    rows = min(cfg.n, args.ref_rows)
+    ref_rows = args.ref_rows or max(20_000, min(100_000, 1_400_000 // max(1, args.steps + args.warmup)))
+    rows = min(cfg.n, ref_rows)
     x, y = S.generate(args.config, n=rows)
     grid = S.grid_for(cfg)
     og = oracle_grid(grid)
