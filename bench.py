@@ -362,8 +362,10 @@ def run_ours(args):
         step(rows)
     phases = ctx.phase_times()
     ctx.enable_phase_timing(False)
-    ph_ms = {k: v[0] / max(v[1], 1) for k, v in phases.items()}
+    # per STEP (a batch above 2^27 rows runs in several device chunks: one K1 launch per chunk)
+    ph_ms = {k: v[0] / args.steps for k, v in phases.items()}
     k1_ms = ph_ms.get("moments", float("nan"))
+    k1_launches = phases.get("moments", (0.0, args.steps))[1] / args.steps
 
     m = grid.num_points()
     s_min = st.n_offsets()
@@ -385,7 +387,8 @@ def run_ours(args):
     flops_ach = flops_pt * n / (k1_ms / 1e3) / 1e12
     hbm = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
            "traffic": traffic, "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
-           "algorithmic_bytes_per_launch": b_pre}
+           "algorithmic_bytes_per_launch": b_pre / k1_launches, "k1_launches_per_step": k1_launches,
+           "rows_per_launch": n / k1_launches, "k1_ms_per_launch": k1_ms / k1_launches}
     if cfg.d == 3:
         # K1 at d = 3 runs its 407 moment MACs per row on the FP64 tensor pipe (DMMA): that pipe,
         # not HBM, binds it (814 flop per 16-byte row).  MEASURED_PEAKS.json has no FP64 figure
@@ -398,7 +401,7 @@ def run_ours(args):
             "traffic": traffic,
             "peak_source": "measured in this run: gsgpc_diag_fp64_tensor (mma.sync.m8n8k4.f64 loop); "
                            "MEASURED_PEAKS.json has no FP64 entry",
-            "flops_per_point": flops_pt, "algorithmic_flops_per_launch": flops_pt * n,
+            "flops_per_point": flops_pt, "algorithmic_flops_per_launch": flops_pt * n / k1_launches,
             "k1_ms": k1_ms, "phase_ms": ph_ms,
             "hbm": hbm,
             "fp64_dfma_peak": fp64_peak,
@@ -406,7 +409,9 @@ def run_ours(args):
                     "512 FMAs per row (8 m8n8k4 per 4 rows)",
         }
     else:
-        roofline = dict(hbm, kernel="k_moments_lane (K1: per-cell polynomial moments)", k1_ms=k1_ms, phase_ms=ph_ms,
+        k1_name = "k_moments_d2c_mma (K1: per-cell polynomial moments, FP64 DMMA)" if cfg.d == 2 else \
+            "k_moments_lane (K1: per-cell polynomial moments)"
+        roofline = dict(hbm, kernel=k1_name, k1_ms=k1_ms, phase_ms=ph_ms,
                         fp64={"achieved": flops_ach, "peak": fp64_peak, "unit": "TFLOP/s",
                               "frac": flops_ach / fp64_peak, "flops_per_point": flops_pt,
                               "peak_source": "measured (gsgpc_diag_fp64_peak DFMA loop, this run)"})
