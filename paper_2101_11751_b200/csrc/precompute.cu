@@ -1219,7 +1219,13 @@ __global__ void __launch_bounds__(128, MINB) k_moments_d3c_mma(RowSrc<T, PK> pay
 // bound the kernel on the shared-memory pipe at config 4).
 constexpr int D2C_QX = 49, D2C_Q = 49 + 16;
 
-__device__ __forceinline__ int d2c_swz(int R) { return ((R & 1) << 3) | ((R >> 1) & 7); }
+// A 64-bit shared load is served per half-warp (16 lanes = 4 elements × the step's 4 rows), so the
+// rows' swizzles must differ in the 8-block bit (row bit 0) AND the 4-block bit (row bit 1);
+// the low two bits take row bits 2-3, which keeps the map a bijection of the row mod 16 (the
+// staging stores, one row per lane, stay conflict-free).  With ((R >> 1) & 7) in the low bits the
+// rows kq = 0 and kq = 2 of a step shared a 4-block: 4 wavefronts per fragment load instead of 2
+// (ncu source page: 7.4 vs 3.7 per batch and load).
+__device__ __forceinline__ int d2c_swz(int R) { return ((R & 1) << 3) | (((R >> 1) & 1) << 2) | ((R >> 2) & 3); }
 
 // row_t plus the flat cell of the row (classify's numbering: row-major over nc[k]).
 template <typename T>
