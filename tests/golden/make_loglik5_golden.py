@@ -7,6 +7,9 @@ numpy rows synthetic.generate(5, 1e6), which are the same on every machine) and 
 tests/test_gpu_solve_parity.py recomputes the GPU side live and compares.
 
     python tests/golden/make_loglik5_golden.py      (CPU only; ~1 h on 8 threads)
+
+The committed file was generated on the GPU box's 16 host threads (stats 105 s, log-likelihood
+1367 s; log in profiles/r2u_loglik5_golden_generation.log), round 2.
 """
 import json
 import os
